@@ -1,0 +1,155 @@
+/*
+ * bitlut_b200 -- C ABI of the B200 (sm_100a) LUT mixed-precision GEMV/GEMM.
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `bitlut` (arXiv 2407.00088 reimplementation, /root/reference/pkg).  The
+ * reference has no native ABI of its own: its "native layer" is numba-JIT'd
+ * Python (`_kernels.py`) called from `kernel.py`.  Each entry point below
+ * names the reference function it replaces (file:line relative to
+ * pkg/src/bitlut/).  Python binds these through ctypes underneath
+ * torch.library custom ops (paper_2407_00088_b200/_native.py); INTEGRATION.md
+ * shows the binding a maintainer would add to the reference itself.
+ *
+ * Conventions:
+ *   - every pointer is a DEVICE pointer allocated by the caller; the library
+ *     never allocates, frees, or synchronizes, and keeps no global state;
+ *   - kernels are enqueued on `stream` (a cudaStream_t passed as void*;
+ *     NULL = legacy default stream);
+ *   - the return value is BITLUT_OK or a negative code mapping 1:1 onto the
+ *     reference's error classes (errors.py:8-69); shape/parameter checks
+ *     happen before any launch, a launch failure returns BITLUT_EINTERNAL;
+ *   - no C++ exception crosses the ABI.
+ */
+#ifndef BITLUT_B200_H
+#define BITLUT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes <-> errors.py classes */
+#define BITLUT_OK          0
+#define BITLUT_EPARAM     -1   /* ParameterError      errors.py:15  */
+#define BITLUT_EDATA      -2   /* DataError           errors.py:21  */
+#define BITLUT_ESHAPE     -3   /* ShapeError          errors.py:27  */
+#define BITLUT_ELAYOUT    -4   /* LayoutError         errors.py:33  */
+#define BITLUT_EOVERFLOW  -5   /* OverflowConfigError errors.py:39  */
+#define BITLUT_EINTERNAL -100  /* BitLutError (launch failure)  errors.py:8 */
+
+/* element types of activations / weight scales / zeros */
+#define BITLUT_DT_F32 0
+#define BITLUT_DT_F16 1
+
+/* lookup-table modes */
+#define BITLUT_TABLE_Q8  0  /* int8 half tables + per-group table scales (vector-q8 semantics) */
+#define BITLUT_TABLE_F16 1  /* fp16 half tables (BASELINE "fp16 tables") */
+
+/* mpgemm flags */
+#define BITLUT_FLAG_PDL 1   /* launch with programmatic dependent launch */
+
+/*
+ * GPU weight layout ("layout v2", this library's own; the reference's v1
+ * layout is docs/formats.md:60-90).  Filled by bitlut_gpu_layout_query.
+ *   tile_channels : output channels per tile (32/bits, or 32 for bits=3)
+ *   stream_groups : 32-stream groups per tile (1, or 3 for bits=3)
+ *   unit_kg       : k-groups (4 activations each) per lane unit
+ *   lanes_per_group : lane units per quantization group
+ *   bytes         : total bytes (== bits*m*k/8, same as v1)
+ */
+typedef struct {
+  int32_t m, k, bits, group_size;
+  int32_t tile_channels, stream_groups, unit_kg, lanes_per_group;
+  int64_t bytes;
+} bitlut_gpu_layout;
+
+/* Validate (m, k, bits, group_size) for the CUDA path and describe layout v2. */
+int bitlut_gpu_layout_query(int m, int k, int bits, int group_size, bitlut_gpu_layout* out);
+
+/* ---------------- offline weight pipeline (weight_prep.py) ---------------- */
+
+/* decompose_bits  weight_prep.py:86-105.
+ * q (m,k) u8 -> indices (bits, m, k/g) u8, index = sum_j bit_i(q[m,kg*g+j]) << j */
+int bitlut_decompose_bits(const uint8_t* q, int m, int k, int bits, int g,
+                          uint8_t* indices, void* stream);
+
+/* pack_and_permute (v1 layout)  weight_prep.py:214-246, _permute_plane :193-201,
+ * interleave_layout :131-156.  indices (bits, m, k/g) -> planes (bits, m*(k/g)/per) */
+int bitlut_pack_v1(const uint8_t* indices, int bits, int m, int k, int g,
+                   int m_tile, int k_tile, int lanes, uint8_t* planes, void* stream);
+
+/* unpack_planes  weight_prep.py:249-257 (inverse of bitlut_pack_v1). */
+int bitlut_unpack_v1(const uint8_t* planes, int bits, int m, int k, int g,
+                     int m_tile, int k_tile, int lanes, uint8_t* indices, void* stream);
+
+/* The offline weight-permutation kernel of the north star: plane indices
+ * (bits, m, k/4) -> layout v2 (mirror-encoded nibbles, 16 B per 32 streams
+ * x 1 k-group, unit-interleaved so each warp load is one coalesced span). */
+int bitlut_repack_gpu(const uint8_t* indices, int bits, int m, int k, int group_size,
+                      uint8_t* wgpu, void* stream);
+
+/* Inverse of bitlut_repack_gpu (verification / round trips). */
+int bitlut_unrepack_gpu(const uint8_t* wgpu, int bits, int m, int k, int group_size,
+                        uint8_t* indices, void* stream);
+
+/* ---------------- online activation tables (lut_build.py) ---------------- */
+
+/* precompute_lut  lut_build.py:105-127.  a (n,k) -> full (n, k/g, 2^g) f32 */
+int bitlut_precompute_lut(const void* a, int a_dtype, int n, int k, int g,
+                          float* full, void* stream);
+
+/* mirror_consolidate  lut_build.py:130-143.  full (n,kg,2^g) -> half (n,kg,2^(g-1));
+ * *asym_flag (device int, caller zeroes it) is set to 1 if the input is not
+ * exactly sign-symmetric (the reference raises DataError). */
+int bitlut_mirror_consolidate(const float* full, int n, int kg, int g, float* half,
+                              int* asym_flag, void* stream);
+
+/* quantize_tables  lut_build.py:153-179.  half (n,kg,w) f32 ->
+ * qentries (n,kg,w) i8 + table_scales (n, kg*g/group_size) f32 */
+int bitlut_quantize_tables(const float* half, int n, int kg, int g, int group_size,
+                           int8_t* qentries, float* table_scales, void* stream);
+
+/* row_sums  lut_build.py:182-194.  a (n,k) -> sums (n, k/group_size) f32 */
+int bitlut_row_sums(const void* a, int a_dtype, int n, int k, int group_size,
+                    float* sums, void* stream);
+
+/* Fused per-call table build used by mpgemm (kernel.py:226-251,
+ * _build_block_tables): one launch produces, for g = 4,
+ *   mode Q8 : tables = int8 (n, k/4, 8) [== quantize_tables(mirror_consolidate(
+ *             precompute_lut(a)))], tscales (n, k/gs) f32, rowsums (n, k/gs) f32
+ *   mode F16: tables = fp16 (n, k/4, 8) [fp16-rounded half tables], rowsums.   */
+int bitlut_build_lut(const void* a, int a_dtype, int n, int k, int group_size, int mode,
+                     void* tables, float* tscales, float* rowsums, void* stream);
+
+/* ---------------- lookup-accumulate (kernel.py / _kernels.py) ---------------- */
+
+/* mpgemm  kernel.py:280-371 with _kernels.gemv_q8_vector :141-192 (mode Q8)
+ * or an fp16-table analogue of _kernels.gemv_real :85-138 (mode F16).
+ *   wgpu      layout-v2 weights (bitlut_repack_gpu)
+ *   wscales   (m, k/gs) per-group weight scales, dtype scale_dtype
+ *   zeros     (m, k/gs) zero points or NULL (= implicit 2^(bits-1), the
+ *             reference's symmetric scheme core.py:86-100)
+ *   tables/tscales/rowsums  from bitlut_build_lut (tscales unused for F16)
+ *   out       (n, m) f32, overwritten
+ *   partials  NULL, or (n, bits, m, k/gs) int32: the exact per-(row, plane,
+ *             channel, group) int32 staging values (Q8 mode only)
+ * In Q8 mode with zeros == NULL, `out` is bitwise identical to the
+ * reference's vector-q8 output. */
+int bitlut_mpgemm(const uint8_t* wgpu, int m, int k, int bits, int group_size,
+                  const void* wscales, const void* zeros, int scale_dtype,
+                  const void* tables, const float* tscales, const float* rowsums,
+                  int mode, int n, float* out, int32_t* partials, int flags,
+                  void* stream);
+
+/* Number of kernel launches one bitlut_mpgemm call enqueues (for accounting). */
+int bitlut_mpgemm_launches(int m, int k, int bits, int group_size, int mode, int n);
+
+/* Library version string. */
+const char* bitlut_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BITLUT_B200_H */

@@ -1,0 +1,70 @@
+// Shared device helpers for the bitlut B200 kernels (sm_100a only).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+
+#include "../../include/bitlut_b200.h"
+
+#define BL_DEV __device__ __forceinline__
+
+namespace bl {
+
+// prmt.b32 in its default mode.  Unlike __byte_perm (which masks each
+// selector nibble to 3 bits), bit 3 of a selector nibble is honoured: the
+// output byte becomes the sign (msb) of the selected byte replicated.  The
+// int8 lookup relies on exactly that (see gemv.cu, "A/B tables").
+BL_DEV uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+
+// d = c + mult.lo16 * b.byte0 + mult.hi16 * b.byte1   (signed)
+BL_DEV int dp2a_lo(uint32_t mult, uint32_t b, int c) {
+  int d;
+  asm("dp2a.lo.s32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(mult), "r"(b), "r"(c));
+  return d;
+}
+// d = c + mult.lo16 * b.byte2 + mult.hi16 * b.byte3   (signed)
+BL_DEV int dp2a_hi(uint32_t mult, uint32_t b, int c) {
+  int d;
+  asm("dp2a.hi.s32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(mult), "r"(b), "r"(c));
+  return d;
+}
+
+struct U8x32 { uint32_t w[8]; };
+
+// 256-bit streaming load (sm_100: LDG.E.256): weights are read exactly once.
+BL_DEV U8x32 ld_stream_256(const void* p) {
+  U8x32 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]),
+                 "=r"(r.w[4]), "=r"(r.w[5]), "=r"(r.w[6]), "=r"(r.w[7])
+               : "l"(p));
+  return r;
+}
+
+BL_DEV uint4 ld_nc_128(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+
+// Programmatic dependent launch (PDL) controls.  Both are no-ops when the
+// kernel was not launched with the programmatic-serialization attribute.
+BL_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+BL_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+BL_DEV float to_f32(float x) { return x; }
+BL_DEV float to_f32(__half x) { return __half2float(x); }
+
+}  // namespace bl
+
+// Host-side launch-status helper: every entry point returns one of the
+// BITLUT_* codes; a CUDA launch failure maps to BITLUT_EINTERNAL.
+static inline int bl_launch_status() {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BITLUT_OK : BITLUT_EINTERNAL;
+}

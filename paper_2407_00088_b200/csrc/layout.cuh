@@ -1,0 +1,63 @@
+// Layout v2: the GPU weight layout consumed by the lookup kernels.
+//
+// Terms:
+//   stream   = (output channel c, bit plane p): one int32 staging accumulator
+//              per quantization group, exactly the reference's `stage[m]` of
+//              plane p (_kernels.py:154-185).
+//   tile     = tile_channels consecutive channels; its streams are flattened
+//              channel-major (c*bits + p) and cut into 32-stream groups (SG).
+//   chunk    = 16 bytes = 32 nibbles = the 32 streams of one SG at one
+//              k-group kg (4 activations).  Nibble j of word w holds stream
+//              8w+j.  The nibble is the mirror-encoded index
+//              x = idx ^ (7 * (idx >> 3)): bit 3 = mirror flag s, bits 0-2 =
+//              the half-table slot eff (_kernels.py:175-177 computes the same
+//              s/eff at run time; here it is done once, offline).
+//   unit     = unit_kg consecutive k-groups of one SG, processed by one lane.
+//              Units are interleaved 32 at a time so that, at step j, the 32
+//              lanes of a warp read 32 consecutive 32-byte spans (2 chunks).
+#pragma once
+#include <cstdint>
+
+namespace bl {
+
+struct LayoutV2 {
+  int m, k, bits, gs;
+  int tile_ch, n_sg, R, Lg;   // channels per tile, SGs per tile, kg per unit, units per group
+  int KG, NQ, U;              // k-groups, quant groups, units per SG row
+  int n_tiles;
+
+  __host__ __device__ int64_t sg_row_base(int tile, int sg) const {
+    return ((int64_t)tile * n_sg + sg) * (int64_t)KG * 16;
+  }
+  // byte offset of the 16-byte chunk (tile, sg, kg)
+  __host__ __device__ int64_t chunk_offset(int tile, int sg, int kg) const {
+    int u = kg / R, r = kg - u * R;
+    int ub = u >> 5, l = u & 31;
+    int nu_b = U - 32 * ub; if (nu_b > 32) nu_b = 32;
+    int jp = r >> 1, kk = r & 1;
+    return sg_row_base(tile, sg) + (int64_t)ub * (32 * R * 16) + (int64_t)(jp * nu_b + l) * 32 + kk * 16;
+  }
+};
+
+// Returns BITLUT_OK or an error code; fills L on success.
+inline int make_layout(int m, int k, int bits, int gs, LayoutV2* L) {
+  if (bits < 1 || bits > 4) return -1;          // EPARAM
+  if (gs < 4 || k <= 0 || m <= 0) return -1;
+  if (gs % 16 != 0) return -1;                   // CUDA path: gs multiple of 16
+  int gpg = gs / 4;
+  if (gpg > 128) return -1;                      // packed int32 accumulator bound
+  int R = (gpg % 8 == 0) ? 8 : 4;
+  int Lg = gpg / R;
+  if (Lg & (Lg - 1)) return -1;                  // lanes per group must be a power of two
+  if (k % gs != 0) return -4;                    // ELAYOUT
+  if (m % 32 != 0) return -4;
+  L->m = m; L->k = k; L->bits = bits; L->gs = gs;
+  L->tile_ch = (bits == 3) ? 32 : 32 / bits;
+  L->n_sg = (bits == 3) ? 3 : 1;
+  L->R = R; L->Lg = Lg;
+  L->KG = k / 4; L->NQ = k / gs; L->U = L->KG / R;
+  L->n_tiles = m / L->tile_ch;
+  return 0;
+}
+
+}  // namespace bl
