@@ -385,3 +385,48 @@ def dequant_gemm(a: np.ndarray, q: np.ndarray, wscales: np.ndarray, bits: int,
     w = (q.reshape(m, k // group_size, group_size).astype(np.float64) - z[:, :, None]) \
         * np.asarray(wscales, dtype=np.float64)[:, :, None]
     return a @ w.reshape(m, k).T
+
+
+# --------------------------------------------------------------------------
+# C restatement (oracle/bitlut_oracle.c): same arithmetic, fast enough to be
+# the timed CPU baseline.  Built by `make -C oracle` (build() runs it).
+# --------------------------------------------------------------------------
+
+_CLIB = None
+
+
+def c_lib():
+    import ctypes
+    import os
+    import subprocess
+    global _CLIB
+    if _CLIB is None:
+        here = os.path.dirname(os.path.abspath(__file__))
+        path = os.path.join(here, "_build", "liboracle.so")
+        if not os.path.exists(path):
+            subprocess.run(["make", "-s", "-C", here], check=True)
+        _CLIB = ctypes.CDLL(path)
+        _CLIB.orc_mpgemm.restype = ctypes.c_int
+        _CLIB.orc_max_threads.restype = ctypes.c_int
+    return _CLIB
+
+
+def c_mpgemm(a, planes_v1, m, k, bits, group_size, wscales, mode="vector-q8",
+             threads=0, m_tile=32, k_tile=128, lanes=16):
+    """Reference mpgemm (kernel.py:280-371) via the C port, v1 planes in."""
+    import ctypes
+    P = ctypes.c_void_p
+    a = np.ascontiguousarray(a, dtype=F32)
+    if a.ndim == 1:
+        a = a.reshape(1, -1)
+    planes = np.ascontiguousarray(planes_v1, dtype=np.uint8)
+    ws = np.ascontiguousarray(wscales, dtype=F32)
+    out = np.empty((a.shape[0], m), dtype=F32)
+    c_lib().orc_mpgemm(a.ctypes.data_as(P), a.shape[0], planes.ctypes.data_as(P), m, k, bits,
+                       group_size, m_tile, k_tile, lanes, ws.ctypes.data_as(P),
+                       0 if mode == "vector-q8" else 1, int(threads), out.ctypes.data_as(P))
+    return out
+
+
+def c_max_threads() -> int:
+    return int(c_lib().orc_max_threads())

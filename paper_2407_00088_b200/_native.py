@@ -1,0 +1,165 @@
+"""Binding of the C ABI (include/bitlut_b200.h) and the torch custom ops.
+
+The shared library ``_lib/libbitlut_b200.so`` is built in-tree by
+``paper_2407_00088_b200.build`` (nvcc, sm_100a).  There is no CPU
+fallback: if the library or a CUDA device is missing, every op raises.
+
+torch.library custom ops (namespace ``bitlut_b200``) wrap the C entry
+points so the ops compose with torch streams, CUDA graphs and
+torch.compile (fake/meta implementations give shapes without a GPU).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import torch
+
+from .errors import BitLutError, raise_for_status
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libbitlut_b200.so")
+
+DT_F32, DT_F16 = 0, 1
+TABLE_Q8, TABLE_F16 = 0, 1
+FLAG_PDL = 1
+
+_vp, _i = ctypes.c_void_p, ctypes.c_int
+
+_SIGS = {
+    "bitlut_gpu_layout_query": [_i, _i, _i, _i, _vp],
+    "bitlut_decompose_bits": [_vp, _i, _i, _i, _i, _vp, _vp],
+    "bitlut_pack_v1": [_vp, _i, _i, _i, _i, _i, _i, _i, _vp, _vp],
+    "bitlut_unpack_v1": [_vp, _i, _i, _i, _i, _i, _i, _i, _vp, _vp],
+    "bitlut_repack_gpu": [_vp, _i, _i, _i, _i, _vp, _vp],
+    "bitlut_unrepack_gpu": [_vp, _i, _i, _i, _i, _vp, _vp],
+    "bitlut_precompute_lut": [_vp, _i, _i, _i, _i, _vp, _vp],
+    "bitlut_mirror_consolidate": [_vp, _i, _i, _i, _vp, _vp, _vp],
+    "bitlut_quantize_tables": [_vp, _i, _i, _i, _i, _vp, _vp, _vp],
+    "bitlut_row_sums": [_vp, _i, _i, _i, _i, _vp, _vp],
+    "bitlut_build_lut": [_vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp],
+    "bitlut_mpgemm": [_vp, _i, _i, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _i, _i, _vp, _vp, _i, _vp],
+    "bitlut_mpgemm_launches": [_i, _i, _i, _i, _i, _i],
+}
+
+
+class GpuLayout(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_int32), ("k", ctypes.c_int32), ("bits", ctypes.c_int32),
+                ("group_size", ctypes.c_int32), ("tile_channels", ctypes.c_int32),
+                ("stream_groups", ctypes.c_int32), ("unit_kg", ctypes.c_int32),
+                ("lanes_per_group", ctypes.c_int32), ("bytes", ctypes.c_int64)]
+
+
+_LIB: Optional[ctypes.CDLL] = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load the CUDA library (raises if it was not built)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise BitLutError(
+                f"native library not found at {LIB_PATH}; build it with "
+                "`python -c 'import __graft_entry__ as g; g.build()'` (nvcc, sm_100a)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, args in _SIGS.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = ctypes.c_int
+        L.bitlut_version.restype = ctypes.c_char_p
+        L.bitlut_version.argtypes = []
+        _LIB = L
+    return _LIB
+
+
+def exported_symbols() -> list[str]:
+    return list(_SIGS) + ["bitlut_version"]
+
+
+def require_cuda(t: torch.Tensor, what: str) -> None:
+    if not t.is_cuda:
+        raise BitLutError(f"{what} must be a CUDA tensor (the B200 package has no CPU path)")
+
+
+def ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def stream_of(t: torch.Tensor):
+    return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+
+def dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return DT_F32
+    if t.dtype == torch.float16:
+        return DT_F16
+    raise BitLutError(f"unsupported dtype {t.dtype} (float32 or float16)")
+
+
+def layout_query(m: int, k: int, bits: int, group_size: int) -> GpuLayout:
+    out = GpuLayout()
+    rc = lib().bitlut_gpu_layout_query(m, k, bits, group_size, ctypes.byref(out))
+    raise_for_status(rc, f"GPU layout for m={m}, k={k}, bits={bits}, group_size={group_size}")
+    return out
+
+
+# ---------------------------------------------------------------------------
+# torch custom ops
+# ---------------------------------------------------------------------------
+
+@torch.library.custom_op("bitlut_b200::build_lut", mutates_args=())
+def build_lut(a: torch.Tensor, group_size: int, mode: int) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    """Fused table build (kernel.py:226-251): a (n, k) f16/f32 ->
+    (tables (n, k/4, 8) int8|fp16, table scales (n, k/gs), row sums (n, k/gs))."""
+    require_cuda(a, "activations")
+    a = a.contiguous()
+    n, k = a.shape
+    nq = k // group_size
+    tdt = torch.int8 if mode == TABLE_Q8 else torch.float16
+    tables = torch.empty((n, k // 4, 8), dtype=tdt, device=a.device)
+    ts = torch.empty((n, nq), dtype=torch.float32, device=a.device)
+    rs = torch.empty((n, nq), dtype=torch.float32, device=a.device)
+    rc = lib().bitlut_build_lut(ptr(a), dtype_code(a), n, k, group_size, mode, ptr(tables),
+                                ptr(ts), ptr(rs), stream_of(a))
+    raise_for_status(rc, "bitlut_build_lut")
+    return tables, ts, rs
+
+
+@build_lut.register_fake
+def _(a, group_size, mode):
+    n, k = a.shape
+    tdt = torch.int8 if mode == TABLE_Q8 else torch.float16
+    nq = k // group_size
+    return (a.new_empty((n, k // 4, 8), dtype=tdt), a.new_empty((n, nq), dtype=torch.float32),
+            a.new_empty((n, nq), dtype=torch.float32))
+
+
+@torch.library.custom_op("bitlut_b200::lookup", mutates_args=())
+def lookup(wgpu: torch.Tensor, wscales: torch.Tensor, zeros: Optional[torch.Tensor],
+           tables: torch.Tensor, tscales: torch.Tensor, rowsums: torch.Tensor,
+           m: int, k: int, bits: int, group_size: int, mode: int, flags: int,
+           want_partials: bool) -> tuple[torch.Tensor, torch.Tensor]:
+    """Lookup-accumulate (kernel.py:280-371 / _kernels.py:141-192):
+    returns (out (n, m) f32, partials (n, bits, m, k/gs) int32 or empty)."""
+    require_cuda(wgpu, "packed weights")
+    n = tables.shape[0]
+    out = torch.empty((n, m), dtype=torch.float32, device=wgpu.device)
+    nq = k // group_size
+    partials = (torch.empty((n, bits, m, nq), dtype=torch.int32, device=wgpu.device)
+                if want_partials else torch.empty(0, dtype=torch.int32, device=wgpu.device))
+    rc = lib().bitlut_mpgemm(ptr(wgpu), m, k, bits, group_size, ptr(wscales), ptr(zeros),
+                             dtype_code(wscales), ptr(tables), ptr(tscales), ptr(rowsums), mode, n,
+                             ptr(out), ptr(partials) if want_partials else None, flags,
+                             stream_of(wgpu))
+    raise_for_status(rc, "bitlut_mpgemm")
+    return out, partials
+
+
+@lookup.register_fake
+def _(wgpu, wscales, zeros, tables, tscales, rowsums, m, k, bits, group_size, mode, flags,
+      want_partials):
+    n = tables.shape[0]
+    nq = k // group_size
+    return (wgpu.new_empty((n, m), dtype=torch.float32),
+            wgpu.new_empty((n, bits, m, nq) if want_partials else (0,), dtype=torch.int32))

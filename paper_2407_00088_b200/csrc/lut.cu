@@ -1,0 +1,289 @@
+// Online activation tables on the GPU (reference: pkg/src/bitlut/lut_build.py).
+//
+// Bit-exactness contract: every float operation below is the one the
+// reference performs, in the same order, with explicit round-to-nearest
+// intrinsics so nvcc cannot contract or reorder (no --use_fast_math):
+//   entries     ((+-a0 +- a1) +- a2) +- a3           lut_build.py:121-125
+//   table scale max|e| / 127  (IEEE division)        lut_build.py:172-173
+//   q           trunc(e/scale + copysign(0.5, .))   lut_build.py:174-176
+//   row sums    left-to-right f32 accumulation        lut_build.py:191-193
+#include "common.cuh"
+
+namespace {
+
+template <typename T>
+__device__ __forceinline__ float load_act(const void* a, int64_t i) {
+  return bl::to_f32(reinterpret_cast<const T*>(a)[i]);
+}
+
+__device__ __forceinline__ float act(const void* a, int dtype, int64_t i) {
+  return dtype == BITLUT_DT_F16 ? load_act<__half>(a, i) : load_act<float>(a, i);
+}
+
+// ---- precompute_lut (lut_build.py:105-127), general g <= 8 ----
+__global__ void precompute_lut_kernel(const void* __restrict__ a, int dtype, int n, int k, int g,
+                                      float* __restrict__ full) {
+  const int kgt = k / g;
+  const int W = 1 << g;
+  const int64_t total = (int64_t)n * kgt;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t row = t / kgt;
+    int kg = (int)(t - row * kgt);
+    float v[8];
+    for (int j = 0; j < g; j++) v[j] = act(a, dtype, row * k + (int64_t)kg * g + j);
+    float* dst = full + t * W;
+    for (int idx = 0; idx < W; idx++) {
+      float e = (idx & 1) ? v[0] : -v[0];
+      for (int j = 1; j < g; j++) e = ((idx >> j) & 1) ? __fadd_rn(e, v[j]) : __fsub_rn(e, v[j]);
+      dst[idx] = e;
+    }
+  }
+}
+
+// ---- mirror_consolidate (lut_build.py:130-143) ----
+__global__ void mirror_kernel(const float* __restrict__ full, int64_t rows, int g,
+                              float* __restrict__ half, int* __restrict__ asym) {
+  const int H = 1 << (g - 1);
+  const int64_t total = rows * H;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = t / H;
+    int w = (int)(t - r * H);
+    const float* src = full + r * 2 * H;
+    float lo = src[w];
+    half[t] = lo;
+    // full[half + w] must equal -full[half - 1 - w]
+    if (src[H + w] != -src[H - 1 - w]) atomicOr(asym, 1);
+  }
+}
+
+// ---- quantize_tables (lut_build.py:153-179), one block per (row, quant group) ----
+__global__ void quantize_tables_kernel(const float* __restrict__ half, int kg, int width, int gpg,
+                                       int8_t* __restrict__ q, float* __restrict__ scales) {
+  const int gq = blockIdx.x, row = blockIdx.y;
+  const int nq = kg / gpg;
+  const int64_t base = ((int64_t)row * kg + (int64_t)gq * gpg) * width;
+  const int cnt = gpg * width;
+  float mx = 0.f;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) mx = fmaxf(mx, fabsf(half[base + i]));
+  __shared__ float red[32];
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  float scale = __fdiv_rn(red[0], 127.0f);
+  if (scale == 0.0f) scale = 1.0f;
+  if (threadIdx.x == 0) scales[(int64_t)row * nq + gq] = scale;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    float s = __fdiv_rn(half[base + i], scale);
+    float r = truncf(__fadd_rn(s, copysignf(0.5f, s)));
+    r = fminf(fmaxf(r, -127.f), 127.f);
+    q[base + i] = (int8_t)(int)r;
+  }
+}
+
+// ---- row_sums (lut_build.py:182-194), one thread per (row, group) ----
+__global__ void row_sums_kernel(const void* __restrict__ a, int dtype, int n, int k, int gs,
+                                float* __restrict__ sums) {
+  const int nq = k / gs;
+  const int64_t total = (int64_t)n * nq;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t row = t / nq;
+    int gq = (int)(t - row * nq);
+    const int64_t base = row * k + (int64_t)gq * gs;
+    float acc = 0.f;
+    for (int j = 0; j < gs; j++) acc = __fadd_rn(acc, act(a, dtype, base + j));
+    sums[t] = acc;
+  }
+}
+
+// ---- fused per-call build for g = 4 (kernel.py:226-251) ----
+// grid (ceil(KG/256), n), 256 threads, one thread per k-group.  Quant groups
+// (gpg k-groups, a power of two <= 128) never straddle a block.
+constexpr int kLutThreads = 256;
+
+template <int MODE, typename AT>
+__global__ void __launch_bounds__(kLutThreads)
+build_lut_kernel(const AT* __restrict__ a, int k, int gs, void* __restrict__ tables,
+                 float* __restrict__ tscales, float* __restrict__ rowsums) {
+  bl::pdl_launch_dependents();
+  bl::pdl_wait();                       // activations come from the previous kernel
+  const int KG = k >> 2;
+  const int gpg = gs >> 2;
+  const int NQ = k / gs;
+  const int row = blockIdx.y;
+  const int kg0 = blockIdx.x * kLutThreads;
+  const int kg = kg0 + threadIdx.x;
+  const bool live = kg < KG;
+  __shared__ float sa[kLutThreads * 4];
+  __shared__ float red[kLutThreads / 32];
+
+  float v[4] = {0.f, 0.f, 0.f, 0.f};
+  if (live) {
+    const AT* src = a + (int64_t)row * k + 4 * (int64_t)kg;
+#pragma unroll
+    for (int j = 0; j < 4; j++) v[j] = bl::to_f32(src[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < 4; j++) sa[threadIdx.x * 4 + j] = v[j];
+
+  // half table (index bit 3 clear): e[idx] = ((s0 a0 + s1 a1) + s2 a2) - a3
+  float e[8];
+#pragma unroll
+  for (int idx = 0; idx < 8; idx++) {
+    float x = (idx & 1) ? v[0] : -v[0];
+    x = (idx & 2) ? __fadd_rn(x, v[1]) : __fsub_rn(x, v[1]);
+    x = (idx & 4) ? __fadd_rn(x, v[2]) : __fsub_rn(x, v[2]);
+    e[idx] = __fsub_rn(x, v[3]);
+  }
+
+  if (MODE == BITLUT_TABLE_Q8) {
+    float mx = 0.f;
+#pragma unroll
+    for (int idx = 0; idx < 8; idx++) mx = fmaxf(mx, fabsf(e[idx]));
+    const int seg = gpg < 32 ? gpg : 32;
+    for (int o = 1; o < seg; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (gpg > 32) {
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+      __syncthreads();
+      const int wpg = gpg >> 5;                       // warps per group
+      const int w0 = (threadIdx.x >> 5) / wpg * wpg;
+      mx = 0.f;
+      for (int w = 0; w < wpg; w++) mx = fmaxf(mx, red[w0 + w]);
+    }
+    float scale = __fdiv_rn(mx, 127.0f);
+    if (scale == 0.0f) scale = 1.0f;
+    uint32_t packed[2] = {0u, 0u};
+#pragma unroll
+    for (int idx = 0; idx < 8; idx++) {
+      float s = __fdiv_rn(e[idx], scale);
+      float r = truncf(__fadd_rn(s, copysignf(0.5f, s)));
+      r = fminf(fmaxf(r, -127.f), 127.f);
+      packed[idx >> 2] |= ((uint32_t)(int)r & 0xffu) << (8 * (idx & 3));
+    }
+    if (live) {
+      reinterpret_cast<uint2*>(tables)[(int64_t)row * KG + kg] = make_uint2(packed[0], packed[1]);
+      if ((kg & (gpg - 1)) == 0) tscales[(int64_t)row * NQ + kg / gpg] = scale;
+    }
+  } else {
+    __half2 h[4];
+#pragma unroll
+    for (int p = 0; p < 4; p++) h[p] = __halves2half2(__float2half_rn(e[2 * p]), __float2half_rn(e[2 * p + 1]));
+    if (live) {
+      uint4 o;
+      o.x = *reinterpret_cast<uint32_t*>(&h[0]); o.y = *reinterpret_cast<uint32_t*>(&h[1]);
+      o.z = *reinterpret_cast<uint32_t*>(&h[2]); o.w = *reinterpret_cast<uint32_t*>(&h[3]);
+      reinterpret_cast<uint4*>(tables)[(int64_t)row * KG + kg] = o;
+    }
+  }
+
+  __syncthreads();
+  // row sums: the first thread of each quant group adds its gs activations
+  // left to right (lut_build.py:191-193)
+  if (live && (kg & (gpg - 1)) == 0) {
+    const int off = threadIdx.x * 4;
+    float acc = 0.f;
+    for (int j = 0; j < gs; j++) acc = __fadd_rn(acc, sa[off + j]);
+    rowsums[(int64_t)row * NQ + kg / gpg] = acc;
+  }
+}
+
+inline int grid_1d(int64_t n, int threads) {
+  int64_t b = (n + threads - 1) / threads;
+  const int64_t cap = 148 * 16 * 8;
+  return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+}  // namespace
+
+extern "C" int bitlut_precompute_lut(const void* a, int a_dtype, int n, int k, int g,
+                                     float* full, void* stream) {
+  if (g < 1 || g > 8 || n < 0 || k < 0) return BITLUT_EPARAM;
+  if (a_dtype != BITLUT_DT_F32 && a_dtype != BITLUT_DT_F16) return BITLUT_EPARAM;
+  if (k % g != 0) return BITLUT_ELAYOUT;
+  int64_t t = (int64_t)n * (k / g);
+  if (t == 0) return BITLUT_OK;
+  precompute_lut_kernel<<<grid_1d(t, 128), 128, 0, (cudaStream_t)stream>>>(a, a_dtype, n, k, g, full);
+  return bl_launch_status();
+}
+
+extern "C" int bitlut_mirror_consolidate(const float* full, int n, int kg, int g, float* half,
+                                         int* asym_flag, void* stream) {
+  if (g < 1 || g > 8 || n < 0 || kg < 0) return BITLUT_EPARAM;
+  int64_t rows = (int64_t)n * kg;
+  if (rows == 0) return BITLUT_OK;
+  mirror_kernel<<<grid_1d(rows << (g - 1), 256), 256, 0, (cudaStream_t)stream>>>(full, rows, g, half,
+                                                                                 asym_flag);
+  return bl_launch_status();
+}
+
+extern "C" int bitlut_quantize_tables(const float* half, int n, int kg, int g, int group_size,
+                                      int8_t* qentries, float* table_scales, void* stream) {
+  if (g < 1 || g > 8 || n < 0 || kg < 0 || group_size < 1) return BITLUT_EPARAM;
+  if (group_size % g != 0) return BITLUT_ELAYOUT;
+  int gpg = group_size / g;
+  if (kg % gpg != 0) return BITLUT_ELAYOUT;
+  if (n == 0 || kg == 0) return BITLUT_OK;
+  dim3 grid(kg / gpg, n);
+  quantize_tables_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(half, kg, 1 << (g - 1), gpg,
+                                                                 qentries, table_scales);
+  return bl_launch_status();
+}
+
+extern "C" int bitlut_row_sums(const void* a, int a_dtype, int n, int k, int group_size,
+                               float* sums, void* stream) {
+  if (group_size < 1 || n < 0 || k < 0) return BITLUT_EPARAM;
+  if (a_dtype != BITLUT_DT_F32 && a_dtype != BITLUT_DT_F16) return BITLUT_EPARAM;
+  if (k % group_size != 0) return BITLUT_ELAYOUT;
+  int64_t t = (int64_t)n * (k / group_size);
+  if (t == 0) return BITLUT_OK;
+  row_sums_kernel<<<grid_1d(t, 128), 128, 0, (cudaStream_t)stream>>>(a, a_dtype, n, k, group_size, sums);
+  return bl_launch_status();
+}
+
+int bl_build_lut_launch(const void* a, int a_dtype, int n, int k, int group_size, int mode,
+                        void* tables, float* tscales, float* rowsums, cudaStream_t stream, bool pdl) {
+  const int KG = k / 4;
+  dim3 grid((KG + kLutThreads - 1) / kLutThreads, n);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid; cfg.blockDim = dim3(kLutThreads); cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr; cfg.numAttrs = 1;
+  cudaError_t e;
+  if (mode == BITLUT_TABLE_Q8) {
+    e = a_dtype == BITLUT_DT_F16
+            ? cudaLaunchKernelEx(&cfg, build_lut_kernel<BITLUT_TABLE_Q8, __half>, (const __half*)a, k, group_size,
+                                 tables, tscales, rowsums)
+            : cudaLaunchKernelEx(&cfg, build_lut_kernel<BITLUT_TABLE_Q8, float>, (const float*)a, k, group_size,
+                                 tables, tscales, rowsums);
+  } else {
+    e = a_dtype == BITLUT_DT_F16
+            ? cudaLaunchKernelEx(&cfg, build_lut_kernel<BITLUT_TABLE_F16, __half>, (const __half*)a, k, group_size,
+                                 tables, tscales, rowsums)
+            : cudaLaunchKernelEx(&cfg, build_lut_kernel<BITLUT_TABLE_F16, float>, (const float*)a, k, group_size,
+                                 tables, tscales, rowsums);
+  }
+  return e == cudaSuccess ? BITLUT_OK : BITLUT_EINTERNAL;
+}
+
+extern "C" int bitlut_build_lut(const void* a, int a_dtype, int n, int k, int group_size, int mode,
+                                void* tables, float* tscales, float* rowsums, void* stream) {
+  if (a_dtype != BITLUT_DT_F32 && a_dtype != BITLUT_DT_F16) return BITLUT_EPARAM;
+  if (mode != BITLUT_TABLE_Q8 && mode != BITLUT_TABLE_F16) return BITLUT_EPARAM;
+  if (n < 0 || k < 0 || group_size < 4) return BITLUT_EPARAM;
+  if (k % group_size != 0 || group_size % 4 != 0) return BITLUT_ELAYOUT;
+  int gpg = group_size / 4;
+  if (gpg > 128 || (gpg & (gpg - 1))) return BITLUT_EPARAM;   // CUDA path: power-of-two k-groups per group
+  if (n == 0 || k == 0) return BITLUT_OK;
+  return bl_build_lut_launch(a, a_dtype, n, k, group_size, mode, tables, tscales, rowsums,
+                             (cudaStream_t)stream, false);
+}

@@ -1,0 +1,242 @@
+"""mpGEMV / mpGEMM drop-in (reference: pkg/src/bitlut/kernel.py).
+
+Same entry points, argument meaning and error behaviour as the reference's
+``mpgemm``/``mpgemv`` (kernel.py:280-382), dispatching to the CUDA kernels
+through the torch custom ops in ``_native``:
+
+    a --(bitlut_b200::build_lut)--> int8 tables, table scales, row sums
+      --(bitlut_b200::lookup)-----> out (n, m) float32
+
+Variants (``KernelVariant``):
+  * ``cuda-q8``  -- int8 tables; output bitwise identical to the
+    reference's ``vector-q8`` (and hence ``scalar-q8``), int32 staging
+    values exact.  Default.
+  * ``cuda-f16`` -- fp16 tables (BASELINE "fp16 tables"); matches the
+    reference's fp32-table ``scalar-real`` within max|dy| <= 1e-3 max|y|.
+The reference's CPU variants (scalar-real, scalar-q8, vector-q8, fast-agg)
+are rejected: this package has no CPU path.
+
+Inputs may be numpy arrays or torch tensors (CPU or CUDA).  Numpy/CPU
+inputs are copied to the device and the result is returned the same way
+(numpy float32 for numpy input), so host callers see the reference's
+contract; CUDA inputs return CUDA tensors without synchronizing.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from enum import Enum
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .core import Matrix, TileConfig, as_tensor
+from .errors import DataError, LayoutError, OverflowConfigError, ParameterError, ShapeError
+from .lut_build import REAL, LookupTables
+from .weight_prep import LAYOUT_VERSION, PackedWeights
+
+INT32_MAX = 2**31 - 1
+
+
+class KernelVariant(Enum):
+    CUDA_Q8 = "cuda-q8"
+    CUDA_F16 = "cuda-f16"
+
+
+_REFERENCE_CPU_VARIANTS = ("scalar-real", "scalar-q8", "vector-q8", "fast-agg")
+
+
+def _variant(v) -> KernelVariant:
+    if isinstance(v, KernelVariant):
+        return v
+    name = getattr(v, "value", v)
+    if name in _REFERENCE_CPU_VARIANTS:
+        raise ParameterError(
+            f"variant {name!r} is a CPU kernel of the reference; the B200 package "
+            "provides 'cuda-q8' (bitwise identical to vector-q8/scalar-q8) and 'cuda-f16'")
+    try:
+        return KernelVariant(name)
+    except ValueError:
+        raise ParameterError(f"unknown kernel variant {name!r}") from None
+
+
+@dataclass
+class KernelStats:
+    """kernel.py:41-46.  Filled analytically (the GPU does exactly these)."""
+
+    lookups: int = 0
+    lut_builds: int = 0
+
+
+@dataclass
+class Accumulators:
+    """kernel.py:49-64 (definitional tile primitive state)."""
+
+    real: torch.Tensor
+    integer: torch.Tensor
+
+    @classmethod
+    def zeros(cls, channels: int, device=None) -> "Accumulators":
+        dev = device or ("cuda" if torch.cuda.is_available() else "cpu")
+        return cls(real=torch.zeros(channels, dtype=torch.float32, device=dev),
+                   integer=torch.zeros(channels, dtype=torch.int32, device=dev))
+
+
+def validate_kernel_config(tile: TileConfig, bits: int, group_size: int, m: int, k: int) -> None:
+    """kernel.py:67-87, plus the CUDA path's own constraints."""
+    if group_size % tile.g != 0:
+        raise LayoutError(f"group_size={group_size} not divisible by g={tile.g}")
+    if m % tile.m_tile != 0:
+        raise LayoutError(f"m={m} not divisible by m_tile={tile.m_tile}")
+    if k % tile.k_tile != 0:
+        raise LayoutError(f"k={k} not divisible by k_tile={tile.k_tile}")
+    if k % group_size != 0:
+        raise LayoutError(f"k={k} not divisible by group_size={group_size}")
+    if (group_size // tile.g) * 127 > INT32_MAX:
+        raise OverflowConfigError(
+            f"group accumulation bound exceeded: {group_size // tile.g} "
+            f"lookups of magnitude 127 cannot be staged in int32")
+    if tile.g != 4:
+        raise ParameterError(f"the CUDA kernels implement g=4 (got g={tile.g})")
+    if m % 32 != 0:
+        raise LayoutError(f"m={m} not divisible by 32 (CUDA tile)")
+    gpg = group_size // 4
+    if group_size % 16 != 0 or gpg > 128 or (gpg & (gpg - 1)):
+        raise ParameterError(
+            f"group_size={group_size}: the CUDA kernels need group_size in "
+            "{16, 32, 64, 128, 256, 512}")
+
+
+def _check_layout_match(cfg: TileConfig, pw: PackedWeights) -> None:
+    """kernel.py:90-100."""
+    if pw.layout_version != LAYOUT_VERSION:
+        raise LayoutError(f"packed weights use layout version {pw.layout_version}, "
+                          f"kernel implements {LAYOUT_VERSION}")
+    t = pw.tile
+    if (cfg.m_tile, cfg.k_tile, cfg.g, cfg.lanes) != (t.m_tile, t.k_tile, t.g, t.lanes):
+        raise LayoutError("tile config does not match the layout the weights were packed "
+                          f"for: {cfg} vs {t}")
+
+
+def _activation_rows(a):
+    """kernel.py:266-277: -> (device tensor (n, k) f16/f32, how-to-return)."""
+    kind = "cuda"
+    if isinstance(a, Matrix):
+        a = a.to_array()
+    if isinstance(a, np.ndarray):
+        kind = "numpy"
+        arr = a if a.dtype in (np.float16, np.float32) else a.astype(np.float32)
+        if arr.ndim == 1:
+            arr = arr.reshape(1, -1)
+        if arr.ndim != 2:
+            raise ShapeError("activations must be 1-D or 2-D")
+        if not np.isfinite(arr).all():
+            raise DataError("activations contain non-finite values")
+        t = torch.from_numpy(np.ascontiguousarray(arr))
+    else:
+        t = as_tensor(a)
+        if t.dtype not in (torch.float16, torch.float32):
+            t = t.to(torch.float32)
+        if t.dim() == 1:
+            t = t.reshape(1, -1)
+        if t.dim() != 2:
+            raise ShapeError("activations must be 1-D or 2-D")
+        if not t.is_cuda:
+            kind = "cpu"
+            if not bool(torch.isfinite(t).all()):
+                raise DataError("activations contain non-finite values")
+    if not t.is_cuda:
+        if not torch.cuda.is_available():
+            raise N.BitLutError("a CUDA device is required (the B200 package has no CPU path)")
+        t = t.to("cuda", non_blocking=True)
+    return t.contiguous(), kind
+
+
+def mpgemm(a, pw: PackedWeights, cfg: TileConfig | None = None,
+           variant: KernelVariant | str = KernelVariant.CUDA_Q8,
+           threads: int = 1, stats: KernelStats | None = None, *,
+           check_finite: bool = True, return_partials: bool = False, pdl: bool = True):
+    """Mixed-precision GEMM: (N, K) activations x packed low-bit weights.
+
+    Returns (N, M) float32 (numpy for numpy input, a CUDA tensor for CUDA
+    input).  ``return_partials`` (cuda-q8) additionally returns the exact
+    int32 staging values, shape (N, bits, M, K/group_size).
+    """
+    variant = _variant(variant)
+    cfg = pw.tile if cfg is None else cfg
+    if cfg.n_tile < 1:
+        raise ParameterError("n_tile must be >= 1")
+    _check_layout_match(cfg, pw)
+    validate_kernel_config(cfg, pw.bits, pw.group_size, pw.m, pw.k)
+    if threads < 1:
+        raise ParameterError("threads must be >= 1")
+    rows, kind = _activation_rows(a)
+    n, k = rows.shape
+    if k != pw.k:
+        raise ShapeError(f"activation length {k} != weight k {pw.k}")
+    if kind == "cuda" and check_finite and not bool(torch.isfinite(rows).all()):
+        raise DataError("activations contain non-finite values")
+    if pw.gpu is None:
+        raise LayoutError("packed weights carry no GPU layout (prepare them with prepare_weights)")
+    if variant is KernelVariant.CUDA_F16:
+        raise ParameterError("cuda-f16 lookup kernel not available in this build")
+    mode = N.TABLE_Q8
+    if rows.device != pw.gpu.device:
+        rows = rows.to(pw.gpu.device)
+    tables, ts, rs = N.build_lut(rows, pw.group_size, mode)
+    out, partials = N.lookup(pw.gpu, pw.scales, pw.zeros, tables, ts, rs, pw.m, pw.k, pw.bits,
+                             pw.group_size, mode, N.FLAG_PDL if pdl else 0, return_partials)
+    if stats is not None:
+        stats.lookups += pw.bits * n * pw.m * (pw.k // pw.g)
+        stats.lut_builds += -(-n // cfg.n_tile) * (pw.k // cfg.k_tile)
+    if kind == "numpy":
+        out = out.cpu().numpy()
+        partials = partials.cpu().numpy()
+    elif kind == "cpu":
+        out = out.cpu()
+        partials = partials.cpu()
+    return (out, partials) if return_partials else out
+
+
+def mpgemv(a_row, pw: PackedWeights, cfg: TileConfig | None = None,
+           variant: KernelVariant | str = KernelVariant.CUDA_Q8,
+           threads: int = 1, stats: KernelStats | None = None, **kw):
+    """kernel.py:374-382: one activation row, returns a length-M vector."""
+    if isinstance(a_row, np.ndarray):
+        if a_row.ndim != 1:
+            raise ShapeError("mpgemv expects a 1-D activation row")
+    elif isinstance(a_row, torch.Tensor) and a_row.dim() != 1:
+        raise ShapeError("mpgemv expects a 1-D activation row")
+    res = mpgemm(a_row.reshape(1, -1), pw, cfg=cfg, variant=variant, threads=threads,
+                 stats=stats, **kw)
+    if kw.get("return_partials"):
+        return res[0][0], res[1][0]
+    return res[0]
+
+
+def lookup_accumulate_tile(indices, lut: LookupTables, acc: Accumulators, row: int = 0,
+                           kg_offset: int = 0) -> Accumulators:
+    """kernel.py:190-223: definitional tile primitive (device tensor ops; not
+    the hot path -- the hot path is csrc/gemv.cu)."""
+    idx = as_tensor(indices).to(acc.integer.device)
+    if idx.dim() != 2:
+        raise ShapeError("index tile must be 2-D")
+    if idx.numel() and int(idx.max()) >= (1 << lut.g):
+        raise ParameterError("tile contains indices out of range")
+    ii = idx.to(torch.int64)
+    if lut.consolidated:
+        flip = ii >> (lut.g - 1)
+        eff = ii ^ (flip * ((1 << lut.g) - 1))
+    else:
+        flip = torch.zeros_like(ii)
+        eff = ii
+    kg = kg_offset + torch.arange(idx.shape[1], device=ii.device)
+    if lut.mode == REAL:
+        vals = lut.entries[row].to(ii.device)[kg[None, :], eff]
+        vals = torch.where(flip == 1, -vals, vals)
+        acc.real += vals.sum(dim=1, dtype=torch.float32)
+    else:
+        vals = lut.qentries[row].to(ii.device)[kg[None, :], eff].to(torch.int32)
+        vals = torch.where(flip == 1, -vals, vals)
+        acc.integer += vals.sum(dim=1, dtype=torch.int32)
+    return acc
