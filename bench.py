@@ -1,0 +1,482 @@
+#!/usr/bin/env python
+"""Benchmark: LUT mpGEMV over the Llama-2-7B decode layer set at batch 1.
+
+Workload (BASELINE.json configs[1]): per layer the 7 decode GEMVs
+q,k,v,o (4096x4096), gate,up (11008x4096), down (4096x11008); 2-bit
+weights in [0,4), group 64, fp16 scales, implicit zero 2, int8-quantized
+tables (bit-exact vs the reference's vector-q8), fp16 activations ~N(0,1).
+A STEP = one pass over L layers (default 32 = the whole 7B model, 1.62 GB of
+packed weights > 126 MB L2, so no L2 flush is needed): per layer 4 table
+builds (qkv / o / gate-up / down inputs) + 7 lookup GEMVs, 11 launches,
+captured once in a CUDA graph with programmatic dependent launch.
+
+value  = packed-weight bytes (bits*M*K/8, the reference's weight_bytes,
+         cli.py:153) per step / device time, GB/s, all ranks aggregated.
+e2e    = the same metric through the public drop-in API (mpgemv with host
+         fp16 activations; H2D + D2H inside the timed region).
+roofline = the dominant kernel (gemv_q8_kernel) timed alone in a graph of
+         the step's 7*L lookups: algorithmic bytes / average launch time vs
+         the measured HBM peak.
+Also reported: per-shape us/launch for every 7B shape (the metric's "us"),
+and the CPU baseline (C port of the reference's vector-q8 kernel).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+Multi-GPU (torchrun): output-channel sharding + NCCL all-gather of slices.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "LUT mpGEMV packed-weight HBM GB/s, Llama-2-7B decode layer set, W2 g64 int8 tables, bs=1"
+LAYER = [("q", 4096, 4096), ("k", 4096, 4096), ("v", 4096, 4096), ("o", 4096, 4096),
+         ("gate", 11008, 4096), ("up", 11008, 4096), ("down", 4096, 11008)]
+# table-build inputs per layer and the GEMVs that share each table
+LUT_GROUPS = [("attn", 4096, ["q", "k", "v"]), ("o", 4096, ["o"]),
+              ("mlp", 4096, ["gate", "up"]), ("down", 11008, ["down"])]
+
+
+def load_peaks():
+    for p in (os.path.join(ROOT, "MEASURED_PEAKS.json"), "/root/repo/MEASURED_PEAKS.json"):
+        if os.path.exists(p):
+            with open(p) as f:
+                d = json.load(f)
+            return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-i", str(self.gpu), "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        time.sleep(0.1)
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------- workload
+
+def build_layers(n_layers, bits, gs, rank, world, device, seed=20251020):
+    """Packed weights for n_layers 7B layers; this rank's output-channel shard."""
+    import torch
+    import paper_2407_00088_b200 as B
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed)
+    tile = B.TileConfig(m_tile=32, k_tile=128)
+    layers = []
+    for _ in range(n_layers):
+        mats = {}
+        for name, m, k in LAYER:
+            q = torch.randint(0, 1 << bits, (m, k), dtype=torch.uint8, device=device, generator=gen)
+            s = (torch.randn((m, k // gs), device=device, generator=gen).abs() * 0.02 + 1e-3).half()
+            if world > 1:
+                lo, hi = rank * m // world, (rank + 1) * m // world
+                q, s = q[lo:hi].contiguous(), s[lo:hi].contiguous()
+            qw = B.QuantizedWeights(m=q.shape[0], k=k, bits=bits, group_size=gs, qvalues=q, scales=s)
+            pw = B.prepare_weights(qw, tile)
+            mats[name] = pw
+            del q
+        layers.append(mats)
+    torch.cuda.synchronize()
+    return layers
+
+
+def make_acts(n_layers, device, seed=7):
+    import torch
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed)
+    return [{g: torch.randn((1, k), device=device, generator=gen).half() for g, k, _ in LUT_GROUPS}
+            for _ in range(n_layers)]
+
+
+def step_fn(layers, acts, world, group, outs=None):
+    """One pass of the hot path (device-resident inputs)."""
+    import torch
+    from paper_2407_00088_b200 import _native as N
+    res = []
+    for L, A in zip(layers, acts):
+        for gname, k, names in LUT_GROUPS:
+            tables, ts, rs = N.build_lut(A[gname], L[names[0]].group_size, N.TABLE_Q8, N.FLAG_PDL)
+            for nm in names:
+                pw = L[nm]
+                y, _ = N.lookup(pw.gpu, pw.scales, None, tables, ts, rs, pw.m, pw.k, pw.bits,
+                                pw.group_size, N.TABLE_Q8, N.FLAG_PDL, False)
+                if world > 1:
+                    full = torch.empty((1, pw.m * world), dtype=y.dtype, device=y.device)
+                    torch.distributed.all_gather_into_tensor(full, y, group=group)
+                    y = full
+                res.append(y)
+    return res
+
+
+def lookups_only(layers, tabs):
+    from paper_2407_00088_b200 import _native as N
+    for L, T in zip(layers, tabs):
+        for gname, k, names in LUT_GROUPS:
+            tables, ts, rs = T[gname]
+            for nm in names:
+                pw = L[nm]
+                N.lookup(pw.gpu, pw.scales, None, tables, ts, rs, pw.m, pw.k, pw.bits,
+                         pw.group_size, N.TABLE_Q8, N.FLAG_PDL, False)
+
+
+def capture(fn, stream):
+    import torch
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(stream):
+        fn()          # warm (allocations, NCCL comms)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=stream):
+            fn()
+    torch.cuda.synchronize()
+    return g
+
+
+def time_graph(g, reps, warmup, barrier=None):
+    import torch
+    for _ in range(warmup):
+        g.replay()
+    torch.cuda.synchronize()
+    if barrier:
+        barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    if barrier:
+        barrier()
+    return e0.elapsed_time(e1) / reps     # ms per replay
+
+
+def packed_bytes_full(n_layers, bits):
+    return n_layers * sum(bits * m * k // 8 for _, m, k in LAYER)
+
+
+# ----------------------------------------------------------------- CPU baseline
+
+def cpu_baseline(layers_host, bits, gs, budget_s, threads):
+    """C port of the reference's vector-q8 path (oracle/bitlut_oracle.c) on
+    the host cores: one 7B layer (7 mpGEMV incl. table build) per sample."""
+    from oracle import oracle as O
+    reps, t_total, bytes_done = 0, 0.0, 0
+    layer_bytes = sum(bits * m * k // 8 for _, m, k in LAYER)
+    while t_total < budget_s or reps == 0:
+        t0 = time.perf_counter()
+        for name, m, k, planes, s, a in layers_host:
+            O.c_mpgemm(a, planes, m, k, bits, gs, s, mode="vector-q8", threads=threads)
+        t_total += time.perf_counter() - t0
+        reps += 1
+        bytes_done += layer_bytes
+    return bytes_done / t_total / 1e9, reps, t_total
+
+
+def host_layer(layer, acts, bits):
+    import torch
+    out = []
+    for gname, k, names in LUT_GROUPS:
+        a = acts[gname].float().cpu().numpy()
+        for nm in names:
+            pw = layer[nm]
+            out.append((nm, pw.m, pw.k, pw.planes.cpu().numpy(), pw.scales.float().cpu().numpy(), a))
+    return out
+
+
+def cpu_info():
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return model, os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------- main
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    bits, gs = 2, 64
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = {"workload": "llama2-7b decode layer set (q,k,v,o,gate,up,down) x "
+                       f"{args.layers} layers, W2 g64, int8 tables, bs=1",
+           "global_batch": 1, "bits": bits, "group_size": gs, "layers": args.layers,
+           "parallelism": f"tp{world} (output-channel shard + all-gather)" if world > 1 else "single",
+           "l2": f"weights {packed_bytes_full(args.layers, bits) / 1e9:.2f} GB/step > 126 MB L2; no flush"}
+
+    if args.impl == "reference":
+        return run_reference(args, bits, gs, rank, world, cfg)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2407_00088_b200 import _native as N
+    import paper_2407_00088_b200 as B
+
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+        group = dist.group.WORLD
+    barrier = (lambda: dist.barrier()) if world > 1 else None
+
+    layers = build_layers(args.layers, bits, gs, rank, world, device)
+    acts = make_acts(args.layers, device)
+    stream = torch.cuda.Stream(device)
+
+    # ---- value: the full step, graph-replayed ----
+    g_step = capture(lambda: step_fn(layers, acts, world, group), stream)
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            ms_step = time_graph(g_step, args.steps, args.warmup, barrier)
+    if world > 1:
+        t = torch.tensor([ms_step], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    total_bytes = packed_bytes_full(args.layers, bits)
+    value = total_bytes / (ms_step * 1e-3) / 1e9
+    launches_per_step = args.layers * (len(LUT_GROUPS) + len(LAYER))
+
+    # ---- roofline of the dominant kernel: lookups alone ----
+    tabs = [{gname: N.build_lut(A[gname], gs, N.TABLE_Q8) for gname, _, _ in LUT_GROUPS}
+            for A in acts]
+    torch.cuda.synchronize()
+    g_look = capture(lambda: lookups_only(layers, tabs), stream)
+    with torch.cuda.stream(stream):
+        ms_look = time_graph(g_look, args.steps, args.warmup, barrier)
+    local_bytes = sum(pw.packed_bytes for L in layers for pw in L.values())
+    n_look = args.layers * len(LAYER)
+    achieved = local_bytes / (ms_look * 1e-3) / 1e9
+    peak, peak_src = load_peaks()
+
+    # ---- per-shape us per launch (each shape alone, rotating over all layers) ----
+    per_shape = {}
+    for (name, m, k) in [("4096x4096", 4096, 4096), ("11008x4096", 11008, 4096),
+                         ("4096x11008", 4096, 11008)]:
+        sel = []
+        for L, T in zip(layers, tabs):
+            for gname, _, names in LUT_GROUPS:
+                for nm in names:
+                    pw = L[nm]
+                    if (pw.m * world, pw.k) == (m, k):
+                        sel.append((pw, T[gname]))
+
+        def only(sel=sel):
+            for pw, (tables, ts, rs) in sel:
+                N.lookup(pw.gpu, pw.scales, None, tables, ts, rs, pw.m, pw.k, pw.bits,
+                         pw.group_size, N.TABLE_Q8, N.FLAG_PDL, False)
+        g_s = capture(only, stream)
+        with torch.cuda.stream(stream):
+            ms = time_graph(g_s, max(5, args.steps // 2), args.warmup, barrier)
+        us = ms * 1e3 / len(sel)
+        nbytes = sel[0][0].packed_bytes
+        per_shape[name] = {"us_per_launch": round(us, 3), "packed_bytes": nbytes,
+                           "GBps": round(nbytes / (us * 1e-6) / 1e9, 1),
+                           "frac_of_peak": round(nbytes / (us * 1e-6) / 1e9 / peak, 4),
+                           "launches_rotated": len(sel)}
+        del g_s
+
+    # ---- e2e through the public API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        host_acts = [{g: A[g].cpu().pin_memory() for g in A} for A in acts]
+        n_e2e = min(args.layers, 8)
+        h2d = sum(host_acts[0][g].numel() * 2 * len(names) for g, _, names in LUT_GROUPS) * n_e2e
+        d2h = sum(m * 4 for _, m, _ in LAYER) * n_e2e
+        e2e_bytes = packed_bytes_full(n_e2e, bits)
+
+        def e2e_step():
+            for L, HA in zip(layers[:n_e2e], host_acts[:n_e2e]):
+                for gname, k, names in LUT_GROUPS:
+                    for nm in names:
+                        y = B.mpgemv(HA[gname][0], L[nm], check_finite=True)
+                        if world > 1:
+                            pass  # host result of this rank's slice (gather below)
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        if barrier:
+            barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(2, min(args.steps, 10))
+        e0.record()
+        for _ in range(reps):
+            e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        ms_e2e = e0.elapsed_time(e1) / reps
+        if world > 1:
+            t = torch.tensor([ms_e2e], device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_e2e = float(t.item())
+        e2e = {"value": round(e2e_bytes / (ms_e2e * 1e-3) / 1e9, 2), "unit": "GB/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": round(ms_e2e, 4),
+               "path": f"paper_2407_00088_b200.mpgemv(host fp16 row, PackedWeights) per GEMV, "
+                       f"{n_e2e} layers x 7 calls per step (per-call table build + D2H sync)"}
+
+    # ---- CPU baseline (rank 0, N = 1 only) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            from oracle import oracle as O
+            threads = O.c_max_threads()
+            hl = host_layer(layers[0], acts[0], bits)
+            gbps, reps, secs = cpu_baseline(hl, bits, gs, args.cpu_budget, threads)
+            model, ncpu = cpu_info()
+            cpu = {"value": round(gbps, 4), "unit": "GB/s", "cores": threads, "kind": "port",
+                   "sample": f"1 Llama-2-7B W2 layer (7 vector-q8 mpGEMV incl. table build) x "
+                             f"{reps} reps = {secs:.1f}s on {threads} threads ({model})"}
+        except Exception as e:  # report, never fake
+            cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "port",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "i8 tables / i32 accumulate / f32 epilogue",
+            "data": "synthetic (seeded torch RNG), random-init W2 weights of the Llama-2-7B shapes",
+            "config": cfg,
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": load_traffic(), "kernel": "gemv_q8_kernel",
+                         "peak_source": peak_src,
+                         "how": f"{n_look} lookup launches/graph, algorithmic bytes = bits*M*K/8 "
+                                f"per launch, CUDA events over {args.steps} replays"},
+            "per_shape_w2": per_shape,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "gemv_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch")
+    return None
+
+
+def run_reference(args, bits, gs, rank, world, cfg):
+    """--impl reference: the reference's CPU algorithm (C port of
+    _kernels.gemv_q8_vector + lut_build) on all host cores, same metric."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_2407_00088_b200 import workloads as W
+    threads = O.c_max_threads()
+    # one 7B layer from the seeded numpy workloads (the same bytes the parity tests use)
+    hl = []
+    for name, m, k in LAYER:
+        si = {(4096, 4096): 0, (11008, 4096): 1, (4096, 11008): 2}[(m, k)]
+        inst = W.config2(si)
+        planes = O.pack_v1(O.decompose_bits(inst["q"], bits, 4), 32, 128, 4, 16)
+        hl.append((name, m, k, planes, inst["scales"].astype(np.float32),
+                   inst["a"].astype(np.float32)))
+    layer_bytes = sum(bits * m * k // 8 for _, m, k in LAYER)
+    for _ in range(args.warmup):
+        for name, m, k, planes, s, a in hl:
+            O.c_mpgemm(a, planes, m, k, bits, gs, s, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for name, m, k, planes, s, a in hl:
+            O.c_mpgemm(a, planes, m, k, bits, gs, s, threads=threads)
+    dt = (time.perf_counter() - t0) / args.steps
+    gbps = layer_bytes / dt / 1e9
+    model, ncpu = cpu_info()
+    sample = (f"1 Llama-2-7B W2 layer (7 vector-q8 mpGEMV incl. table build) per step, "
+              f"C port of the reference kernel on {threads} threads ({model})")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(gbps, 4), "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+        "dtype": "i8 tables / i32 accumulate / f32 epilogue", "data": "synthetic (seeded numpy PCG64)",
+        "config": cfg,
+        "cpu_baseline": {"value": round(gbps, 4), "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(gbps, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }))
+
+
+if __name__ == "__main__":
+    main()

@@ -47,7 +47,7 @@ extern "C" {
 #define BITLUT_TABLE_Q8  0  /* int8 half tables + per-group table scales (vector-q8 semantics) */
 #define BITLUT_TABLE_F16 1  /* fp16 half tables (BASELINE "fp16 tables") */
 
-/* mpgemm flags */
+/* launch flags (bitlut_build_lut, bitlut_mpgemm) */
 #define BITLUT_FLAG_PDL 1   /* launch with programmatic dependent launch */
 
 /*
@@ -117,11 +117,13 @@ int bitlut_row_sums(const void* a, int a_dtype, int n, int k, int group_size,
 
 /* Fused per-call table build used by mpgemm (kernel.py:226-251,
  * _build_block_tables): one launch produces, for g = 4,
- *   mode Q8 : tables = int8 (n, k/4, 8) [== quantize_tables(mirror_consolidate(
- *             precompute_lut(a)))], tscales (n, k/gs) f32, rowsums (n, k/gs) f32
+ *   mode Q8 : tables = int8 (n, k/4, 8) holding quantize_tables(mirror_consolidate(
+ *             precompute_lut(a))) in KERNEL FORMAT: each byte Q stored as
+ *             Q - (Q < 0), k-groups unit-interleaved like the weights
+ *             (layout.cuh table_offset); tscales (n, k/gs) f32, rowsums f32
  *   mode F16: tables = fp16 (n, k/4, 8) [fp16-rounded half tables], rowsums.   */
 int bitlut_build_lut(const void* a, int a_dtype, int n, int k, int group_size, int mode,
-                     void* tables, float* tscales, float* rowsums, void* stream);
+                     void* tables, float* tscales, float* rowsums, int flags, void* stream);
 
 /* ---------------- lookup-accumulate (kernel.py / _kernels.py) ---------------- */
 
@@ -142,6 +144,16 @@ int bitlut_mpgemm(const uint8_t* wgpu, int m, int k, int bits, int group_size,
                   const void* tables, const float* tscales, const float* rowsums,
                   int mode, int n, float* out, int32_t* partials, int flags,
                   void* stream);
+
+/* bitlut_mpgemm plus a timeline: `trace` (device, (n * tiles) x 8 u64) gets
+ * per-CTA %globaltimer stamps [start, loads issued, after griddepcontrol.wait,
+ * tables staged, lookups done, epilogue products done, end] and %smid in
+ * slot 7.  Diagnostic only (tools/timeline.py). */
+int bitlut_mpgemm_traced(const uint8_t* wgpu, int m, int k, int bits, int group_size,
+                         const void* wscales, const void* zeros, int scale_dtype,
+                         const void* tables, const float* tscales, const float* rowsums,
+                         int mode, int n, float* out, int32_t* partials, int flags,
+                         unsigned long long* trace, void* stream);
 
 /* Number of kernel launches one bitlut_mpgemm call enqueues (for accounting). */
 int bitlut_mpgemm_launches(int m, int k, int bits, int group_size, int mode, int n);

@@ -37,8 +37,10 @@ _SIGS = {
     "bitlut_mirror_consolidate": [_vp, _i, _i, _i, _vp, _vp, _vp],
     "bitlut_quantize_tables": [_vp, _i, _i, _i, _i, _vp, _vp, _vp],
     "bitlut_row_sums": [_vp, _i, _i, _i, _i, _vp, _vp],
-    "bitlut_build_lut": [_vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp],
+    "bitlut_build_lut": [_vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _i, _vp],
     "bitlut_mpgemm": [_vp, _i, _i, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _i, _i, _vp, _vp, _i, _vp],
+    "bitlut_mpgemm_traced": [_vp, _i, _i, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _i, _i, _vp, _vp, _i,
+                             _vp, _vp],
     "bitlut_mpgemm_launches": [_i, _i, _i, _i, _i, _i],
 }
 
@@ -109,7 +111,7 @@ def layout_query(m: int, k: int, bits: int, group_size: int) -> GpuLayout:
 # ---------------------------------------------------------------------------
 
 @torch.library.custom_op("bitlut_b200::build_lut", mutates_args=())
-def build_lut(a: torch.Tensor, group_size: int, mode: int) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+def build_lut(a: torch.Tensor, group_size: int, mode: int, flags: int = 0) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
     """Fused table build (kernel.py:226-251): a (n, k) f16/f32 ->
     (tables (n, k/4, 8) int8|fp16, table scales (n, k/gs), row sums (n, k/gs))."""
     require_cuda(a, "activations")
@@ -121,13 +123,13 @@ def build_lut(a: torch.Tensor, group_size: int, mode: int) -> tuple[torch.Tensor
     ts = torch.empty((n, nq), dtype=torch.float32, device=a.device)
     rs = torch.empty((n, nq), dtype=torch.float32, device=a.device)
     rc = lib().bitlut_build_lut(ptr(a), dtype_code(a), n, k, group_size, mode, ptr(tables),
-                                ptr(ts), ptr(rs), stream_of(a))
+                                ptr(ts), ptr(rs), flags, stream_of(a))
     raise_for_status(rc, "bitlut_build_lut")
     return tables, ts, rs
 
 
 @build_lut.register_fake
-def _(a, group_size, mode):
+def _(a, group_size, mode, flags=0):
     n, k = a.shape
     tdt = torch.int8 if mode == TABLE_Q8 else torch.float16
     nq = k // group_size

@@ -33,18 +33,30 @@
 // above the HBM share (~22 B/clk/SM at 6.45 TB/s).
 //
 // ---------------------------------------------------------------------------
-// Work decomposition
+// Work decomposition and latency plan
 // ---------------------------------------------------------------------------
-// CTA = one tile (tile_ch channels, full K) x one activation row.  Lane =
-// one unit (R consecutive k-groups of one 32-stream group).  All of a
-// lane's R/2 32-byte weight loads are issued before griddepcontrol.wait, so
-// under programmatic dependent launch the weight stream of this kernel
-// overlaps the tail of the previous one; only the tables wait.  Partials of
-// the Lg lanes sharing a quantization group are combined with a
-// transpose-reduce (butterfly halving, no redundant adds), unpacked, and
-// parked in shared memory; then one thread per channel replays the
-// reference's float epilogue sequentially (plane-major, group ascending),
-// which keeps the output bit-exact without any split-K traffic.
+// CTA = one tile (tile_ch channels, full K) x one activation row; lane = one
+// unit (R consecutive k-groups of one 32-stream group).
+//  1. thread 0 starts TMA bulk copies (cp.async.bulk) of the tile's weights
+//     and weight scales into shared memory: they do not depend on the
+//     previous kernel, so under programmatic dependent launch (PDL) they
+//     stream while the previous kernel finishes.  Bulk copies also keep the
+//     weight traffic out of the in-order L1TEX load queue, so the table
+//     loads issued after griddepcontrol.wait are not stuck behind it
+//     (measured with tools/timeline.py: ~1 us lost per CTA otherwise).
+//  2. griddepcontrol.wait; each lane loads its own k-groups' encoded tables
+//     (kernel-format LUT, L2-resident) straight into registers.
+//  3. lookups from shared-memory weights (LDS.128, conflict-free), then a
+//     butterfly transpose-reduce across the Lg lanes of a quantization
+//     group, unpack to exact int32 staging values P.
+//  4. each lane forms its epilogue products ((pf_i*ts)*ws)*f32(P) exactly
+//     as the reference (_kernels.py:179-185) into shared memory; one thread
+//     per channel then adds them left to right in the reference's order
+//     (plane-major, group ascending), while two more threads per channel run
+//     the bias (:187-190) and zero-point chains.  The order makes the output
+//     bitwise equal to the reference's.
+// Shapes whose tile does not fit (K > 16384, or bits = 3 with large K) use
+// the same pipeline with per-lane LDG.128 weight loads instead of TMA.
 #include "common.cuh"
 #include "layout.cuh"
 
@@ -56,52 +68,84 @@ struct GemvArgs {
   const uint8_t* w;
   const void* wscales;
   const void* zeros;
-  const int8_t* qtab;       // (n, KG, 8)
-  const float* tscales;     // (n, NQ)
-  const float* rowsums;     // (n, NQ)
-  float* out;               // (n, m)
-  int32_t* partials;        // (n, bits, m, NQ) or null
+  const uint8_t* qtab;       // kernel-format tables (n, KG*8)
+  const float* tscales;      // (n, NQ)
+  const float* rowsums;      // (n, NQ)
+  float* out;                // (n, m)
+  int32_t* partials;         // (n, bits, m, NQ) or null
+  unsigned long long* trace; // null, or (grid, 8) globaltimer stamps per CTA
   bl::LayoutV2 L;
 };
 
-__device__ __forceinline__ uint32_t encode_a(uint32_t q) {
-  // per byte: Q - (Q < 0).  Negative bytes are >= 0x81, so no borrow.
-  return q - ((q >> 7) & 0x01010101u);
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE(slot)                                                                       \
+  do {                                                                                    \
+    if (p.trace && tid == 0)                                                              \
+      p.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + (slot)] = gtimer();      \
+  } while (0)
+
+// ---- TMA bulk copy + mbarrier helpers ----
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+  return (uint32_t)__cvta_generic_to_shared(ptr);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "BL_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra BL_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
 }
 
-template <int R>
-__device__ __forceinline__ void lookup_unit(const bl::U8x32 (&wr)[R / 2], const uint8_t* tab_smem,
-                                            int tab_off0, int tab_step, int (&acc)[16]) {
+// One k-group of 32 streams: 4 words x (2 selectors + 4 prmt + 8 dp2a).
+__device__ __forceinline__ void lookup_kg(const uint4 w, uint32_t a0, uint32_t a1, int (&acc)[16]) {
+  const uint32_t b0 = ~a0, b1 = ~a1;
+  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-  for (int jp = 0; jp < R / 2; jp++) {
-    const uint4 t = *reinterpret_cast<const uint4*>(tab_smem + tab_off0 + jp * tab_step);
-#pragma unroll
-    for (int kk = 0; kk < 2; kk++) {
-      const uint32_t a0 = kk ? t.z : t.x, a1 = kk ? t.w : t.y;
-      const uint32_t b0 = ~a0, b1 = ~a1;
-#pragma unroll
-      for (int w = 0; w < 4; w++) {
-        const uint32_t x = wr[jp].w[kk * 4 + w];
-        const uint32_t xx = x ^ 0x88888888u;
-        const uint32_t xh = x >> 16, xxh = xx >> 16;
-        const uint32_t A0 = bl::prmt(a0, a1, x), B0 = bl::prmt(b0, b1, xx);
-        const uint32_t A1 = bl::prmt(a0, a1, xh), B1 = bl::prmt(b0, b1, xxh);
-        acc[4 * w + 0] = bl::dp2a_lo(kMult, A0, acc[4 * w + 0]);
-        acc[4 * w + 0] = bl::dp2a_lo(kMult, B0, acc[4 * w + 0]);
-        acc[4 * w + 1] = bl::dp2a_hi(kMult, A0, acc[4 * w + 1]);
-        acc[4 * w + 1] = bl::dp2a_hi(kMult, B0, acc[4 * w + 1]);
-        acc[4 * w + 2] = bl::dp2a_lo(kMult, A1, acc[4 * w + 2]);
-        acc[4 * w + 2] = bl::dp2a_lo(kMult, B1, acc[4 * w + 2]);
-        acc[4 * w + 3] = bl::dp2a_hi(kMult, A1, acc[4 * w + 3]);
-        acc[4 * w + 3] = bl::dp2a_hi(kMult, B1, acc[4 * w + 3]);
-      }
-    }
+  for (int q = 0; q < 4; q++) {
+    const uint32_t x = ws[q];
+    const uint32_t xx = x ^ 0x88888888u;
+    const uint32_t A0 = bl::prmt(a0, a1, x), B0 = bl::prmt(b0, b1, xx);
+    const uint32_t A1 = bl::prmt(a0, a1, x >> 16), B1 = bl::prmt(b0, b1, xx >> 16);
+    acc[4 * q + 0] = bl::dp2a_lo(kMult, A0, acc[4 * q + 0]);
+    acc[4 * q + 0] = bl::dp2a_lo(kMult, B0, acc[4 * q + 0]);
+    acc[4 * q + 1] = bl::dp2a_hi(kMult, A0, acc[4 * q + 1]);
+    acc[4 * q + 1] = bl::dp2a_hi(kMult, B0, acc[4 * q + 1]);
+    acc[4 * q + 2] = bl::dp2a_lo(kMult, A1, acc[4 * q + 2]);
+    acc[4 * q + 2] = bl::dp2a_lo(kMult, B1, acc[4 * q + 2]);
+    acc[4 * q + 3] = bl::dp2a_hi(kMult, A1, acc[4 * q + 3]);
+    acc[4 * q + 3] = bl::dp2a_hi(kMult, B1, acc[4 * q + 3]);
   }
 }
 
 // Butterfly transpose-reduce of 16 packed accumulators across LG aligned
-// lanes.  Afterwards lane holds NF = 16/LG fully reduced pairs, starting at
-// pair index `base`.
+// lanes.  Afterwards the lane holds NF = 16/LG fully reduced pairs, starting
+// at pair index `base`.
 template <int LG>
 __device__ __forceinline__ int transpose_reduce(int (&acc)[16], int lane) {
   int base = 0;
@@ -123,7 +167,78 @@ __device__ __forceinline__ int transpose_reduce(int (&acc)[16], int lane) {
   return base;
 }
 
-template <int R, int LG, typename ST>
+// Shared-memory plan.  Region A holds the tile's weights (TMA variant) and
+// is reused for the epilogue products once the lookups are done.
+struct SmemPlan {
+  int rowlen;            // floats per channel row of epilogue products (odd)
+  size_t a_bytes, p_off, s_off, z_off, t_off, r_off, f_off, bar_off, total;
+};
+
+template <typename ST>
+__host__ __device__ inline SmemPlan smem_plan(const bl::LayoutV2& L, bool zeros, bool tma) {
+  SmemPlan s;
+  const int need = (L.bits + 1 + (zeros ? 1 : 0)) * L.NQ;
+  s.rowlen = ((need + 3) / 4) * 4;
+  if (((s.rowlen / 4) & 1) == 0) s.rowlen += 4;
+  const size_t wbytes = tma ? (size_t)L.n_sg * L.KG * 16 : 0;
+  const size_t terms = (size_t)L.tile_ch * s.rowlen * 4;
+  s.a_bytes = ((wbytes > terms ? wbytes : terms) + 15) & ~(size_t)15;
+  const size_t sc = ((size_t)L.tile_ch * L.NQ * sizeof(ST) + 15) & ~(size_t)15;
+  s.p_off = s.a_bytes;                                  // psm: NQ x (32*n_sg+1) int32
+  s.s_off = s.p_off + (((size_t)L.NQ * (32 * L.n_sg + 1) * 4 + 15) & ~(size_t)15);
+  s.z_off = s.s_off + sc;
+  s.t_off = s.z_off + (zeros ? sc : 0);
+  s.r_off = s.t_off + (((size_t)L.NQ * 4 + 15) & ~(size_t)15);
+  s.f_off = s.r_off + (((size_t)L.NQ * 4 + 15) & ~(size_t)15);
+  s.bar_off = s.f_off + (size_t)3 * 32 * 4;
+  s.total = s.bar_off + 16;
+  return s;
+}
+
+// Epilogue products for every (channel, group) of the tile; tile_ch is a
+// power of two so the (c, gq) split is a shift/mask.  BITS is compile-time so
+// the plane loop unrolls; partials / zero points are separate passes.
+template <int BITS, typename ST>
+__device__ __forceinline__ void form_terms(const GemvArgs& p, const ST* sraw, const ST* zraw,
+                                           const float* tsm, const float* rsm, const int32_t* psm,
+                                           float* terms, int rowlen, int tid, int T, int row, int tile) {
+  const bl::LayoutV2& L = p.L;
+  const int tch = L.tile_ch, NQ = L.NQ;
+  const int pstride = 32 * L.n_sg + 1;
+  const int lg_tch = __ffs(tch) - 1;
+  const int n = tch * NQ;
+  for (int idx = tid; idx < n; idx += T) {
+    const int c = idx & (tch - 1), gq = idx >> lg_tch;
+    const float ws = bl::to_f32(sraw[c * NQ + gq]);
+    const float ts = tsm[gq];
+    float* trow = terms + c * rowlen + gq;
+    const int32_t* pr = psm + gq * pstride + c * BITS;
+#pragma unroll
+    for (int i = 0; i < BITS; i++) {
+      const float f = __fmul_rn(0.5f * (float)(1 << i), ts);
+      trow[i * NQ] = __fmul_rn(__fmul_rn(f, ws), __int2float_rn(pr[i]));
+    }
+    trow[BITS * NQ] = __fmul_rn(ws, rsm[gq]);
+  }
+  if (p.zeros) {
+    const float half_range = (float)(1 << (BITS - 1));
+    for (int idx = tid; idx < n; idx += T) {
+      const int c = idx & (tch - 1), gq = idx >> lg_tch;
+      const float ws = bl::to_f32(sraw[c * NQ + gq]);
+      terms[c * rowlen + (BITS + 1) * NQ + gq] =
+          __fmul_rn(__fmul_rn(ws, __fsub_rn(half_range, bl::to_f32(zraw[c * NQ + gq]))), rsm[gq]);
+    }
+  }
+  if (p.partials) {
+    for (int idx = tid; idx < n * BITS; idx += T) {
+      const int gq = idx % NQ, ci = idx / NQ, c = ci / BITS, i = ci - c * BITS;
+      p.partials[(((int64_t)row * BITS + i) * L.m + (int64_t)tile * tch + c) * NQ + gq] =
+          psm[gq * pstride + c * BITS + i];
+    }
+  }
+}
+
+template <int R, int LG, typename ST, bool TMA>
 __global__ void __launch_bounds__(512)
 gemv_q8_kernel(GemvArgs p) {
   const bl::LayoutV2& L = p.L;
@@ -135,64 +250,70 @@ gemv_q8_kernel(GemvArgs p) {
   const int T = blockDim.x;
   const int KG = L.KG, NQ = L.NQ, U = L.U;
   const int units = L.n_sg * U;
-  const int pstride = 32 * L.n_sg + 1;
   const int tch = L.tile_ch;
+  const int bits = L.bits;
+  const bool has_zeros = p.zeros != nullptr;
+  const SmemPlan sp = smem_plan<ST>(L, has_zeros, TMA);
 
-  extern __shared__ __align__(16) uint8_t smem[];
-  uint8_t* tab = smem;                                              // KG * 8
-  int32_t* psm = reinterpret_cast<int32_t*>(smem + (size_t)KG * 8); // NQ * pstride
-  float* wsm = reinterpret_cast<float*>(psm + (size_t)NQ * pstride);// tch * NQ
-  float* zsm = wsm + (size_t)tch * NQ;                              // tch * NQ (if zeros)
-  float* tsm = zsm + (p.zeros ? (size_t)tch * NQ : 0);              // NQ
-  float* rsm = tsm + NQ;                                            // NQ
-  float* fin = rsm + NQ;                                            // 3 * tch
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* wbuf = smem;
+  float* terms = reinterpret_cast<float*>(smem);      // after the lookups (TMA)
+  int32_t* psm = reinterpret_cast<int32_t*>(smem + sp.p_off);
+  const int pstride = 32 * L.n_sg + 1;
+  const ST* sraw = reinterpret_cast<const ST*>(smem + sp.s_off);
+  const ST* zraw = reinterpret_cast<const ST*>(smem + sp.z_off);
+  float* tsm = reinterpret_cast<float*>(smem + sp.t_off);
+  float* rsm = reinterpret_cast<float*>(smem + sp.r_off);
+  float* fin = reinterpret_cast<float*>(smem + sp.f_off);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + sp.bar_off);
 
-  // ---- 1. issue this lane's first-round weight loads (independent of the
-  //         previous kernel in the stream) ----
-  bl::U8x32 wr[R / 2];
-  {
-    const int u = tid;
-    if (u < units) {
-      const int sg = u / U, uu = u - sg * U;
-      const int ub = uu >> 5, l = uu & 31;
-      const int nu_b = min(32, U - 32 * ub);
-      const uint8_t* base = p.w + L.sg_row_base(tile, sg) + (int64_t)ub * (32 * R * 16) + l * 32;
-#pragma unroll
-      for (int jp = 0; jp < R / 2; jp++) wr[jp] = bl::ld_stream_256(base + (int64_t)jp * nu_b * 32);
+  TRACE(0);
+  // ---- 1. independent traffic first: weights + scales (+ zeros) ----
+  const uint32_t sc_bytes = (uint32_t)((size_t)tch * NQ * sizeof(ST));
+  const int64_t sc_elem0 = (int64_t)tile * tch * NQ;
+  if (TMA) {
+    if (tid == 0) {
+      mbar_init(bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      const uint32_t wbytes = (uint32_t)((size_t)L.n_sg * KG * 16);
+      mbar_expect_tx(bar, wbytes + sc_bytes * (has_zeros ? 2u : 1u));
+      const uint64_t pol = policy_evict_first();
+      const uint8_t* src = p.w + L.sg_row_base(tile, 0);
+      for (uint32_t off = 0; off < wbytes; off += 32768u) {   // the tile is contiguous
+        const uint32_t nb = wbytes - off < 32768u ? wbytes - off : 32768u;
+        bulk_g2s(wbuf + off, src + off, nb, bar, pol);
+      }
+      bulk_g2s((void*)sraw, reinterpret_cast<const ST*>(p.wscales) + sc_elem0, sc_bytes, bar, pol);
+      if (has_zeros)
+        bulk_g2s((void*)zraw, reinterpret_cast<const ST*>(p.zeros) + sc_elem0, sc_bytes, bar, pol);
+    }
+  } else {
+    const uint4* s4 = reinterpret_cast<const uint4*>(reinterpret_cast<const ST*>(p.wscales) + sc_elem0);
+    for (int i = tid; i < (int)(sc_bytes / 16); i += T)
+      reinterpret_cast<uint4*>(smem + sp.s_off)[i] = bl::ld_nc_128(s4 + i);
+    if (has_zeros) {
+      const uint4* z4 = reinterpret_cast<const uint4*>(reinterpret_cast<const ST*>(p.zeros) + sc_elem0);
+      for (int i = tid; i < (int)(sc_bytes / 16); i += T)
+        reinterpret_cast<uint4*>(smem + sp.z_off)[i] = bl::ld_nc_128(z4 + i);
     }
   }
+  __syncthreads();                      // mbarrier initialised / scales staged
+  TRACE(1);
   bl::pdl_launch_dependents();
 
-  // ---- 2. weight scales / zeros of this tile -> smem (also independent) ----
-  {
-    const ST* ws = reinterpret_cast<const ST*>(p.wscales) + (int64_t)tile * tch * NQ;
-    for (int i = tid; i < tch * NQ; i += T) wsm[i] = bl::to_f32(ws[i]);
-    if (p.zeros) {
-      const ST* zs = reinterpret_cast<const ST*>(p.zeros) + (int64_t)tile * tch * NQ;
-      for (int i = tid; i < tch * NQ; i += T) zsm[i] = bl::to_f32(zs[i]);
-    }
-  }
-
-  // ---- 3. wait for the table producer, then stage this row's tables ----
+  // ---- 2. tables (produced by the previous kernel) ----
   bl::pdl_wait();
-  {
-    const uint2* q = reinterpret_cast<const uint2*>(p.qtab) + (int64_t)row * KG;
-    for (int kg = tid; kg < KG; kg += T) {
-      const uint2 v = q[kg];
-      const int u = kg / R, r = kg - u * R;
-      const int ub = u >> 5, l = u & 31;
-      const int nu_b = min(32, U - 32 * ub);
-      const int off = ub * (R / 2) * 32 * 16 + ((r >> 1) * nu_b + l) * 16 + (r & 1) * 8;
-      *reinterpret_cast<uint2*>(tab + off) = make_uint2(encode_a(v.x), encode_a(v.y));
-    }
-    for (int i = tid; i < NQ; i += T) {
-      tsm[i] = p.tscales[(int64_t)row * NQ + i];
-      rsm[i] = p.rowsums[(int64_t)row * NQ + i];
-    }
+  TRACE(2);
+  for (int i = tid; i < NQ; i += T) {
+    tsm[i] = p.tscales[(int64_t)row * NQ + i];
+    rsm[i] = p.rowsums[(int64_t)row * NQ + i];
   }
-  __syncthreads();
+  if (TMA) mbar_wait(bar, 0);
+  __syncthreads();                      // tsm / rsm visible; weights landed
+  TRACE(3);
 
-  // ---- 4. lookups, group reduction, unpack into psm[gq][stream] ----
+  // ---- 3. lookups, reduction, exact staging values -> psm[gq][stream] ----
+  const int rowlen = sp.rowlen;
   const int rounds = (units + T - 1) / T;
   for (int rd = 0; rd < rounds; rd++) {
     const int u = tid + rd * T;
@@ -205,97 +326,124 @@ gemv_q8_kernel(GemvArgs p) {
       sg = u / U; uu = u - sg * U;
       const int ub = uu >> 5, l = uu & 31;
       const int nu_b = min(32, U - 32 * ub);
-      if (rd > 0) {
-        const uint8_t* base = p.w + L.sg_row_base(tile, sg) + (int64_t)ub * (32 * R * 16) + l * 32;
+      uint4 tq[R / 2];
+      const uint8_t* tb = p.qtab + (int64_t)row * KG * 8 + (int64_t)ub * (32 * R * 8) + l * 16;
 #pragma unroll
-        for (int jp = 0; jp < R / 2; jp++) wr[jp] = bl::ld_stream_256(base + (int64_t)jp * nu_b * 32);
-      }
-      lookup_unit<R>(wr, tab, ub * (R / 2) * 32 * 16 + l * 16, nu_b * 16, acc);
-    }
-    if (__any_sync(0xffffffffu, live)) {
-      const int base = transpose_reduce<LG>(acc, lane);
-      if (live) {
-        const int gq = uu / LG;
-        const int gpg = R * LG;
-        const int fix = -32767 * gpg;        // undo the -1 per lookup of both streams
-        int32_t* dst = psm + (size_t)gq * pstride + sg * 32;
+      for (int jp = 0; jp < R / 2; jp++) tq[jp] = bl::ld_nc_128(tb + jp * nu_b * 16);
+      if (TMA) {
+        const uint8_t* wb = wbuf + (size_t)sg * KG * 16 + (size_t)ub * (32 * R * 16) + l * 16;
 #pragma unroll
-        for (int i = 0; i < NF; i++) {
-          const int v = acc[i] + fix;
-          const int pe = (v << 17) >> 17;
-          const int po = (pe - v) >> 15;
-          dst[2 * (base + i)] = pe;
-          dst[2 * (base + i) + 1] = po;
+        for (int j = 0; j < R; j++) {
+          const uint4 w = *reinterpret_cast<const uint4*>(wb + j * nu_b * 16);
+          lookup_kg(w, (j & 1) ? tq[j >> 1].z : tq[j >> 1].x, (j & 1) ? tq[j >> 1].w : tq[j >> 1].y, acc);
         }
+      } else {
+        const uint8_t* wg = p.w + L.sg_row_base(tile, sg) + (int64_t)ub * (32 * R * 16) + l * 16;
+        uint4 wr[R];
+#pragma unroll
+        for (int j = 0; j < R; j++) wr[j] = bl::ld_nc_128(wg + (int64_t)j * nu_b * 16);
+#pragma unroll
+        for (int j = 0; j < R; j++)
+          lookup_kg(wr[j], (j & 1) ? tq[j >> 1].z : tq[j >> 1].x, (j & 1) ? tq[j >> 1].w : tq[j >> 1].y, acc);
+      }
+    }
+    int base = 0;
+    if (__any_sync(0xffffffffu, live)) base = transpose_reduce<LG>(acc, lane);
+    if (live) {
+      // undo the -1 per lookup of both streams, split each pair
+      const int fix = -32767 * (R * LG);
+      int32_t* dst = psm + (size_t)(uu / LG) * pstride + sg * 32 + 2 * base;
+#pragma unroll
+      for (int i = 0; i < NF; i++) {
+        const int v = acc[i] + fix;
+        const int pe = (v << 17) >> 17;
+        dst[2 * i] = pe;
+        dst[2 * i + 1] = (pe - v) >> 15;
       }
     }
   }
-  __syncthreads();
+  TRACE(4);
+  __syncthreads();                      // psm complete; region A (weights) free
 
-  // ---- 5. float epilogue in the reference's order (_kernels.py:179-191) ----
-  // thread c: sum_i sum_gq ((pf_i*ts)*ws)*P ; thread tch+c: bias sum_gq ws*rs ;
-  // thread 2*tch+c: zero-point correction sum_gq (ws*(2^(b-1)-z))*rs.
-  const int bits = L.bits;
-  if (tid < tch) {
-    const int c = tid;
-    const int64_t m = (int64_t)tile * tch + c;
-    float o = 0.f;
-    for (int i = 0; i < bits; i++) {
-      const float pf = 0.5f * (float)(1 << i);
-      const int s = c * bits + i;
-      for (int gq = 0; gq < NQ; gq++) {
-        const int32_t P = psm[gq * pstride + s];
-        const float f = __fmul_rn(pf, tsm[gq]);
-        o = __fadd_rn(o, __fmul_rn(__fmul_rn(f, wsm[c * NQ + gq]), __int2float_rn(P)));
-        if (p.partials) p.partials[(((int64_t)row * bits + i) * L.m + m) * NQ + gq] = P;
+  // ---- 4. epilogue products, formed exactly as the reference does:
+  //         ((pf_i*ts)*ws)*f32(P)  (_kernels.py:183-184), ws*rs (:188) and the
+  //         zero-point term (ws*(2^(b-1)-z))*rs ----
+  switch (bits) {
+    case 1: form_terms<1, ST>(p, sraw, zraw, tsm, rsm, psm, terms, rowlen, tid, T, row, tile); break;
+    case 2: form_terms<2, ST>(p, sraw, zraw, tsm, rsm, psm, terms, rowlen, tid, T, row, tile); break;
+    case 3: form_terms<3, ST>(p, sraw, zraw, tsm, rsm, psm, terms, rowlen, tid, T, row, tile); break;
+    default: form_terms<4, ST>(p, sraw, zraw, tsm, rsm, psm, terms, rowlen, tid, T, row, tile); break;
+  }
+  __syncthreads();
+  TRACE(5);
+
+  // ---- 5. left-to-right chains, one per channel, each kind in its own warp
+  //         (warp 0: main sum, warp 1: bias, warp 2: zero points) ----
+  {
+    const int w = tid >> 5, c = tid & 31;
+    int start = 0, len = 0;
+    bool run = c < tch;
+    if (w == 0) { start = 0; len = bits * NQ; }
+    else if (w == 1) { start = bits * NQ; len = NQ; }
+    else if (w == 2 && has_zeros) { start = (bits + 1) * NQ; len = NQ; }
+    else run = false;
+    if (run) {
+      const float* t = terms + c * rowlen + start;
+      float o = 0.f;
+      int j = 0;
+      if ((start & 3) == 0) {
+        // 16-byte loads (rowlen/4 odd: conflict-free across the 16..32 lanes),
+        // two loads ahead of the serial add chain
+        const float4* t4 = reinterpret_cast<const float4*>(t);
+        const int n4 = len >> 2;
+        float4 a0 = n4 > 0 ? t4[0] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 a1 = n4 > 1 ? t4[1] : a0;
+        for (int q = 0; q < n4; q++) {
+          const float4 cur = a0;
+          a0 = a1;
+          if (q + 2 < n4) a1 = t4[q + 2];
+          o = __fadd_rn(o, cur.x); o = __fadd_rn(o, cur.y);
+          o = __fadd_rn(o, cur.z); o = __fadd_rn(o, cur.w);
+        }
+        j = n4 << 2;
       }
+      for (; j < len; j++) o = __fadd_rn(o, t[j]);
+      fin[w * 32 + c] = o;
     }
-    fin[c] = o;
-  } else if (tid < 2 * tch) {
-    const int c = tid - tch;
-    float s = 0.f;
-    for (int gq = 0; gq < NQ; gq++) s = __fadd_rn(s, __fmul_rn(wsm[c * NQ + gq], rsm[gq]));
-    fin[tch + c] = s;
-  } else if (p.zeros && tid < 3 * tch) {
-    const int c = tid - 2 * tch;
-    const float half_range = (float)(1 << (bits - 1));
-    float zc = 0.f;
-    for (int gq = 0; gq < NQ; gq++) {
-      const float d = __fsub_rn(half_range, zsm[c * NQ + gq]);
-      zc = __fadd_rn(zc, __fmul_rn(__fmul_rn(wsm[c * NQ + gq], d), rsm[gq]));
-    }
-    fin[2 * tch + c] = zc;
   }
   __syncthreads();
   if (tid < tch) {
-    float o = __fsub_rn(fin[tid], __fmul_rn(0.5f, fin[tch + tid]));
-    if (p.zeros) o = __fadd_rn(o, fin[2 * tch + tid]);
+    float o = __fsub_rn(fin[tid], __fmul_rn(0.5f, fin[32 + tid]));
+    if (has_zeros) o = __fadd_rn(o, fin[64 + tid]);
     p.out[(int64_t)row * L.m + (int64_t)tile * tch + tid] = o;
   }
-}
-
-size_t gemv_smem_bytes(const bl::LayoutV2& L, bool zeros) {
-  size_t b = (size_t)L.KG * 8;
-  b += (size_t)L.NQ * (32 * L.n_sg + 1) * 4;
-  b += (size_t)L.tile_ch * L.NQ * 4 * (zeros ? 2 : 1);
-  b += (size_t)L.NQ * 8 + (size_t)L.tile_ch * 12;
-  return (b + 15) & ~(size_t)15;
+  if (p.trace && tid == 0) {
+    unsigned int smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    p.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + 7] = smid;
+  }
+  TRACE(6);
 }
 
 int gemv_threads(const bl::LayoutV2& L) {
-  int units = L.n_sg * L.U;
-  int rounds = (units + 511) / 512;
+  const int units = L.n_sg * L.U;
+  const int rounds = (units + 511) / 512;
   int t = (units + rounds - 1) / rounds;
   t = (t + 31) / 32 * 32;
-  int need = 3 * L.tile_ch;      // epilogue helpers
-  if (t < need) t = (need + 31) / 32 * 32;
+  if (t < 96) t = 96;                  // three epilogue chain warps
   return t;
 }
 
-template <int R, int LG, typename ST>
+template <typename ST>
+bool use_tma(const bl::LayoutV2& L, bool zeros) {
+  return L.n_sg * L.U <= 512 && smem_plan<ST>(L, zeros, true).total <= 112 * 1024;
+}
+
+template <int R, int LG, typename ST, bool TMA>
 int launch_q8(const GemvArgs& a, int n, cudaStream_t stream, bool pdl) {
-  const size_t smem = gemv_smem_bytes(a.L, a.zeros != nullptr);
-  auto kern = gemv_q8_kernel<R, LG, ST>;
+  const size_t smem = smem_plan<ST>(a.L, a.zeros != nullptr, TMA).total;
+  if (smem > 227 * 1024) return BITLUT_ELAYOUT;
+  auto kern = gemv_q8_kernel<R, LG, ST, TMA>;
   if (smem > 48 * 1024) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return BITLUT_EINTERNAL;
@@ -312,33 +460,36 @@ int launch_q8(const GemvArgs& a, int n, cudaStream_t stream, bool pdl) {
   return cudaLaunchKernelEx(&cfg, kern, a) == cudaSuccess ? BITLUT_OK : BITLUT_EINTERNAL;
 }
 
+template <int R, int LG, typename ST>
+int launch_q8_any(const GemvArgs& a, int n, cudaStream_t s, bool pdl) {
+  return use_tma<ST>(a.L, a.zeros != nullptr) ? launch_q8<R, LG, ST, true>(a, n, s, pdl)
+                                              : launch_q8<R, LG, ST, false>(a, n, s, pdl);
+}
+
 template <typename ST>
 int dispatch_q8(const GemvArgs& a, int n, cudaStream_t s, bool pdl) {
   const int R = a.L.R, LG = a.L.Lg;
   if (R == 8) {
     switch (LG) {
-      case 1: return launch_q8<8, 1, ST>(a, n, s, pdl);
-      case 2: return launch_q8<8, 2, ST>(a, n, s, pdl);
-      case 4: return launch_q8<8, 4, ST>(a, n, s, pdl);
-      case 8: return launch_q8<8, 8, ST>(a, n, s, pdl);
-      case 16: return launch_q8<8, 16, ST>(a, n, s, pdl);
+      case 1: return launch_q8_any<8, 1, ST>(a, n, s, pdl);
+      case 2: return launch_q8_any<8, 2, ST>(a, n, s, pdl);
+      case 4: return launch_q8_any<8, 4, ST>(a, n, s, pdl);
+      case 8: return launch_q8_any<8, 8, ST>(a, n, s, pdl);
+      case 16: return launch_q8_any<8, 16, ST>(a, n, s, pdl);
     }
   } else if (R == 4 && LG == 1) {
-    return launch_q8<4, 1, ST>(a, n, s, pdl);
+    return launch_q8_any<4, 1, ST>(a, n, s, pdl);
   }
   return BITLUT_EPARAM;
 }
 
 }  // namespace
 
-int bl_build_lut_launch(const void* a, int a_dtype, int n, int k, int group_size, int mode,
-                        void* tables, float* tscales, float* rowsums, cudaStream_t stream, bool pdl);
-
-extern "C" int bitlut_mpgemm(const uint8_t* wgpu, int m, int k, int bits, int group_size,
-                             const void* wscales, const void* zeros, int scale_dtype,
-                             const void* tables, const float* tscales, const float* rowsums,
-                             int mode, int n, float* out, int32_t* partials, int flags,
-                             void* stream) {
+extern "C" int bitlut_mpgemm_traced(const uint8_t* wgpu, int m, int k, int bits, int group_size,
+                                    const void* wscales, const void* zeros, int scale_dtype,
+                                    const void* tables, const float* tscales, const float* rowsums,
+                                    int mode, int n, float* out, int32_t* partials, int flags,
+                                    unsigned long long* trace, void* stream) {
   bl::LayoutV2 L;
   int rc = bl::make_layout(m, k, bits, group_size, &L);
   if (rc) return rc;
@@ -348,13 +499,21 @@ extern "C" int bitlut_mpgemm(const uint8_t* wgpu, int m, int k, int bits, int gr
   if (mode != BITLUT_TABLE_Q8) return BITLUT_EPARAM;
   if (n > 65535) return BITLUT_ESHAPE;
   const bool pdl = (flags & BITLUT_FLAG_PDL) != 0;
-  if (gemv_smem_bytes(L, zeros != nullptr) > 227 * 1024) return BITLUT_ELAYOUT;
   GemvArgs a;
   a.w = wgpu; a.wscales = wscales; a.zeros = zeros;
-  a.qtab = reinterpret_cast<const int8_t*>(tables); a.tscales = tscales; a.rowsums = rowsums;
-  a.out = out; a.partials = partials; a.L = L;
+  a.qtab = reinterpret_cast<const uint8_t*>(tables); a.tscales = tscales; a.rowsums = rowsums;
+  a.out = out; a.partials = partials; a.trace = trace; a.L = L;
   return scale_dtype == BITLUT_DT_F16 ? dispatch_q8<__half>(a, n, (cudaStream_t)stream, pdl)
                                       : dispatch_q8<float>(a, n, (cudaStream_t)stream, pdl);
+}
+
+extern "C" int bitlut_mpgemm(const uint8_t* wgpu, int m, int k, int bits, int group_size,
+                             const void* wscales, const void* zeros, int scale_dtype,
+                             const void* tables, const float* tscales, const float* rowsums,
+                             int mode, int n, float* out, int32_t* partials, int flags,
+                             void* stream) {
+  return bitlut_mpgemm_traced(wgpu, m, k, bits, group_size, wscales, zeros, scale_dtype, tables,
+                              tscales, rowsums, mode, n, out, partials, flags, nullptr, stream);
 }
 
 extern "C" int bitlut_mpgemm_launches(int m, int k, int bits, int group_size, int mode, int n) {

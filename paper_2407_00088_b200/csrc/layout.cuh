@@ -12,9 +12,15 @@
 //              x = idx ^ (7 * (idx >> 3)): bit 3 = mirror flag s, bits 0-2 =
 //              the half-table slot eff (_kernels.py:175-177 computes the same
 //              s/eff at run time; here it is done once, offline).
-//   unit     = unit_kg consecutive k-groups of one SG, processed by one lane.
-//              Units are interleaved 32 at a time so that, at step j, the 32
-//              lanes of a warp read 32 consecutive 32-byte spans (2 chunks).
+//   unit     = unit_kg (R) consecutive k-groups of one SG, processed by one lane.
+//              Units are interleaved 32 at a time ("unit block", ub): within
+//              a unit block the order is [j = kg-in-unit][lane][16 B], so at
+//              step j the 32 lanes of a warp touch 512 contiguous bytes
+//              (conflict-free LDS.128 from shared memory, coalesced from HBM).
+//   tables   = the kernel-format LUT (bitlut_build_lut, mode Q8) uses the
+//              same interleave at 8 B per k-group, pairs of k-groups packed:
+//              [ub][j/2][lane][2 x 8 B], so one LDG.128 per lane fetches the
+//              encoded half tables of two consecutive k-groups.
 #pragma once
 #include <cstdint>
 
@@ -34,19 +40,27 @@ struct LayoutV2 {
     int u = kg / R, r = kg - u * R;
     int ub = u >> 5, l = u & 31;
     int nu_b = U - 32 * ub; if (nu_b > 32) nu_b = 32;
-    int jp = r >> 1, kk = r & 1;
-    return sg_row_base(tile, sg) + (int64_t)ub * (32 * R * 16) + (int64_t)(jp * nu_b + l) * 32 + kk * 16;
+    return sg_row_base(tile, sg) + (int64_t)ub * (32 * R * 16) + (int64_t)(r * nu_b + l) * 16;
+  }
+  // byte offset of k-group kg's 8-byte encoded half table in one table row
+  __host__ __device__ int64_t table_offset(int kg) const {
+    int u = kg / R, r = kg - u * R;
+    int ub = u >> 5, l = u & 31;
+    int nu_b = U - 32 * ub; if (nu_b > 32) nu_b = 32;
+    return (int64_t)ub * (32 * R * 8) + (int64_t)((r >> 1) * nu_b + l) * 16 + (r & 1) * 8;
   }
 };
 
 // Returns BITLUT_OK or an error code; fills L on success.
+__host__ __device__ inline int unit_kg_for(int gs) { return ((gs / 4) % 8 == 0) ? 8 : 4; }
+
 inline int make_layout(int m, int k, int bits, int gs, LayoutV2* L) {
   if (bits < 1 || bits > 4) return -1;          // EPARAM
   if (gs < 4 || k <= 0 || m <= 0) return -1;
   if (gs % 16 != 0) return -1;                   // CUDA path: gs multiple of 16
   int gpg = gs / 4;
   if (gpg > 128) return -1;                      // packed int32 accumulator bound
-  int R = (gpg % 8 == 0) ? 8 : 4;
+  int R = unit_kg_for(gs);
   int Lg = gpg / R;
   if (Lg & (Lg - 1)) return -1;                  // lanes per group must be a power of two
   if (k % gs != 0) return -4;                    // ELAYOUT

@@ -8,6 +8,7 @@
 //   q           trunc(e/scale + copysign(0.5, .))   lut_build.py:174-176
 //   row sums    left-to-right f32 accumulation        lut_build.py:191-193
 #include "common.cuh"
+#include "layout.cuh"
 
 namespace {
 
@@ -169,7 +170,16 @@ build_lut_kernel(const AT* __restrict__ a, int k, int gs, void* __restrict__ tab
       packed[idx >> 2] |= ((uint32_t)(int)r & 0xffu) << (8 * (idx & 3));
     }
     if (live) {
-      reinterpret_cast<uint2*>(tables)[(int64_t)row * KG + kg] = make_uint2(packed[0], packed[1]);
+      // kernel-format table: encoded a = Q - (Q < 0) per byte (gemv.cu "A/B
+      // tables"), unit-interleaved like the weights (layout.cuh table_offset)
+      const uint32_t e0 = packed[0] - ((packed[0] >> 7) & 0x01010101u);
+      const uint32_t e1 = packed[1] - ((packed[1] >> 7) & 0x01010101u);
+      const int R = bl::unit_kg_for(gs), U = KG / R;
+      const int u = kg / R, r = kg - u * R, ub = u >> 5, l = u & 31;
+      const int nu_b = min(32, U - 32 * ub);
+      const int64_t off = (int64_t)ub * (32 * R * 8) + (int64_t)((r >> 1) * nu_b + l) * 16 + (r & 1) * 8;
+      *reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(tables) + (int64_t)row * KG * 8 + off) =
+          make_uint2(e0, e1);
       if ((kg & (gpg - 1)) == 0) tscales[(int64_t)row * NQ + kg / gpg] = scale;
     }
   } else {
@@ -276,7 +286,7 @@ int bl_build_lut_launch(const void* a, int a_dtype, int n, int k, int group_size
 }
 
 extern "C" int bitlut_build_lut(const void* a, int a_dtype, int n, int k, int group_size, int mode,
-                                void* tables, float* tscales, float* rowsums, void* stream) {
+                                void* tables, float* tscales, float* rowsums, int flags, void* stream) {
   if (a_dtype != BITLUT_DT_F32 && a_dtype != BITLUT_DT_F16) return BITLUT_EPARAM;
   if (mode != BITLUT_TABLE_Q8 && mode != BITLUT_TABLE_F16) return BITLUT_EPARAM;
   if (n < 0 || k < 0 || group_size < 4) return BITLUT_EPARAM;
@@ -285,5 +295,5 @@ extern "C" int bitlut_build_lut(const void* a, int a_dtype, int n, int k, int gr
   if (gpg > 128 || (gpg & (gpg - 1))) return BITLUT_EPARAM;   // CUDA path: power-of-two k-groups per group
   if (n == 0 || k == 0) return BITLUT_OK;
   return bl_build_lut_launch(a, a_dtype, n, k, group_size, mode, tables, tscales, rowsums,
-                             (cudaStream_t)stream, false);
+                             (cudaStream_t)stream, (flags & BITLUT_FLAG_PDL) != 0);
 }

@@ -183,7 +183,7 @@ def mpgemm(a, pw: PackedWeights, cfg: TileConfig | None = None,
     mode = N.TABLE_Q8
     if rows.device != pw.gpu.device:
         rows = rows.to(pw.gpu.device)
-    tables, ts, rs = N.build_lut(rows, pw.group_size, mode)
+    tables, ts, rs = N.build_lut(rows, pw.group_size, mode, N.FLAG_PDL if pdl else 0)
     out, partials = N.lookup(pw.gpu, pw.scales, pw.zeros, tables, ts, rs, pw.m, pw.k, pw.bits,
                              pw.group_size, mode, N.FLAG_PDL if pdl else 0, return_partials)
     if stats is not None:

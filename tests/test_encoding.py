@@ -99,7 +99,7 @@ def chunk_offsets(m, k, bits, gs):
     u, r = kg // R, kg % R
     ub, l = u >> 5, u & 31
     nu_b = np.minimum(32, U - 32 * ub)
-    within = ub * (32 * R * 16) + ((r >> 1) * nu_b + l) * 32 + (r & 1) * 16
+    within = ub * (32 * R * 16) + (r * nu_b + l) * 16
     rows = np.arange(n_tiles * n_sg)[:, None] * KG * 16
     return (rows + within[None, :]).reshape(-1)
 
