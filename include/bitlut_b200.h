@@ -121,7 +121,9 @@ int bitlut_row_sums(const void* a, int a_dtype, int n, int k, int group_size,
  *             precompute_lut(a))) in KERNEL FORMAT: each byte Q stored as
  *             Q - (Q < 0), k-groups unit-interleaved like the weights
  *             (layout.cuh table_offset); tscales (n, k/gs) f32, rowsums f32
- *   mode F16: tables = fp16 (n, k/4, 8) [fp16-rounded half tables], rowsums.   */
+ *   mode F16: tables = fp16-rounded half tables (n, k/4, 8 x 2 B) in KERNEL
+ *             FORMAT: per k-group 8 low bytes then 8 high bytes of the 8
+ *             entries, unit-interleaved at 16 B; rowsums (tscales unused). */
 int bitlut_build_lut(const void* a, int a_dtype, int n, int k, int group_size, int mode,
                      void* tables, float* tscales, float* rowsums, int flags, void* stream);
 

@@ -143,28 +143,57 @@ __device__ __forceinline__ void lookup_kg(const uint4 w, uint32_t a0, uint32_t a
   }
 }
 
-// Butterfly transpose-reduce of 16 packed accumulators across LG aligned
-// lanes.  Afterwards the lane holds NF = 16/LG fully reduced pairs, starting
-// at pair index `base`.
-template <int LG>
-__device__ __forceinline__ int transpose_reduce(int (&acc)[16], int lane) {
+// Butterfly transpose-reduce of NV accumulators across LG aligned lanes
+// (no redundant adds).  Afterwards the lane holds NV/LG fully reduced values,
+// starting at index `base`.  Fixed order -> deterministic for floats too.
+template <int LG, int NV, typename T>
+__device__ __forceinline__ int transpose_reduce(T (&acc)[NV], int lane) {
   int base = 0;
-  int n = 16;
+  int n = NV;
 #pragma unroll
   for (int o = LG / 2; o >= 1; o >>= 1) {
     n >>= 1;
     const bool up = (lane & o) != 0;
 #pragma unroll
-    for (int i = 0; i < 8; i++) {
+    for (int i = 0; i < NV / 2; i++) {
       if (i < n) {
-        const int send = up ? acc[i] : acc[i + n];
-        const int keep = up ? acc[i + n] : acc[i];
+        const T send = up ? acc[i] : acc[i + n];
+        const T keep = up ? acc[i + n] : acc[i];
         acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
       }
     }
     if (up) base += n;
   }
   return base;
+}
+
+// fp16-table lookup of one k-group for 32 streams ("cuda-f16").  Tables:
+// lo0/lo1 = low bytes of the 8 fp16 half-table entries, hi0/hi1 = high
+// bytes.  Per 4 nibbles: two prmt gather the bytes (selector bit 3 masked),
+// a third prmt in sign-replicate mode turns the mirror flags into a byte
+// mask (flag -> 0x80) that flips the fp16 sign, two prmt interleave the
+// bytes into half2, and FHADD (f32 += f16 half) accumulates in fp32.
+__device__ __forceinline__ void lookup_kg_f16(const uint4 w, const uint4 t, float (&acc)[32]) {
+  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const uint32_t x = ws[q];
+    const uint32_t e = x & 0x77777777u;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const uint32_t eh = h ? e >> 16 : e, xh = h ? x >> 16 : x;
+      const uint32_t lo = bl::prmt(t.x, t.y, eh);
+      uint32_t hi = bl::prmt(t.z, t.w, eh);
+      const uint32_t one = bl::prmt(0x01010101u, 0x01010101u, xh);   // 1 where s = 0
+      hi ^= 0x80808080u - one * 128u;                                  // 0x80 where s = 1
+      const uint32_t h01 = bl::prmt(lo, hi, 0x5140u), h23 = bl::prmt(lo, hi, 0x7362u);
+      float* a = acc + 8 * q + 4 * h;
+      asm("add.rn.f32.f16 %0, %1, %0;" : "+f"(a[0]) : "h"((unsigned short)(h01 & 0xffffu)));
+      asm("add.rn.f32.f16 %0, %1, %0;" : "+f"(a[1]) : "h"((unsigned short)(h01 >> 16)));
+      asm("add.rn.f32.f16 %0, %1, %0;" : "+f"(a[2]) : "h"((unsigned short)(h23 & 0xffffu)));
+      asm("add.rn.f32.f16 %0, %1, %0;" : "+f"(a[3]) : "h"((unsigned short)(h23 >> 16)));
+    }
+  }
 }
 
 // Shared-memory plan.  Region A holds the tile's weights (TMA variant) and
@@ -198,7 +227,7 @@ __host__ __device__ inline SmemPlan smem_plan(const bl::LayoutV2& L, bool zeros,
 // Epilogue products for every (channel, group) of the tile; tile_ch is a
 // power of two so the (c, gq) split is a shift/mask.  BITS is compile-time so
 // the plane loop unrolls; partials / zero points are separate passes.
-template <int BITS, typename ST>
+template <int BITS, int MODE, typename ST>
 __device__ __forceinline__ void form_terms(const GemvArgs& p, const ST* sraw, const ST* zraw,
                                            const float* tsm, const float* rsm, const int32_t* psm,
                                            float* terms, int rowlen, int tid, int T, int row, int tile) {
@@ -215,8 +244,14 @@ __device__ __forceinline__ void form_terms(const GemvArgs& p, const ST* sraw, co
     const int32_t* pr = psm + gq * pstride + c * BITS;
 #pragma unroll
     for (int i = 0; i < BITS; i++) {
-      const float f = __fmul_rn(0.5f * (float)(1 << i), ts);
-      trow[i * NQ] = __fmul_rn(__fmul_rn(f, ws), __int2float_rn(pr[i]));
+      if (MODE == BITLUT_TABLE_Q8) {
+        // _kernels.py:183-184: ((pf * ts) * ws) * f32(stage)
+        const float f = __fmul_rn(0.5f * (float)(1 << i), ts);
+        trow[i * NQ] = __fmul_rn(__fmul_rn(f, ws), __int2float_rn(pr[i]));
+      } else {
+        // _kernels.py:131: (pf * ws) * stage, stage = f32 sum of fp16 lookups
+        trow[i * NQ] = __fmul_rn(__fmul_rn(0.5f * (float)(1 << i), ws), __int_as_float(pr[i]));
+      }
     }
     trow[BITS * NQ] = __fmul_rn(ws, rsm[gq]);
   }
@@ -229,7 +264,7 @@ __device__ __forceinline__ void form_terms(const GemvArgs& p, const ST* sraw, co
           __fmul_rn(__fmul_rn(ws, __fsub_rn(half_range, bl::to_f32(zraw[c * NQ + gq]))), rsm[gq]);
     }
   }
-  if (p.partials) {
+  if (MODE == BITLUT_TABLE_Q8 && p.partials) {
     for (int idx = tid; idx < n * BITS; idx += T) {
       const int gq = idx % NQ, ci = idx / NQ, c = ci / BITS, i = ci - c * BITS;
       p.partials[(((int64_t)row * BITS + i) * L.m + (int64_t)tile * tch + c) * NQ + gq] =
@@ -238,9 +273,9 @@ __device__ __forceinline__ void form_terms(const GemvArgs& p, const ST* sraw, co
   }
 }
 
-template <int R, int LG, typename ST, bool TMA>
+template <int R, int LG, typename ST, bool TMA, int MODE>
 __global__ void __launch_bounds__(512)
-gemv_q8_kernel(GemvArgs p) {
+gemv_kernel(GemvArgs p) {
   const bl::LayoutV2& L = p.L;
   constexpr int NF = 16 / LG;
   const int tile = blockIdx.x;
@@ -305,7 +340,7 @@ gemv_q8_kernel(GemvArgs p) {
   bl::pdl_wait();
   TRACE(2);
   for (int i = tid; i < NQ; i += T) {
-    tsm[i] = p.tscales[(int64_t)row * NQ + i];
+    if (MODE == BITLUT_TABLE_Q8) tsm[i] = p.tscales[(int64_t)row * NQ + i];
     rsm[i] = p.rowsums[(int64_t)row * NQ + i];
   }
   if (TMA) mbar_wait(bar, 0);
@@ -318,47 +353,66 @@ gemv_q8_kernel(GemvArgs p) {
   for (int rd = 0; rd < rounds; rd++) {
     const int u = tid + rd * T;
     const bool live = u < units;
-    int acc[16];
-#pragma unroll
-    for (int i = 0; i < 16; i++) acc[i] = 0;
-    int sg = 0, uu = 0;
+    int sg = 0, uu = 0, ub = 0, l = 0, nu_b = 32;
     if (live) {
       sg = u / U; uu = u - sg * U;
-      const int ub = uu >> 5, l = uu & 31;
-      const int nu_b = min(32, U - 32 * ub);
-      uint4 tq[R / 2];
-      const uint8_t* tb = p.qtab + (int64_t)row * KG * 8 + (int64_t)ub * (32 * R * 8) + l * 16;
+      ub = uu >> 5; l = uu & 31;
+      nu_b = min(32, U - 32 * ub);
+    }
+    const uint8_t* wsrc = TMA ? wbuf + (size_t)sg * KG * 16 + (size_t)ub * (32 * R * 16) + l * 16
+                              : p.w + L.sg_row_base(tile, sg) + (int64_t)ub * (32 * R * 16) + l * 16;
+    if constexpr (MODE == BITLUT_TABLE_Q8) {
+      int acc[16];
 #pragma unroll
-      for (int jp = 0; jp < R / 2; jp++) tq[jp] = bl::ld_nc_128(tb + jp * nu_b * 16);
-      if (TMA) {
-        const uint8_t* wb = wbuf + (size_t)sg * KG * 16 + (size_t)ub * (32 * R * 16) + l * 16;
+      for (int i = 0; i < 16; i++) acc[i] = 0;
+      if (live) {
+        uint4 tq[R / 2];
+        const uint8_t* tb = p.qtab + (int64_t)row * KG * 8 + (int64_t)ub * (32 * R * 8) + l * 16;
 #pragma unroll
-        for (int j = 0; j < R; j++) {
-          const uint4 w = *reinterpret_cast<const uint4*>(wb + j * nu_b * 16);
-          lookup_kg(w, (j & 1) ? tq[j >> 1].z : tq[j >> 1].x, (j & 1) ? tq[j >> 1].w : tq[j >> 1].y, acc);
-        }
-      } else {
-        const uint8_t* wg = p.w + L.sg_row_base(tile, sg) + (int64_t)ub * (32 * R * 16) + l * 16;
+        for (int jp = 0; jp < R / 2; jp++) tq[jp] = bl::ld_nc_128(tb + jp * nu_b * 16);
         uint4 wr[R];
 #pragma unroll
-        for (int j = 0; j < R; j++) wr[j] = bl::ld_nc_128(wg + (int64_t)j * nu_b * 16);
+        for (int j = 0; j < R; j++)
+          wr[j] = TMA ? *reinterpret_cast<const uint4*>(wsrc + j * nu_b * 16)
+                      : bl::ld_nc_128(wsrc + (int64_t)j * nu_b * 16);
 #pragma unroll
         for (int j = 0; j < R; j++)
           lookup_kg(wr[j], (j & 1) ? tq[j >> 1].z : tq[j >> 1].x, (j & 1) ? tq[j >> 1].w : tq[j >> 1].y, acc);
       }
-    }
-    int base = 0;
-    if (__any_sync(0xffffffffu, live)) base = transpose_reduce<LG>(acc, lane);
-    if (live) {
-      // undo the -1 per lookup of both streams, split each pair
-      const int fix = -32767 * (R * LG);
-      int32_t* dst = psm + (size_t)(uu / LG) * pstride + sg * 32 + 2 * base;
+      int base = 0;
+      if (__any_sync(0xffffffffu, live)) base = transpose_reduce<LG, 16, int>(acc, lane);
+      if (live) {
+        // undo the -1 per lookup of both streams, split each pair
+        const int fix = -32767 * (R * LG);
+        int32_t* dst = psm + (size_t)(uu / LG) * pstride + sg * 32 + 2 * base;
 #pragma unroll
-      for (int i = 0; i < NF; i++) {
-        const int v = acc[i] + fix;
-        const int pe = (v << 17) >> 17;
-        dst[2 * i] = pe;
-        dst[2 * i + 1] = (pe - v) >> 15;
+        for (int i = 0; i < NF; i++) {
+          const int v = acc[i] + fix;
+          const int pe = (v << 17) >> 17;
+          dst[2 * i] = pe;
+          dst[2 * i + 1] = (pe - v) >> 15;
+        }
+      }
+    } else {
+      float acc[32];
+#pragma unroll
+      for (int i = 0; i < 32; i++) acc[i] = 0.f;
+      if (live) {
+        const uint8_t* tb = p.qtab + (int64_t)row * KG * 16 + (int64_t)ub * (32 * R * 16) + l * 16;
+#pragma unroll
+        for (int j = 0; j < R; j++) {
+          const uint4 t = bl::ld_nc_128(tb + j * nu_b * 16);
+          const uint4 w = TMA ? *reinterpret_cast<const uint4*>(wsrc + j * nu_b * 16)
+                              : bl::ld_nc_128(wsrc + (int64_t)j * nu_b * 16);
+          lookup_kg_f16(w, t, acc);
+        }
+      }
+      int base = 0;
+      if (__any_sync(0xffffffffu, live)) base = transpose_reduce<LG, 32, float>(acc, lane);
+      if (live) {
+        int32_t* dst = psm + (size_t)(uu / LG) * pstride + sg * 32 + base;
+#pragma unroll
+        for (int i = 0; i < 32 / LG; i++) dst[i] = __float_as_int(acc[i]);
       }
     }
   }
@@ -369,10 +423,10 @@ gemv_q8_kernel(GemvArgs p) {
   //         ((pf_i*ts)*ws)*f32(P)  (_kernels.py:183-184), ws*rs (:188) and the
   //         zero-point term (ws*(2^(b-1)-z))*rs ----
   switch (bits) {
-    case 1: form_terms<1, ST>(p, sraw, zraw, tsm, rsm, psm, terms, rowlen, tid, T, row, tile); break;
-    case 2: form_terms<2, ST>(p, sraw, zraw, tsm, rsm, psm, terms, rowlen, tid, T, row, tile); break;
-    case 3: form_terms<3, ST>(p, sraw, zraw, tsm, rsm, psm, terms, rowlen, tid, T, row, tile); break;
-    default: form_terms<4, ST>(p, sraw, zraw, tsm, rsm, psm, terms, rowlen, tid, T, row, tile); break;
+    case 1: form_terms<1, MODE, ST>(p, sraw, zraw, tsm, rsm, psm, terms, rowlen, tid, T, row, tile); break;
+    case 2: form_terms<2, MODE, ST>(p, sraw, zraw, tsm, rsm, psm, terms, rowlen, tid, T, row, tile); break;
+    case 3: form_terms<3, MODE, ST>(p, sraw, zraw, tsm, rsm, psm, terms, rowlen, tid, T, row, tile); break;
+    default: form_terms<4, MODE, ST>(p, sraw, zraw, tsm, rsm, psm, terms, rowlen, tid, T, row, tile); break;
   }
   __syncthreads();
   TRACE(5);
@@ -439,11 +493,11 @@ bool use_tma(const bl::LayoutV2& L, bool zeros) {
   return L.n_sg * L.U <= 512 && smem_plan<ST>(L, zeros, true).total <= 112 * 1024;
 }
 
-template <int R, int LG, typename ST, bool TMA>
+template <int R, int LG, typename ST, bool TMA, int MODE>
 int launch_q8(const GemvArgs& a, int n, cudaStream_t stream, bool pdl) {
   const size_t smem = smem_plan<ST>(a.L, a.zeros != nullptr, TMA).total;
   if (smem > 227 * 1024) return BITLUT_ELAYOUT;
-  auto kern = gemv_q8_kernel<R, LG, ST, TMA>;
+  auto kern = gemv_kernel<R, LG, ST, TMA, MODE>;
   if (smem > 48 * 1024) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return BITLUT_EINTERNAL;
@@ -461,24 +515,28 @@ int launch_q8(const GemvArgs& a, int n, cudaStream_t stream, bool pdl) {
 }
 
 template <int R, int LG, typename ST>
-int launch_q8_any(const GemvArgs& a, int n, cudaStream_t s, bool pdl) {
-  return use_tma<ST>(a.L, a.zeros != nullptr) ? launch_q8<R, LG, ST, true>(a, n, s, pdl)
-                                              : launch_q8<R, LG, ST, false>(a, n, s, pdl);
+int launch_q8_any(const GemvArgs& a, int n, cudaStream_t s, bool pdl, int mode) {
+  const bool tma = use_tma<ST>(a.L, a.zeros != nullptr);
+  if (mode == BITLUT_TABLE_Q8)
+    return tma ? launch_q8<R, LG, ST, true, BITLUT_TABLE_Q8>(a, n, s, pdl)
+               : launch_q8<R, LG, ST, false, BITLUT_TABLE_Q8>(a, n, s, pdl);
+  return tma ? launch_q8<R, LG, ST, true, BITLUT_TABLE_F16>(a, n, s, pdl)
+             : launch_q8<R, LG, ST, false, BITLUT_TABLE_F16>(a, n, s, pdl);
 }
 
 template <typename ST>
-int dispatch_q8(const GemvArgs& a, int n, cudaStream_t s, bool pdl) {
+int dispatch_q8(const GemvArgs& a, int n, cudaStream_t s, bool pdl, int mode) {
   const int R = a.L.R, LG = a.L.Lg;
   if (R == 8) {
     switch (LG) {
-      case 1: return launch_q8_any<8, 1, ST>(a, n, s, pdl);
-      case 2: return launch_q8_any<8, 2, ST>(a, n, s, pdl);
-      case 4: return launch_q8_any<8, 4, ST>(a, n, s, pdl);
-      case 8: return launch_q8_any<8, 8, ST>(a, n, s, pdl);
-      case 16: return launch_q8_any<8, 16, ST>(a, n, s, pdl);
+      case 1: return launch_q8_any<8, 1, ST>(a, n, s, pdl, mode);
+      case 2: return launch_q8_any<8, 2, ST>(a, n, s, pdl, mode);
+      case 4: return launch_q8_any<8, 4, ST>(a, n, s, pdl, mode);
+      case 8: return launch_q8_any<8, 8, ST>(a, n, s, pdl, mode);
+      case 16: return launch_q8_any<8, 16, ST>(a, n, s, pdl, mode);
     }
   } else if (R == 4 && LG == 1) {
-    return launch_q8_any<4, 1, ST>(a, n, s, pdl);
+    return launch_q8_any<4, 1, ST>(a, n, s, pdl, mode);
   }
   return BITLUT_EPARAM;
 }
@@ -496,15 +554,16 @@ extern "C" int bitlut_mpgemm_traced(const uint8_t* wgpu, int m, int k, int bits,
   if (n < 0) return BITLUT_ESHAPE;
   if (n == 0) return BITLUT_OK;
   if (scale_dtype != BITLUT_DT_F32 && scale_dtype != BITLUT_DT_F16) return BITLUT_EPARAM;
-  if (mode != BITLUT_TABLE_Q8) return BITLUT_EPARAM;
+  if (mode != BITLUT_TABLE_Q8 && mode != BITLUT_TABLE_F16) return BITLUT_EPARAM;
+  if (mode == BITLUT_TABLE_F16 && partials) return BITLUT_EPARAM;   // int32 partials: Q8 only
   if (n > 65535) return BITLUT_ESHAPE;
   const bool pdl = (flags & BITLUT_FLAG_PDL) != 0;
   GemvArgs a;
   a.w = wgpu; a.wscales = wscales; a.zeros = zeros;
   a.qtab = reinterpret_cast<const uint8_t*>(tables); a.tscales = tscales; a.rowsums = rowsums;
   a.out = out; a.partials = partials; a.trace = trace; a.L = L;
-  return scale_dtype == BITLUT_DT_F16 ? dispatch_q8<__half>(a, n, (cudaStream_t)stream, pdl)
-                                      : dispatch_q8<float>(a, n, (cudaStream_t)stream, pdl);
+  return scale_dtype == BITLUT_DT_F16 ? dispatch_q8<__half>(a, n, (cudaStream_t)stream, pdl, mode)
+                                      : dispatch_q8<float>(a, n, (cudaStream_t)stream, pdl, mode);
 }
 
 extern "C" int bitlut_mpgemm(const uint8_t* wgpu, int m, int k, int bits, int group_size,

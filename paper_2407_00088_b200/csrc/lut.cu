@@ -183,14 +183,23 @@ build_lut_kernel(const AT* __restrict__ a, int k, int gs, void* __restrict__ tab
       if ((kg & (gpg - 1)) == 0) tscales[(int64_t)row * NQ + kg / gpg] = scale;
     }
   } else {
-    __half2 h[4];
+    // fp16 half table, kernel format: 8 low bytes then 8 high bytes of the
+    // 8 entries (byte planes for prmt lookups), unit-interleaved at 16 B
+    // per k-group like the weights (layout.cuh chunk order)
+    uint32_t lo[2] = {0u, 0u}, hi[2] = {0u, 0u};
 #pragma unroll
-    for (int p = 0; p < 4; p++) h[p] = __halves2half2(__float2half_rn(e[2 * p]), __float2half_rn(e[2 * p + 1]));
+    for (int idx = 0; idx < 8; idx++) {
+      const uint32_t h = __half_as_ushort(__float2half_rn(e[idx]));
+      lo[idx >> 2] |= (h & 0xffu) << (8 * (idx & 3));
+      hi[idx >> 2] |= (h >> 8) << (8 * (idx & 3));
+    }
     if (live) {
-      uint4 o;
-      o.x = *reinterpret_cast<uint32_t*>(&h[0]); o.y = *reinterpret_cast<uint32_t*>(&h[1]);
-      o.z = *reinterpret_cast<uint32_t*>(&h[2]); o.w = *reinterpret_cast<uint32_t*>(&h[3]);
-      reinterpret_cast<uint4*>(tables)[(int64_t)row * KG + kg] = o;
+      const int R = bl::unit_kg_for(gs), U = KG / R;
+      const int u = kg / R, r = kg - u * R, ub = u >> 5, l = u & 31;
+      const int nu_b = min(32, U - 32 * ub);
+      const int64_t off = (int64_t)ub * (32 * R * 16) + (int64_t)(r * nu_b + l) * 16;
+      *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(tables) + (int64_t)row * KG * 16 + off) =
+          make_uint4(lo[0], lo[1], hi[0], hi[1]);
     }
   }
 

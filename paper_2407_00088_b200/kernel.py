@@ -178,9 +178,9 @@ def mpgemm(a, pw: PackedWeights, cfg: TileConfig | None = None,
         raise DataError("activations contain non-finite values")
     if pw.gpu is None:
         raise LayoutError("packed weights carry no GPU layout (prepare them with prepare_weights)")
-    if variant is KernelVariant.CUDA_F16:
-        raise ParameterError("cuda-f16 lookup kernel not available in this build")
-    mode = N.TABLE_Q8
+    mode = N.TABLE_Q8 if variant is KernelVariant.CUDA_Q8 else N.TABLE_F16
+    if return_partials and mode != N.TABLE_Q8:
+        raise ParameterError("exact int32 partials exist only for int8 tables (cuda-q8)")
     if rows.device != pw.gpu.device:
         rows = rows.to(pw.gpu.device)
     tables, ts, rs = N.build_lut(rows, pw.group_size, mode, N.FLAG_PDL if pdl else 0)

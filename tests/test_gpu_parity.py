@@ -262,3 +262,66 @@ def test_errors(small_golden):
         B.mpgemv(c["a"][0], pw, cfg=B.TileConfig(m_tile=16, k_tile=128))
     with pytest.raises(B.ParameterError):
         B.mpgemv(c["a"][0], pw, variant="vector-q8")
+
+
+# ---------------------------------------------------------------- fp16 tables
+
+def rel_maxnorm(y, ref):
+    return float(np.abs(y - ref).max() / np.abs(ref).max())
+
+
+def test_f16_small_vs_scalar_real(small_golden):
+    """cuda-f16 vs the reference's fp32-table scalar-real: max|dy| <= 1e-3 max|y|
+    (north-star tolerance; element-wise rtol is not meaningful)."""
+    for name, c in small_golden.items():
+        inst = small_inst(c)
+        _, pw = make_pw(inst)
+        y = B.mpgemm(c["a"], pw, variant="cuda-f16")
+        if inst["zeros"] is None:
+            ref = c["y_scalar_real"]
+        else:
+            ref = O.mpgemm_real(c["a"], c["q"], c["scales"].astype(np.float32), inst["bits"],
+                                inst["group_size"], zeros=c["zeros"])
+        assert rel_maxnorm(y, ref) <= 1e-3, (name, rel_maxnorm(y, ref))
+
+
+def test_f16_config1_w4_asym_fp16_tables(config_golden):
+    """BASELINE config 1 exactly: 4096x4096 W4 asymmetric zeros g128, fp16
+    tables, compared against the reference (scalar-real + zero correction)."""
+    inst = W.config1()
+    g = config_golden[inst["name"]]
+    _, pw = make_pw(inst)
+    y = B.mpgemm(inst["a"], pw, variant="cuda-f16")[0]
+    rs = O.row_sums(inst["a"].astype(np.float32), inst["group_size"])
+    ref = (g["y_scalar-real"][0] + O.zero_correction(inst["scales"], inst["zeros"], 4, rs[0])).astype(np.float32)
+    assert rel_maxnorm(y, ref) <= 1e-3, rel_maxnorm(y, ref)
+    assert rel_maxnorm(y, g["y_dequant_ref"][0]) <= 1e-3
+
+
+@pytest.mark.parametrize("si", [0, 1, 2])
+@pytest.mark.parametrize("kind", ["sign", "ternary"])
+def test_f16_config3(config_golden, si, kind):
+    inst = W.config3(si, kind)
+    g = config_golden[inst["name"]]
+    _, pw = make_pw(inst)
+    y = B.mpgemm(inst["a"], pw, variant="cuda-f16")[0]
+    rs = O.row_sums(inst["a"].astype(np.float32), inst["group_size"])
+    ref = (g["y_scalar-real"][0] + O.zero_correction(inst["scales"], inst["zeros"], inst["bits"], rs[0])).astype(np.float32)
+    assert rel_maxnorm(y, ref) <= 1e-3, rel_maxnorm(y, ref)
+
+
+@pytest.mark.parametrize("si", [0, 1, 2])
+def test_f16_config2(config_golden, si):
+    inst = W.config2(si)
+    g = config_golden[inst["name"]]
+    _, pw = make_pw(inst)
+    y = B.mpgemm(inst["a"], pw, variant="cuda-f16")[0]
+    assert rel_maxnorm(y, g["y_scalar-real"][0]) <= 1e-3
+
+
+def test_f16_deterministic(small_golden):
+    c = plain(small_golden, 3)
+    _, pw = make_pw(small_inst(c))
+    y0 = B.mpgemm(c["a"], pw, variant="cuda-f16")
+    for _ in range(3):
+        assert np.array_equal(B.mpgemm(c["a"], pw, variant="cuda-f16"), y0)
