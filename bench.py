@@ -155,9 +155,8 @@ def step_fn(layers, acts, world, group, outs=None):
                 y, _ = N.lookup(pw.gpu, pw.scales, None, tables, ts, rs, pw.m, pw.k, pw.bits,
                                 pw.group_size, N.TABLE_Q8, N.FLAG_PDL, False)
                 if world > 1:
-                    full = torch.empty((1, pw.m * world), dtype=y.dtype, device=y.device)
-                    torch.distributed.all_gather_into_tensor(full, y, group=group)
-                    y = full
+                    from paper_2407_00088_b200.parallel import gather_rows
+                    y = gather_rows(y, [pw.m] * world, group)
                 res.append(y)
     return res
 

@@ -1,0 +1,119 @@
+"""Output-channel sharding across GPUs.
+
+Rows of W (output channels) are independent -- the reference itself
+partitions them across threads (kernel.py:254-263) with results identical
+for any partition.  Rank r of P owns a contiguous block of channels (a
+multiple of the 32-channel CUDA tile), builds its own tables for the
+replicated activations, runs the lookup kernel on its shard, and the
+slices are concatenated with one all-gather (NCCL over NVLink/NVSwitch in
+production; gloo in the CPU tests).  No partial sums cross ranks, so the
+result is bitwise identical to the single-GPU result for every P.
+
+One process per GPU; the process group comes from torch.distributed.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import torch
+import torch.distributed as dist
+
+from .core import QuantizedWeights, TileConfig, as_tensor
+from .errors import LayoutError, ParameterError
+
+SHARD_ALIGN = 32      # CUDA tile granularity along M (layout.cuh)
+
+
+def shard_bounds(m: int, rank: int, world: int, align: int = SHARD_ALIGN) -> tuple[int, int]:
+    """Contiguous [lo, hi) channel range of `rank`: blocks of `align`
+    channels dealt as evenly as possible (kernel.py:254-263 uses the same
+    base/extra split over m-blocks)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ParameterError(f"bad rank/world {rank}/{world}")
+    if m % align != 0:
+        raise LayoutError(f"m={m} not divisible by the shard alignment {align}")
+    blocks = m // align
+    base, extra = divmod(blocks, world)
+    lo = rank * base + min(rank, extra)
+    hi = lo + base + (1 if rank < extra else 0)
+    return lo * align, hi * align
+
+
+def shard_sizes(m: int, world: int, align: int = SHARD_ALIGN) -> list[int]:
+    return [b - a for a, b in (shard_bounds(m, r, world, align) for r in range(world))]
+
+
+def shard_quantized_weights(qw: QuantizedWeights, rank: int, world: int) -> QuantizedWeights:
+    """The rows of `qw` owned by `rank` (scales / zeros sliced alike)."""
+    lo, hi = shard_bounds(qw.m, rank, world)
+    q = as_tensor(qw.qvalues)[lo:hi]
+    s = as_tensor(qw.scales)[lo:hi]
+    z = None if qw.zeros is None else as_tensor(qw.zeros)[lo:hi]
+    return QuantizedWeights(m=hi - lo, k=qw.k, bits=qw.bits, group_size=qw.group_size,
+                            qvalues=q.contiguous(), scales=s.contiguous(),
+                            zeros=None if z is None else z.contiguous())
+
+
+@dataclass
+class ShardedWeights:
+    """This rank's PackedWeights plus the global row partition."""
+
+    local: object            # PackedWeights (or any operand local_fn accepts)
+    m_total: int
+    rank: int
+    world: int
+
+    @property
+    def sizes(self) -> list[int]:
+        return shard_sizes(self.m_total, self.world)
+
+
+def prepare_sharded(qw: QuantizedWeights, tile: TileConfig = None, rank: Optional[int] = None,
+                    world: Optional[int] = None) -> ShardedWeights:
+    """Shard then prepare (decompose / pack / repack on this rank's GPU)."""
+    from .weight_prep import prepare_weights
+    rank = dist.get_rank() if rank is None else rank
+    world = dist.get_world_size() if world is None else world
+    local = shard_quantized_weights(qw, rank, world)
+    pw = prepare_weights(local, tile) if tile is not None else prepare_weights(local)
+    return ShardedWeights(local=pw, m_total=qw.m, rank=rank, world=world)
+
+
+def gather_rows(y_local: torch.Tensor, sizes: list[int], group=None) -> torch.Tensor:
+    """All-gather (n, m_r) slices into (n, sum m_r), in rank order."""
+    world = len(sizes)
+    if world == 1:
+        return y_local
+    n = y_local.shape[0]
+    if len(set(sizes)) == 1:
+        # equal shards: one all_gather_into_tensor over a (world, n, m_r) buffer
+        buf = torch.empty((world * n, sizes[0]), dtype=y_local.dtype, device=y_local.device)
+        dist.all_gather_into_tensor(buf, y_local.contiguous(), group=group)
+        return buf.reshape(world, n, sizes[0]).permute(1, 0, 2).reshape(n, world * sizes[0])
+    # uneven shards: pad to the largest slice, gather, drop the padding
+    mx = max(sizes)
+    pad = torch.zeros((n, mx), dtype=y_local.dtype, device=y_local.device)
+    pad[:, :y_local.shape[1]] = y_local
+    buf = torch.empty((world * n, mx), dtype=y_local.dtype, device=y_local.device)
+    dist.all_gather_into_tensor(buf, pad, group=group)
+    buf = buf.reshape(world, n, mx)
+    return torch.cat([buf[r, :, :sizes[r]] for r in range(world)], dim=1)
+
+
+def sharded_mpgemm(a, sw: ShardedWeights, group=None, variant="cuda-q8",
+                   local_fn: Optional[Callable] = None, **kw) -> torch.Tensor:
+    """Tensor-parallel mpGEMM: local lookup kernel on this rank's channels,
+    then one all-gather of the output slices.  ``local_fn(a, local, **kw)``
+    defaults to the CUDA ``mpgemm``; tests substitute a CPU oracle to check
+    the partition/gather logic under gloo."""
+    if local_fn is None:
+        from .kernel import mpgemm
+
+        def local_fn(x, pw, **k):
+            return mpgemm(x, pw, variant=variant, **k)
+    y = local_fn(a, sw.local, **kw)
+    y = as_tensor(y)
+    if y.dim() == 1:
+        y = y.reshape(1, -1)
+    return gather_rows(y, sw.sizes, group)

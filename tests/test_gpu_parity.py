@@ -325,3 +325,21 @@ def test_f16_deterministic(small_golden):
     y0 = B.mpgemm(c["a"], pw, variant="cuda-f16")
     for _ in range(3):
         assert np.array_equal(B.mpgemm(c["a"], pw, variant="cuda-f16"), y0)
+
+
+# ---------------------------------------------------------------- sharding
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_sharded_slices_bitwise_on_one_gpu(world):
+    """Every rank's shard, run through the CUDA kernel on one GPU and
+    concatenated, equals the unsharded output bitwise (what the all-gather
+    assembles on P GPUs; the gather itself is tested under gloo)."""
+    from paper_2407_00088_b200 import parallel as PAR
+    inst = W.config5(3, 2, 8)          # 1024 x 8192 W2, batch 8
+    qw, pw = make_pw(inst)
+    full = B.mpgemm(inst["a"], pw)
+    parts = []
+    for r in range(world):
+        local = PAR.shard_quantized_weights(qw, r, world)
+        parts.append(B.mpgemm(inst["a"], B.prepare_weights(local, B.TileConfig(m_tile=32, k_tile=128))))
+    assert np.array_equal(np.concatenate(parts, axis=1), full)
