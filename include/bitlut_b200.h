@@ -49,6 +49,12 @@ extern "C" {
 
 /* launch flags (bitlut_build_lut, bitlut_mpgemm) */
 #define BITLUT_FLAG_PDL 1   /* launch with programmatic dependent launch */
+/* With BITLUT_FLAG_PDL: the call's inputs (tables, weights, scales) were
+ * complete before the PREVIOUS kernel in the stream started (e.g. k and v
+ * after q, all reading one table).  The kernel then does its whole
+ * computation without griddepcontrol.wait and waits only before exiting, so
+ * completion order is preserved while the work overlaps the predecessor. */
+#define BITLUT_FLAG_INDEPENDENT 2
 
 /*
  * GPU weight layout ("layout v2", this library's own; the reference's v1

@@ -23,6 +23,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "lib
 DT_F32, DT_F16 = 0, 1
 TABLE_Q8, TABLE_F16 = 0, 1
 FLAG_PDL = 1
+FLAG_INDEPENDENT = 2
 
 _vp, _i = ctypes.c_void_p, ctypes.c_int
 

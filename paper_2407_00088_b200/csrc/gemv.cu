@@ -74,6 +74,7 @@ struct GemvArgs {
   float* out;                // (n, m)
   int32_t* partials;         // (n, bits, m, NQ) or null
   unsigned long long* trace; // null, or (grid, 8) globaltimer stamps per CTA
+  int independent;           // BITLUT_FLAG_INDEPENDENT: wait only before exiting
   bl::LayoutV2 L;
 };
 
@@ -236,6 +237,45 @@ __device__ __forceinline__ void form_terms(const GemvArgs& p, const ST* sraw, co
   const int pstride = 32 * L.n_sg + 1;
   const int lg_tch = __ffs(tch) - 1;
   const int n = tch * NQ;
+  if ((NQ & 3) == 0) {
+    // 4 consecutive groups per thread step: float4 / 8-byte vector traffic
+    const int n4 = n >> 2;
+    for (int idx = tid; idx < n4; idx += T) {
+      const int c = idx & (tch - 1), gq = (idx >> lg_tch) << 2;
+      float ws[4];
+      if (sizeof(ST) == 2) {
+        const uint2 v = *reinterpret_cast<const uint2*>(sraw + c * NQ + gq);
+        const __half2 h0 = *reinterpret_cast<const __half2*>(&v.x), h1 = *reinterpret_cast<const __half2*>(&v.y);
+        ws[0] = __low2float(h0); ws[1] = __high2float(h0); ws[2] = __low2float(h1); ws[3] = __high2float(h1);
+      } else {
+        const float4 v = *reinterpret_cast<const float4*>(sraw + c * NQ + gq);
+        ws[0] = v.x; ws[1] = v.y; ws[2] = v.z; ws[3] = v.w;
+      }
+      const float4 ts4 = *reinterpret_cast<const float4*>(tsm + gq);
+      const float4 rs4 = *reinterpret_cast<const float4*>(rsm + gq);
+      const float ts[4] = {ts4.x, ts4.y, ts4.z, ts4.w}, rs[4] = {rs4.x, rs4.y, rs4.z, rs4.w};
+      float* trow = terms + c * rowlen + gq;
+      const int32_t* pr = psm + gq * pstride + c * BITS;
+#pragma unroll
+      for (int i = 0; i < BITS; i++) {
+        float t[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const int32_t P = pr[q * pstride + i];
+          if (MODE == BITLUT_TABLE_Q8) {
+            const float f = __fmul_rn(0.5f * (float)(1 << i), ts[q]);
+            t[q] = __fmul_rn(__fmul_rn(f, ws[q]), __int2float_rn(P));
+          } else {
+            t[q] = __fmul_rn(__fmul_rn(0.5f * (float)(1 << i), ws[q]), __int_as_float(P));
+          }
+        }
+        *reinterpret_cast<float4*>(trow + i * NQ) = make_float4(t[0], t[1], t[2], t[3]);
+      }
+      *reinterpret_cast<float4*>(trow + BITS * NQ) =
+          make_float4(__fmul_rn(ws[0], rs[0]), __fmul_rn(ws[1], rs[1]), __fmul_rn(ws[2], rs[2]),
+                      __fmul_rn(ws[3], rs[3]));
+    }
+  } else
   for (int idx = tid; idx < n; idx += T) {
     const int c = idx & (tch - 1), gq = idx >> lg_tch;
     const float ws = bl::to_f32(sraw[c * NQ + gq]);
@@ -334,10 +374,13 @@ gemv_kernel(GemvArgs p) {
   }
   __syncthreads();                      // mbarrier initialised / scales staged
   TRACE(1);
-  bl::pdl_launch_dependents();
 
-  // ---- 2. tables (produced by the previous kernel) ----
-  bl::pdl_wait();
+  // ---- 2. tables (produced by the previous kernel, unless independent).
+  //         A dependent launch lets its successor start only after its own
+  //         inputs are complete, so an INDEPENDENT successor (same tables)
+  //         can read them without waiting. ----
+  if (!p.independent) bl::pdl_wait();
+  bl::pdl_launch_dependents();
   TRACE(2);
   for (int i = tid; i < NQ; i += T) {
     if (MODE == BITLUT_TABLE_Q8) tsm[i] = p.tscales[(int64_t)row * NQ + i];
@@ -367,14 +410,16 @@ gemv_kernel(GemvArgs p) {
       for (int i = 0; i < 16; i++) acc[i] = 0;
       if (live) {
         uint4 tq[R / 2];
-        const uint8_t* tb = p.qtab + (int64_t)row * KG * 8 + (int64_t)ub * (32 * R * 8) + l * 16;
-#pragma unroll
-        for (int jp = 0; jp < R / 2; jp++) tq[jp] = bl::ld_nc_128(tb + jp * nu_b * 16);
         uint4 wr[R];
+        const uint8_t* tb = p.qtab + (int64_t)row * KG * 8 + (int64_t)ub * (32 * R * 8) + l * 16;
+        // full unit blocks (nu_b == 32) get compile-time strides
+        const int stride = nu_b == 32 ? 512 : nu_b * 16;
+#pragma unroll
+        for (int jp = 0; jp < R / 2; jp++) tq[jp] = bl::ld_nc_128(tb + jp * stride);
 #pragma unroll
         for (int j = 0; j < R; j++)
-          wr[j] = TMA ? *reinterpret_cast<const uint4*>(wsrc + j * nu_b * 16)
-                      : bl::ld_nc_128(wsrc + (int64_t)j * nu_b * 16);
+          wr[j] = TMA ? *reinterpret_cast<const uint4*>(wsrc + j * stride)
+                      : bl::ld_nc_128(wsrc + (int64_t)j * stride);
 #pragma unroll
         for (int j = 0; j < R; j++)
           lookup_kg(wr[j], (j & 1) ? tq[j >> 1].z : tq[j >> 1].x, (j & 1) ? tq[j >> 1].w : tq[j >> 1].y, acc);
@@ -471,6 +516,7 @@ gemv_kernel(GemvArgs p) {
     if (has_zeros) o = __fadd_rn(o, fin[64 + tid]);
     p.out[(int64_t)row * L.m + (int64_t)tile * tch + tid] = o;
   }
+  if (p.independent) bl::pdl_wait();    // keep stream completion order
   if (p.trace && tid == 0) {
     unsigned int smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -562,6 +608,7 @@ extern "C" int bitlut_mpgemm_traced(const uint8_t* wgpu, int m, int k, int bits,
   a.w = wgpu; a.wscales = wscales; a.zeros = zeros;
   a.qtab = reinterpret_cast<const uint8_t*>(tables); a.tscales = tscales; a.rowsums = rowsums;
   a.out = out; a.partials = partials; a.trace = trace; a.L = L;
+  a.independent = pdl && (flags & BITLUT_FLAG_INDEPENDENT) != 0;
   return scale_dtype == BITLUT_DT_F16 ? dispatch_q8<__half>(a, n, (cudaStream_t)stream, pdl, mode)
                                       : dispatch_q8<float>(a, n, (cudaStream_t)stream, pdl, mode);
 }

@@ -343,3 +343,23 @@ def test_sharded_slices_bitwise_on_one_gpu(world):
         local = PAR.shard_quantized_weights(qw, r, world)
         parts.append(B.mpgemm(inst["a"], B.prepare_weights(local, B.TileConfig(m_tile=32, k_tile=128))))
     assert np.array_equal(np.concatenate(parts, axis=1), full)
+
+
+def test_independent_launch_chain_matches():
+    """k/v-style INDEPENDENT launches after a dependent one reading the same
+    fresh table give the same (bitwise) results as fully dependent ones."""
+    from paper_2407_00088_b200 import _native as N
+    insts = [W.small_instance(40 + i, 512, 2048, 2, 64) for i in range(3)]
+    pws = [make_pw(i)[1] for i in insts]
+    a = torch.from_numpy(insts[0]["a"]).cuda()
+    ref = [B.mpgemm(a, pw) for pw in pws]
+    for _ in range(5):
+        t, ts, rs = N.build_lut(a, 64, N.TABLE_Q8, N.FLAG_PDL)
+        outs = []
+        for j, pw in enumerate(pws):
+            fl = N.FLAG_PDL | (N.FLAG_INDEPENDENT if j > 0 else 0)
+            y, _ = N.lookup(pw.gpu, pw.scales, None, t, ts, rs, pw.m, pw.k, pw.bits, pw.group_size,
+                            N.TABLE_Q8, fl, False)
+            outs.append(y)
+        for y, r in zip(outs, ref):
+            assert torch.equal(y, r)

@@ -26,6 +26,7 @@ ap.add_argument("--gs", type=int, default=64)
 ap.add_argument("--bufs", type=int, default=64)
 ap.add_argument("--reps", type=int, default=16)
 ap.add_argument("--pdl", type=int, default=1)
+ap.add_argument("--indep", type=int, default=0)
 args = ap.parse_args()
 
 g = torch.Generator(device="cuda").manual_seed(0)
@@ -51,7 +52,7 @@ def run():
         pw = pws[r % len(pws)]
         rc = L.bitlut_mpgemm_traced(N.ptr(pw.gpu), pw.m, pw.k, pw.bits, pw.group_size, N.ptr(pw.scales),
                                     None, N.DT_F16, N.ptr(t), N.ptr(ts), N.ptr(rs), N.TABLE_Q8, 1,
-                                    N.ptr(outs[r]), None, N.FLAG_PDL if args.pdl else 0,
+                                    N.ptr(outs[r]), None, (N.FLAG_PDL if args.pdl else 0) | (N.FLAG_INDEPENDENT if args.indep and r > 0 else 0),
                                     N.ptr(traces[r]), st)
         assert rc == 0
 
