@@ -164,6 +164,26 @@ def step_fn(layers, acts, world, group, outs=None):
     return res
 
 
+def build_pipeline(layers, acts, fast=False):
+    """The same step as step_fn as ONE persistent launch (pipeline.py), with
+    the decode chain's real dependencies: a layer's qkv table build waits for
+    the previous layer's down GEMV, o's for q,k,v, gate/up's for o, down's
+    for gate,up; every GEMV waits for its own table build only."""
+    from paper_2407_00088_b200.pipeline import Pipeline
+    pl = Pipeline()
+    prev = []
+    outs = []
+    for L, A in zip(layers, acts):
+        done = {}
+        for gname, k, names in LUT_GROUPS:
+            t = pl.tables(A[gname], L[names[0]].group_size, deps=prev)
+            ys = [pl.lookup(L[nm], t, fast_epilogue=fast) for nm in names]
+            outs += ys
+            prev = [pl.op_of(y) for y in ys]
+    pl.compile()
+    return pl, outs
+
+
 def lookups_only(layers, tabs):
     """The step's 7*L lookups with tables prebuilt, in the step's dependency
     structure (first GEMV after each table build dependent, the rest not)."""
@@ -299,30 +319,70 @@ def main():
     acts = make_acts(args.layers, device)
     stream = torch.cuda.Stream(device)
 
-    # ---- value: the full step, graph-replayed ----
-    g_step = capture(lambda: step_fn(layers, acts, world, group), stream)
-    with ClockSampler(local) as clk:
+    # ---- value: the full step as one persistent pipeline launch ----
+    total_bytes = packed_bytes_full(args.layers, bits)
+    launches_per_step = 1
+    pipe_ok = world == 1
+    if pipe_ok:
+        pl, _ = build_pipeline(layers, acts)
         with torch.cuda.stream(stream):
-            ms_step = time_graph(g_step, args.steps, args.warmup, barrier)
+            for _ in range(2):
+                pl.run(stream)
+        torch.cuda.synchronize()
+        with ClockSampler(local) as clk:
+            with torch.cuda.stream(stream):
+                for _ in range(args.warmup):
+                    pl.run(stream)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(args.steps):
+                    pl.run(stream)
+                e1.record(stream)
+                torch.cuda.synchronize()
+        ms_step = e0.elapsed_time(e1) / args.steps
+    # ---- the same step as per-op launches (CUDA graph + PDL), for comparison
+    g_step = capture(lambda: step_fn(layers, acts, world, group), stream)
+    if pipe_ok:
+        with torch.cuda.stream(stream):
+            ms_graph = time_graph(g_step, args.steps, args.warmup, barrier)
+    else:
+        with ClockSampler(local) as clk:
+            with torch.cuda.stream(stream):
+                ms_graph = time_graph(g_step, args.steps, args.warmup, barrier)
+        ms_step = ms_graph
+        launches_per_step = args.layers * (len(LUT_GROUPS) + len(LAYER))
+    del g_step
     if world > 1:
         t = torch.tensor([ms_step], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
-    total_bytes = packed_bytes_full(args.layers, bits)
     value = total_bytes / (ms_step * 1e-3) / 1e9
-    launches_per_step = args.layers * (len(LUT_GROUPS) + len(LAYER))
+    per_op_graph = {"ms_per_step": round(ms_graph, 5),
+                    "GBps": round(total_bytes / (ms_graph * 1e-3) / 1e9, 2),
+                    "launches_per_step": args.layers * (len(LUT_GROUPS) + len(LAYER))}
 
-    # ---- roofline of the dominant kernel: lookups alone ----
+    # ---- lookups alone (tables prebuilt), per-op launches, step's dependency flags ----
     tabs = [{gname: N.build_lut(A[gname], gs, N.TABLE_Q8) for gname, _, _ in LUT_GROUPS}
             for A in acts]
     torch.cuda.synchronize()
     g_look = capture(lambda: lookups_only(layers, tabs), stream)
     with torch.cuda.stream(stream):
         ms_look = time_graph(g_look, args.steps, args.warmup, barrier)
+    del g_look
     local_bytes = sum(pw.packed_bytes for L in layers for pw in L.values())
     n_look = args.layers * len(LAYER)
-    achieved = local_bytes / (ms_look * 1e-3) / 1e9
     peak, peak_src = load_peaks()
+    if pipe_ok:
+        kernel_name, achieved = "pipeline_kernel (whole step, 1 launch)", value
+        how = (f"1 persistent launch per step ({args.layers * 11} ops), algorithmic bytes = "
+               f"sum bits*M*K/8 = {total_bytes} per launch, CUDA events over {args.steps} launches")
+    else:
+        kernel_name, achieved = "gemv_kernel", local_bytes / (ms_look * 1e-3) / 1e9
+        how = (f"{n_look} lookup launches/graph, algorithmic bytes = bits*M*K/8 per launch, "
+               f"CUDA events over {args.steps} replays")
+    lookups_graph = {"ms": round(ms_look, 5), "GBps": round(local_bytes / (ms_look * 1e-3) / 1e9, 1),
+                     "launches": n_look}
 
     # ---- per-shape us per launch (each shape alone, rotating over all layers) ----
     per_shape = {}
@@ -418,10 +478,10 @@ def main():
             "config": cfg,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": load_traffic(), "kernel": "gemv_q8_kernel",
-                         "peak_source": peak_src,
-                         "how": f"{n_look} lookup launches/graph, algorithmic bytes = bits*M*K/8 "
-                                f"per launch, CUDA events over {args.steps} replays"},
+                         "traffic": load_traffic(), "kernel": kernel_name,
+                         "peak_source": peak_src, "how": how},
+            "per_op_graph": per_op_graph,
+            "lookups_only_graph": lookups_graph,
             "per_shape_w2": per_shape,
             "cpu_baseline": cpu,
             "e2e": e2e,

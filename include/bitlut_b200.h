@@ -55,6 +55,10 @@ extern "C" {
  * computation without griddepcontrol.wait and waits only before exiting, so
  * completion order is preserved while the work overlaps the predecessor. */
 #define BITLUT_FLAG_INDEPENDENT 2
+/* Fast epilogue: the int32 staging values are the same exact ones, but the
+ * float combination is a fixed-order parallel reduction instead of the
+ * reference's left-to-right chain (deterministic; last-bits differences). */
+#define BITLUT_FLAG_FAST_EPILOGUE 4
 
 /*
  * GPU weight layout ("layout v2", this library's own; the reference's v1
@@ -162,6 +166,47 @@ int bitlut_mpgemm_traced(const uint8_t* wgpu, int m, int k, int bits, int group_
                          const void* tables, const float* tscales, const float* rowsums,
                          int mode, int n, float* out, int32_t* partials, int flags,
                          unsigned long long* trace, void* stream);
+
+/* ---------------- persistent pipeline (this library's executor) ----------------
+ * A whole op list -- table builds and lookup GEMVs, e.g. every projection of
+ * every decoder layer of a batch-1 decode step -- runs in ONE cooperative
+ * launch.  Each op names up to three earlier ops it depends on; completion
+ * counters in global memory replace kernel boundaries.  Per-op arithmetic is
+ * identical to bitlut_build_lut (mode Q8) + bitlut_mpgemm (mode Q8). */
+#define BITLUT_OP_TABLES 0
+#define BITLUT_OP_LOOKUP 1
+typedef struct {
+  int type;                 /* BITLUT_OP_TABLES or BITLUT_OP_LOOKUP */
+  int dep[3];               /* earlier op indices this op needs complete, -1 = none */
+  const void* a;            /* TABLES: activations (n, k), a_dtype */
+  int a_dtype;
+  int n, k, group_size;     /* rows, reduction length, quantization group */
+  void* tables;             /* TABLES: written; LOOKUP: read (kernel-format int8) */
+  float* tscales;           /* (n, k/gs) */
+  float* rowsums;           /* (n, k/gs) */
+  const uint8_t* wgpu;      /* LOOKUP: layout-v2 weights */
+  const void* wscales;      /* LOOKUP: (m, k/gs), scale_dtype */
+  const void* zeros;        /* LOOKUP: (m, k/gs) or NULL */
+  int scale_dtype;
+  int m, bits;
+  float* out;               /* LOOKUP: (n, m) f32 */
+  int flags;                /* LOOKUP: BITLUT_FLAG_FAST_EPILOGUE or 0 */
+} bitlut_pipe_op;
+
+/* Bytes of the encoded op table for n_ops ops. */
+size_t bitlut_pipeline_table_bytes(int n_ops);
+/* Validate the specs and encode them into `table_host` (caller-allocated,
+ * bitlut_pipeline_table_bytes(n_ops) bytes).  All LOOKUP ops must share the
+ * group size's kernel configuration and the scale dtype. */
+int bitlut_pipeline_encode(const bitlut_pipe_op* specs, int n_ops, void* table_host, size_t table_bytes);
+/* Run an encoded table: `table_dev` is a device copy of `table_host`;
+ * `counters` is device scratch of 2*n_ops uint32 (zeroed by the call). */
+int bitlut_pipeline_launch(const void* table_host, const void* table_dev, unsigned* counters, void* stream);
+/* Diagnostic variant: `trace` gets 4 %globaltimer stamps per (op, unit)
+ * [start, dependencies met, inputs staged, done] at (unit_base[op] + unit)*4;
+ * unit_base: device int array of per-op unit offsets (tools/pipeline_timeline.py). */
+int bitlut_pipeline_launch_traced(const void* table_host, const void* table_dev, unsigned* counters,
+                                  unsigned long long* trace, const int* unit_base, void* stream);
 
 /* Number of kernel launches one bitlut_mpgemm call enqueues (for accounting). */
 int bitlut_mpgemm_launches(int m, int k, int bits, int group_size, int mode, int n);

@@ -24,6 +24,7 @@ DT_F32, DT_F16 = 0, 1
 TABLE_Q8, TABLE_F16 = 0, 1
 FLAG_PDL = 1
 FLAG_INDEPENDENT = 2
+FLAG_FAST_EPILOGUE = 4
 
 _vp, _i = ctypes.c_void_p, ctypes.c_int
 
@@ -76,7 +77,8 @@ def lib() -> ctypes.CDLL:
 
 
 def exported_symbols() -> list[str]:
-    return list(_SIGS) + ["bitlut_version"]
+    return list(_SIGS) + ["bitlut_version", "bitlut_pipeline_table_bytes", "bitlut_pipeline_encode",
+                          "bitlut_pipeline_launch", "bitlut_pipeline_launch_traced"]
 
 
 def require_cuda(t: torch.Tensor, what: str) -> None:

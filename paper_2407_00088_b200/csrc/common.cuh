@@ -45,6 +45,20 @@ BL_DEV U8x32 ld_stream_256(const void* p) {
   return r;
 }
 
+// L2-coherent loads (bypass L1): data written by other CTAs of the same
+// launch (pipeline.cu) must not be read through the non-coherent path.
+BL_DEV uint4 ld_cg_128(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+BL_DEV float ld_cg_f32(const float* p) {
+  float r;
+  asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(r) : "l"(p));
+  return r;
+}
+
 BL_DEV uint4 ld_nc_128(const void* p) {
   uint4 r;
   asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"

@@ -7,8 +7,7 @@
 //   table scale max|e| / 127  (IEEE division)        lut_build.py:172-173
 //   q           trunc(e/scale + copysign(0.5, .))   lut_build.py:174-176
 //   row sums    left-to-right f32 accumulation        lut_build.py:191-193
-#include "common.cuh"
-#include "layout.cuh"
+#include "lut_core.cuh"
 
 namespace {
 
@@ -116,102 +115,10 @@ build_lut_kernel(const AT* __restrict__ a, int k, int gs, void* __restrict__ tab
                  float* __restrict__ tscales, float* __restrict__ rowsums) {
   bl::pdl_launch_dependents();
   bl::pdl_wait();                       // activations come from the previous kernel
-  const int KG = k >> 2;
-  const int gpg = gs >> 2;
-  const int NQ = k / gs;
-  const int row = blockIdx.y;
-  const int kg0 = blockIdx.x * kLutThreads;
-  const int kg = kg0 + threadIdx.x;
-  const bool live = kg < KG;
-  __shared__ float sa[kLutThreads * 4];
+  __shared__ __align__(16) float sa[kLutThreads * 4];
   __shared__ float red[kLutThreads / 32];
-
-  float v[4] = {0.f, 0.f, 0.f, 0.f};
-  if (live) {
-    const AT* src = a + (int64_t)row * k + 4 * (int64_t)kg;
-#pragma unroll
-    for (int j = 0; j < 4; j++) v[j] = bl::to_f32(src[j]);
-  }
-#pragma unroll
-  for (int j = 0; j < 4; j++) sa[threadIdx.x * 4 + j] = v[j];
-
-  // half table (index bit 3 clear): e[idx] = ((s0 a0 + s1 a1) + s2 a2) - a3
-  float e[8];
-#pragma unroll
-  for (int idx = 0; idx < 8; idx++) {
-    float x = (idx & 1) ? v[0] : -v[0];
-    x = (idx & 2) ? __fadd_rn(x, v[1]) : __fsub_rn(x, v[1]);
-    x = (idx & 4) ? __fadd_rn(x, v[2]) : __fsub_rn(x, v[2]);
-    e[idx] = __fsub_rn(x, v[3]);
-  }
-
-  if (MODE == BITLUT_TABLE_Q8) {
-    float mx = 0.f;
-#pragma unroll
-    for (int idx = 0; idx < 8; idx++) mx = fmaxf(mx, fabsf(e[idx]));
-    const int seg = gpg < 32 ? gpg : 32;
-    for (int o = 1; o < seg; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if (gpg > 32) {
-      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-      __syncthreads();
-      const int wpg = gpg >> 5;                       // warps per group
-      const int w0 = (threadIdx.x >> 5) / wpg * wpg;
-      mx = 0.f;
-      for (int w = 0; w < wpg; w++) mx = fmaxf(mx, red[w0 + w]);
-    }
-    float scale = __fdiv_rn(mx, 127.0f);
-    if (scale == 0.0f) scale = 1.0f;
-    uint32_t packed[2] = {0u, 0u};
-#pragma unroll
-    for (int idx = 0; idx < 8; idx++) {
-      float s = __fdiv_rn(e[idx], scale);
-      float r = truncf(__fadd_rn(s, copysignf(0.5f, s)));
-      r = fminf(fmaxf(r, -127.f), 127.f);
-      packed[idx >> 2] |= ((uint32_t)(int)r & 0xffu) << (8 * (idx & 3));
-    }
-    if (live) {
-      // kernel-format table: encoded a = Q - (Q < 0) per byte (gemv.cu "A/B
-      // tables"), unit-interleaved like the weights (layout.cuh table_offset)
-      const uint32_t e0 = packed[0] - ((packed[0] >> 7) & 0x01010101u);
-      const uint32_t e1 = packed[1] - ((packed[1] >> 7) & 0x01010101u);
-      const int R = bl::unit_kg_for(gs), U = KG / R;
-      const int u = kg / R, r = kg - u * R, ub = u >> 5, l = u & 31;
-      const int nu_b = min(32, U - 32 * ub);
-      const int64_t off = (int64_t)ub * (32 * R * 8) + (int64_t)((r >> 1) * nu_b + l) * 16 + (r & 1) * 8;
-      *reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(tables) + (int64_t)row * KG * 8 + off) =
-          make_uint2(e0, e1);
-      if ((kg & (gpg - 1)) == 0) tscales[(int64_t)row * NQ + kg / gpg] = scale;
-    }
-  } else {
-    // fp16 half table, kernel format: 8 low bytes then 8 high bytes of the
-    // 8 entries (byte planes for prmt lookups), unit-interleaved at 16 B
-    // per k-group like the weights (layout.cuh chunk order)
-    uint32_t lo[2] = {0u, 0u}, hi[2] = {0u, 0u};
-#pragma unroll
-    for (int idx = 0; idx < 8; idx++) {
-      const uint32_t h = __half_as_ushort(__float2half_rn(e[idx]));
-      lo[idx >> 2] |= (h & 0xffu) << (8 * (idx & 3));
-      hi[idx >> 2] |= (h >> 8) << (8 * (idx & 3));
-    }
-    if (live) {
-      const int R = bl::unit_kg_for(gs), U = KG / R;
-      const int u = kg / R, r = kg - u * R, ub = u >> 5, l = u & 31;
-      const int nu_b = min(32, U - 32 * ub);
-      const int64_t off = (int64_t)ub * (32 * R * 16) + (int64_t)(r * nu_b + l) * 16;
-      *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(tables) + (int64_t)row * KG * 16 + off) =
-          make_uint4(lo[0], lo[1], hi[0], hi[1]);
-    }
-  }
-
-  __syncthreads();
-  // row sums: the first thread of each quant group adds its gs activations
-  // left to right (lut_build.py:191-193)
-  if (live && (kg & (gpg - 1)) == 0) {
-    const int off = threadIdx.x * 4;
-    float acc = 0.f;
-    for (int j = 0; j < gs; j++) acc = __fadd_rn(acc, sa[off + j]);
-    rowsums[(int64_t)row * NQ + kg / gpg] = acc;
-  }
+  lutk::lut_block<MODE, AT>(a, k, gs, tables, tscales, rowsums, blockIdx.y, blockIdx.x * kLutThreads,
+                            sa, red);
 }
 
 inline int grid_1d(int64_t n, int threads) {

@@ -155,12 +155,16 @@ def _activation_rows(a):
 def mpgemm(a, pw: PackedWeights, cfg: TileConfig | None = None,
            variant: KernelVariant | str = KernelVariant.CUDA_Q8,
            threads: int = 1, stats: KernelStats | None = None, *,
-           check_finite: bool = True, return_partials: bool = False, pdl: bool = True):
+           check_finite: bool = True, return_partials: bool = False, pdl: bool = True,
+           exact_epilogue: bool = True):
     """Mixed-precision GEMM: (N, K) activations x packed low-bit weights.
 
     Returns (N, M) float32 (numpy for numpy input, a CUDA tensor for CUDA
     input).  ``return_partials`` (cuda-q8) additionally returns the exact
     int32 staging values, shape (N, bits, M, K/group_size).
+    ``exact_epilogue=False`` keeps those exact int32 values but combines
+    them with a fixed-order parallel float reduction instead of the
+    reference's sequential one (faster; last-bits differences only).
     """
     variant = _variant(variant)
     cfg = pw.tile if cfg is None else cfg
@@ -184,8 +188,9 @@ def mpgemm(a, pw: PackedWeights, cfg: TileConfig | None = None,
     if rows.device != pw.gpu.device:
         rows = rows.to(pw.gpu.device)
     tables, ts, rs = N.build_lut(rows, pw.group_size, mode, N.FLAG_PDL if pdl else 0)
+    flags = (N.FLAG_PDL if pdl else 0) | (0 if exact_epilogue else N.FLAG_FAST_EPILOGUE)
     out, partials = N.lookup(pw.gpu, pw.scales, pw.zeros, tables, ts, rs, pw.m, pw.k, pw.bits,
-                             pw.group_size, mode, N.FLAG_PDL if pdl else 0, return_partials)
+                             pw.group_size, mode, flags, return_partials)
     if stats is not None:
         stats.lookups += pw.bits * n * pw.m * (pw.k // pw.g)
         stats.lut_builds += -(-n // cfg.n_tile) * (pw.k // cfg.k_tile)

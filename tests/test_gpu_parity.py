@@ -363,3 +363,68 @@ def test_independent_launch_chain_matches():
             outs.append(y)
         for y, r in zip(outs, ref):
             assert torch.equal(y, r)
+
+
+# ---------------------------------------------------------------- pipeline
+
+def test_pipeline_matches_per_op_bitwise():
+    """Two decoder-like layers (shared-table q/k/v, dependent o, gate/up,
+    down) through the persistent pipeline == per-op mpgemm, bitwise."""
+    from paper_2407_00088_b200.pipeline import Pipeline
+    gs, bits = 64, 2
+    shapes = {"q": (256, 512), "k": (256, 512), "v": (256, 512), "o": (256, 512),
+              "gate": (352, 512), "up": (352, 512), "down": (256, 1024)}
+    g = torch.Generator(device="cuda").manual_seed(3)
+    layers = []
+    for _ in range(2):
+        L = {}
+        for nm, (m, k) in shapes.items():
+            q = torch.randint(0, 4, (m, k), dtype=torch.uint8, device="cuda", generator=g)
+            sc = (torch.randn((m, k // gs), device="cuda", generator=g).abs() * 0.02 + 1e-3).half()
+            L[nm] = B.prepare_weights(B.QuantizedWeights(m=m, k=k, bits=bits, group_size=gs, qvalues=q, scales=sc))
+        layers.append(L)
+    xs = [{nm: torch.randn((1, k), device="cuda", generator=g).half() for nm, k in
+           (("attn", 512), ("o", 512), ("mlp", 512), ("down", 1024))} for _ in layers]
+    pl = Pipeline()
+    outs, prev = [], []
+    for L, X in zip(layers, xs):
+        t = pl.tables(X["attn"], gs, deps=prev)
+        yq, yk, yv = pl.lookup(L["q"], t), pl.lookup(L["k"], t), pl.lookup(L["v"], t)
+        t2 = pl.tables(X["o"], gs, deps=[pl.op_of(yq), pl.op_of(yk), pl.op_of(yv)])
+        yo = pl.lookup(L["o"], t2)
+        t3 = pl.tables(X["mlp"], gs, deps=[pl.op_of(yo)])
+        yg, yu = pl.lookup(L["gate"], t3), pl.lookup(L["up"], t3)
+        t4 = pl.tables(X["down"], gs, deps=[pl.op_of(yg), pl.op_of(yu)])
+        yd = pl.lookup(L["down"], t4)
+        prev = [pl.op_of(yd)]
+        outs.append({"q": yq, "k": yk, "v": yv, "o": yo, "gate": yg, "up": yu, "down": yd})
+    pl.compile()
+    for _ in range(3):
+        pl.run()
+        torch.cuda.synchronize()
+        for L, X, O in zip(layers, xs, outs):
+            for nm, xk in (("q", "attn"), ("k", "attn"), ("v", "attn"), ("o", "o"), ("gate", "mlp"),
+                           ("up", "mlp"), ("down", "down")):
+                ref = B.mpgemm(X[xk], L[nm])
+                assert torch.equal(O[nm], ref), nm
+
+
+def test_fast_epilogue_exact_partials_and_tolerance(small_golden, config_golden):
+    """Fast epilogue: same exact int32 partials; float output within 1e-5
+    (max-norm) of the reference's vector-q8 output; deterministic."""
+    for name, c in small_golden.items():
+        inst = small_inst(c)
+        _, pw = make_pw(inst)
+        y, P = B.mpgemm(c["a"], pw, return_partials=True, exact_epilogue=False)
+        assert np.array_equal(P.transpose(1, 0, 2, 3), c["partials"]), name
+        ref = c["y_vector_q8"] if inst["zeros"] is None else O.mpgemm_q8(
+            c["a"], c["q"], c["scales"].astype(np.float32), inst["bits"], inst["group_size"], zeros=c["zeros"])
+        assert rel_maxnorm(y, ref) <= 1e-5, (name, rel_maxnorm(y, ref))
+        assert np.array_equal(B.mpgemm(c["a"], pw, exact_epilogue=False), y)
+    for si in range(3):
+        inst = W.config2(si)
+        _, pw = make_pw(inst)
+        y = B.mpgemm(inst["a"], pw, exact_epilogue=False)
+        assert rel_maxnorm(y, config_golden[inst["name"]]["y_vector-q8"]) <= 1e-5
+        yf = B.mpgemm(inst["a"], pw, variant="cuda-f16", exact_epilogue=False)
+        assert rel_maxnorm(yf, config_golden[inst["name"]]["y_scalar-real"]) <= 1e-3
