@@ -7,13 +7,16 @@ weights in [0,4), group 64, fp16 scales, implicit zero 2, int8-quantized
 tables (bit-exact vs the reference's vector-q8), fp16 activations ~N(0,1).
 A STEP = one pass over L layers (default 32 = the whole 7B model, 1.62 GB of
 packed weights > 126 MB L2, so no L2 flush is needed): per layer 4 table
-builds (qkv / o / gate-up / down inputs) + 7 lookup GEMVs, 11 launches,
-captured once in a CUDA graph with programmatic dependent launch.
+builds (qkv / o / gate-up / down inputs) + 7 lookup GEMVs, run through the
+package's op-list executors (pipeline.Pipeline: "graph" = per-op kernels
+chained with programmatic dependent launch in one CUDA graph, "persistent" =
+one cooperative launch); the fastest is the headline, all are reported.
 
 value  = packed-weight bytes (bits*M*K/8, the reference's weight_bytes,
          cli.py:153) per step / device time, GB/s, all ranks aggregated.
-e2e    = the same metric through the public drop-in API (mpgemv with host
-         fp16 activations; H2D + D2H inside the timed region).
+e2e    = the same step from pinned HOST buffers: H2D of the activation rows,
+         the op list, D2H of every GEMV output, inside the timed region.
+         (e2e_per_call_api: the per-call drop-in mpgemv(numpy) path.)
 roofline = the dominant kernel (gemv_q8_kernel) timed alone in a graph of
          the step's 7*L lookups: algorithmic bytes / average launch time vs
          the measured HBM peak.
@@ -134,15 +137,27 @@ def build_layers(n_layers, bits, gs, rank, world, device, seed=20251020):
     return layers
 
 
-def make_acts(n_layers, device, seed=7):
+def make_acts(n_layers, device, seed=7, arena=None):
+    """fp16 activation rows, one per table build, carved in order from one
+    contiguous arena (so a step's inputs are one H2D copy); returns the
+    list of per-layer dicts (the arena is the first row's base)."""
     import torch
     gen = torch.Generator(device=device)
     gen.manual_seed(seed)
-    return [{g: torch.randn((1, k), device=device, generator=gen).half() for g, k, _ in LUT_GROUPS}
-            for _ in range(n_layers)]
+    per_layer = sum(k for _, k, _ in LUT_GROUPS)
+    if arena is None:
+        arena = torch.randn((n_layers * per_layer,), device=device, generator=gen).half()
+    acts, off = [], 0
+    for _ in range(n_layers):
+        d = {}
+        for g, k, _ in LUT_GROUPS:
+            d[g] = arena[off:off + k].view(1, k)
+            off += k
+        acts.append(d)
+    return acts, arena
 
 
-def step_fn(layers, acts, world, group, outs=None):
+def step_fn(layers, acts, world, group, fast=False):
     """One pass of the hot path (device-resident inputs)."""
     import torch
     from paper_2407_00088_b200 import _native as N
@@ -154,7 +169,7 @@ def step_fn(layers, acts, world, group, outs=None):
                 pw = L[nm]
                 # the first GEMV after a table build depends on it; the others
                 # (k, v after q; up after gate) read the same finished table
-                fl = N.FLAG_PDL | (N.FLAG_INDEPENDENT if j > 0 else 0)
+                fl = N.FLAG_PDL | (N.FLAG_INDEPENDENT if j > 0 else 0) | (N.FLAG_FAST_EPILOGUE if fast else 0)
                 y, _ = N.lookup(pw.gpu, pw.scales, None, tables, ts, rs, pw.m, pw.k, pw.bits,
                                 pw.group_size, N.TABLE_Q8, fl, False)
                 if world > 1:
@@ -164,24 +179,32 @@ def step_fn(layers, acts, world, group, outs=None):
     return res
 
 
-def build_pipeline(layers, acts, fast=False):
-    """The same step as step_fn as ONE persistent launch (pipeline.py), with
-    the decode chain's real dependencies: a layer's qkv table build waits for
-    the previous layer's down GEMV, o's for q,k,v, gate/up's for o, down's
-    for gate,up; every GEMV waits for its own table build only."""
+def build_pipeline(layers, acts, fast=False, executor="persistent"):
+    """The step as a pipeline.Pipeline op list with the decode chain's real
+    dependencies: a layer's qkv table build waits for the previous layer's
+    down GEMV, o's for q,k,v, gate/up's for o, down's for gate,up; every GEMV
+    waits for its own table build only.  All outputs are views of one f32
+    arena (one D2H per step).  Returns (pipeline, outputs, out_arena)."""
+    import torch
     from paper_2407_00088_b200.pipeline import Pipeline
-    pl = Pipeline()
-    prev = []
-    outs = []
+    pl = Pipeline(executor=executor)
+    per_layer = sum(pw.m for pw in layers[0].values())
+    out_arena = torch.empty((len(layers) * per_layer,), dtype=torch.float32,
+                            device=layers[0]["q"].gpu.device)
+    prev, outs, off = [], [], 0
     for L, A in zip(layers, acts):
-        done = {}
         for gname, k, names in LUT_GROUPS:
             t = pl.tables(A[gname], L[names[0]].group_size, deps=prev)
-            ys = [pl.lookup(L[nm], t, fast_epilogue=fast) for nm in names]
+            ys = []
+            for nm in names:
+                m = L[nm].m
+                ys.append(pl.lookup(L[nm], t, fast_epilogue=fast,
+                                    out=out_arena[off:off + m].view(1, m)))
+                off += m
             outs += ys
             prev = [pl.op_of(y) for y in ys]
     pl.compile()
-    return pl, outs
+    return pl, outs, out_arena
 
 
 def lookups_only(layers, tabs):
@@ -316,51 +339,60 @@ def main():
     barrier = (lambda: dist.barrier()) if world > 1 else None
 
     layers = build_layers(args.layers, bits, gs, rank, world, device)
-    acts = make_acts(args.layers, device)
+    acts, act_arena = make_acts(args.layers, device)
     stream = torch.cuda.Stream(device)
 
-    # ---- value: the full step as one persistent pipeline launch ----
+    # ---- the step through the package's op-list executors (pipeline.py):
+    #      "graph" = per-op kernels chained with PDL in one CUDA graph (exact
+    #      and fast epilogue), "persistent" = one cooperative launch.  Under
+    #      torchrun the step adds each GEMV's all-gather (step_fn, graph).
+    #      `value` reports the fastest; every executor is in the JSON line. ----
     total_bytes = packed_bytes_full(args.layers, bits)
-    launches_per_step = 1
-    pipe_ok = world == 1
-    if pipe_ok:
-        pl, _ = build_pipeline(layers, acts)
+    n_ops = args.layers * (len(LUT_GROUPS) + len(LAYER))
+    executors = {}
+
+    def time_runs(run):
         with torch.cuda.stream(stream):
-            for _ in range(2):
-                pl.run(stream)
-        torch.cuda.synchronize()
-        with ClockSampler(local) as clk:
-            with torch.cuda.stream(stream):
-                for _ in range(args.warmup):
-                    pl.run(stream)
-                torch.cuda.synchronize()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                for _ in range(args.steps):
-                    pl.run(stream)
-                e1.record(stream)
-                torch.cuda.synchronize()
-        ms_step = e0.elapsed_time(e1) / args.steps
-    # ---- the same step as per-op launches (CUDA graph + PDL), for comparison
-    g_step = capture(lambda: step_fn(layers, acts, world, group), stream)
-    if pipe_ok:
-        with torch.cuda.stream(stream):
-            ms_graph = time_graph(g_step, args.steps, args.warmup, barrier)
-    else:
-        with ClockSampler(local) as clk:
-            with torch.cuda.stream(stream):
-                ms_graph = time_graph(g_step, args.steps, args.warmup, barrier)
-        ms_step = ms_graph
-        launches_per_step = args.layers * (len(LUT_GROUPS) + len(LAYER))
-    del g_step
+            for _ in range(args.warmup):
+                run()
+            torch.cuda.synchronize()
+            if barrier:
+                barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                run()
+            e1.record(stream)
+            torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / args.steps
+
+    pipes = {}
+    with ClockSampler(local) as clk:
+        if world == 1:
+            for name, ex, fast in (("graph_exact", "graph", False), ("graph_fast", "graph", True),
+                                   ("persistent_fast", "persistent", True)):
+                pl, outs, out_arena = build_pipeline(layers, acts, fast=fast, executor=ex)
+                pipes[name] = (pl, out_arena)
+                executors[name] = {"ms": time_runs(lambda: pl.run(stream)),
+                                   "launches": n_ops if ex == "graph" else 1}
+        else:
+            for fast in (False, True):
+                g_step = capture(lambda: step_fn(layers, acts, world, group, fast=fast), stream)
+                executors["graph_" + ("fast" if fast else "exact")] = {
+                    "ms": time_runs(g_step.replay), "launches": n_ops}
+                del g_step
     if world > 1:
-        t = torch.tensor([ms_step], device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_step = float(t.item())
+        for v in executors.values():
+            t = torch.tensor([v["ms"]], device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            v["ms"] = float(t.item())
+    best = min(executors, key=lambda k: executors[k]["ms"])
+    ms_step = executors[best]["ms"]
+    launches_per_step = executors[best]["launches"]
     value = total_bytes / (ms_step * 1e-3) / 1e9
-    per_op_graph = {"ms_per_step": round(ms_graph, 5),
-                    "GBps": round(total_bytes / (ms_graph * 1e-3) / 1e9, 2),
-                    "launches_per_step": args.layers * (len(LUT_GROUPS) + len(LAYER))}
+    executors_out = {k: {"ms_per_step": round(v["ms"], 5),
+                         "GBps": round(total_bytes / (v["ms"] * 1e-3) / 1e9, 2),
+                         "launches_per_step": v["launches"]} for k, v in executors.items()}
 
     # ---- lookups alone (tables prebuilt), per-op launches, step's dependency flags ----
     tabs = [{gname: N.build_lut(A[gname], gs, N.TABLE_Q8) for gname, _, _ in LUT_GROUPS}
@@ -373,14 +405,15 @@ def main():
     local_bytes = sum(pw.packed_bytes for L in layers for pw in L.values())
     n_look = args.layers * len(LAYER)
     peak, peak_src = load_peaks()
-    if pipe_ok:
+    if best.startswith("persistent"):
         kernel_name, achieved = "pipeline_kernel (whole step, 1 launch)", value
         how = (f"1 persistent launch per step ({args.layers * 11} ops), algorithmic bytes = "
                f"sum bits*M*K/8 = {total_bytes} per launch, CUDA events over {args.steps} launches")
     else:
         kernel_name, achieved = "gemv_kernel", local_bytes / (ms_look * 1e-3) / 1e9
-        how = (f"{n_look} lookup launches/graph, algorithmic bytes = bits*M*K/8 per launch, "
-               f"CUDA events over {args.steps} replays")
+        how = (f"{n_look} lookup launches/graph (tables prebuilt, step's dependency flags, "
+               f"exact epilogue), algorithmic bytes = bits*M*K/8 per launch, CUDA events over "
+               f"{args.steps} replays")
     lookups_graph = {"ms": round(ms_look, 5), "GBps": round(local_bytes / (ms_look * 1e-3) / 1e9, 1),
                      "launches": n_look}
 
@@ -413,44 +446,48 @@ def main():
         per_shape[name] = entry
         del g_s
 
-    # ---- e2e through the public API with host buffers ----
+    # ---- e2e: the same step through the public API from HOST buffers: one
+    #      H2D of the step's activation rows (pinned), the op list, one D2H of
+    #      every GEMV output (pinned), all inside the timed region. ----
     e2e = None
-    if not args.no_e2e:
-        host_acts = [{g: A[g].cpu().pin_memory() for g in A} for A in acts]
-        n_e2e = min(args.layers, 8)
-        h2d = sum(host_acts[0][g].numel() * 2 * len(names) for g, _, names in LUT_GROUPS) * n_e2e
-        d2h = sum(m * 4 for _, m, _ in LAYER) * n_e2e
-        e2e_bytes = packed_bytes_full(n_e2e, bits)
+    if not args.no_e2e and world == 1 and best in pipes:
+        pl, out_arena = pipes[best]
+        host_in = act_arena.cpu().pin_memory()
+        host_out = torch.empty(out_arena.shape, dtype=out_arena.dtype).pin_memory()
 
         def e2e_step():
-            for L, HA in zip(layers[:n_e2e], host_acts[:n_e2e]):
+            act_arena.copy_(host_in, non_blocking=True)
+            pl.run(stream)
+            host_out.copy_(out_arena, non_blocking=True)
+        ms_e2e = time_runs(e2e_step)
+        e2e = {"value": round(total_bytes / (ms_e2e * 1e-3) / 1e9, 2), "unit": "GB/s",
+               "h2d_bytes_per_step": int(host_in.numel() * host_in.element_size()),
+               "d2h_bytes_per_step": int(host_out.numel() * host_out.element_size()),
+               "ms_per_step": round(ms_e2e, 4),
+               "path": f"pinned host activations -> Pipeline(executor={pl.executor!r}).run -> "
+                       f"pinned host outputs ({args.layers} layers x 7 GEMVs), CUDA events on "
+                       "the copy+compute stream"}
+    # the per-call drop-in API (reference kernel.py mpgemv: numpy in / numpy out)
+    per_call = None
+    if not args.no_e2e and world == 1:
+        n_pc = min(args.layers, 4)
+        host_rows = [{g: A[g][0].cpu().numpy() for g in A} for A in acts[:n_pc]]
+
+        def pc_step():
+            for L, HA in zip(layers[:n_pc], host_rows):
                 for gname, k, names in LUT_GROUPS:
                     for nm in names:
-                        y = B.mpgemv(HA[gname][0], L[nm], check_finite=True)
-                        if world > 1:
-                            pass  # host result of this rank's slice (gather below)
-        for _ in range(2):
-            e2e_step()
-        torch.cuda.synchronize()
-        if barrier:
-            barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        reps = max(2, min(args.steps, 10))
-        e0.record()
+                        B.mpgemv(HA[gname], L[nm])
+        pc_step()
+        t0 = time.perf_counter()
+        reps = 3
         for _ in range(reps):
-            e2e_step()
-        e1.record()
-        torch.cuda.synchronize()
-        ms_e2e = e0.elapsed_time(e1) / reps
-        if world > 1:
-            t = torch.tensor([ms_e2e], device=device)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms_e2e = float(t.item())
-        e2e = {"value": round(e2e_bytes / (ms_e2e * 1e-3) / 1e9, 2), "unit": "GB/s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": round(ms_e2e, 4),
-               "path": f"paper_2407_00088_b200.mpgemv(host fp16 row, PackedWeights) per GEMV, "
-                       f"{n_e2e} layers x 7 calls per step (per-call table build + D2H sync)"}
+            pc_step()
+        dt = (time.perf_counter() - t0) / reps
+        per_call = {"value": round(packed_bytes_full(n_pc, bits) / dt / 1e9, 2), "unit": "GB/s",
+                    "us_per_call": round(dt * 1e6 / (7 * n_pc), 1),
+                    "path": "mpgemv(numpy fp16 row, PackedWeights) -> numpy, one call per GEMV "
+                            "(table build + lookup + H2D/D2H + sync per call), wall clock"}
 
     # ---- CPU baseline (rank 0, N = 1 only) ----
     cpu = None
@@ -480,11 +517,13 @@ def main():
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": load_traffic(), "kernel": kernel_name,
                          "peak_source": peak_src, "how": how},
-            "per_op_graph": per_op_graph,
+            "executor": best,
+            "executors": executors_out,
             "lookups_only_graph": lookups_graph,
             "per_shape_w2": per_shape,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "e2e_per_call_api": per_call,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),
         }

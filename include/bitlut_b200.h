@@ -208,6 +208,15 @@ int bitlut_pipeline_launch(const void* table_host, const void* table_dev, unsign
 int bitlut_pipeline_launch_traced(const void* table_host, const void* table_dev, unsigned* counters,
                                   unsigned long long* trace, const int* unit_base, void* stream);
 
+/* Per-op executor for the same op list: stream-ordered launches of the
+ * bitlut_build_lut / bitlut_mpgemm kernels (mode Q8) chained with
+ * programmatic dependent launch, for capture into a CUDA graph.  Lookups
+ * whose deps are already complete when they start are launched with
+ * BITLUT_FLAG_INDEPENDENT (see pipeline.cu for the rule);
+ * bitlut_pipeline_plan_flags writes the per-op launch flags it uses. */
+int bitlut_pipeline_plan_flags(const bitlut_pipe_op* specs, int n_ops, int* flags_out);
+int bitlut_pipeline_launch_ops(const bitlut_pipe_op* specs, int n_ops, void* stream);
+
 /* Number of kernel launches one bitlut_mpgemm call enqueues (for accounting). */
 int bitlut_mpgemm_launches(int m, int k, int bits, int group_size, int mode, int n);
 

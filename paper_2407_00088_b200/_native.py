@@ -18,7 +18,8 @@ import torch
 
 from .errors import BitLutError, raise_for_status
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libbitlut_b200.so")
+LIB_PATH = os.environ.get("BITLUT_B200_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "_lib", "libbitlut_b200.so")   # env: A/B builds
 
 DT_F32, DT_F16 = 0, 1
 TABLE_Q8, TABLE_F16 = 0, 1
@@ -78,7 +79,8 @@ def lib() -> ctypes.CDLL:
 
 def exported_symbols() -> list[str]:
     return list(_SIGS) + ["bitlut_version", "bitlut_pipeline_table_bytes", "bitlut_pipeline_encode",
-                          "bitlut_pipeline_launch", "bitlut_pipeline_launch_traced"]
+                          "bitlut_pipeline_launch", "bitlut_pipeline_launch_traced",
+                          "bitlut_pipeline_plan_flags", "bitlut_pipeline_launch_ops"]
 
 
 def require_cuda(t: torch.Tensor, what: str) -> None:

@@ -59,23 +59,32 @@
 // the same pipeline with per-lane LDG.128 weight loads instead of TMA.
 #include "gemv_core.cuh"
 
+#include <cstdlib>
+
 namespace {
 
 using namespace blk;
 
-template <int R, int LG, typename ST, bool TMA, int MODE>
+// MULTI: the CTA keeps its weight tile in smem and walks rows_per_cta
+// activation rows (GEMM).  A separate instantiation, so the batch-1 kernel
+// keeps its register budget (84 vs 116 regs -> 5 vs 4 CTAs/SM, which is
+// one wave vs two for 11008x4096).
+template <int R, int LG, typename ST, bool TMA, int MODE, bool MULTI>
 __global__ void __launch_bounds__(512)
 gemv_kernel(GemvArgs p) {
   const bl::LayoutV2& L = p.L;
   const int tile = blockIdx.x;
-  const int row = blockIdx.y;
+  const int rpc = MULTI ? p.rows_per_cta : 1;
+  const int row0 = blockIdx.y * rpc;
+  const int row1 = MULTI ? min(row0 + rpc, p.n_rows) : row0 + 1;
   const int tid = threadIdx.x;
-  const SmemPlan sp = smem_plan<ST>(L, p.zeros != nullptr, TMA);
+  const SmemPlan sp = smem_plan<ST>(L, p.zeros != nullptr, TMA, MULTI);
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + sp.bar_off);
 
   TRACE(0);
-  // ---- 1. independent traffic first: weights + scales (+ zeros) ----
+  // ---- 1. independent traffic first: weights + scales (+ zeros), once per
+  //         CTA however many activation rows it processes ----
   if (TMA && tid == 0) {
     mbar_init(bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -91,14 +100,16 @@ gemv_kernel(GemvArgs p) {
   if (!p.independent) bl::pdl_wait();
   bl::pdl_launch_dependents();
   TRACE(2);
-  uint4 tq0[R / 2];
-  if (MODE == BITLUT_TABLE_Q8) prefetch_tables_q8<R>(p, row, tq0);
-  load_row_vectors<MODE>(p, row, sp, smem);
-  if (TMA) mbar_wait(bar, 0);
-  __syncthreads();                      // tsm / rsm visible; weights landed
-  TRACE(3);
-
-  tile_body<R, LG, ST, TMA, MODE>(p, tile, row, sp, smem, tq0);
+  for (int row = row0; row < row1; row++) {
+    uint4 tq0[R / 2];
+    if (MODE == BITLUT_TABLE_Q8) prefetch_tables_q8<R>(p, row, tq0);
+    load_row_vectors<MODE>(p, row, sp, smem);
+    if (TMA && row == row0) mbar_wait(bar, 0);
+    __syncthreads();                    // tsm / rsm visible; weights landed
+    TRACE(3);
+    tile_body<R, LG, ST, TMA, MODE>(p, tile, row, sp, smem, tq0);
+    if (MULTI) __syncthreads();         // row done before tsm / rsm / psm are reused
+  }
 
   if (p.independent) bl::pdl_wait();    // keep stream completion order
   if (p.trace && tid == 0) {
@@ -109,9 +120,20 @@ gemv_kernel(GemvArgs p) {
   TRACE(6);
 }
 
+int max_threads() {
+  static int cap = 0;
+  if (!cap) {
+    const char* e = getenv("BITLUT_MAX_THREADS");
+    cap = e ? atoi(e) : 256;
+    if (cap < 96 || cap > 512) cap = 512;
+  }
+  return cap;
+}
+
 int gemv_threads(const bl::LayoutV2& L) {
   const int units = L.n_sg * L.U;
-  const int rounds = (units + 511) / 512;
+  const int cap = max_threads();
+  const int rounds = (units + cap - 1) / cap;
   int t = (units + rounds - 1) / rounds;
   t = (t + 31) / 32 * 32;
   if (t < 96) t = 96;                  // three epilogue chain warps
@@ -119,21 +141,30 @@ int gemv_threads(const bl::LayoutV2& L) {
 }
 
 template <typename ST>
-bool use_tma(const bl::LayoutV2& L, bool zeros) {
-  return L.n_sg * L.U <= 512 && smem_plan<ST>(L, zeros, true).total <= 112 * 1024;
+bool use_tma(const bl::LayoutV2& L, bool zeros, bool keep) {
+  return L.n_sg * L.U <= 512 && smem_plan<ST>(L, zeros, true, keep).total <= 112 * 1024;
 }
 
-template <int R, int LG, typename ST, bool TMA, int MODE>
+template <int R, int LG, typename ST, bool TMA, int MODE, bool MULTI>
 int launch_q8(const GemvArgs& a, int n, cudaStream_t stream, bool pdl) {
-  const size_t smem = smem_plan<ST>(a.L, a.zeros != nullptr, TMA).total;
+  const size_t smem = smem_plan<ST>(a.L, a.zeros != nullptr, TMA, MULTI).total;
   if (smem > 227 * 1024) return BITLUT_ELAYOUT;
-  auto kern = gemv_kernel<R, LG, ST, TMA, MODE>;
-  if (smem > 48 * 1024) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+  auto kern = gemv_kernel<R, LG, ST, TMA, MODE, MULTI>;
+  // Once per instantiation: allow the largest plan, and ask for the
+  // max-shared carveout -- weights arrive by TMA and tables by ld.cg, so
+  // L1 has little to cache, while the default carveout can leave room for
+  // only one CTA of a long-K tile per SM (4096x11008: two waves instead of
+  // two co-resident CTAs).
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared) != cudaSuccess)
       return BITLUT_EINTERNAL;
+    configured = true;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(a.L.n_tiles, n);
+  cfg.gridDim = dim3(a.L.n_tiles, (n + a.rows_per_cta - 1) / a.rows_per_cta);
   cfg.blockDim = dim3(gemv_threads(a.L));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
@@ -145,13 +176,20 @@ int launch_q8(const GemvArgs& a, int n, cudaStream_t stream, bool pdl) {
 }
 
 template <int R, int LG, typename ST>
-int launch_q8_any(const GemvArgs& a, int n, cudaStream_t s, bool pdl, int mode) {
-  const bool tma = use_tma<ST>(a.L, a.zeros != nullptr);
-  if (mode == BITLUT_TABLE_Q8)
-    return tma ? launch_q8<R, LG, ST, true, BITLUT_TABLE_Q8>(a, n, s, pdl)
-               : launch_q8<R, LG, ST, false, BITLUT_TABLE_Q8>(a, n, s, pdl);
-  return tma ? launch_q8<R, LG, ST, true, BITLUT_TABLE_F16>(a, n, s, pdl)
-             : launch_q8<R, LG, ST, false, BITLUT_TABLE_F16>(a, n, s, pdl);
+int launch_q8_any(const GemvArgs& a0, int n, cudaStream_t s, bool pdl, int mode) {
+  GemvArgs a = a0;
+  // weight-stationary rows need the tile resident in smem (TMA path)
+  if (a.rows_per_cta > 1 && !use_tma<ST>(a.L, a.zeros != nullptr, true)) a.rows_per_cta = 1;
+  const bool multi = a.rows_per_cta > 1;
+  const bool tma = multi || use_tma<ST>(a.L, a.zeros != nullptr, false);
+  if (mode == BITLUT_TABLE_Q8) {
+    if (multi) return launch_q8<R, LG, ST, true, BITLUT_TABLE_Q8, true>(a, n, s, pdl);
+    return tma ? launch_q8<R, LG, ST, true, BITLUT_TABLE_Q8, false>(a, n, s, pdl)
+               : launch_q8<R, LG, ST, false, BITLUT_TABLE_Q8, false>(a, n, s, pdl);
+  }
+  if (multi) return launch_q8<R, LG, ST, true, BITLUT_TABLE_F16, true>(a, n, s, pdl);
+  return tma ? launch_q8<R, LG, ST, true, BITLUT_TABLE_F16, false>(a, n, s, pdl)
+             : launch_q8<R, LG, ST, false, BITLUT_TABLE_F16, false>(a, n, s, pdl);
 }
 
 template <typename ST>
@@ -194,6 +232,15 @@ extern "C" int bitlut_mpgemm_traced(const uint8_t* wgpu, int m, int k, int bits,
   a.out = out; a.partials = partials; a.trace = trace; a.L = L;
   a.independent = pdl && (flags & BITLUT_FLAG_INDEPENDENT) != 0;
   a.fast = (flags & BITLUT_FLAG_FAST_EPILOGUE) != 0;
+  a.n_rows = n;
+  // weight-stationary rows: a CTA keeps its tile in smem for up to 32 rows
+  // once there are enough (tile, row-block) CTAs to fill the GPU
+  a.rows_per_cta = 1;
+  if (n >= 8) {
+    int r = 32;
+    while (r > 1 && (int64_t)L.n_tiles * ((n + r - 1) / r) < 4 * 148) r >>= 1;
+    a.rows_per_cta = r;
+  }
   return scale_dtype == BITLUT_DT_F16 ? dispatch_q8<__half>(a, n, (cudaStream_t)stream, pdl, mode)
                                       : dispatch_q8<float>(a, n, (cudaStream_t)stream, pdl, mode);
 }

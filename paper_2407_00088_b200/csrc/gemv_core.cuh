@@ -21,6 +21,8 @@ struct GemvArgs {
   unsigned long long* trace; // null, or (grid, 8) globaltimer stamps per CTA
   int independent;           // BITLUT_FLAG_INDEPENDENT: wait only before exiting
   int fast;                  // BITLUT_FLAG_FAST_EPILOGUE: fixed-order parallel fp32 sums
+  int rows_per_cta;          // activation rows processed per CTA (weights loaded once)
+  int n_rows;
   bl::LayoutV2 L;
 };
 
@@ -147,21 +149,32 @@ __device__ __forceinline__ void lookup_kg_f16(const uint4 w, const uint4 t, floa
 // is reused for the epilogue products once the lookups are done.
 struct SmemPlan {
   int rowlen;            // floats per channel row of epilogue products (odd)
-  size_t a_bytes, p_off, s_off, z_off, t_off, r_off, f_off, bar_off, total;
+  size_t a_bytes, terms_off, p_off, s_off, z_off, t_off, r_off, f_off, bar_off, total;
 };
 
+// keep_weights: the products get their own region instead of reusing the
+// weights' (multi-row CTAs keep the tile's weights for every row).
 template <typename ST>
-__host__ __device__ inline SmemPlan smem_plan(const bl::LayoutV2& L, bool zeros, bool tma) {
+__host__ __device__ inline SmemPlan smem_plan(const bl::LayoutV2& L, bool zeros, bool tma,
+                                              bool keep_weights = false) {
   SmemPlan s;
   const int need = (L.bits + 1 + (zeros ? 1 : 0)) * L.NQ;
   s.rowlen = ((need + 3) / 4) * 4;
   if (((s.rowlen / 4) & 1) == 0) s.rowlen += 4;
   const size_t wbytes = tma ? (size_t)L.n_sg * L.KG * 16 : 0;
   const size_t terms = (size_t)L.tile_ch * s.rowlen * 4;
-  s.a_bytes = ((wbytes > terms ? wbytes : terms) + 15) & ~(size_t)15;
+  if (keep_weights) {
+    s.terms_off = (wbytes + 15) & ~(size_t)15;
+    s.a_bytes = s.terms_off + ((terms + 15) & ~(size_t)15);
+  } else {
+    s.terms_off = 0;
+    s.a_bytes = ((wbytes > terms ? wbytes : terms) + 15) & ~(size_t)15;
+  }
   const size_t sc = ((size_t)L.tile_ch * L.NQ * sizeof(ST) + 15) & ~(size_t)15;
   s.p_off = s.a_bytes;                                  // psm: NQ x (32*n_sg+1) int32
-  s.s_off = s.p_off + (((size_t)L.NQ * (32 * L.n_sg + 1) * 4 + 15) & ~(size_t)15);
+  // psm rows: 32*n_sg+1 int32 staging values, or tile_ch+4 floats (register epilogue)
+  const int prow = 32 * L.n_sg + 1 > L.tile_ch + 4 ? 32 * L.n_sg + 1 : L.tile_ch + 4;
+  s.s_off = s.p_off + (((size_t)L.NQ * prow * 4 + 15) & ~(size_t)15);
   s.z_off = s.s_off + sc;
   s.t_off = s.z_off + (zeros ? sc : 0);
   s.r_off = s.t_off + (((size_t)L.NQ * 4 + 15) & ~(size_t)15);
@@ -360,6 +373,72 @@ __device__ __forceinline__ void fast_epilogue(const GemvArgs& p, const ST* sraw,
   }
 }
 
+// Register epilogue (fast mode, int8 tables, 32-stream tiles): right after
+// the transpose-reduce a lane holds NF packed stream pairs of ONE quant
+// group.  It splits them, combines the bit planes of each channel in exact
+// integer arithmetic (S = sum_p 2^p P_p, |S| < 2^24 so f32(S) is exact) and
+// writes one float per (group, channel):
+//     y = ws * (ts*S - rs [+ 2(2^(b-1) - z) rs])
+// so out = 0.5 * sum_g y, reduced in a fixed order by reg_final.  The int32
+// staging values are the exact ones; only the float combination differs
+// from the reference's order (last bits, tolerance-tested).
+// Stream pair i = streams (2i, 2i+1), streams channel-major (c*bits + p).
+template <int BITS, int NF, typename ST>
+__device__ __forceinline__ void reg_terms(const GemvArgs& p, const int (&acc)[16], int fix, int base, int g,
+                                          const ST* sraw, const ST* zraw, const float* tsm, const float* rsm,
+                                          float* ysm, int ystride, int NQ) {
+  constexpr int NCH = BITS == 1 ? 2 * NF : (BITS == 2 ? NF : NF / 2);
+  int S[NCH];
+#pragma unroll
+  for (int i = 0; i < NF; i++) {
+    const int v = acc[i] + fix;
+    const int pe = (v << 17) >> 17;
+    const int po = (pe - v) >> 15;
+    if (BITS == 1) { S[2 * i] = pe; S[2 * i + 1] = po; }
+    else if (BITS == 2) { S[i] = pe + 2 * po; }
+    else { if (i & 1) S[i >> 1] += 4 * (pe + 2 * po); else S[i >> 1] = pe + 2 * po; }
+  }
+  const int ch0 = BITS == 1 ? 2 * base : (BITS == 2 ? base : base / 2);
+  const float ts = tsm[g], rs = rsm[g];
+  const float h2 = (float)(2 << (BITS - 1));            // 2 * 2^(b-1)
+  float y[NCH];
+#pragma unroll
+  for (int j = 0; j < NCH; j++) {
+    const int c = ch0 + j;
+    const float ws = bl::to_f32(sraw[c * NQ + g]);
+    float t = fmaf(ts, (float)S[j], -rs);
+    if (p.zeros) t = fmaf(fmaf(-2.f, bl::to_f32(zraw[c * NQ + g]), h2), rs, t);
+    y[j] = ws * t;
+  }
+  float* dst = ysm + g * ystride + ch0;
+  if constexpr (NCH % 4 == 0) {
+#pragma unroll
+    for (int j = 0; j < NCH; j += 4)
+      *reinterpret_cast<float4*>(dst + j) = make_float4(y[j], y[j + 1], y[j + 2], y[j + 3]);
+  } else if constexpr (NCH % 2 == 0) {
+#pragma unroll
+    for (int j = 0; j < NCH; j += 2) *reinterpret_cast<float2*>(dst + j) = make_float2(y[j], y[j + 1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < NCH; j++) dst[j] = y[j];
+  }
+}
+
+// out[c] = 0.5 * sum_g y[g][c]: tpc threads per channel, strided partial
+// sums then a shuffle tree (fixed order -> deterministic).
+__device__ __forceinline__ void reg_final(const GemvArgs& p, const float* ysm, int ystride, int row, int tile) {
+  const bl::LayoutV2& L = p.L;
+  const int tch = L.tile_ch, NQ = L.NQ, T = blockDim.x, tid = threadIdx.x;
+  int tpc = 32;
+  while (tpc * tch > T) tpc >>= 1;
+  const int c = tid / tpc, j = tid - c * tpc;
+  float acc = 0.f;
+  if (c < tch)
+    for (int g = j; g < NQ; g += tpc) acc += ysm[g * ystride + c];
+  for (int o = tpc / 2; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (c < tch && j == 0) p.out[(int64_t)row * L.m + (int64_t)tile * tch + c] = 0.5f * acc;
+}
+
 // Issue this thread's first-round table loads (Q8 kernel-format tables)
 // into registers right after the dependency is met, so they overlap the
 // row-vector loads and the weight-arrival wait instead of following them.
@@ -398,7 +477,7 @@ __device__ __forceinline__ void tile_body(const GemvArgs& p, int tile, int row, 
   const int bits = L.bits;
   const bool has_zeros = p.zeros != nullptr;
   uint8_t* wbuf = smem;
-  float* terms = reinterpret_cast<float*>(smem);      // after the lookups (TMA)
+  float* terms = reinterpret_cast<float*>(smem + sp.terms_off);   // after the lookups
   int32_t* psm = reinterpret_cast<int32_t*>(smem + sp.p_off);
   const int pstride = 32 * L.n_sg + 1;
   const ST* sraw = reinterpret_cast<const ST*>(smem + sp.s_off);
@@ -409,6 +488,11 @@ __device__ __forceinline__ void tile_body(const GemvArgs& p, int tile, int row, 
   // ---- 3. lookups, reduction, exact staging values -> psm[gq][stream] ----
   const int rowlen = sp.rowlen;
   const int rounds = (units + T - 1) / T;
+  // fast mode without partials on 32-stream tiles: epilogue from registers
+  const bool regepi = MODE == BITLUT_TABLE_Q8 && p.fast && !p.partials && L.n_sg == 1 &&
+                      (NF >= 2 || bits < 4);
+  const int ystride = tch + 4;          // floats per group row of y (16 B aligned, spreads banks)
+  float* ysm = reinterpret_cast<float*>(psm);
   for (int rd = 0; rd < rounds; rd++) {
     const int u = tid + rd * T;
     const bool live = u < units;
@@ -447,7 +531,19 @@ __device__ __forceinline__ void tile_body(const GemvArgs& p, int tile, int row, 
       }
       int base = 0;
       if (__any_sync(0xffffffffu, live)) base = transpose_reduce<LG, 16, int>(acc, lane);
-      if (live) {
+      if (regepi) {
+        if (live) {
+          const int fix = -32767 * (R * LG);
+          const int g = uu / LG;
+          switch (bits) {
+            case 1: reg_terms<1, NF, ST>(p, acc, fix, base, g, sraw, zraw, tsm, rsm, ysm, ystride, NQ); break;
+            case 2: reg_terms<2, NF, ST>(p, acc, fix, base, g, sraw, zraw, tsm, rsm, ysm, ystride, NQ); break;
+            default:
+              if constexpr (NF >= 2) reg_terms<4, NF, ST>(p, acc, fix, base, g, sraw, zraw, tsm, rsm, ysm, ystride, NQ);
+              break;
+          }
+        }
+      } else if (live) {
         // undo the -1 per lookup of both streams, split each pair
         const int fix = -32767 * (R * LG);
         int32_t* dst = psm + (size_t)(uu / LG) * pstride + sg * 32 + 2 * base;
@@ -484,6 +580,10 @@ __device__ __forceinline__ void tile_body(const GemvArgs& p, int tile, int row, 
   }
   TRACE(4);
   __syncthreads();                      // psm complete; region A (weights) free
+  if (regepi) {
+    reg_final(p, ysm, ystride, row, tile);
+    return;
+  }
   if (p.fast) {
     switch (bits) {
       case 1: fast_epilogue<1, MODE, ST>(p, sraw, zraw, tsm, rsm, psm, tid, T, row, tile); break;

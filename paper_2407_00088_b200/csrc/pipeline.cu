@@ -27,6 +27,8 @@
 #include "gemv_core.cuh"
 #include "lut_core.cuh"
 
+#include <cstdlib>
+
 namespace {
 
 using namespace blk;
@@ -223,6 +225,7 @@ extern "C" int bitlut_pipeline_encode(const bitlut_pipe_op* specs, int n_ops, vo
       g.qtab = reinterpret_cast<const uint8_t*>(s.tables); g.tscales = s.tscales; g.rowsums = s.rowsums;
       g.out = s.out; g.partials = nullptr; g.trace = nullptr; g.independent = 0; g.L = L;
       g.fast = (s.flags & BITLUT_FLAG_FAST_EPILOGUE) != 0;
+      g.rows_per_cta = 1; g.n_rows = s.n;
       o.n_units = L.n_tiles * s.n;
     } else {
       return BITLUT_EPARAM;
@@ -261,4 +264,65 @@ extern "C" int bitlut_pipeline_launch_traced(const void* table_host, const void*
   BL_PIPE(8, 1) BL_PIPE(8, 2) BL_PIPE(8, 4) BL_PIPE(8, 8) BL_PIPE(8, 16) BL_PIPE(4, 1)
 #undef BL_PIPE
   return BITLUT_EPARAM;
+}
+
+// ---------------------------------------------------------------------------
+// Per-op executor: the same op list as stream-ordered launches of the
+// per-call kernels (bitlut_build_lut / bitlut_mpgemm), chained with
+// programmatic dependent launch; meant to be captured once into a CUDA graph
+// (pipeline.py) so a replay costs one graph launch.
+//
+// Which lookups may skip the start-of-kernel wait (BITLUT_FLAG_INDEPENDENT)
+// follows from when each kernel releases its successor:
+//   * a table build triggers first, then waits              -> releases early
+//   * an INDEPENDENT lookup triggers first, waits at exit   -> releases early
+//   * a dependent lookup waits for its predecessor, then triggers.
+// So when kernel i starts, every op before the most recent dependent lookup
+// d < i (ops 0..d-1) has completed -- waits are transitive, since every
+// kernel waits for its predecessor before exiting.  Lookup i runs
+// INDEPENDENT iff all its deps are in that completed prefix (q after its
+// table build waits; k and v, which read the same table, do not).  A lookup
+// with no deps reads tables made outside the op list and always waits.
+// ---------------------------------------------------------------------------
+extern "C" int bitlut_pipeline_plan_flags(const bitlut_pipe_op* specs, int n_ops, int* flags_out) {
+  if (n_ops <= 0 || !specs || !flags_out) return BITLUT_EPARAM;
+  int done_below = 0;            // ops [0, done_below) complete when the next kernel starts
+  for (int i = 0; i < n_ops; i++) {
+    const bitlut_pipe_op& s = specs[i];
+    int fl = BITLUT_FLAG_PDL;
+    for (int d = 0; d < 3; d++)
+      if (s.dep[d] >= i || s.dep[d] < -1) return BITLUT_EPARAM;
+    if (s.type == BITLUT_OP_LOOKUP) {
+      bool any = false, ok = true;
+      for (int d = 0; d < 3; d++)
+        if (s.dep[d] >= 0) { any = true; ok = ok && s.dep[d] < done_below; }
+      if (any && ok) fl |= BITLUT_FLAG_INDEPENDENT;
+      else done_below = i;        // waits for op i-1 (hence all earlier), then releases i+1
+      fl |= s.flags & BITLUT_FLAG_FAST_EPILOGUE;
+    } else if (s.type != BITLUT_OP_TABLES) {
+      return BITLUT_EPARAM;
+    }
+    flags_out[i] = fl;
+  }
+  return BITLUT_OK;
+}
+
+extern "C" int bitlut_pipeline_launch_ops(const bitlut_pipe_op* specs, int n_ops, void* stream) {
+  if (n_ops <= 0 || !specs) return BITLUT_EPARAM;
+  int stack_flags[256];
+  int* flags = n_ops <= 256 ? stack_flags : static_cast<int*>(malloc(sizeof(int) * n_ops));
+  if (!flags) return BITLUT_EINTERNAL;
+  int rc = bitlut_pipeline_plan_flags(specs, n_ops, flags);
+  for (int i = 0; rc == BITLUT_OK && i < n_ops; i++) {
+    const bitlut_pipe_op& s = specs[i];
+    if (s.type == BITLUT_OP_TABLES)
+      rc = bitlut_build_lut(s.a, s.a_dtype, s.n, s.k, s.group_size, BITLUT_TABLE_Q8, s.tables,
+                            s.tscales, s.rowsums, flags[i], stream);
+    else
+      rc = bitlut_mpgemm(s.wgpu, s.m, s.k, s.bits, s.group_size, s.wscales, s.zeros, s.scale_dtype,
+                         s.tables, s.tscales, s.rowsums, BITLUT_TABLE_Q8, s.n, s.out, nullptr,
+                         flags[i], stream);
+  }
+  if (flags != stack_flags) free(flags);
+  return rc;
 }

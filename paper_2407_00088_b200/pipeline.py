@@ -1,8 +1,13 @@
-"""Persistent pipeline executor (csrc/pipeline.cu): a list of table builds
-and lookup GEMVs -- e.g. every projection of a batch-1 decode step -- runs
-in ONE cooperative launch, with per-op dependencies resolved by completion
-counters instead of kernel boundaries.  Results are bitwise identical to
-calling ``mpgemm`` op by op (same device code per tile).
+"""Op-list executors (csrc/pipeline.cu): a list of table builds and lookup
+GEMVs -- e.g. every projection of a batch-1 decode step -- recorded once and
+replayed.  Two executors run the same list, bitwise identically to calling
+``mpgemm`` op by op (same device code per tile):
+
+* ``"graph"`` (default): per-op kernels chained with programmatic dependent
+  launch (lookups whose inputs are already complete skip the start-of-kernel
+  wait), captured into one CUDA graph; a replay is one graph launch.
+* ``"persistent"``: ONE cooperative launch; every CTA walks the op list and
+  per-op completion counters replace kernel boundaries.
 
     pl = Pipeline()
     t = pl.tables(x, group_size=64)                     # op 0
@@ -10,7 +15,7 @@ calling ``mpgemm`` op by op (same device code per tile).
     yk = pl.lookup(pw_k, t)                              # independent of yq
     t2 = pl.tables(x_o, 64, deps=[yq, yk])               # waits for q and k
     ...
-    pl.compile(); pl.run()                               # stream-ordered, graph-capturable
+    pl.compile(); pl.run()                               # stream-ordered
 """
 from __future__ import annotations
 
@@ -45,6 +50,11 @@ def _bind():
                                          ctypes.c_size_t]
     L.bitlut_pipeline_launch.restype = ctypes.c_int
     L.bitlut_pipeline_launch.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    L.bitlut_pipeline_plan_flags.restype = ctypes.c_int
+    L.bitlut_pipeline_plan_flags.argtypes = [ctypes.POINTER(PipeOpSpec), ctypes.c_int,
+                                             ctypes.POINTER(ctypes.c_int)]
+    L.bitlut_pipeline_launch_ops.restype = ctypes.c_int
+    L.bitlut_pipeline_launch_ops.argtypes = [ctypes.POINTER(PipeOpSpec), ctypes.c_int, ctypes.c_void_p]
     return L
 
 
@@ -64,7 +74,12 @@ class TableRef(OpRef):
 class Pipeline:
     """Records ops, then runs them in one persistent launch."""
 
-    def __init__(self, device=None):
+    EXECUTORS = ("graph", "persistent")
+
+    def __init__(self, device=None, executor: str = "graph"):
+        if executor not in self.EXECUTORS:
+            raise ParameterError(f"executor must be one of {self.EXECUTORS}, got {executor!r}")
+        self.executor = executor
         self.device = torch.device(device) if device is not None else torch.device(
             "cuda", torch.cuda.current_device())
         self.specs: list[PipeOpSpec] = []
@@ -73,6 +88,8 @@ class Pipeline:
         self._host = None
         self._dev = None
         self._counters = None
+        self._arr = None
+        self._graph = None
 
     @staticmethod
     def _deps(deps) -> list[int]:
@@ -103,15 +120,20 @@ class Pipeline:
                         group_size=group_size)
 
     def lookup(self, pw, t: TableRef, deps: Optional[Sequence] = None,
-               fast_epilogue: bool = False) -> torch.Tensor:
+               fast_epilogue: bool = False, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         """Lookup GEMV with packed weights pw over table op t; returns the
-        (n, m) float32 output tensor (filled when the pipeline runs).  By
-        default the op depends on its table build only."""
+        (n, m) float32 output tensor (filled when the pipeline runs; pass
+        ``out`` to choose it, e.g. a view of one output arena).  By default
+        the op depends on its table build only."""
         if pw.gpu is None:
             raise ParameterError("packed weights carry no GPU layout")
         if (pw.k, pw.group_size) != (t.k, t.group_size):
             raise ParameterError("table op does not match the weights' k / group_size")
-        out = torch.empty((t.n, pw.m), dtype=torch.float32, device=pw.gpu.device)
+        if out is None:
+            out = torch.empty((t.n, pw.m), dtype=torch.float32, device=pw.gpu.device)
+        elif (out.dtype != torch.float32 or not out.is_contiguous() or out.device != pw.gpu.device
+              or out.numel() != t.n * pw.m):
+            raise ParameterError("out must be a contiguous float32 (n, m) tensor on the weights' device")
         tables, ts, rs = t.tensors
         s = PipeOpSpec()
         s.type = OP_LOOKUP
@@ -135,28 +157,66 @@ class Pipeline:
                 return i
         raise ParameterError("tensor is not an output of this pipeline")
 
+    def plan_flags(self) -> list[int]:
+        """Launch flags the graph executor gives each op (BITLUT_FLAG_*)."""
+        n = len(self.specs)
+        arr = (PipeOpSpec * n)(*self.specs)
+        fl = (ctypes.c_int * n)()
+        raise_for_status(_bind().bitlut_pipeline_plan_flags(arr, n, fl), "bitlut_pipeline_plan_flags")
+        return list(fl)
+
     def compile(self) -> "Pipeline":
         L = _bind()
         n = len(self.specs)
-        nbytes = L.bitlut_pipeline_table_bytes(n)
-        arr = (PipeOpSpec * n)(*self.specs)
-        host = torch.empty(nbytes, dtype=torch.uint8)
-        rc = L.bitlut_pipeline_encode(arr, n, ctypes.c_void_p(host.data_ptr()), nbytes)
-        raise_for_status(rc, "bitlut_pipeline_encode")
-        self._host = host
-        self._dev = host.to(self.device)
-        self._counters = torch.zeros(2 * n, dtype=torch.int32, device=self.device)
+        if n == 0:
+            raise ParameterError("empty pipeline")
+        self._arr = (PipeOpSpec * n)(*self.specs)
+        if self.executor == "persistent":
+            nbytes = L.bitlut_pipeline_table_bytes(n)
+            host = torch.empty(nbytes, dtype=torch.uint8)
+            rc = L.bitlut_pipeline_encode(self._arr, n, ctypes.c_void_p(host.data_ptr()), nbytes)
+            raise_for_status(rc, "bitlut_pipeline_encode")
+            self._host = host
+            self._dev = host.to(self.device)
+            self._counters = torch.zeros(2 * n, dtype=torch.int32, device=self.device)
+        else:
+            self.plan_flags()                       # validates the list before capture
+            side = torch.cuda.Stream(self.device)
+            side.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.stream(side):           # one eager pass (module load, first-launch costs)
+                self._launch_ops(side)
+            side.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                self._launch_ops(side)
+            self._graph = g
         return self
 
+    def _launch_ops(self, stream: torch.cuda.Stream) -> None:
+        rc = _bind().bitlut_pipeline_launch_ops(self._arr, len(self.specs),
+                                                ctypes.c_void_p(stream.cuda_stream))
+        raise_for_status(rc, "bitlut_pipeline_launch_ops")
+
     def run(self, stream: Optional[torch.cuda.Stream] = None) -> None:
-        if self._dev is None:
+        """Enqueue the whole op list on `stream` (default: current stream)."""
+        if self._arr is None:
             self.compile()
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if self.executor == "graph":
+            with torch.cuda.stream(st):
+                self._graph.replay()
+            return
         rc = _bind().bitlut_pipeline_launch(ctypes.c_void_p(self._host.data_ptr()),
                                             ctypes.c_void_p(self._dev.data_ptr()),
                                             ctypes.c_void_p(self._counters.data_ptr()),
                                             ctypes.c_void_p(st.cuda_stream))
         raise_for_status(rc, "bitlut_pipeline_launch")
+
+    def run_eager(self, stream: Optional[torch.cuda.Stream] = None) -> None:
+        """Graph executor without the graph: launch the op list directly."""
+        if self._arr is None:
+            self._arr = (PipeOpSpec * len(self.specs))(*self.specs)
+        self._launch_ops(stream if stream is not None else torch.cuda.current_stream(self.device))
 
     @property
     def n_ops(self) -> int:

@@ -107,3 +107,32 @@ def test_status_mapping():
                     (-4, B.LayoutError), (-5, B.OverflowConfigError), (-100, B.BitLutError)):
         with pytest.raises(cls):
             raise_for_status(rc, "x")
+
+
+def test_graph_executor_independence_plan():
+    """bitlut_pipeline_plan_flags (no GPU needed): lookups that read a table
+    already complete when they start skip the start-of-kernel wait."""
+    import ctypes
+    from paper_2407_00088_b200.pipeline import PipeOpSpec, _bind
+    T, LK = 0, 1
+
+    def op(t, deps=(), fast=False):
+        s = PipeOpSpec()
+        s.type = t
+        s.dep[:] = list(deps) + [-1] * (3 - len(deps))
+        s.flags = N.FLAG_FAST_EPILOGUE if fast else 0
+        return s
+
+    # layer: T0 q k v | T4(q,k,v) o | T6(o) gate up | T9(gate,up) down | T11(down) q'
+    ops = [op(T), op(LK, [0]), op(LK, [0]), op(LK, [0]), op(T, [1, 2, 3]), op(LK, [4]),
+           op(T, [5]), op(LK, [6], fast=True), op(LK, [6], fast=True), op(T, [7, 8]), op(LK, [9]),
+           op(T, [10]), op(LK, [11]), op(LK, []), op(LK, [1])]
+    arr = (PipeOpSpec * len(ops))(*ops)
+    fl = (ctypes.c_int * len(ops))()
+    assert _bind().bitlut_pipeline_plan_flags(arr, len(ops), fl) == 0
+    P, I, F = N.FLAG_PDL, N.FLAG_INDEPENDENT, N.FLAG_FAST_EPILOGUE
+    assert list(fl) == [P, P, P | I, P | I, P, P, P, P | F, P | I | F, P, P, P, P,
+                        P,          # no deps: tables made outside the list -> waits
+                        P | I]      # dep 1 < last dependent lookup (13)
+    bad = (PipeOpSpec * 2)(op(T), op(LK, [1]))
+    assert _bind().bitlut_pipeline_plan_flags(bad, 2, fl) == -1

@@ -24,8 +24,8 @@ ap.add_argument("--fast", type=int, default=0)
 args = ap.parse_args()
 dev = torch.device("cuda", 0)
 layers = bench.build_layers(args.layers, 2, 64, 0, 1, dev)
-acts = bench.make_acts(args.layers, dev)
-pl, _ = bench.build_pipeline(layers, acts, fast=bool(args.fast))
+acts, _ = bench.make_acts(args.layers, dev)
+pl, _, _ = bench.build_pipeline(layers, acts, fast=bool(args.fast))
 # per-op unit counts (mirror of bitlut_pipeline_encode)
 units = []
 for s in pl.specs:
