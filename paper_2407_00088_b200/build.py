@@ -15,7 +15,7 @@ import sys
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-SOURCES = ["weight_prep.cu", "lut.cu", "gemv.cu", "pipeline.cu"]
+SOURCES = ["weight_prep.cu", "lut.cu", "gemv.cu", "gemv_b1.cu", "pipeline.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
 
@@ -42,18 +42,35 @@ def needs_build() -> bool:
 
 
 def build_lib(force: bool = False, verbose: bool = False) -> str:
+    """nvcc each translation unit (in parallel), then link the shared library."""
+    from concurrent.futures import ThreadPoolExecutor
     out = lib_path()
     if not force and not needs_build():
         return out
     os.makedirs(os.path.dirname(out), exist_ok=True)
+    objdir = os.path.join(os.path.dirname(out), "obj")
+    os.makedirs(objdir, exist_ok=True)
+    flags = [f for f in NVCC_FLAGS if f != "-shared"]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        cmd = [nvcc(), *flags, "-c", "-o", obj, os.path.join(PKG, "csrc", src)]
+        return obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    for obj, res in results:
+        if res.returncode != 0:
+            sys.stderr.write(res.stdout + res.stderr)
+            raise RuntimeError(f"nvcc failed compiling {os.path.basename(obj)}")
+        if verbose:
+            sys.stderr.write(res.stderr)
     tmp = out + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", tmp] + [os.path.join(PKG, "csrc", s) for s in SOURCES]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    res = subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp]
+                         + [o for o, _ in results], capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libbitlut_b200.so")
-    if verbose:
-        sys.stderr.write(res.stderr)
+        raise RuntimeError("nvcc failed linking libbitlut_b200.so")
     os.replace(tmp, out)
     return out
 

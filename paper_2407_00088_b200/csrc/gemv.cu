@@ -209,7 +209,19 @@ int dispatch_q8(const GemvArgs& a, int n, cudaStream_t s, bool pdl, int mode) {
   return BITLUT_EPARAM;
 }
 
+bool b1_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("BITLUT_B1");             // diagnostic: 0 disables the batch-1 kernel
+    on = e ? atoi(e) != 0 : 1;
+  }
+  return on != 0;
+}
+
 }  // namespace
+
+// gemv_b1.cu: persistent batch-1 kernel (fast epilogue, 32-stream tiles)
+int bl_gemv_b1_launch(const blk::GemvArgs& g, int scale_dtype, cudaStream_t s, bool pdl);
 
 extern "C" int bitlut_mpgemm_traced(const uint8_t* wgpu, int m, int k, int bits, int group_size,
                                     const void* wscales, const void* zeros, int scale_dtype,
@@ -240,6 +252,10 @@ extern "C" int bitlut_mpgemm_traced(const uint8_t* wgpu, int m, int k, int bits,
     int r = 32;
     while (r > 1 && (int64_t)L.n_tiles * ((n + r - 1) / r) < 4 * 148) r >>= 1;
     a.rows_per_cta = r;
+  }
+  if (mode == BITLUT_TABLE_Q8 && a.fast && !partials && !trace && n == 1 && L.n_sg == 1 && b1_enabled()) {
+    rc = bl_gemv_b1_launch(a, scale_dtype, (cudaStream_t)stream, pdl);
+    if (rc != BITLUT_ELAYOUT) return rc;              // else: shape exceeds its smem plan
   }
   return scale_dtype == BITLUT_DT_F16 ? dispatch_q8<__half>(a, n, (cudaStream_t)stream, pdl, mode)
                                       : dispatch_q8<float>(a, n, (cudaStream_t)stream, pdl, mode);

@@ -1,0 +1,411 @@
+// Batch-1 lookup kernel for the decode path (fast epilogue, int8 tables,
+// 1/2/4-bit weights): persistent CTAs that walk tiles with a 2-stage TMA
+// pipeline, so the per-CTA setup (barriers, tables, table scales / row sums)
+// is paid once and tile i+1's weights stream in while tile i is looked up.
+//
+// Per tile (tile_ch channels x bits planes = 32 streams, all k-groups):
+//   lookups   the A/B prmt lookup of gemv.cu with the bit planes merged by
+//             the dp2a multipliers instead of packed as independent streams:
+//               W2  pair (c, p0 p1)           mult (1, 2)     -> S_c
+//               W4  pairs (c, p0 p1)(c, p2 p3) mult (1,2),(4,8) -> S_c
+//               W1  pair (c, c+1)             mult (1, -32768) (packed, split later)
+//             so each accumulator already holds the exact integer
+//             S = sum_p 2^p P_p of one channel (|S| < 2^24: exact in f32);
+//   epilogue  y_c += ws_cg * (ts_g * S - rs_g [+ 2 (2^(b-1) - z) rs_g]) per
+//             (channel, group) in registers, fixed-order shuffle + smem
+//             reduction, out_c = 0.5 * sum.  Deterministic; the int32 sums
+//             are exact, only the float combination order differs from the
+//             reference (<= 1e-5 relative, tests/test_gpu_parity.py).
+// The reference-order (bit-exact float) epilogue stays in gemv.cu.
+#include "gemv_core.cuh"
+
+#include <cstdlib>
+
+namespace {
+
+using namespace blk;
+
+constexpr int kMaxStages = 2;
+
+struct B1Args {
+  GemvArgs g;
+  int rounds;                 // unit rounds per tile (units = KG / R)
+  int stages;                 // weight pipeline depth: 1 (one tile per CTA) or 2
+  int tab_smem;               // tables staged in smem (rounds > 1), else registers
+  uint32_t stage_bytes;       // per pipeline stage: weights | scales | zeros
+  uint32_t w_bytes, s_off, s_bytes, z_off;
+  uint32_t tab_off, ts_off, rs_off, y_off, bar_off;
+};
+
+struct B1Plan {
+  uint32_t stage_bytes, w_bytes, s_off, s_bytes, z_off, tab_off, ts_off, rs_off, y_off, bar_off, total;
+};
+
+__host__ __device__ inline uint32_t al16(size_t x) { return (uint32_t)((x + 15) & ~(size_t)15); }
+
+template <typename ST>
+B1Plan b1_plan(const bl::LayoutV2& L, bool zeros, bool tab_smem, int T, int stages) {
+  B1Plan s;
+  s.w_bytes = (uint32_t)((size_t)L.KG * 16);
+  s.s_bytes = (uint32_t)((size_t)L.tile_ch * L.NQ * sizeof(ST));
+  s.s_off = al16(s.w_bytes);
+  s.z_off = s.s_off + al16(s.s_bytes);
+  s.stage_bytes = s.z_off + (zeros ? al16(s.s_bytes) : 0);
+  s.stage_bytes = (s.stage_bytes + 127) & ~127u;
+  s.tab_off = stages * s.stage_bytes;
+  s.ts_off = s.tab_off + (tab_smem ? al16((size_t)L.KG * 8) : 0);
+  s.rs_off = s.ts_off + al16((size_t)L.NQ * 4);
+  s.y_off = s.rs_off + al16((size_t)L.NQ * 4);
+  s.bar_off = s.y_off + al16((size_t)2 * (T / 32) * L.tile_ch * 4);
+  s.total = s.bar_off + 8 * (kMaxStages + 1);
+  return s;
+}
+
+// Lookup of one k-group for 32 streams with plane-merging multipliers.
+template <int BITS, int NACC>
+__device__ __forceinline__ void lookup_kg_merged(const uint4 w, uint32_t a0, uint32_t a1, int (&acc)[NACC]) {
+  const uint32_t b0 = ~a0, b1 = ~a1;
+  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const uint32_t x = ws[q];
+    const uint32_t xx = x ^ 0x88888888u;
+    const uint32_t A0 = bl::prmt(a0, a1, x), B0 = bl::prmt(b0, b1, xx);
+    const uint32_t A1 = bl::prmt(a0, a1, x >> 16), B1 = bl::prmt(b0, b1, xx >> 16);
+    if constexpr (BITS == 4) {
+      // bytes 0..3 of A0/B0 = planes 0..3 of channel 2q; of A1/B1: channel 2q+1
+      constexpr uint32_t M01 = 0x00020001u, M23 = 0x00080004u;
+      acc[2 * q] = bl::dp2a_lo(M01, A0, acc[2 * q]);
+      acc[2 * q] = bl::dp2a_lo(M01, B0, acc[2 * q]);
+      acc[2 * q] = bl::dp2a_hi(M23, A0, acc[2 * q]);
+      acc[2 * q] = bl::dp2a_hi(M23, B0, acc[2 * q]);
+      acc[2 * q + 1] = bl::dp2a_lo(M01, A1, acc[2 * q + 1]);
+      acc[2 * q + 1] = bl::dp2a_lo(M01, B1, acc[2 * q + 1]);
+      acc[2 * q + 1] = bl::dp2a_hi(M23, A1, acc[2 * q + 1]);
+      acc[2 * q + 1] = bl::dp2a_hi(M23, B1, acc[2 * q + 1]);
+    } else {
+      // pair i = streams (2i, 2i+1): W2 -> channel i planes (0, 1); W1 -> channels (2i, 2i+1)
+      constexpr uint32_t M = BITS == 2 ? 0x00020001u : kMult;
+      acc[4 * q + 0] = bl::dp2a_lo(M, A0, acc[4 * q + 0]);
+      acc[4 * q + 0] = bl::dp2a_lo(M, B0, acc[4 * q + 0]);
+      acc[4 * q + 1] = bl::dp2a_hi(M, A0, acc[4 * q + 1]);
+      acc[4 * q + 1] = bl::dp2a_hi(M, B0, acc[4 * q + 1]);
+      acc[4 * q + 2] = bl::dp2a_lo(M, A1, acc[4 * q + 2]);
+      acc[4 * q + 2] = bl::dp2a_lo(M, B1, acc[4 * q + 2]);
+      acc[4 * q + 3] = bl::dp2a_hi(M, A1, acc[4 * q + 3]);
+      acc[4 * q + 3] = bl::dp2a_hi(M, B1, acc[4 * q + 3]);
+    }
+  }
+}
+
+// Reduce NV values across the lanes that differ in lane bits [O0, O1):
+// halving exchanges while more than one value is left (each lane keeps a
+// disjoint half, no redundant adds), plain butterfly adds afterwards.
+// Returns the index of the lane's first remaining value; the count is
+// reduced_count<NV, O0, O1>().
+template <int NV, int O0, int O1>
+__host__ __device__ constexpr int reduced_count() {
+  int n = NV;
+  for (int o = O0; o < O1; o <<= 1)
+    if (n > 1) n >>= 1;
+  return n;
+}
+
+template <int NV, int O0, int O1, typename T>
+__device__ __forceinline__ int reduce_lanes(T (&v)[NV], int lane) {
+  int base = 0;
+#pragma unroll
+  for (int o = O0, n = NV; o < O1; o <<= 1) {
+    if (n > 1) {
+      n >>= 1;
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int i = 0; i < NV / 2; i++) {
+        if (i < n) {
+          const T send = up ? v[i] : v[i + n];
+          const T keep = up ? v[i + n] : v[i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      if (up) base += n;
+    } else {
+      v[0] = v[0] + __shfl_xor_sync(0xffffffffu, v[0], o);
+    }
+  }
+  return base;
+}
+
+template <typename ST>
+__device__ __forceinline__ void issue_stage(const B1Args& a, int tile, uint8_t* sb, uint64_t* bar, uint64_t pol) {
+  const GemvArgs& p = a.g;
+  const bl::LayoutV2& L = p.L;
+  const bool zeros = p.zeros != nullptr;
+  mbar_expect_tx(bar, a.w_bytes + a.s_bytes * (zeros ? 2u : 1u));
+  const uint8_t* src = p.w + L.sg_row_base(tile, 0);
+  for (uint32_t off = 0; off < a.w_bytes; off += 32768u) {
+    const uint32_t nb = a.w_bytes - off < 32768u ? a.w_bytes - off : 32768u;
+    bulk_g2s(sb + off, src + off, nb, bar, pol);
+  }
+  const int64_t e0 = (int64_t)tile * L.tile_ch * L.NQ;
+  bulk_g2s(sb + a.s_off, reinterpret_cast<const ST*>(p.wscales) + e0, a.s_bytes, bar, pol);
+  if (zeros) bulk_g2s(sb + a.z_off, reinterpret_cast<const ST*>(p.zeros) + e0, a.s_bytes, bar, pol);
+}
+
+template <int R, int LG, int BITS, typename ST>
+__global__ void __launch_bounds__(256) gemv_b1_kernel(const __grid_constant__ B1Args a) {
+  const GemvArgs& p = a.g;
+  const bl::LayoutV2& L = p.L;
+  constexpr int TCH = 32 / BITS;                        // channels per tile
+  constexpr int NACC = BITS == 4 ? 8 : 16;              // int accumulators per lane
+  constexpr int NV = reduced_count<NACC, 1, LG>();      // after the in-group reduction
+  constexpr int NCH = BITS == 1 ? 2 * NV : NV;          // float channel values per lane
+  constexpr int NF = reduced_count<NCH, LG, 32>();      // after the cross-group reduction
+  constexpr int KGF = BITS == 4 ? 15 : (BITS == 2 ? 3 : -32767);  // per-kg offset of the A/B trick
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int T = blockDim.x, NW = T >> 5;
+  const int NQ = L.NQ, KG = L.KG, U = L.U;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + a.bar_off);
+  float* tsm = reinterpret_cast<float*>(smem + a.ts_off);
+  float* rsm = reinterpret_cast<float*>(smem + a.rs_off);
+  float* ysm = reinterpret_cast<float*>(smem + a.y_off);
+  const uint8_t* tab = smem + a.tab_off;
+  const int ntl = L.n_tiles, step = gridDim.x;
+  const int S = a.stages;
+
+  // ---- 1. weights + scales of the first tiles: independent of the predecessor ----
+  if (tid == 0) {
+    for (int s = 0; s <= kMaxStages; s++) mbar_init(bar + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint64_t pol = policy_evict_first();
+    for (int s = 0; s < S; s++) {
+      const int t = blockIdx.x + s * step;
+      if (t < ntl) issue_stage<ST>(a, t, smem + s * a.stage_bytes, bar + s, pol);
+    }
+  }
+  // ---- 2. tables / table scales / row sums come from the previous kernel ----
+  if (!p.independent) bl::pdl_wait();
+  bl::pdl_launch_dependents();
+  if (a.tab_smem && tid == 0) {
+    const uint32_t tb = (uint32_t)KG * 8;
+    mbar_expect_tx(bar + kMaxStages, tb);
+    for (uint32_t off = 0; off < tb; off += 32768u) {
+      const uint32_t nb = tb - off < 32768u ? tb - off : 32768u;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(smem + a.tab_off + off)),
+          "l"(p.qtab + off), "r"(nb), "r"(smem_u32(bar + kMaxStages))
+          : "memory");
+    }
+  }
+  uint4 tq0[R / 2];
+  if (!a.tab_smem && tid < U) {
+    const int ub = tid >> 5, l = tid & 31;
+    const int nu_b = min(32, U - 32 * ub);
+    const uint8_t* tb = p.qtab + (int64_t)ub * (32 * R * 8) + l * 16;
+#pragma unroll
+    for (int jp = 0; jp < R / 2; jp++) tq0[jp] = bl::ld_cg_128(tb + jp * nu_b * 16);
+  }
+  for (int i = tid; i < NQ; i += T) {
+    tsm[i] = bl::ld_cg_f32(p.tscales + i);
+    rsm[i] = bl::ld_cg_f32(p.rowsums + i);
+  }
+  __syncthreads();                                      // barriers initialised, tsm / rsm ready
+  if (a.tab_smem) mbar_wait(bar + kMaxStages, 0);
+
+  const bool has_zeros = p.zeros != nullptr;
+  const float h2 = (float)(2 << (BITS - 1));
+  int it = 0;
+  for (int tile = blockIdx.x; tile < ntl; tile += step, it++) {
+    const int stage = S == 1 ? 0 : (it & 1);
+    uint8_t* sb = smem + stage * a.stage_bytes;
+    mbar_wait(bar + stage, (S == 1 ? it : it >> 1) & 1);
+    const ST* sraw = reinterpret_cast<const ST*>(sb + a.s_off);
+    const ST* zraw = reinterpret_cast<const ST*>(sb + a.z_off);
+
+    float y[NCH];
+#pragma unroll
+    for (int j = 0; j < NCH; j++) y[j] = 0.f;
+    int ch0 = 0;
+    for (int rd = 0; rd < a.rounds; rd++) {
+      const int u = tid + rd * T;
+      const bool live = u < U;
+      int acc[NACC];
+#pragma unroll
+      for (int i = 0; i < NACC; i++) acc[i] = BITS == 1 ? 0 : KGF * R;   // undo A/B's -1 per lookup
+      if (live) {
+        const int ub = u >> 5, l = u & 31;
+        const int nu_b = min(32, U - 32 * ub);
+        const int stride = nu_b == 32 ? 512 : nu_b * 16;
+        uint4 tq[R / 2];
+        if (a.tab_smem) {
+          const uint8_t* tb = tab + ub * (32 * R * 8) + l * 16;
+#pragma unroll
+          for (int jp = 0; jp < R / 2; jp++) tq[jp] = *reinterpret_cast<const uint4*>(tb + jp * stride);
+        } else {
+#pragma unroll
+          for (int jp = 0; jp < R / 2; jp++) tq[jp] = tq0[jp];
+        }
+        const uint8_t* wsrc = sb + ub * (32 * R * 16) + l * 16;
+#pragma unroll
+        for (int j = 0; j < R; j++) {
+          const uint4 wr = *reinterpret_cast<const uint4*>(wsrc + j * stride);
+          lookup_kg_merged<BITS, NACC>(wr, (j & 1) ? tq[j >> 1].z : tq[j >> 1].x,
+                                       (j & 1) ? tq[j >> 1].w : tq[j >> 1].y, acc);
+        }
+      }
+      // sum the LG lanes of each quantization group (exact int32)
+      const int base = reduce_lanes<NACC, 1, LG>(acc, lane);
+      ch0 = BITS == 1 ? 2 * base : base;
+      if (live) {
+        const int g = u / LG;
+        const float ts = tsm[g], rs = rsm[g];
+        int S[NCH];
+        if constexpr (BITS == 1) {
+#pragma unroll
+          for (int i = 0; i < NV; i++) {
+            const int v = acc[i] + KGF * R * LG;
+            const int pe = (v << 17) >> 17;
+            S[2 * i] = pe;
+            S[2 * i + 1] = (pe - v) >> 15;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < NV; i++) S[i] = acc[i];
+        }
+#pragma unroll
+        for (int j = 0; j < NCH; j++) {
+          const int c = ch0 + j;
+          float t = fmaf(ts, (float)S[j], -rs);
+          if (has_zeros) t = fmaf(fmaf(-2.f, bl::to_f32(zraw[c * NQ + g]), h2), rs, t);
+          y[j] = fmaf(bl::to_f32(sraw[c * NQ + g]), t, y[j]);
+        }
+      }
+    }
+    // ---- cross-group reduction: lanes of this warp, then the warps ----
+    const int fb = reduce_lanes<NCH, LG, 32>(y, lane);
+    float* yb = ysm + (it & 1) * NW * TCH + warp * TCH;
+#pragma unroll
+    for (int j = 0; j < NF; j++) yb[ch0 + fb + j] = y[j];   // lanes holding a duplicate write the same value
+    __syncthreads();                                    // stage consumed, ysm complete
+    if (tid == 0) {
+      const int t = tile + S * step;
+      if (t < ntl) issue_stage<ST>(a, t, sb, bar + stage, policy_evict_first());
+    }
+    if (tid < TCH) {
+      const float* yr = ysm + (it & 1) * NW * TCH + tid;
+      float s = 0.f;
+      for (int w = 0; w < NW; w++) s += yr[w * TCH];
+      p.out[(int64_t)tile * TCH + tid] = 0.5f * s;
+    }
+  }
+  if (p.independent) bl::pdl_wait();                    // keep stream completion order
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int R, int LG, int BITS, typename ST>
+int launch_b1(const GemvArgs& g, cudaStream_t stream, bool pdl) {
+  const bl::LayoutV2& L = g.L;
+  const int T = L.U > 128 ? 256 : 128;
+  B1Args a;
+  a.g = g;
+  a.rounds = (L.U + T - 1) / T;
+  a.tab_smem = a.rounds > 1;
+  auto kern = gemv_b1_kernel<R, LG, BITS, ST>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared) != cudaSuccess)
+      return BITLUT_EINTERNAL;
+    configured = true;
+  }
+  // Tiles per CTA: a dependent launch wants the most CTAs (shortest path
+  // once its inputs are ready); an INDEPENDENT one overlaps its predecessor
+  // and gains from amortising the CTA setup over two tiles.
+  static int tpc_env = -1;
+  if (tpc_env < 0) {
+    const char* e = getenv("BITLUT_B1_TILES_PER_CTA");   // diagnostic override
+    tpc_env = e ? atoi(e) : 0;
+  }
+  const int tiles_per_cta = tpc_env > 0 ? tpc_env : (g.independent ? 2 : 1);
+  // one stage when every CTA gets a single tile, else double-buffer
+  B1Plan s = b1_plan<ST>(L, g.zeros != nullptr, a.tab_smem, T, 1);
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, s.total) != cudaSuccess || per_sm < 1)
+    return BITLUT_ELAYOUT;
+  const int want = (L.n_tiles + tiles_per_cta - 1) / tiles_per_cta;
+  a.stages = 1;
+  if (want < L.n_tiles || sm_count() * per_sm < L.n_tiles) {
+    const B1Plan s2 = b1_plan<ST>(L, g.zeros != nullptr, a.tab_smem, T, 2);
+    int per_sm2 = 0;
+    if (s2.total <= 227 * 1024 &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, kern, T, s2.total) == cudaSuccess && per_sm2 >= 1) {
+      s = s2; per_sm = per_sm2; a.stages = 2;
+    }
+  }
+  if (s.total > 227 * 1024) return BITLUT_ELAYOUT;
+  a.stage_bytes = s.stage_bytes; a.w_bytes = s.w_bytes; a.s_off = s.s_off; a.s_bytes = s.s_bytes;
+  a.z_off = s.z_off; a.tab_off = s.tab_off; a.ts_off = s.ts_off; a.rs_off = s.rs_off;
+  a.y_off = s.y_off; a.bar_off = s.bar_off;
+  int grid = sm_count() * per_sm;
+  if (grid > want) grid = want;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(T);
+  cfg.dynamicSmemBytes = s.total;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a) == cudaSuccess ? BITLUT_OK : BITLUT_EINTERNAL;
+}
+
+template <int R, int LG, typename ST>
+int launch_b1_bits(const GemvArgs& g, cudaStream_t s, bool pdl) {
+  switch (g.L.bits) {
+    case 1: return launch_b1<R, LG, 1, ST>(g, s, pdl);
+    case 2: return launch_b1<R, LG, 2, ST>(g, s, pdl);
+    case 4: return launch_b1<R, LG, 4, ST>(g, s, pdl);
+  }
+  return BITLUT_EPARAM;
+}
+
+template <typename ST>
+int dispatch_b1(const GemvArgs& g, cudaStream_t s, bool pdl) {
+  const int R = g.L.R, LG = g.L.Lg;
+  if (R == 8) {
+    switch (LG) {
+      case 1: return launch_b1_bits<8, 1, ST>(g, s, pdl);
+      case 2: return launch_b1_bits<8, 2, ST>(g, s, pdl);
+      case 4: return launch_b1_bits<8, 4, ST>(g, s, pdl);
+      case 8: return launch_b1_bits<8, 8, ST>(g, s, pdl);
+      case 16: return launch_b1_bits<8, 16, ST>(g, s, pdl);
+    }
+  } else if (R == 4 && LG == 1) {
+    return launch_b1_bits<4, 1, ST>(g, s, pdl);
+  }
+  return BITLUT_EPARAM;
+}
+
+}  // namespace
+
+// Internal entry used by bitlut_mpgemm_traced (gemv.cu) for batch-1 fast
+// calls: returns BITLUT_ELAYOUT when the shape does not fit the kernel's
+// shared-memory plan (the caller then uses the per-tile kernel).
+int bl_gemv_b1_launch(const GemvArgs& g, int scale_dtype, cudaStream_t s, bool pdl) {
+  if (g.L.n_sg != 1) return BITLUT_ELAYOUT;
+  return scale_dtype == BITLUT_DT_F16 ? dispatch_b1<__half>(g, s, pdl) : dispatch_b1<float>(g, s, pdl);
+}
