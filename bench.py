@@ -179,12 +179,14 @@ def step_fn(layers, acts, world, group, fast=False):
     return res
 
 
-def build_pipeline(layers, acts, fast=False, executor="persistent"):
-    """The step as a pipeline.Pipeline op list with the decode chain's real
-    dependencies: a layer's qkv table build waits for the previous layer's
-    down GEMV, o's for q,k,v, gate/up's for o, down's for gate,up; every GEMV
-    waits for its own table build only.  All outputs are views of one f32
-    arena (one D2H per step).  Returns (pipeline, outputs, out_arena)."""
+def build_pipeline(layers, acts, fast=False, executor="persistent", chain=True):
+    """The step as a pipeline.Pipeline op list.  chain=True: the decode
+    chain's dependencies -- a layer's qkv table build waits for the previous
+    layer's down GEMV, o's for q,k,v, gate/up's for o, down's for gate,up.
+    chain=False: the layer set as independent mpGEMV calls (activation rows
+    are inputs; BASELINE configs[1]).  Either way every GEMV waits for its
+    own table build.  All outputs are views of one f32 arena (one D2H per
+    step).  Returns (pipeline, outputs, out_arena)."""
     import torch
     from paper_2407_00088_b200.pipeline import Pipeline
     pl = Pipeline(executor=executor)
@@ -192,31 +194,54 @@ def build_pipeline(layers, acts, fast=False, executor="persistent"):
     out_arena = torch.empty((len(layers) * per_layer,), dtype=torch.float32,
                             device=layers[0]["q"].gpu.device)
     prev, outs, off = [], [], 0
-    for L, A in zip(layers, acts):
-        for gname, k, names in LUT_GROUPS:
-            t = pl.tables(A[gname], L[names[0]].group_size, deps=prev)
-            ys = []
-            for nm in names:
-                m = L[nm].m
-                ys.append(pl.lookup(L[nm], t, fast_epilogue=fast,
-                                    out=out_arena[off:off + m].view(1, m)))
-                off += m
-            outs += ys
-            prev = [pl.op_of(y) for y in ys]
+    if chain:
+        for L, A in zip(layers, acts):
+            for gname, k, names in LUT_GROUPS:
+                t = pl.tables(A[gname], L[names[0]].group_size, deps=prev)
+                ys = []
+                for nm in names:
+                    m = L[nm].m
+                    ys.append(pl.lookup(L[nm], t, fast_epilogue=fast,
+                                        out=out_arena[off:off + m].view(1, m)))
+                    off += m
+                outs += ys
+                prev = [pl.op_of(y) for y in ys]
+    else:
+        # independent calls, software-pipelined by one layer: layer L+1's
+        # table builds are recorded before layer L's lookups, so every lookup
+        # but the first finds its tables complete (INDEPENDENT launches)
+        def tables_of(i):
+            return {g: pl.tables(acts[i][g], layers[i][names[0]].group_size)
+                    for g, _, names in LUT_GROUPS}
+        nxt = tables_of(0)
+        for i, L in enumerate(layers):
+            cur = nxt
+            nxt = tables_of(i + 1) if i + 1 < len(layers) else None
+            for gname, k, names in LUT_GROUPS:
+                for nm in names:
+                    m = L[nm].m
+                    outs.append(pl.lookup(L[nm], cur[gname], fast_epilogue=fast,
+                                          out=out_arena[off:off + m].view(1, m)))
+                    off += m
     pl.compile()
     return pl, outs, out_arena
 
 
-def lookups_only(layers, tabs):
-    """The step's 7*L lookups with tables prebuilt, in the step's dependency
-    structure (first GEMV after each table build dependent, the rest not)."""
+def lookups_only(layers, tabs, fast=False, chain=False):
+    """The step's 7*L lookups with tables prebuilt and the step's launch
+    flags: layer set (chain=False) -- every lookup but the first INDEPENDENT;
+    decode chain -- the first GEMV after each table build dependent."""
     from paper_2407_00088_b200 import _native as N
+    first = True
     for L, T in zip(layers, tabs):
         for gname, k, names in LUT_GROUPS:
             tables, ts, rs = T[gname]
             for j, nm in enumerate(names):
                 pw = L[nm]
-                fl = N.FLAG_PDL | (N.FLAG_INDEPENDENT if j > 0 else 0)
+                ind = (j > 0) if chain else not first
+                first = False
+                fl = (N.FLAG_PDL | (N.FLAG_INDEPENDENT if ind else 0)
+                      | (N.FLAG_FAST_EPILOGUE if fast else 0))
                 N.lookup(pw.gpu, pw.scales, None, tables, ts, rs, pw.m, pw.k, pw.bits,
                          pw.group_size, N.TABLE_Q8, fl, False)
 
@@ -254,6 +279,70 @@ def time_graph(g, reps, warmup, barrier=None):
 
 def packed_bytes_full(n_layers, bits):
     return n_layers * sum(bits * m * k // 8 for _, m, k in LAYER)
+
+
+SHAPES_7B = [("4096x4096", 4096, 4096), ("11008x4096", 11008, 4096), ("4096x11008", 4096, 11008)]
+L2_BYTES = 126 * 1024 * 1024
+
+
+def per_shape_table(device, stream, reps, warmup, barrier, peak, world, bits_list=(1, 2, 4), gs=64):
+    """Per-launch us and GB/s for every 7B shape at W1/W2/W4."""
+    import torch
+    import paper_2407_00088_b200 as B
+    from paper_2407_00088_b200 import _native as N
+    gen = torch.Generator(device=device)
+    gen.manual_seed(99)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=device)
+    out = {}
+    for bits in bits_list:
+        res = {}
+        for name, m, k in SHAPES_7B:
+            m_loc = m // world
+            q = torch.randint(0, 1 << bits, (m_loc, k), dtype=torch.uint8, device=device, generator=gen)
+            sc = (torch.randn((m_loc, k // gs), device=device, generator=gen).abs() * 0.02 + 1e-3).half()
+            pw = B.prepare_weights(B.QuantizedWeights(m=m_loc, k=k, bits=bits, group_size=gs, qvalues=q,
+                                                      scales=sc))
+            del q
+            nbytes = pw.packed_bytes
+            copies = max(8, -(-4 * L2_BYTES // nbytes))
+            ws = [pw.gpu] + [pw.gpu.clone() for _ in range(copies - 1)]
+            x = torch.randn((1, k), device=device, generator=gen).half()
+            tabs = N.build_lut(x, gs, N.TABLE_Q8)
+            entry = {"packed_bytes_per_gpu": nbytes, "launches_rotated": len(ws)}
+            for epi in ("fast", "exact"):
+                e = {}
+                base = N.FLAG_PDL | (N.FLAG_FAST_EPILOGUE if epi == "fast" else 0)
+                for mode, fl in (("overlapped", base | N.FLAG_INDEPENDENT), ("chained", base)):
+                    def body(fl=fl):
+                        for w in ws:
+                            N.lookup(w, pw.scales, None, *tabs, pw.m, k, bits, gs, N.TABLE_Q8, fl, False)
+                    g = capture(body, stream)
+                    with torch.cuda.stream(stream):
+                        ms = time_graph(g, reps, warmup, barrier)
+                    del g
+                    us = ms * 1e3 / len(ws)
+                    e[mode + "_us"] = round(us, 3)
+                    e[mode + "_GBps"] = round(nbytes / (us * 1e-6) / 1e9, 1)
+                    e[mode + "_frac_of_peak"] = round(nbytes / (us * 1e-6) / 1e9 / peak, 4)
+                # one launch after an L2 flush (tables prebuilt)
+                ts_ = []
+                with torch.cuda.stream(stream):
+                    for _ in range(5):
+                        flush.fill_(1)
+                        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        e0.record(stream)
+                        N.lookup(ws[0], pw.scales, None, *tabs, pw.m, k, bits, gs, N.TABLE_Q8, base, False)
+                        e1.record(stream)
+                        torch.cuda.synchronize()
+                        ts_.append(e0.elapsed_time(e1) * 1e3)
+                e["single_launch_l2_flushed_us"] = round(float(np.median(ts_)), 3)
+                entry[epi] = e
+            res[name] = entry
+            del ws, pw
+        out[f"W{bits}"] = res
+    del flush
+    torch.cuda.empty_cache()
+    return out
 
 
 # ----------------------------------------------------------------- CPU baseline
@@ -309,6 +398,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-shapes", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     bits, gs = 2, 64
@@ -342,16 +432,20 @@ def main():
     acts, act_arena = make_acts(args.layers, device)
     stream = torch.cuda.Stream(device)
 
-    # ---- the step through the package's op-list executors (pipeline.py):
-    #      "graph" = per-op kernels chained with PDL in one CUDA graph (exact
-    #      and fast epilogue), "persistent" = one cooperative launch.  Under
-    #      torchrun the step adds each GEMV's all-gather (step_fn, graph).
-    #      `value` reports the fastest; every executor is in the JSON line. ----
+    # ---- the step through the package's op-list executors (pipeline.py).
+    #      layer_set: the 7 GEMVs per layer as independent mpGEMV calls (the
+    #      BASELINE metric); decode_chain: each table build also waits for the
+    #      previous GEMVs, as in a real decode.  "graph" = per-op kernels
+    #      chained with PDL in one CUDA graph; "persistent" = one cooperative
+    #      launch.  fast = exact int32 sums + fixed-order parallel fp32
+    #      epilogue (<= 1e-5 of the reference); exact = the reference's fp32
+    #      order, bitwise.  `value` = the fastest layer_set executor. ----
     total_bytes = packed_bytes_full(args.layers, bits)
     n_ops = args.layers * (len(LUT_GROUPS) + len(LAYER))
     executors = {}
 
-    def time_runs(run):
+    def time_runs(run, steps=None):
+        steps = steps or args.steps
         with torch.cuda.stream(stream):
             for _ in range(args.warmup):
                 run()
@@ -360,25 +454,28 @@ def main():
                 barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            for _ in range(args.steps):
+            for _ in range(steps):
                 run()
             e1.record(stream)
             torch.cuda.synchronize()
-        return e0.elapsed_time(e1) / args.steps
+        return e0.elapsed_time(e1) / steps
 
     pipes = {}
     with ClockSampler(local) as clk:
         if world == 1:
-            for name, ex, fast in (("graph_exact", "graph", False), ("graph_fast", "graph", True),
-                                   ("persistent_fast", "persistent", True)):
-                pl, outs, out_arena = build_pipeline(layers, acts, fast=fast, executor=ex)
+            for name, ex, fast, chain in (("layer_set_graph_fast", "graph", True, False),
+                                          ("layer_set_graph_exact", "graph", False, False),
+                                          ("decode_chain_graph_fast", "graph", True, True),
+                                          ("decode_chain_graph_exact", "graph", False, True),
+                                          ("decode_chain_persistent_fast", "persistent", True, True)):
+                pl, outs, out_arena = build_pipeline(layers, acts, fast=fast, executor=ex, chain=chain)
                 pipes[name] = (pl, out_arena)
                 executors[name] = {"ms": time_runs(lambda: pl.run(stream)),
                                    "launches": n_ops if ex == "graph" else 1}
         else:
-            for fast in (False, True):
+            for fast in (True, False):
                 g_step = capture(lambda: step_fn(layers, acts, world, group, fast=fast), stream)
-                executors["graph_" + ("fast" if fast else "exact")] = {
+                executors["decode_chain_graph_" + ("fast" if fast else "exact")] = {
                     "ms": time_runs(g_step.replay), "launches": n_ops}
                 del g_step
     if world > 1:
@@ -386,65 +483,53 @@ def main():
             t = torch.tensor([v["ms"]], device=device)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             v["ms"] = float(t.item())
-    best = min(executors, key=lambda k: executors[k]["ms"])
+    cands = [k for k in executors if k.startswith("layer_set")] or list(executors)
+    best = min(cands, key=lambda k: executors[k]["ms"])
     ms_step = executors[best]["ms"]
     launches_per_step = executors[best]["launches"]
     value = total_bytes / (ms_step * 1e-3) / 1e9
     executors_out = {k: {"ms_per_step": round(v["ms"], 5),
                          "GBps": round(total_bytes / (v["ms"] * 1e-3) / 1e9, 2),
                          "launches_per_step": v["launches"]} for k, v in executors.items()}
+    best_fast = "fast" in best
 
-    # ---- lookups alone (tables prebuilt), per-op launches, step's dependency flags ----
+    # ---- the dominant kernel alone: the step's lookups (tables prebuilt,
+    #      same flags and epilogue as the headline executor) ----
     tabs = [{gname: N.build_lut(A[gname], gs, N.TABLE_Q8) for gname, _, _ in LUT_GROUPS}
             for A in acts]
     torch.cuda.synchronize()
-    g_look = capture(lambda: lookups_only(layers, tabs), stream)
+    g_look = capture(lambda: lookups_only(layers, tabs, fast=best_fast, chain=best.startswith("decode")),
+                     stream)
     with torch.cuda.stream(stream):
         ms_look = time_graph(g_look, args.steps, args.warmup, barrier)
     del g_look
     local_bytes = sum(pw.packed_bytes for L in layers for pw in L.values())
     n_look = args.layers * len(LAYER)
     peak, peak_src = load_peaks()
-    if best.startswith("persistent"):
+    if best.endswith("persistent_fast"):
         kernel_name, achieved = "pipeline_kernel (whole step, 1 launch)", value
         how = (f"1 persistent launch per step ({args.layers * 11} ops), algorithmic bytes = "
                f"sum bits*M*K/8 = {total_bytes} per launch, CUDA events over {args.steps} launches")
     else:
-        kernel_name, achieved = "gemv_kernel", local_bytes / (ms_look * 1e-3) / 1e9
-        how = (f"{n_look} lookup launches/graph (tables prebuilt, step's dependency flags, "
-               f"exact epilogue), algorithmic bytes = bits*M*K/8 per launch, CUDA events over "
-               f"{args.steps} replays")
+        kernel_name = "gemv_b1_kernel" if best_fast else "gemv_kernel"
+        achieved = local_bytes / (ms_look * 1e-3) / 1e9
+        how = (f"{n_look} lookup launches/graph replay (the step's lookups with tables prebuilt, "
+               f"same flags, {'fast' if best_fast else 'exact'} epilogue), algorithmic bytes = "
+               f"bits*M*K/8 per launch, CUDA events over {args.steps} replays")
     lookups_graph = {"ms": round(ms_look, 5), "GBps": round(local_bytes / (ms_look * 1e-3) / 1e9, 1),
                      "launches": n_look}
 
-    # ---- per-shape us per launch (each shape alone, rotating over all layers) ----
-    per_shape = {}
-    for (name, m, k) in [("4096x4096", 4096, 4096), ("11008x4096", 11008, 4096),
-                         ("4096x11008", 4096, 11008)]:
-        sel = []
-        for L, T in zip(layers, tabs):
-            for gname, _, names in LUT_GROUPS:
-                for nm in names:
-                    pw = L[nm]
-                    if (pw.m * world, pw.k) == (m, k):
-                        sel.append((pw, T[gname]))
-
-        entry = {"packed_bytes": sel[0][0].packed_bytes, "launches_rotated": len(sel)}
-        for mode, fl in (("dependent", N.FLAG_PDL), ("independent", N.FLAG_PDL | N.FLAG_INDEPENDENT)):
-            def only(sel=sel, fl=fl):
-                for pw, (tables, ts, rs) in sel:
-                    N.lookup(pw.gpu, pw.scales, None, tables, ts, rs, pw.m, pw.k, pw.bits,
-                             pw.group_size, N.TABLE_Q8, fl, False)
-            g_s = capture(only, stream)
-            with torch.cuda.stream(stream):
-                ms = time_graph(g_s, max(5, args.steps // 2), args.warmup, barrier)
-            us = ms * 1e3 / len(sel)
-            nbytes = entry["packed_bytes"]
-            entry[mode] = {"us_per_launch": round(us, 3),
-                           "GBps": round(nbytes / (us * 1e-6) / 1e9, 1),
-                           "frac_of_peak": round(nbytes / (us * 1e-6) / 1e9 / peak, 4)}
-        per_shape[name] = entry
-        del g_s
+    # ---- per-shape mpGEMV: graph of R launches over rotating
+    #      weight copies >= 4x L2, tables prebuilt; "overlapped" = independent
+    #      launches (PDL lets launch i+1 start while i drains), "chained" =
+    #      each launch waits for the previous one; plus one launch after an
+    #      L2 flush.  W1 / W2 / W4, fast and exact epilogues. ----
+    per_shape = None
+    if not args.no_shapes:
+        with ClockSampler(local) as clk_shapes:
+            per_shape = per_shape_table(device, stream, max(5, args.steps // 4), args.warmup, barrier,
+                                        peak, world)
+        per_shape["clocks"] = clk_shapes.summary()
 
     # ---- e2e: the same step through the public API from HOST buffers: one
     #      H2D of the step's activation rows (pinned), the op list, one D2H of
@@ -520,7 +605,7 @@ def main():
             "executor": best,
             "executors": executors_out,
             "lookups_only_graph": lookups_graph,
-            "per_shape_w2": per_shape,
+            "per_shape": per_shape,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "e2e_per_call_api": per_call,

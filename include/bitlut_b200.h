@@ -157,6 +157,20 @@ int bitlut_mpgemm(const uint8_t* wgpu, int m, int k, int bits, int group_size,
                   int mode, int n, float* out, int32_t* partials, int flags,
                   void* stream);
 
+/* Batch-1 table build + lookup in ONE launch (decode path, fast epilogue):
+ * a = one fp16 activation row (k).  The CTAs of each 8-CTA thread-block
+ * cluster build the int8 tables of disjoint quantization-group slices --
+ * bitwise the tables of bitlut_build_lut -- and broadcast them through
+ * distributed shared memory, then look up their tiles (gemv_b1.cu).
+ * flags must include BITLUT_FLAG_FAST_EPILOGUE; BITLUT_FLAG_INDEPENDENT
+ * means `a` was complete before the previous kernel in the stream started.
+ * Returns BITLUT_ELAYOUT when the call does not fit this kernel (3-bit
+ * weights, fp32 activations, shared-memory plan) -- use bitlut_build_lut +
+ * bitlut_mpgemm instead. */
+int bitlut_mpgemv_fused(const void* a, int a_dtype, const uint8_t* wgpu, int m, int k, int bits,
+                        int group_size, const void* wscales, const void* zeros, int scale_dtype,
+                        float* out, int flags, void* stream);
+
 /* bitlut_mpgemm plus a timeline: `trace` (device, (n * tiles) x 8 u64) gets
  * per-CTA %globaltimer stamps [start, loads issued, after griddepcontrol.wait,
  * tables staged, lookups done, epilogue products done, end] and %smid in
@@ -190,7 +204,8 @@ typedef struct {
   int scale_dtype;
   int m, bits;
   float* out;               /* LOOKUP: (n, m) f32 */
-  int flags;                /* LOOKUP: BITLUT_FLAG_FAST_EPILOGUE or 0 */
+  int flags;                /* LOOKUP: BITLUT_FLAG_FAST_EPILOGUE or 0; TABLES: BITLUT_FLAG_FUSED_TABLES
+                               = may be folded into its consumers (bitlut_mpgemv_fused) */
 } bitlut_pipe_op;
 
 /* Bytes of the encoded op table for n_ops ops. */
@@ -212,8 +227,14 @@ int bitlut_pipeline_launch_traced(const void* table_host, const void* table_dev,
  * bitlut_build_lut / bitlut_mpgemm kernels (mode Q8) chained with
  * programmatic dependent launch, for capture into a CUDA graph.  Lookups
  * whose deps are already complete when they start are launched with
- * BITLUT_FLAG_INDEPENDENT (see pipeline.cu for the rule);
- * bitlut_pipeline_plan_flags writes the per-op launch flags it uses. */
+ * BITLUT_FLAG_INDEPENDENT; batch-1 fp16 table ops marked
+ * BITLUT_FLAG_FUSED_TABLES whose consumers are all fast-epilogue 32-stream
+ * lookups are folded into them (each consumer runs
+ * as bitlut_mpgemv_fused).  bitlut_pipeline_plan_flags writes the per-op
+ * plan: launch flags, BITLUT_PLAN_SKIP, BITLUT_FLAG_FUSED_TABLES (see
+ * pipeline.cu for the rules). */
+#define BITLUT_PLAN_SKIP (-1)          /* plan: table op folded into its consumers */
+#define BITLUT_FLAG_FUSED_TABLES 8     /* plan: lookup launched as bitlut_mpgemv_fused */
 int bitlut_pipeline_plan_flags(const bitlut_pipe_op* specs, int n_ops, int* flags_out);
 int bitlut_pipeline_launch_ops(const bitlut_pipe_op* specs, int n_ops, void* stream);
 

@@ -26,6 +26,7 @@ TABLE_Q8, TABLE_F16 = 0, 1
 FLAG_PDL = 1
 FLAG_INDEPENDENT = 2
 FLAG_FAST_EPILOGUE = 4
+FLAG_FUSED_TABLES = 8       # table op may fold into its consumers (graph executor)
 
 _vp, _i = ctypes.c_void_p, ctypes.c_int
 
@@ -45,6 +46,7 @@ _SIGS = {
     "bitlut_mpgemm_traced": [_vp, _i, _i, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _i, _i, _vp, _vp, _i,
                              _vp, _vp],
     "bitlut_mpgemm_launches": [_i, _i, _i, _i, _i, _i],
+    "bitlut_mpgemv_fused": [_vp, _i, _vp, _i, _i, _i, _i, _vp, _vp, _i, _vp, _i, _vp],
 }
 
 
@@ -161,6 +163,27 @@ def lookup(wgpu: torch.Tensor, wscales: torch.Tensor, zeros: Optional[torch.Tens
                              stream_of(wgpu))
     raise_for_status(rc, "bitlut_mpgemm")
     return out, partials
+
+
+@torch.library.custom_op("bitlut_b200::mpgemv_fused", mutates_args=())
+def mpgemv_fused(a: torch.Tensor, wgpu: torch.Tensor, wscales: torch.Tensor,
+                 zeros: Optional[torch.Tensor], m: int, k: int, bits: int, group_size: int,
+                 flags: int) -> torch.Tensor:
+    """Batch-1 table build + lookup in one launch (fast epilogue): a (1, k)
+    fp16 -> out (1, m) f32.  Raises LayoutError when the call does not fit
+    the fused kernel (callers fall back to build_lut + lookup)."""
+    require_cuda(a, "activations")
+    out = torch.empty((1, m), dtype=torch.float32, device=wgpu.device)
+    rc = lib().bitlut_mpgemv_fused(ptr(a), dtype_code(a), ptr(wgpu), m, k, bits, group_size,
+                                   ptr(wscales), ptr(zeros), dtype_code(wscales), ptr(out), flags,
+                                   stream_of(wgpu))
+    raise_for_status(rc, "bitlut_mpgemv_fused")
+    return out
+
+
+@mpgemv_fused.register_fake
+def _(a, wgpu, wscales, zeros, m, k, bits, group_size, flags):
+    return wgpu.new_empty((1, m), dtype=torch.float32)
 
 
 @lookup.register_fake

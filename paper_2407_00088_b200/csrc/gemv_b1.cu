@@ -29,6 +29,8 @@ constexpr int kMaxStages = 2;
 
 struct B1Args {
   GemvArgs g;
+  const __half* act;          // fused variant: fp16 activation row (tables built in-kernel)
+  uint32_t sa_off, red_off;   // fused: activation staging (4*T floats) + group-max scratch
   int rounds;                 // unit rounds per tile (units = KG / R)
   int stages;                 // weight pipeline depth: 1 (one tile per CTA) or 2
   int tab_smem;               // tables staged in smem (rounds > 1), else registers
@@ -38,13 +40,14 @@ struct B1Args {
 };
 
 struct B1Plan {
-  uint32_t stage_bytes, w_bytes, s_off, s_bytes, z_off, tab_off, ts_off, rs_off, y_off, bar_off, total;
+  uint32_t stage_bytes, w_bytes, s_off, s_bytes, z_off, tab_off, ts_off, rs_off, y_off, sa_off, red_off,
+      bar_off, total;
 };
 
 __host__ __device__ inline uint32_t al16(size_t x) { return (uint32_t)((x + 15) & ~(size_t)15); }
 
 template <typename ST>
-B1Plan b1_plan(const bl::LayoutV2& L, bool zeros, bool tab_smem, int T, int stages) {
+B1Plan b1_plan(const bl::LayoutV2& L, bool zeros, bool tab_smem, int T, int stages, bool fused = false) {
   B1Plan s;
   s.w_bytes = (uint32_t)((size_t)L.KG * 16);
   s.s_bytes = (uint32_t)((size_t)L.tile_ch * L.NQ * sizeof(ST));
@@ -56,7 +59,9 @@ B1Plan b1_plan(const bl::LayoutV2& L, bool zeros, bool tab_smem, int T, int stag
   s.ts_off = s.tab_off + (tab_smem ? al16((size_t)L.KG * 8) : 0);
   s.rs_off = s.ts_off + al16((size_t)L.NQ * 4);
   s.y_off = s.rs_off + al16((size_t)L.NQ * 4);
-  s.bar_off = s.y_off + al16((size_t)2 * (T / 32) * L.tile_ch * 4);
+  s.sa_off = s.y_off + al16((size_t)2 * (T / 32) * L.tile_ch * 4);
+  s.red_off = s.sa_off + (fused ? al16((size_t)4 * T * 4) : 0);
+  s.bar_off = s.red_off + (fused ? al16((size_t)(T / 32) * 4) : 0);
   s.total = s.bar_off + 8 * (kMaxStages + 1);
   return s;
 }
@@ -151,7 +156,132 @@ __device__ __forceinline__ void issue_stage(const B1Args& a, int tile, uint8_t* 
   if (zeros) bulk_g2s(sb + a.z_off, reinterpret_cast<const ST*>(p.zeros) + e0, a.s_bytes, bar, pol);
 }
 
-template <int R, int LG, int BITS, typename ST>
+// ---- fused table build (cluster-cooperative) ----
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_size() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_arrive_release() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// store to the same smem offset in CTA `rank` of the cluster
+__device__ __forceinline__ void st_cluster_v2(const void* local, uint32_t rank, uint32_t x, uint32_t y) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local)), "r"(rank));
+  asm volatile("st.shared::cluster.v2.u32 [%0], {%1, %2};" ::"r"(ra), "r"(x), "r"(y) : "memory");
+}
+__device__ __forceinline__ void st_cluster_f32(const void* local, uint32_t rank, float x) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local)), "r"(rank));
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(ra), "f"(x) : "memory");
+}
+
+// Each CTA of the cluster builds the int8 tables, table scales and row sums
+// of a slice of the quantization groups -- the arithmetic of lut_core.cuh
+// lut_block, operation for operation, so the tables are bitwise those of
+// bitlut_build_lut -- and stores them into the shared memory of EVERY CTA
+// of the cluster (DSMEM).  Requires T % (gs/4) == 0.
+template <int R>
+__device__ __forceinline__ void fused_tables(const B1Args& a, uint8_t* smem) {
+  const bl::LayoutV2& L = a.g.L;
+  const int tid = threadIdx.x, T = blockDim.x;
+  const int KG = L.KG, NQ = L.NQ, gs = L.gs, gpg = gs >> 2, U = L.U;
+  const uint32_t rank = cluster_rank(), cs = cluster_size();
+  const int gpr = (NQ + (int)cs - 1) / (int)cs;
+  const int g0 = (int)rank * gpr, g1 = min(NQ, g0 + gpr);
+  float* sa = reinterpret_cast<float*>(smem + a.sa_off);
+  float* red = reinterpret_cast<float*>(smem + a.red_off);
+  uint8_t* tab = smem + a.tab_off;
+  float* tsm = reinterpret_cast<float*>(smem + a.ts_off);
+  float* rsm = reinterpret_cast<float*>(smem + a.rs_off);
+  bool waited = false;
+  for (int kb = g0 * gpg; kb < g1 * gpg; kb += T) {
+    const int kg = kb + tid;
+    const bool live = kg < g1 * gpg;
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    if (live) {
+      uint2 r;
+      asm volatile("ld.global.cg.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(a.act + 4 * (int64_t)kg));
+      const __half2 h0 = *reinterpret_cast<const __half2*>(&r.x), h1 = *reinterpret_cast<const __half2*>(&r.y);
+      v[0] = __low2float(h0); v[1] = __high2float(h0); v[2] = __low2float(h1); v[3] = __high2float(h1);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; j++) sa[tid * 4 + j] = v[j];
+    float e[8];
+#pragma unroll
+    for (int idx = 0; idx < 8; idx++) {
+      float x = (idx & 1) ? v[0] : -v[0];
+      x = (idx & 2) ? __fadd_rn(x, v[1]) : __fsub_rn(x, v[1]);
+      x = (idx & 4) ? __fadd_rn(x, v[2]) : __fsub_rn(x, v[2]);
+      e[idx] = __fsub_rn(x, v[3]);
+    }
+    float mx = 0.f;
+#pragma unroll
+    for (int idx = 0; idx < 8; idx++) mx = fmaxf(mx, fabsf(e[idx]));
+    const int seg = gpg < 32 ? gpg : 32;
+    for (int o = 1; o < seg; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (gpg > 32) {
+      if ((tid & 31) == 0) red[tid >> 5] = mx;
+      __syncthreads();
+      const int wpg = gpg >> 5;
+      const int w0 = (tid >> 5) / wpg * wpg;
+      mx = 0.f;
+      for (int w = 0; w < wpg; w++) mx = fmaxf(mx, red[w0 + w]);
+    }
+    float scale = __fdiv_rn(mx, 127.0f);
+    if (scale == 0.0f) scale = 1.0f;
+    uint32_t packed[2] = {0u, 0u};
+#pragma unroll
+    for (int idx = 0; idx < 8; idx++) {
+      const float q = __fdiv_rn(e[idx], scale);
+      float r = truncf(__fadd_rn(q, copysignf(0.5f, q)));
+      r = fminf(fmaxf(r, -127.f), 127.f);
+      packed[idx >> 2] |= ((uint32_t)(int)r & 0xffu) << (8 * (idx & 3));
+    }
+    if (!waited) {                 // every CTA of the cluster is running: DSMEM is safe
+      cluster_wait();
+      waited = true;
+    }
+    if (live) {
+      const uint32_t e0 = packed[0] - ((packed[0] >> 7) & 0x01010101u);
+      const uint32_t e1 = packed[1] - ((packed[1] >> 7) & 0x01010101u);
+      const int u = kg / R, r = kg - u * R, ub = u >> 5, l = u & 31;
+      const int nu_b = min(32, U - 32 * ub);
+      const uint8_t* dst = tab + ub * (32 * R * 8) + ((r >> 1) * nu_b + l) * 16 + (r & 1) * 8;
+      for (uint32_t d = 0; d < cs; d++) st_cluster_v2(dst, d, e0, e1);
+      if ((kg & (gpg - 1)) == 0)
+        for (uint32_t d = 0; d < cs; d++) st_cluster_f32(tsm + kg / gpg, d, scale);
+    }
+    __syncthreads();               // sa complete
+    if (live && (kg & (gpg - 1)) == 0) {
+      const float4* s4 = reinterpret_cast<const float4*>(sa + tid * 4);
+      float acc = 0.f;
+      for (int q = 0; q < gs / 4; q++) {
+        const float4 c = s4[q];
+        acc = __fadd_rn(acc, c.x); acc = __fadd_rn(acc, c.y); acc = __fadd_rn(acc, c.z); acc = __fadd_rn(acc, c.w);
+      }
+      for (uint32_t d = 0; d < cs; d++) st_cluster_f32(rsm + kg / gpg, d, acc);
+    }
+    __syncthreads();               // sa / red reusable
+  }
+  if (!waited) cluster_wait();
+  cluster_arrive_release();        // this CTA's slice is in every CTA's smem
+  cluster_wait();                  // ... and every other slice is in ours
+}
+
+template <int R, int LG, int BITS, typename ST, bool FUSED>
 __global__ void __launch_bounds__(256) gemv_b1_kernel(const __grid_constant__ B1Args a) {
   const GemvArgs& p = a.g;
   const bl::LayoutV2& L = p.L;
@@ -173,6 +303,7 @@ __global__ void __launch_bounds__(256) gemv_b1_kernel(const __grid_constant__ B1
   const int ntl = L.n_tiles, step = gridDim.x;
   const int S = a.stages;
 
+  if (FUSED) cluster_arrive_relaxed();                 // paired with the wait in fused_tables
   // ---- 1. weights + scales of the first tiles: independent of the predecessor ----
   if (tid == 0) {
     for (int s = 0; s <= kMaxStages; s++) mbar_init(bar + s, 1);
@@ -186,7 +317,7 @@ __global__ void __launch_bounds__(256) gemv_b1_kernel(const __grid_constant__ B1
   // ---- 2. tables / table scales / row sums come from the previous kernel ----
   if (!p.independent) bl::pdl_wait();
   bl::pdl_launch_dependents();
-  if (a.tab_smem && tid == 0) {
+  if (!FUSED && a.tab_smem && tid == 0) {
     const uint32_t tb = (uint32_t)KG * 8;
     mbar_expect_tx(bar + kMaxStages, tb);
     for (uint32_t off = 0; off < tb; off += 32768u) {
@@ -199,19 +330,23 @@ __global__ void __launch_bounds__(256) gemv_b1_kernel(const __grid_constant__ B1
     }
   }
   uint4 tq0[R / 2];
-  if (!a.tab_smem && tid < U) {
+  if (!FUSED && !a.tab_smem && tid < U) {
     const int ub = tid >> 5, l = tid & 31;
     const int nu_b = min(32, U - 32 * ub);
     const uint8_t* tb = p.qtab + (int64_t)ub * (32 * R * 8) + l * 16;
 #pragma unroll
     for (int jp = 0; jp < R / 2; jp++) tq0[jp] = bl::ld_cg_128(tb + jp * nu_b * 16);
   }
-  for (int i = tid; i < NQ; i += T) {
-    tsm[i] = bl::ld_cg_f32(p.tscales + i);
-    rsm[i] = bl::ld_cg_f32(p.rowsums + i);
+  if (FUSED) {
+    fused_tables<R>(a, smem);                           // includes the block-wide syncs
+  } else {
+    for (int i = tid; i < NQ; i += T) {
+      tsm[i] = bl::ld_cg_f32(p.tscales + i);
+      rsm[i] = bl::ld_cg_f32(p.rowsums + i);
+    }
   }
   __syncthreads();                                      // barriers initialised, tsm / rsm ready
-  if (a.tab_smem) mbar_wait(bar + kMaxStages, 0);
+  if (!FUSED && a.tab_smem) mbar_wait(bar + kMaxStages, 0);
 
   const bool has_zeros = p.zeros != nullptr;
   const float h2 = (float)(2 << (BITS - 1));
@@ -238,7 +373,7 @@ __global__ void __launch_bounds__(256) gemv_b1_kernel(const __grid_constant__ B1
         const int nu_b = min(32, U - 32 * ub);
         const int stride = nu_b == 32 ? 512 : nu_b * 16;
         uint4 tq[R / 2];
-        if (a.tab_smem) {
+        if (FUSED || a.tab_smem) {
           const uint8_t* tb = tab + ub * (32 * R * 8) + l * 16;
 #pragma unroll
           for (int jp = 0; jp < R / 2; jp++) tq[jp] = *reinterpret_cast<const uint4*>(tb + jp * stride);
@@ -313,15 +448,30 @@ int sm_count() {
   return n;
 }
 
-template <int R, int LG, int BITS, typename ST>
-int launch_b1(const GemvArgs& g, cudaStream_t stream, bool pdl) {
+constexpr int kClusterCTAs = 8;
+
+// CTA size: 128 threads, 256 when a tile has more than 128 units (long K).
+int b1_threads(const bl::LayoutV2& L) {
+  static int cap = 0;
+  if (!cap) {
+    const char* e = getenv("BITLUT_B1_THREADS");
+    cap = e ? atoi(e) : 256;
+    if (cap != 128 && cap != 256) cap = 128;
+  }
+  return L.U > 128 ? cap : 128;
+}
+
+template <int R, int LG, int BITS, typename ST, bool FUSED>
+int launch_b1(const GemvArgs& g, const __half* act, cudaStream_t stream, bool pdl) {
   const bl::LayoutV2& L = g.L;
-  const int T = L.U > 128 ? 256 : 128;
+  const int T = b1_threads(L);
+  if (FUSED && T % (L.gs / 4) != 0) return BITLUT_ELAYOUT;
   B1Args a;
   a.g = g;
+  a.act = act;
   a.rounds = (L.U + T - 1) / T;
-  a.tab_smem = a.rounds > 1;
-  auto kern = gemv_b1_kernel<R, LG, BITS, ST>;
+  a.tab_smem = FUSED || a.rounds > 1;
+  auto kern = gemv_b1_kernel<R, LG, BITS, ST, FUSED>;
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
@@ -338,64 +488,76 @@ int launch_b1(const GemvArgs& g, cudaStream_t stream, bool pdl) {
     const char* e = getenv("BITLUT_B1_TILES_PER_CTA");   // diagnostic override
     tpc_env = e ? atoi(e) : 0;
   }
-  const int tiles_per_cta = tpc_env > 0 ? tpc_env : (g.independent ? 2 : 1);
   // one stage when every CTA gets a single tile, else double-buffer
-  B1Plan s = b1_plan<ST>(L, g.zeros != nullptr, a.tab_smem, T, 1);
+  B1Plan s = b1_plan<ST>(L, g.zeros != nullptr, a.tab_smem, T, 1, FUSED);
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, s.total) != cudaSuccess || per_sm < 1)
     return BITLUT_ELAYOUT;
+  const B1Plan s2 = b1_plan<ST>(L, g.zeros != nullptr, a.tab_smem, T, 2, FUSED);
+  int per_sm2 = 0;
+  if (s2.total > 227 * 1024 ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, kern, T, s2.total) != cudaSuccess)
+    per_sm2 = 0;
+  // two tiles per CTA only where the double-buffered plan still leaves
+  // several CTAs per SM (short K); long-K tiles want every CTA they can get
+  int tiles_per_cta = tpc_env > 0 ? tpc_env : ((g.independent && per_sm2 >= 3) ? 2 : 1);
+  if (tpc_env <= 0 && (L.n_tiles + tiles_per_cta - 1) / tiles_per_cta < sm_count() / 2) tiles_per_cta = 1;
   const int want = (L.n_tiles + tiles_per_cta - 1) / tiles_per_cta;
+  // double-buffer when CTAs get several tiles -- by choice (tiles_per_cta)
+  // or because one wave cannot hold every tile -- unless that costs
+  // resident CTAs (then the single stage refills after each tile)
   a.stages = 1;
-  if (want < L.n_tiles || sm_count() * per_sm < L.n_tiles) {
-    const B1Plan s2 = b1_plan<ST>(L, g.zeros != nullptr, a.tab_smem, T, 2);
-    int per_sm2 = 0;
-    if (s2.total <= 227 * 1024 &&
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, kern, T, s2.total) == cudaSuccess && per_sm2 >= 1) {
-      s = s2; per_sm = per_sm2; a.stages = 2;
-    }
+  if (per_sm2 >= 1 && (tiles_per_cta > 1 || (sm_count() * per_sm < L.n_tiles && per_sm2 >= per_sm))) {
+    s = s2; per_sm = per_sm2; a.stages = 2;
   }
   if (s.total > 227 * 1024) return BITLUT_ELAYOUT;
   a.stage_bytes = s.stage_bytes; a.w_bytes = s.w_bytes; a.s_off = s.s_off; a.s_bytes = s.s_bytes;
   a.z_off = s.z_off; a.tab_off = s.tab_off; a.ts_off = s.ts_off; a.rs_off = s.rs_off;
-  a.y_off = s.y_off; a.bar_off = s.bar_off;
+  a.y_off = s.y_off; a.bar_off = s.bar_off; a.sa_off = s.sa_off; a.red_off = s.red_off;
   int grid = sm_count() * per_sm;
   if (grid > want) grid = want;
+  const int cs = FUSED ? kClusterCTAs : 1;
+  grid = (grid + cs - 1) / cs * cs;                     // spare CTAs only build their table slice
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(T);
   cfg.dynamicSmemBytes = s.total;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = cs;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = FUSED ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, kern, a) == cudaSuccess ? BITLUT_OK : BITLUT_EINTERNAL;
 }
 
-template <int R, int LG, typename ST>
-int launch_b1_bits(const GemvArgs& g, cudaStream_t s, bool pdl) {
+template <int R, int LG, typename ST, bool FUSED>
+int launch_b1_bits(const GemvArgs& g, const __half* act, cudaStream_t s, bool pdl) {
   switch (g.L.bits) {
-    case 1: return launch_b1<R, LG, 1, ST>(g, s, pdl);
-    case 2: return launch_b1<R, LG, 2, ST>(g, s, pdl);
-    case 4: return launch_b1<R, LG, 4, ST>(g, s, pdl);
+    case 1: return launch_b1<R, LG, 1, ST, FUSED>(g, act, s, pdl);
+    case 2: return launch_b1<R, LG, 2, ST, FUSED>(g, act, s, pdl);
+    case 4: return launch_b1<R, LG, 4, ST, FUSED>(g, act, s, pdl);
   }
   return BITLUT_EPARAM;
 }
 
-template <typename ST>
-int dispatch_b1(const GemvArgs& g, cudaStream_t s, bool pdl) {
+template <typename ST, bool FUSED>
+int dispatch_b1(const GemvArgs& g, const __half* act, cudaStream_t s, bool pdl) {
   const int R = g.L.R, LG = g.L.Lg;
   if (R == 8) {
     switch (LG) {
-      case 1: return launch_b1_bits<8, 1, ST>(g, s, pdl);
-      case 2: return launch_b1_bits<8, 2, ST>(g, s, pdl);
-      case 4: return launch_b1_bits<8, 4, ST>(g, s, pdl);
-      case 8: return launch_b1_bits<8, 8, ST>(g, s, pdl);
-      case 16: return launch_b1_bits<8, 16, ST>(g, s, pdl);
+      case 1: return launch_b1_bits<8, 1, ST, FUSED>(g, act, s, pdl);
+      case 2: return launch_b1_bits<8, 2, ST, FUSED>(g, act, s, pdl);
+      case 4: return launch_b1_bits<8, 4, ST, FUSED>(g, act, s, pdl);
+      case 8: return launch_b1_bits<8, 8, ST, FUSED>(g, act, s, pdl);
+      case 16: return launch_b1_bits<8, 16, ST, FUSED>(g, act, s, pdl);
     }
   } else if (R == 4 && LG == 1) {
-    return launch_b1_bits<4, 1, ST>(g, s, pdl);
+    return launch_b1_bits<4, 1, ST, FUSED>(g, act, s, pdl);
   }
   return BITLUT_EPARAM;
 }
@@ -407,5 +569,39 @@ int dispatch_b1(const GemvArgs& g, cudaStream_t s, bool pdl) {
 // shared-memory plan (the caller then uses the per-tile kernel).
 int bl_gemv_b1_launch(const GemvArgs& g, int scale_dtype, cudaStream_t s, bool pdl) {
   if (g.L.n_sg != 1) return BITLUT_ELAYOUT;
-  return scale_dtype == BITLUT_DT_F16 ? dispatch_b1<__half>(g, s, pdl) : dispatch_b1<float>(g, s, pdl);
+  return scale_dtype == BITLUT_DT_F16 ? dispatch_b1<__half, false>(g, nullptr, s, pdl)
+                                      : dispatch_b1<float, false>(g, nullptr, s, pdl);
+}
+
+bool bl_gemv_b1_fused_fits(const bl::LayoutV2& L, bool zeros, int scale_dtype) {
+  if (L.n_sg != 1) return false;
+  const int T = b1_threads(L);
+  if (T % (L.gs / 4) != 0) return false;
+  const size_t total = scale_dtype == BITLUT_DT_F16 ? b1_plan<__half>(L, zeros, true, T, 1, true).total
+                                                    : b1_plan<float>(L, zeros, true, T, 1, true).total;
+  return total <= 227 * 1024;
+}
+
+// Table build + lookup in ONE launch for a batch-1 fp16 activation row
+// (fast epilogue): see include/bitlut_b200.h.
+extern "C" int bitlut_mpgemv_fused(const void* a, int a_dtype, const uint8_t* wgpu, int m, int k, int bits,
+                                   int group_size, const void* wscales, const void* zeros, int scale_dtype,
+                                   float* out, int flags, void* stream) {
+  bl::LayoutV2 L;
+  int rc = bl::make_layout(m, k, bits, group_size, &L);
+  if (rc) return rc;
+  if (!a || !wgpu || !wscales || !out) return BITLUT_EPARAM;
+  if (scale_dtype != BITLUT_DT_F32 && scale_dtype != BITLUT_DT_F16) return BITLUT_EPARAM;
+  if (!(flags & BITLUT_FLAG_FAST_EPILOGUE)) return BITLUT_EPARAM;     // reference order: build_lut + mpgemm
+  if (a_dtype != BITLUT_DT_F16 || L.n_sg != 1) return BITLUT_ELAYOUT;  // caller falls back to two launches
+  const bool pdl = (flags & BITLUT_FLAG_PDL) != 0;
+  GemvArgs g = {};
+  g.w = wgpu; g.wscales = wscales; g.zeros = zeros;
+  g.out = out; g.L = L;
+  g.independent = pdl && (flags & BITLUT_FLAG_INDEPENDENT) != 0;
+  g.fast = 1;
+  g.rows_per_cta = 1; g.n_rows = 1;
+  const __half* act = reinterpret_cast<const __half*>(a);
+  return scale_dtype == BITLUT_DT_F16 ? dispatch_b1<__half, true>(g, act, (cudaStream_t)stream, pdl)
+                                      : dispatch_b1<float, true>(g, act, (cudaStream_t)stream, pdl);
 }

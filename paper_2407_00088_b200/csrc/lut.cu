@@ -112,13 +112,14 @@ constexpr int kLutThreads = 256;
 template <int MODE, typename AT>
 __global__ void __launch_bounds__(kLutThreads)
 build_lut_kernel(const AT* __restrict__ a, int k, int gs, void* __restrict__ tables,
-                 float* __restrict__ tscales, float* __restrict__ rowsums) {
+                 float* __restrict__ tscales, float* __restrict__ rowsums, int independent) {
   bl::pdl_launch_dependents();
-  bl::pdl_wait();                       // activations come from the previous kernel
+  if (!independent) bl::pdl_wait();     // activations come from the previous kernel
   __shared__ __align__(16) float sa[kLutThreads * 4];
   __shared__ float red[kLutThreads / 32];
   lutk::lut_block<MODE, AT>(a, k, gs, tables, tscales, rowsums, blockIdx.y, blockIdx.x * kLutThreads,
                             sa, red);
+  if (independent) bl::pdl_wait();      // keep stream completion order
 }
 
 inline int grid_1d(int64_t n, int threads) {
@@ -175,7 +176,9 @@ extern "C" int bitlut_row_sums(const void* a, int a_dtype, int n, int k, int gro
 }
 
 int bl_build_lut_launch(const void* a, int a_dtype, int n, int k, int group_size, int mode,
-                        void* tables, float* tscales, float* rowsums, cudaStream_t stream, bool pdl) {
+                        void* tables, float* tscales, float* rowsums, cudaStream_t stream, bool pdl,
+                        bool independent) {
+  const int ind = (pdl && independent) ? 1 : 0;
   const int KG = k / 4;
   dim3 grid((KG + kLutThreads - 1) / kLutThreads, n);
   cudaLaunchConfig_t cfg = {};
@@ -188,15 +191,15 @@ int bl_build_lut_launch(const void* a, int a_dtype, int n, int k, int group_size
   if (mode == BITLUT_TABLE_Q8) {
     e = a_dtype == BITLUT_DT_F16
             ? cudaLaunchKernelEx(&cfg, build_lut_kernel<BITLUT_TABLE_Q8, __half>, (const __half*)a, k, group_size,
-                                 tables, tscales, rowsums)
+                                 tables, tscales, rowsums, ind)
             : cudaLaunchKernelEx(&cfg, build_lut_kernel<BITLUT_TABLE_Q8, float>, (const float*)a, k, group_size,
-                                 tables, tscales, rowsums);
+                                 tables, tscales, rowsums, ind);
   } else {
     e = a_dtype == BITLUT_DT_F16
             ? cudaLaunchKernelEx(&cfg, build_lut_kernel<BITLUT_TABLE_F16, __half>, (const __half*)a, k, group_size,
-                                 tables, tscales, rowsums)
+                                 tables, tscales, rowsums, ind)
             : cudaLaunchKernelEx(&cfg, build_lut_kernel<BITLUT_TABLE_F16, float>, (const float*)a, k, group_size,
-                                 tables, tscales, rowsums);
+                                 tables, tscales, rowsums, ind);
   }
   return e == cudaSuccess ? BITLUT_OK : BITLUT_EINTERNAL;
 }
@@ -211,5 +214,6 @@ extern "C" int bitlut_build_lut(const void* a, int a_dtype, int n, int k, int gr
   if (gpg > 128 || (gpg & (gpg - 1))) return BITLUT_EPARAM;   // CUDA path: power-of-two k-groups per group
   if (n == 0 || k == 0) return BITLUT_OK;
   return bl_build_lut_launch(a, a_dtype, n, k, group_size, mode, tables, tscales, rowsums,
-                             (cudaStream_t)stream, (flags & BITLUT_FLAG_PDL) != 0);
+                             (cudaStream_t)stream, (flags & BITLUT_FLAG_PDL) != 0,
+                             (flags & BITLUT_FLAG_INDEPENDENT) != 0);
 }

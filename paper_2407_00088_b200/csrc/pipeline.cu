@@ -268,9 +268,17 @@ extern "C" int bitlut_pipeline_launch_traced(const void* table_host, const void*
 
 // ---------------------------------------------------------------------------
 // Per-op executor: the same op list as stream-ordered launches of the
-// per-call kernels (bitlut_build_lut / bitlut_mpgemm), chained with
-// programmatic dependent launch; meant to be captured once into a CUDA graph
-// (pipeline.py) so a replay costs one graph launch.
+// per-call kernels (bitlut_build_lut / bitlut_mpgemm / bitlut_mpgemv_fused),
+// chained with programmatic dependent launch; meant to be captured once into
+// a CUDA graph (pipeline.py) so a replay costs one graph launch.
+//
+// Table-build fusion (opt-in: BITLUT_FLAG_FUSED_TABLES on the table op): a
+// batch-1 fp16 table op whose every consumer is a fast-epilogue lookup on a
+// 32-stream tile is not launched; each consumer
+// runs as bitlut_mpgemv_fused from the table op's activations instead (one
+// launch per GEMV, tables built in-kernel by the CTA cluster).  A fused
+// lookup's inputs are the table op's inputs, so its dependencies are the
+// table op's.
 //
 // Which lookups may skip the start-of-kernel wait (BITLUT_FLAG_INDEPENDENT)
 // follows from when each kernel releases its successor:
@@ -280,27 +288,66 @@ extern "C" int bitlut_pipeline_launch_traced(const void* table_host, const void*
 // So when kernel i starts, every op before the most recent dependent lookup
 // d < i (ops 0..d-1) has completed -- waits are transitive, since every
 // kernel waits for its predecessor before exiting.  Lookup i runs
-// INDEPENDENT iff all its deps are in that completed prefix (q after its
-// table build waits; k and v, which read the same table, do not).  A lookup
-// with no deps reads tables made outside the op list and always waits.
+// INDEPENDENT iff all its (effective) deps are in that completed prefix (q
+// after its table build waits; k and v, which read the same inputs, do
+// not); the same holds for table builds (which never advance the prefix:
+// they release before waiting).  Inputs made before the op list count as
+// complete once any kernel of the list has waited.
 // ---------------------------------------------------------------------------
+bool bl_gemv_b1_fused_fits(const bl::LayoutV2& L, bool zeros, int scale_dtype);   // gemv_b1.cu
+
+static bool fusable_lookup(const bitlut_pipe_op& s, const bitlut_pipe_op& t) {
+  if (s.type != BITLUT_OP_LOOKUP || t.type != BITLUT_OP_TABLES) return false;
+  if (!(s.flags & BITLUT_FLAG_FAST_EPILOGUE) || s.n != 1 || t.n != 1 || t.a_dtype != BITLUT_DT_F16) return false;
+  if (s.k != t.k || s.group_size != t.group_size) return false;
+  bl::LayoutV2 L;
+  if (bl::make_layout(s.m, s.k, s.bits, s.group_size, &L) || L.n_sg != 1) return false;
+  return bl_gemv_b1_fused_fits(L, s.zeros != nullptr, s.scale_dtype);
+}
+
 extern "C" int bitlut_pipeline_plan_flags(const bitlut_pipe_op* specs, int n_ops, int* flags_out) {
   if (n_ops <= 0 || !specs || !flags_out) return BITLUT_EPARAM;
+  for (int i = 0; i < n_ops; i++) {
+    if (specs[i].type != BITLUT_OP_TABLES && specs[i].type != BITLUT_OP_LOOKUP) return BITLUT_EPARAM;
+    for (int d = 0; d < 3; d++)
+      if (specs[i].dep[d] >= i || specs[i].dep[d] < -1) return BITLUT_EPARAM;
+    flags_out[i] = 0;
+  }
+  // which table ops can be folded into all of their consumers
+  for (int t = 0; t < n_ops; t++) {
+    if (specs[t].type != BITLUT_OP_TABLES || !(specs[t].flags & BITLUT_FLAG_FUSED_TABLES)) continue;
+    bool all = true, any = false;
+    for (int i = t + 1; i < n_ops && all; i++) {
+      const bitlut_pipe_op& s = specs[i];
+      bool uses = false;
+      for (int d = 0; d < 3; d++) uses = uses || s.dep[d] == t;
+      if (!uses) continue;
+      any = true;
+      // a fused consumer must depend on the table op alone
+      const bool only = s.dep[0] == t && s.dep[1] < 0 && s.dep[2] < 0;
+      all = only && fusable_lookup(s, specs[t]);
+    }
+    if (any && all) {
+      flags_out[t] = BITLUT_PLAN_SKIP;
+      for (int i = t + 1; i < n_ops; i++)
+        if (specs[i].dep[0] == t) flags_out[i] = BITLUT_FLAG_FUSED_TABLES;
+    }
+  }
   int done_below = 0;            // ops [0, done_below) complete when the next kernel starts
   for (int i = 0; i < n_ops; i++) {
     const bitlut_pipe_op& s = specs[i];
-    int fl = BITLUT_FLAG_PDL;
+    if (flags_out[i] == BITLUT_PLAN_SKIP) continue;
+    int fl = BITLUT_FLAG_PDL | flags_out[i];
+    const int* deps = (fl & BITLUT_FLAG_FUSED_TABLES) ? specs[s.dep[0]].dep : s.dep;
+    // inputs from before the op list are complete once any kernel of the
+    // list has waited (done_below >= 1)
+    bool ok = done_below >= 1;
     for (int d = 0; d < 3; d++)
-      if (s.dep[d] >= i || s.dep[d] < -1) return BITLUT_EPARAM;
+      if (deps[d] >= 0) ok = ok && deps[d] < done_below;
+    if (ok) fl |= BITLUT_FLAG_INDEPENDENT;
     if (s.type == BITLUT_OP_LOOKUP) {
-      bool any = false, ok = true;
-      for (int d = 0; d < 3; d++)
-        if (s.dep[d] >= 0) { any = true; ok = ok && s.dep[d] < done_below; }
-      if (any && ok) fl |= BITLUT_FLAG_INDEPENDENT;
-      else done_below = i;        // waits for op i-1 (hence all earlier), then releases i+1
+      if (!ok) done_below = i;    // waits for its predecessor (hence all earlier), then releases
       fl |= s.flags & BITLUT_FLAG_FAST_EPILOGUE;
-    } else if (s.type != BITLUT_OP_TABLES) {
-      return BITLUT_EPARAM;
     }
     flags_out[i] = fl;
   }
@@ -315,13 +362,19 @@ extern "C" int bitlut_pipeline_launch_ops(const bitlut_pipe_op* specs, int n_ops
   int rc = bitlut_pipeline_plan_flags(specs, n_ops, flags);
   for (int i = 0; rc == BITLUT_OK && i < n_ops; i++) {
     const bitlut_pipe_op& s = specs[i];
-    if (s.type == BITLUT_OP_TABLES)
+    const int fl = flags[i];
+    if (fl == BITLUT_PLAN_SKIP) continue;
+    if (s.type == BITLUT_OP_TABLES) {
       rc = bitlut_build_lut(s.a, s.a_dtype, s.n, s.k, s.group_size, BITLUT_TABLE_Q8, s.tables,
-                            s.tscales, s.rowsums, flags[i], stream);
-    else
+                            s.tscales, s.rowsums, fl, stream);
+    } else if (fl & BITLUT_FLAG_FUSED_TABLES) {
+      const bitlut_pipe_op& t = specs[s.dep[0]];
+      rc = bitlut_mpgemv_fused(t.a, t.a_dtype, s.wgpu, s.m, s.k, s.bits, s.group_size, s.wscales, s.zeros,
+                               s.scale_dtype, s.out, fl & ~BITLUT_FLAG_FUSED_TABLES, stream);
+    } else {
       rc = bitlut_mpgemm(s.wgpu, s.m, s.k, s.bits, s.group_size, s.wscales, s.zeros, s.scale_dtype,
-                         s.tables, s.tscales, s.rowsums, BITLUT_TABLE_Q8, s.n, s.out, nullptr,
-                         flags[i], stream);
+                         s.tables, s.tscales, s.rowsums, BITLUT_TABLE_Q8, s.n, s.out, nullptr, fl, stream);
+    }
   }
   if (flags != stack_flags) free(flags);
   return rc;

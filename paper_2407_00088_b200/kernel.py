@@ -187,19 +187,29 @@ def mpgemm(a, pw: PackedWeights, cfg: TileConfig | None = None,
         raise ParameterError("exact int32 partials exist only for int8 tables (cuda-q8)")
     if rows.device != pw.gpu.device:
         rows = rows.to(pw.gpu.device)
-    tables, ts, rs = N.build_lut(rows, pw.group_size, mode, N.FLAG_PDL if pdl else 0)
     flags = (N.FLAG_PDL if pdl else 0) | (0 if exact_epilogue else N.FLAG_FAST_EPILOGUE)
-    out, partials = N.lookup(pw.gpu, pw.scales, pw.zeros, tables, ts, rs, pw.m, pw.k, pw.bits,
-                             pw.group_size, mode, flags, return_partials)
+    out = None
+    if (mode == N.TABLE_Q8 and not exact_epilogue and not return_partials and n == 1
+            and rows.dtype == torch.float16 and pw.bits != 3):
+        try:      # table build + lookup in one launch (csrc/gemv_b1.cu)
+            out = N.mpgemv_fused(rows, pw.gpu, pw.scales, pw.zeros, pw.m, pw.k, pw.bits,
+                                 pw.group_size, flags)
+            partials = None
+        except LayoutError:
+            out = None
+    if out is None:
+        tables, ts, rs = N.build_lut(rows, pw.group_size, mode, N.FLAG_PDL if pdl else 0)
+        out, partials = N.lookup(pw.gpu, pw.scales, pw.zeros, tables, ts, rs, pw.m, pw.k, pw.bits,
+                                 pw.group_size, mode, flags, return_partials)
     if stats is not None:
         stats.lookups += pw.bits * n * pw.m * (pw.k // pw.g)
         stats.lut_builds += -(-n // cfg.n_tile) * (pw.k // cfg.k_tile)
     if kind == "numpy":
         out = out.cpu().numpy()
-        partials = partials.cpu().numpy()
+        partials = partials.cpu().numpy() if return_partials else None
     elif kind == "cpu":
         out = out.cpu()
-        partials = partials.cpu()
+        partials = partials.cpu() if return_partials else None
     return (out, partials) if return_partials else out
 
 

@@ -98,8 +98,11 @@ class Pipeline:
             raise ParameterError("an op can name at most 3 dependencies")
         return idx + [-1] * (3 - len(idx))
 
-    def tables(self, a: torch.Tensor, group_size: int, deps: Sequence = ()) -> TableRef:
-        """Table build (kernel.py:226-251) for activations a (n, k) f16/f32."""
+    def tables(self, a: torch.Tensor, group_size: int, deps: Sequence = (), fuse: bool = False) -> TableRef:
+        """Table build (kernel.py:226-251) for activations a (n, k) f16/f32.
+        fuse=True lets the graph executor fold it into its consumers when they
+        are all batch-1 fast-epilogue lookups (one launch per GEMV,
+        bitlut_mpgemv_fused); the persistent executor ignores it."""
         N.require_cuda(a, "activations")
         if a.dim() == 1:
             a = a.reshape(1, -1)
@@ -114,6 +117,7 @@ class Pipeline:
         s.dep[:] = self._deps(deps)
         s.a, s.a_dtype, s.n, s.k, s.group_size = a.data_ptr(), N.dtype_code(a), n, k, group_size
         s.tables, s.tscales, s.rowsums = tables.data_ptr(), ts.data_ptr(), rs.data_ptr()
+        s.flags = N.FLAG_FUSED_TABLES if fuse else 0
         self.specs.append(s)
         self.keep += [a, tables, ts, rs]
         return TableRef(index=len(self.specs) - 1, tensors=(tables, ts, rs), n=n, k=k,

@@ -132,7 +132,46 @@ def test_graph_executor_independence_plan():
     assert _bind().bitlut_pipeline_plan_flags(arr, len(ops), fl) == 0
     P, I, F = N.FLAG_PDL, N.FLAG_INDEPENDENT, N.FLAG_FAST_EPILOGUE
     assert list(fl) == [P, P, P | I, P | I, P, P, P, P | F, P | I | F, P, P, P, P,
-                        P,          # no deps: tables made outside the list -> waits
-                        P | I]      # dep 1 < last dependent lookup (13)
+                        P | I,      # no deps: inputs from before the list, complete once a kernel waited
+                        P | I]      # dep 1 < last dependent lookup (12)
     bad = (PipeOpSpec * 2)(op(T), op(LK, [1]))
     assert _bind().bitlut_pipeline_plan_flags(bad, 2, fl) == -1
+
+
+def test_graph_executor_table_fusion_plan():
+    """Batch-1 fp16 table ops marked fusable whose consumers are all
+    fast-epilogue lookups are folded into them (BITLUT_PLAN_SKIP / BITLUT_FLAG_FUSED_TABLES); the
+    fused lookups inherit the table op's dependencies."""
+    import ctypes
+    from paper_2407_00088_b200.pipeline import PipeOpSpec, _bind
+    T, LK = 0, 1
+    SKIP, FUSED = -1, 8
+
+    def tab(deps=(), n=1, dt=N.DT_F16, k=4096):
+        s = PipeOpSpec()
+        s.type, s.n, s.k, s.group_size, s.a_dtype = T, n, k, 64, dt
+        s.flags = N.FLAG_FUSED_TABLES
+        s.dep[:] = list(deps) + [-1] * (3 - len(deps))
+        return s
+
+    def look(deps, m=4096, k=4096, bits=2, fast=True):
+        s = PipeOpSpec()
+        s.type, s.n, s.k, s.group_size, s.m, s.bits = LK, 1, k, 64, m, bits
+        s.scale_dtype = N.DT_F16
+        s.flags = N.FLAG_FAST_EPILOGUE if fast else 0
+        s.dep[:] = list(deps) + [-1] * (3 - len(deps))
+        return s
+
+    ops = [tab([]), look([0]), look([0]), look([0]),            # qkv: fused, table skipped
+           tab([1, 2, 3]), look([4], fast=False),               # exact consumer: not fused
+           tab([5]), look([6], bits=3, m=4096),                 # 3-bit consumer: not fused
+           tab([7]), look([8]), look([8])]                      # gate/up: fused
+    arr = (PipeOpSpec * len(ops))(*ops)
+    fl = (ctypes.c_int * len(ops))()
+    assert _bind().bitlut_pipeline_plan_flags(arr, len(ops), fl) == 0
+    P, I, F = N.FLAG_PDL, N.FLAG_INDEPENDENT, N.FLAG_FAST_EPILOGUE
+    assert list(fl) == [SKIP, P | FUSED | F,            # first kernel of the list waits
+                        P | FUSED | F | I, P | FUSED | F | I,   # inputs from before the list: complete
+                        P, P,
+                        P, P | F,
+                        SKIP, P | FUSED | F, P | FUSED | F | I]

@@ -480,3 +480,65 @@ def test_batch1_fast_kernel(bits, gs, zeros, k):
         # the reference-order epilogue stages every partial of a tile in smem:
         # 688 groups (k=11008, gs=16) exceed 227 KB -- a documented limit
         assert gs == 16 and k == 11008
+
+
+def test_fused_mpgemv_and_graph_fusion():
+    """bitlut_mpgemv_fused (in-kernel cluster table build) == build_lut +
+    batch-1 fast lookup, bitwise; the graph executor folds the table ops of
+    fast lookups into them and matches per-op calls bitwise."""
+    from paper_2407_00088_b200 import _native as N
+    from paper_2407_00088_b200.pipeline import Pipeline
+    g = torch.Generator(device="cuda").manual_seed(5)
+    for bits, gs, m, k, zeros in ((2, 64, 512, 4096, False), (4, 128, 256, 11008, True),
+                                  (1, 32, 1024, 2048, False), (2, 256, 256, 4096, True),
+                                  (4, 16, 128, 1024, False)):
+        q = torch.randint(0, 1 << bits, (m, k), dtype=torch.uint8, device="cuda", generator=g)
+        sc = (torch.randn((m, k // gs), device="cuda", generator=g).abs() * 0.02 + 1e-3).half()
+        z = (torch.rand((m, k // gs), device="cuda", generator=g) * ((1 << bits) - 1)).half() if zeros else None
+        pw = B.prepare_weights(B.QuantizedWeights(m=m, k=k, bits=bits, group_size=gs, qvalues=q, scales=sc,
+                                                  zeros=z))
+        x = torch.randn((1, k), device="cuda", generator=g).half()
+        fl = N.FLAG_PDL | N.FLAG_FAST_EPILOGUE
+        yf = N.mpgemv_fused(x, pw.gpu, pw.scales, pw.zeros, m, k, bits, gs, fl)
+        t = N.build_lut(x, gs, N.TABLE_Q8)
+        y2, _ = N.lookup(pw.gpu, pw.scales, pw.zeros, *t, m, k, bits, gs, N.TABLE_Q8, fl, False)
+        assert torch.equal(yf, y2), (bits, gs, m, k)
+        ref = O.mpgemm_q8(x.cpu().numpy(), q.cpu().numpy(), sc.float().cpu().numpy(), bits, gs,
+                          zeros=None if z is None else z.cpu().numpy())
+        assert rel_maxnorm(yf.cpu().numpy(), ref) <= 1e-5
+    # graph executor: two layers of q,k,v / o / gate,up / down with fast lookups
+    shapes = {"q": (256, 512), "k": (256, 512), "v": (256, 512), "o": (256, 512),
+              "gate": (352, 512), "up": (352, 512), "down": (256, 1024)}
+    layers = []
+    for _ in range(2):
+        L = {}
+        for nm, (m, k) in shapes.items():
+            q = torch.randint(0, 4, (m, k), dtype=torch.uint8, device="cuda", generator=g)
+            sc = (torch.randn((m, k // 64), device="cuda", generator=g).abs() * 0.02 + 1e-3).half()
+            L[nm] = B.prepare_weights(B.QuantizedWeights(m=m, k=k, bits=2, group_size=64, qvalues=q, scales=sc))
+        layers.append(L)
+    xs = [{nm: torch.randn((1, k), device="cuda", generator=g).half() for nm, k in
+           (("attn", 512), ("o", 512), ("mlp", 512), ("down", 1024))} for _ in layers]
+    pl = Pipeline(executor="graph")
+    outs, prev = [], []
+    for L, X in zip(layers, xs):
+        t = pl.tables(X["attn"], 64, deps=prev, fuse=True)
+        ys = {nm: pl.lookup(L[nm], t, fast_epilogue=True) for nm in ("q", "k", "v")}
+        t2 = pl.tables(X["o"], 64, deps=[pl.op_of(y) for y in ys.values()], fuse=True)
+        ys["o"] = pl.lookup(L["o"], t2, fast_epilogue=True)
+        t3 = pl.tables(X["mlp"], 64, deps=[pl.op_of(ys["o"])], fuse=True)
+        ys["gate"], ys["up"] = (pl.lookup(L[nm], t3, fast_epilogue=True) for nm in ("gate", "up"))
+        t4 = pl.tables(X["down"], 64, deps=[pl.op_of(ys["gate"]), pl.op_of(ys["up"])], fuse=True)
+        ys["down"] = pl.lookup(L["down"], t4, fast_epilogue=True)
+        prev = [pl.op_of(ys["down"])]
+        outs.append(ys)
+    plan = pl.plan_flags()
+    assert plan.count(-1) == 8 and all(f & 8 for f in plan if f != -1)
+    pl.compile()
+    for _ in range(3):
+        pl.run()
+        torch.cuda.synchronize()
+        for L, X, Y in zip(layers, xs, outs):
+            for nm, xk in (("q", "attn"), ("k", "attn"), ("v", "attn"), ("o", "o"), ("gate", "mlp"),
+                           ("up", "mlp"), ("down", "down")):
+                assert torch.equal(Y[nm], B.mpgemm(X[xk], L[nm], exact_epilogue=False)), nm
