@@ -179,7 +179,7 @@ def step_fn(layers, acts, world, group, fast=False):
     return res
 
 
-def build_pipeline(layers, acts, fast=False, executor="persistent", chain=True):
+def build_pipeline(layers, acts, fast=False, executor="persistent", chain=True, sync="pdl", lookahead=None):
     """The step as a pipeline.Pipeline op list.  chain=True: the decode
     chain's dependencies -- a layer's qkv table build waits for the previous
     layer's down GEMV, o's for q,k,v, gate/up's for o, down's for gate,up.
@@ -189,7 +189,7 @@ def build_pipeline(layers, acts, fast=False, executor="persistent", chain=True):
     step).  Returns (pipeline, outputs, out_arena)."""
     import torch
     from paper_2407_00088_b200.pipeline import Pipeline
-    pl = Pipeline(executor=executor)
+    pl = Pipeline(executor=executor, sync=sync)
     per_layer = sum(pw.m for pw in layers[0].values())
     out_arena = torch.empty((len(layers) * per_layer,), dtype=torch.float32,
                             device=layers[0]["q"].gpu.device)
@@ -207,20 +207,26 @@ def build_pipeline(layers, acts, fast=False, executor="persistent", chain=True):
                 outs += ys
                 prev = [pl.op_of(y) for y in ys]
     else:
-        # independent calls, software-pipelined by one layer: layer L+1's
-        # table builds are recorded before layer L's lookups, so every lookup
-        # but the first finds its tables complete (INDEPENDENT launches)
+        # independent calls, software-pipelined: the table builds of layer
+        # L+D are recorded before layer L's lookups (D = lookahead), so a
+        # lookup finds its tables complete (INDEPENDENT launch) except right
+        # after the planner's completed-prefix has to advance (every D+1 layers)
+        D = int(os.environ.get("BENCH_LOOKAHEAD", "8")) if lookahead is None else lookahead
+        D = max(1, min(D, len(layers)))
+
         def tables_of(i):
             return {g: pl.tables(acts[i][g], layers[i][names[0]].group_size)
                     for g, _, names in LUT_GROUPS}
-        nxt = tables_of(0)
+        tabs = {}
+        for i in range(D):
+            tabs[i] = tables_of(i)
         for i, L in enumerate(layers):
-            cur = nxt
-            nxt = tables_of(i + 1) if i + 1 < len(layers) else None
+            if i + D < len(layers):
+                tabs[i + D] = tables_of(i + D)
             for gname, k, names in LUT_GROUPS:
                 for nm in names:
                     m = L[nm].m
-                    outs.append(pl.lookup(L[nm], cur[gname], fast_epilogue=fast,
+                    outs.append(pl.lookup(L[nm], tabs[i][gname], fast_epilogue=fast,
                                           out=out_arena[off:off + m].view(1, m)))
                     off += m
     pl.compile()
@@ -463,15 +469,18 @@ def main():
     pipes = {}
     with ClockSampler(local) as clk:
         if world == 1:
-            for name, ex, fast, chain in (("layer_set_graph_fast", "graph", True, False),
-                                          ("layer_set_graph_exact", "graph", False, False),
-                                          ("decode_chain_graph_fast", "graph", True, True),
-                                          ("decode_chain_graph_exact", "graph", False, True),
-                                          ("decode_chain_persistent_fast", "persistent", True, True)):
-                pl, outs, out_arena = build_pipeline(layers, acts, fast=fast, executor=ex, chain=chain)
+            for name, ex, fast, chain, sync in (
+                    ("layer_set_graph_fast", "graph", True, False, "pdl"),
+                    ("layer_set_graph_exact", "graph", False, False, "pdl"),
+                    ("layer_set_graph_fast_counters", "graph", True, False, "counters"),
+                    ("decode_chain_graph_fast", "graph", True, True, "pdl"),
+                    ("decode_chain_graph_exact", "graph", False, True, "pdl"),
+                    ("decode_chain_graph_fast_counters", "graph", True, True, "counters"),
+                    ("decode_chain_persistent_fast", "persistent", True, True, "pdl")):
+                pl, outs, out_arena = build_pipeline(layers, acts, fast=fast, executor=ex, chain=chain,
+                                                     sync=sync)
                 pipes[name] = (pl, out_arena)
-                executors[name] = {"ms": time_runs(lambda: pl.run(stream)),
-                                   "launches": n_ops if ex == "graph" else 1}
+                executors[name] = {"ms": time_runs(lambda: pl.run(stream)), "launches": pl.n_launches()}
         else:
             for fast in (True, False):
                 g_step = capture(lambda: step_fn(layers, acts, world, group, fast=fast), stream)

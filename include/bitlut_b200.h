@@ -137,6 +137,17 @@ int bitlut_row_sums(const void* a, int a_dtype, int n, int k, int group_size,
 int bitlut_build_lut(const void* a, int a_dtype, int n, int k, int group_size, int mode,
                      void* tables, float* tscales, float* rowsums, int flags, void* stream);
 
+/* Several table builds (up to 8 activation blocks, one dtype) in ONE launch:
+ * each job is exactly a bitlut_build_lut call. */
+typedef struct {
+  const void* a;            /* (n, k) activations */
+  int a_dtype, n, k, group_size;
+  void* tables;
+  float* tscales;
+  float* rowsums;
+} bitlut_lut_job;
+int bitlut_build_lut_multi(const bitlut_lut_job* jobs, int n_jobs, int mode, int flags, void* stream);
+
 /* ---------------- lookup-accumulate (kernel.py / _kernels.py) ---------------- */
 
 /* mpgemm  kernel.py:280-371 with _kernels.gemv_q8_vector :141-192 (mode Q8)
@@ -170,6 +181,22 @@ int bitlut_mpgemm(const uint8_t* wgpu, int m, int k, int bits, int group_size,
 int bitlut_mpgemv_fused(const void* a, int a_dtype, const uint8_t* wgpu, int m, int k, int bits,
                         int group_size, const void* wscales, const void* zeros, int scale_dtype,
                         float* out, int flags, void* stream);
+
+/* Several weight matrices that read the same activation row's tables
+ * (q/k/v, gate/up) looked up by ONE batch-1 launch (fast epilogue; 1/2/4-bit
+ * weights sharing k, bits, group_size, scale dtype and zero-point presence).
+ * tables / tscales / rowsums as produced by bitlut_build_lut (mode Q8, n = 1).
+ * Up to 4 matrices.  Returns BITLUT_ELAYOUT for 3-bit weights. */
+typedef struct {
+  const uint8_t* wgpu;      /* layout-v2 weights (m, k) */
+  const void* wscales;      /* (m, k/gs) */
+  const void* zeros;        /* (m, k/gs) or NULL (all or none) */
+  int m;
+  float* out;               /* (1, m) f32 */
+} bitlut_mat;
+int bitlut_mpgemv_multi(const bitlut_mat* mats, int n_mats, int k, int bits, int group_size,
+                        int scale_dtype, const void* tables, const float* tscales, const float* rowsums,
+                        int flags, void* stream);
 
 /* bitlut_mpgemm plus a timeline: `trace` (device, (n * tiles) x 8 u64) gets
  * per-CTA %globaltimer stamps [start, loads issued, after griddepcontrol.wait,
@@ -230,13 +257,22 @@ int bitlut_pipeline_launch_traced(const void* table_host, const void* table_dev,
  * BITLUT_FLAG_INDEPENDENT; batch-1 fp16 table ops marked
  * BITLUT_FLAG_FUSED_TABLES whose consumers are all fast-epilogue 32-stream
  * lookups are folded into them (each consumer runs
- * as bitlut_mpgemv_fused).  bitlut_pipeline_plan_flags writes the per-op
- * plan: launch flags, BITLUT_PLAN_SKIP, BITLUT_FLAG_FUSED_TABLES (see
+ * as bitlut_mpgemv_fused); consecutive table builds, and consecutive
+ * batch-1 fast lookups over the same tables, share one launch.
+ * bitlut_pipeline_plan_flags writes the per-op plan: launch flags,
+ * BITLUT_PLAN_SKIP, BITLUT_FLAG_FUSED_TABLES, BITLUT_PLAN_JOINED (see
  * pipeline.cu for the rules). */
 #define BITLUT_PLAN_SKIP (-1)          /* plan: table op folded into its consumers */
 #define BITLUT_FLAG_FUSED_TABLES 8     /* plan: lookup launched as bitlut_mpgemv_fused */
+#define BITLUT_PLAN_JOINED 16          /* plan: launched together with the previous op
+                                          (bitlut_build_lut_multi / bitlut_mpgemv_multi) */
 int bitlut_pipeline_plan_flags(const bitlut_pipe_op* specs, int n_ops, int* flags_out);
 int bitlut_pipeline_launch_ops(const bitlut_pipe_op* specs, int n_ops, void* stream);
+/* The same launches, but inputs are tracked with per-launch completion
+ * counters instead of PDL waits (no launch drains the stream): `counters` =
+ * device scratch of n_ops + 1 uint32, zeroed by the call (a captured memset);
+ * a final 1-CTA join kernel completes when every CTA of the list has. */
+int bitlut_pipeline_launch_ops_counted(const bitlut_pipe_op* specs, int n_ops, unsigned* counters, void* stream);
 
 /* Number of kernel launches one bitlut_mpgemm call enqueues (for accounting). */
 int bitlut_mpgemm_launches(int m, int k, int bits, int group_size, int mode, int n);

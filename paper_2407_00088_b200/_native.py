@@ -27,6 +27,7 @@ FLAG_PDL = 1
 FLAG_INDEPENDENT = 2
 FLAG_FAST_EPILOGUE = 4
 FLAG_FUSED_TABLES = 8       # table op may fold into its consumers (graph executor)
+PLAN_JOINED = 16            # plan: launched together with the previous op
 
 _vp, _i = ctypes.c_void_p, ctypes.c_int
 
@@ -82,7 +83,9 @@ def lib() -> ctypes.CDLL:
 def exported_symbols() -> list[str]:
     return list(_SIGS) + ["bitlut_version", "bitlut_pipeline_table_bytes", "bitlut_pipeline_encode",
                           "bitlut_pipeline_launch", "bitlut_pipeline_launch_traced",
-                          "bitlut_pipeline_plan_flags", "bitlut_pipeline_launch_ops"]
+                          "bitlut_pipeline_plan_flags", "bitlut_pipeline_launch_ops",
+                          "bitlut_build_lut_multi", "bitlut_mpgemv_multi",
+                          "bitlut_pipeline_launch_ops_counted"]
 
 
 def require_cuda(t: torch.Tensor, what: str) -> None:

@@ -71,6 +71,48 @@ BL_DEV uint4 ld_nc_128(const void* p) {
 BL_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 BL_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// Op-list dependency counters (pipeline.cu graph executor).  A kernel
+// launched with counters uses no griddepcontrol.wait at all: it spins (one
+// thread) until every producer launch has counted all of its CTAs, counts
+// itself when done, and exits without waiting for its stream predecessor
+// (the list ends with a join kernel that waits for every launch's count).  Producers are always resident when a consumer
+// spins: PDL launches a kernel only after every CTA of its predecessor has
+// started, and each kernel of the list is launched after its producers.
+constexpr int kMaxDepWaits = 8;
+struct DepSync {
+  const unsigned* wait_cnt[kMaxDepWaits];
+  unsigned wait_target[kMaxDepWaits];
+  int n_wait;
+  int counted;                // 1: launched by the counted executor (no PDL waits at all)
+  unsigned* done;             // +1 per CTA after its last global write, or null
+  unsigned* total;            // optional: +1 per CTA of every counted launch, or null
+};
+
+BL_DEV unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// every thread of the CTA must call these
+// Callers that read producer data through the async proxy (TMA) afterwards
+// must issue fence_proxy_async() in the issuing thread first.
+BL_DEV void dep_wait(const DepSync& d) {
+  if (threadIdx.x == 0)
+    for (int i = 0; i < d.n_wait; i++)
+      while (ld_acquire_u32(d.wait_cnt[i]) < d.wait_target[i]) __nanosleep(20);
+  __syncthreads();
+}
+BL_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+BL_DEV void dep_signal(const DepSync& d) {
+  if (!d.done) return;
+  __syncthreads();           // the CTA's writes happen-before thread 0's release (bar.sync cumulativity)
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(d.done) : "memory");
+    if (d.total) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(d.total) : "memory");
+  }
+}
+
 BL_DEV float to_f32(float x) { return x; }
 BL_DEV float to_f32(__half x) { return __half2float(x); }
 

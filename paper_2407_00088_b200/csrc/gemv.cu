@@ -97,7 +97,8 @@ gemv_kernel(GemvArgs p) {
   //         A dependent launch lets its successor start only after its own
   //         inputs are complete, so an INDEPENDENT successor (same tables)
   //         can read them without waiting. ----
-  if (!p.independent) bl::pdl_wait();
+  if (p.dep.counted) bl::dep_wait(p.dep);
+  else if (!p.independent) bl::pdl_wait();
   bl::pdl_launch_dependents();
   TRACE(2);
   for (int row = row0; row < row1; row++) {
@@ -111,6 +112,7 @@ gemv_kernel(GemvArgs p) {
     if (MULTI) __syncthreads();         // row done before tsm / rsm / psm are reused
   }
 
+  bl::dep_signal(p.dep);
   if (p.independent) bl::pdl_wait();    // keep stream completion order
   if (p.trace && tid == 0) {
     unsigned int smid;
@@ -165,6 +167,7 @@ int launch_q8(const GemvArgs& a, int n, cudaStream_t stream, bool pdl) {
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.L.n_tiles, (n + a.rows_per_cta - 1) / a.rows_per_cta);
+  if (a.grid_out) *a.grid_out = (int)(cfg.gridDim.x * cfg.gridDim.y);
   cfg.blockDim = dim3(gemv_threads(a.L));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
@@ -223,11 +226,12 @@ bool b1_enabled() {
 // gemv_b1.cu: persistent batch-1 kernel (fast epilogue, 32-stream tiles)
 int bl_gemv_b1_launch(const blk::GemvArgs& g, int scale_dtype, cudaStream_t s, bool pdl);
 
-extern "C" int bitlut_mpgemm_traced(const uint8_t* wgpu, int m, int k, int bits, int group_size,
-                                    const void* wscales, const void* zeros, int scale_dtype,
-                                    const void* tables, const float* tscales, const float* rowsums,
-                                    int mode, int n, float* out, int32_t* partials, int flags,
-                                    unsigned long long* trace, void* stream) {
+// Internal launcher shared by the C entry points and the op-list executor
+// (pipeline.cu), which passes dependency counters and reads the grid size.
+int bl_mpgemm_launch(const uint8_t* wgpu, int m, int k, int bits, int group_size, const void* wscales,
+                     const void* zeros, int scale_dtype, const void* tables, const float* tscales,
+                     const float* rowsums, int mode, int n, float* out, int32_t* partials, int flags,
+                     unsigned long long* trace, void* stream, const bl::DepSync& dep, int* grid_out) {
   bl::LayoutV2 L;
   int rc = bl::make_layout(m, k, bits, group_size, &L);
   if (rc) return rc;
@@ -238,7 +242,9 @@ extern "C" int bitlut_mpgemm_traced(const uint8_t* wgpu, int m, int k, int bits,
   if (mode == BITLUT_TABLE_F16 && partials) return BITLUT_EPARAM;   // int32 partials: Q8 only
   if (n > 65535) return BITLUT_ESHAPE;
   const bool pdl = (flags & BITLUT_FLAG_PDL) != 0;
-  GemvArgs a;
+  GemvArgs a = {};
+  a.dep = dep;
+  a.grid_out = grid_out;
   a.w = wgpu; a.wscales = wscales; a.zeros = zeros;
   a.qtab = reinterpret_cast<const uint8_t*>(tables); a.tscales = tscales; a.rowsums = rowsums;
   a.out = out; a.partials = partials; a.trace = trace; a.L = L;
@@ -259,6 +265,16 @@ extern "C" int bitlut_mpgemm_traced(const uint8_t* wgpu, int m, int k, int bits,
   }
   return scale_dtype == BITLUT_DT_F16 ? dispatch_q8<__half>(a, n, (cudaStream_t)stream, pdl, mode)
                                       : dispatch_q8<float>(a, n, (cudaStream_t)stream, pdl, mode);
+}
+
+extern "C" int bitlut_mpgemm_traced(const uint8_t* wgpu, int m, int k, int bits, int group_size,
+                                    const void* wscales, const void* zeros, int scale_dtype,
+                                    const void* tables, const float* tscales, const float* rowsums,
+                                    int mode, int n, float* out, int32_t* partials, int flags,
+                                    unsigned long long* trace, void* stream) {
+  const bl::DepSync none = {};
+  return bl_mpgemm_launch(wgpu, m, k, bits, group_size, wscales, zeros, scale_dtype, tables, tscales, rowsums,
+                          mode, n, out, partials, flags, trace, stream, none, nullptr);
 }
 
 extern "C" int bitlut_mpgemm(const uint8_t* wgpu, int m, int k, int bits, int group_size,

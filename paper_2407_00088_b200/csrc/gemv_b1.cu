@@ -27,8 +27,23 @@ using namespace blk;
 
 constexpr int kMaxStages = 2;
 
+constexpr int kMaxMats = 4;
+
+// One weight matrix of a (multi-matrix) launch: matrices that share the
+// activation tables (q/k/v, gate/up) are looked up by one launch whose tiles
+// are numbered matrix after matrix.
+struct B1Mat {
+  const uint8_t* w;
+  const void* wscales;
+  const void* zeros;
+  float* out;
+  int tile_end;               // cumulative tile count up to and including this matrix
+};
+
 struct B1Args {
-  GemvArgs g;
+  GemvArgs g;                 // L: the shared layout (k, bits, gs); tables, flags
+  int n_mats, total_tiles;
+  B1Mat mats[kMaxMats];
   const __half* act;          // fused variant: fp16 activation row (tables built in-kernel)
   uint32_t sa_off, red_off;   // fused: activation staging (4*T floats) + group-max scratch
   int rounds;                 // unit rounds per tile (units = KG / R)
@@ -140,20 +155,28 @@ __device__ __forceinline__ int reduce_lanes(T (&v)[NV], int lane) {
   return base;
 }
 
+__device__ __forceinline__ int find_mat(const B1Args& a, int tile, int& local) {
+  int j = 0;
+  while (j + 1 < a.n_mats && tile >= a.mats[j].tile_end) j++;
+  local = tile - (j ? a.mats[j - 1].tile_end : 0);
+  return j;
+}
+
 template <typename ST>
 __device__ __forceinline__ void issue_stage(const B1Args& a, int tile, uint8_t* sb, uint64_t* bar, uint64_t pol) {
-  const GemvArgs& p = a.g;
-  const bl::LayoutV2& L = p.L;
-  const bool zeros = p.zeros != nullptr;
+  const bl::LayoutV2& L = a.g.L;
+  int local;
+  const B1Mat& mt = a.mats[find_mat(a, tile, local)];
+  const bool zeros = mt.zeros != nullptr;
   mbar_expect_tx(bar, a.w_bytes + a.s_bytes * (zeros ? 2u : 1u));
-  const uint8_t* src = p.w + L.sg_row_base(tile, 0);
+  const uint8_t* src = mt.w + L.sg_row_base(local, 0);
   for (uint32_t off = 0; off < a.w_bytes; off += 32768u) {
     const uint32_t nb = a.w_bytes - off < 32768u ? a.w_bytes - off : 32768u;
     bulk_g2s(sb + off, src + off, nb, bar, pol);
   }
-  const int64_t e0 = (int64_t)tile * L.tile_ch * L.NQ;
-  bulk_g2s(sb + a.s_off, reinterpret_cast<const ST*>(p.wscales) + e0, a.s_bytes, bar, pol);
-  if (zeros) bulk_g2s(sb + a.z_off, reinterpret_cast<const ST*>(p.zeros) + e0, a.s_bytes, bar, pol);
+  const int64_t e0 = (int64_t)local * L.tile_ch * L.NQ;
+  bulk_g2s(sb + a.s_off, reinterpret_cast<const ST*>(mt.wscales) + e0, a.s_bytes, bar, pol);
+  if (zeros) bulk_g2s(sb + a.z_off, reinterpret_cast<const ST*>(mt.zeros) + e0, a.s_bytes, bar, pol);
 }
 
 // ---- fused table build (cluster-cooperative) ----
@@ -197,7 +220,7 @@ template <int R>
 __device__ __forceinline__ void fused_tables(const B1Args& a, uint8_t* smem) {
   const bl::LayoutV2& L = a.g.L;
   const int tid = threadIdx.x, T = blockDim.x;
-  const int KG = L.KG, NQ = L.NQ, gs = L.gs, gpg = gs >> 2, U = L.U;
+  const int NQ = L.NQ, gs = L.gs, gpg = gs >> 2, U = L.U;
   const uint32_t rank = cluster_rank(), cs = cluster_size();
   const int gpr = (NQ + (int)cs - 1) / (int)cs;
   const int g0 = (int)rank * gpr, g1 = min(NQ, g0 + gpr);
@@ -300,7 +323,7 @@ __global__ void __launch_bounds__(256) gemv_b1_kernel(const __grid_constant__ B1
   float* rsm = reinterpret_cast<float*>(smem + a.rs_off);
   float* ysm = reinterpret_cast<float*>(smem + a.y_off);
   const uint8_t* tab = smem + a.tab_off;
-  const int ntl = L.n_tiles, step = gridDim.x;
+  const int ntl = a.total_tiles, step = gridDim.x;
   const int S = a.stages;
 
   if (FUSED) cluster_arrive_relaxed();                 // paired with the wait in fused_tables
@@ -315,9 +338,11 @@ __global__ void __launch_bounds__(256) gemv_b1_kernel(const __grid_constant__ B1
     }
   }
   // ---- 2. tables / table scales / row sums come from the previous kernel ----
-  if (!p.independent) bl::pdl_wait();
+  if (p.dep.counted) bl::dep_wait(p.dep);
+  else if (!p.independent) bl::pdl_wait();
   bl::pdl_launch_dependents();
   if (!FUSED && a.tab_smem && tid == 0) {
+    if (p.dep.counted) bl::fence_proxy_async();        // tables were written by another launch
     const uint32_t tb = (uint32_t)KG * 8;
     mbar_expect_tx(bar + kMaxStages, tb);
     for (uint32_t off = 0; off < tb; off += 32768u) {
@@ -348,7 +373,7 @@ __global__ void __launch_bounds__(256) gemv_b1_kernel(const __grid_constant__ B1
   __syncthreads();                                      // barriers initialised, tsm / rsm ready
   if (!FUSED && a.tab_smem) mbar_wait(bar + kMaxStages, 0);
 
-  const bool has_zeros = p.zeros != nullptr;
+  const bool has_zeros = a.mats[0].zeros != nullptr;     // uniform across the matrices
   const float h2 = (float)(2 << (BITS - 1));
   int it = 0;
   for (int tile = blockIdx.x; tile < ntl; tile += step, it++) {
@@ -431,9 +456,12 @@ __global__ void __launch_bounds__(256) gemv_b1_kernel(const __grid_constant__ B1
       const float* yr = ysm + (it & 1) * NW * TCH + tid;
       float s = 0.f;
       for (int w = 0; w < NW; w++) s += yr[w * TCH];
-      p.out[(int64_t)tile * TCH + tid] = 0.5f * s;
+      int local;
+      const int j = find_mat(a, tile, local);
+      a.mats[j].out[(int64_t)local * TCH + tid] = 0.5f * s;
     }
   }
+  bl::dep_signal(p.dep);
   if (p.independent) bl::pdl_wait();                    // keep stream completion order
 }
 
@@ -462,13 +490,18 @@ int b1_threads(const bl::LayoutV2& L) {
 }
 
 template <int R, int LG, int BITS, typename ST, bool FUSED>
-int launch_b1(const GemvArgs& g, const __half* act, cudaStream_t stream, bool pdl) {
+int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* act, cudaStream_t stream,
+              bool pdl) {
   const bl::LayoutV2& L = g.L;
   const int T = b1_threads(L);
   if (FUSED && T % (L.gs / 4) != 0) return BITLUT_ELAYOUT;
+  if (n_mats < 1 || n_mats > kMaxMats) return BITLUT_EPARAM;
   B1Args a;
   a.g = g;
   a.act = act;
+  a.n_mats = n_mats;
+  for (int j = 0; j < n_mats; j++) a.mats[j] = mats[j];
+  a.total_tiles = mats[n_mats - 1].tile_end;
   a.rounds = (L.U + T - 1) / T;
   a.tab_smem = FUSED || a.rounds > 1;
   auto kern = gemv_b1_kernel<R, LG, BITS, ST, FUSED>;
@@ -489,25 +522,26 @@ int launch_b1(const GemvArgs& g, const __half* act, cudaStream_t stream, bool pd
     tpc_env = e ? atoi(e) : 0;
   }
   // one stage when every CTA gets a single tile, else double-buffer
-  B1Plan s = b1_plan<ST>(L, g.zeros != nullptr, a.tab_smem, T, 1, FUSED);
+  const bool zeros = mats[0].zeros != nullptr;
+  B1Plan s = b1_plan<ST>(L, zeros, a.tab_smem, T, 1, FUSED);
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, s.total) != cudaSuccess || per_sm < 1)
     return BITLUT_ELAYOUT;
-  const B1Plan s2 = b1_plan<ST>(L, g.zeros != nullptr, a.tab_smem, T, 2, FUSED);
+  const B1Plan s2 = b1_plan<ST>(L, zeros, a.tab_smem, T, 2, FUSED);
   int per_sm2 = 0;
   if (s2.total > 227 * 1024 ||
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, kern, T, s2.total) != cudaSuccess)
     per_sm2 = 0;
   // two tiles per CTA only where the double-buffered plan still leaves
   // several CTAs per SM (short K); long-K tiles want every CTA they can get
-  int tiles_per_cta = tpc_env > 0 ? tpc_env : ((g.independent && per_sm2 >= 3) ? 2 : 1);
-  if (tpc_env <= 0 && (L.n_tiles + tiles_per_cta - 1) / tiles_per_cta < sm_count() / 2) tiles_per_cta = 1;
-  const int want = (L.n_tiles + tiles_per_cta - 1) / tiles_per_cta;
+  int tiles_per_cta = tpc_env > 0 ? tpc_env : (((g.independent || g.dep.counted) && per_sm2 >= 3) ? 2 : 1);
+  if (tpc_env <= 0 && (a.total_tiles + tiles_per_cta - 1) / tiles_per_cta < sm_count() / 2) tiles_per_cta = 1;
+  const int want = (a.total_tiles + tiles_per_cta - 1) / tiles_per_cta;
   // double-buffer when CTAs get several tiles -- by choice (tiles_per_cta)
   // or because one wave cannot hold every tile -- unless that costs
   // resident CTAs (then the single stage refills after each tile)
   a.stages = 1;
-  if (per_sm2 >= 1 && (tiles_per_cta > 1 || (sm_count() * per_sm < L.n_tiles && per_sm2 >= per_sm))) {
+  if (per_sm2 >= 1 && (tiles_per_cta > 1 || (sm_count() * per_sm < a.total_tiles && per_sm2 >= per_sm))) {
     s = s2; per_sm = per_sm2; a.stages = 2;
   }
   if (s.total > 227 * 1024) return BITLUT_ELAYOUT;
@@ -518,6 +552,7 @@ int launch_b1(const GemvArgs& g, const __half* act, cudaStream_t stream, bool pd
   if (grid > want) grid = want;
   const int cs = FUSED ? kClusterCTAs : 1;
   grid = (grid + cs - 1) / cs * cs;                     // spare CTAs only build their table slice
+  if (g.grid_out) *g.grid_out = grid;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(T);
@@ -536,30 +571,36 @@ int launch_b1(const GemvArgs& g, const __half* act, cudaStream_t stream, bool pd
 }
 
 template <int R, int LG, typename ST, bool FUSED>
-int launch_b1_bits(const GemvArgs& g, const __half* act, cudaStream_t s, bool pdl) {
+int launch_b1_bits(const GemvArgs& g, const B1Mat* m, int nm, const __half* act, cudaStream_t s, bool pdl) {
   switch (g.L.bits) {
-    case 1: return launch_b1<R, LG, 1, ST, FUSED>(g, act, s, pdl);
-    case 2: return launch_b1<R, LG, 2, ST, FUSED>(g, act, s, pdl);
-    case 4: return launch_b1<R, LG, 4, ST, FUSED>(g, act, s, pdl);
+    case 1: return launch_b1<R, LG, 1, ST, FUSED>(g, m, nm, act, s, pdl);
+    case 2: return launch_b1<R, LG, 2, ST, FUSED>(g, m, nm, act, s, pdl);
+    case 4: return launch_b1<R, LG, 4, ST, FUSED>(g, m, nm, act, s, pdl);
   }
   return BITLUT_EPARAM;
 }
 
 template <typename ST, bool FUSED>
-int dispatch_b1(const GemvArgs& g, const __half* act, cudaStream_t s, bool pdl) {
+int dispatch_b1(const GemvArgs& g, const B1Mat* m, int nm, const __half* act, cudaStream_t s, bool pdl) {
   const int R = g.L.R, LG = g.L.Lg;
   if (R == 8) {
     switch (LG) {
-      case 1: return launch_b1_bits<8, 1, ST, FUSED>(g, act, s, pdl);
-      case 2: return launch_b1_bits<8, 2, ST, FUSED>(g, act, s, pdl);
-      case 4: return launch_b1_bits<8, 4, ST, FUSED>(g, act, s, pdl);
-      case 8: return launch_b1_bits<8, 8, ST, FUSED>(g, act, s, pdl);
-      case 16: return launch_b1_bits<8, 16, ST, FUSED>(g, act, s, pdl);
+      case 1: return launch_b1_bits<8, 1, ST, FUSED>(g, m, nm, act, s, pdl);
+      case 2: return launch_b1_bits<8, 2, ST, FUSED>(g, m, nm, act, s, pdl);
+      case 4: return launch_b1_bits<8, 4, ST, FUSED>(g, m, nm, act, s, pdl);
+      case 8: return launch_b1_bits<8, 8, ST, FUSED>(g, m, nm, act, s, pdl);
+      case 16: return launch_b1_bits<8, 16, ST, FUSED>(g, m, nm, act, s, pdl);
     }
   } else if (R == 4 && LG == 1) {
-    return launch_b1_bits<4, 1, ST, FUSED>(g, act, s, pdl);
+    return launch_b1_bits<4, 1, ST, FUSED>(g, m, nm, act, s, pdl);
   }
   return BITLUT_EPARAM;
+}
+
+B1Mat single_mat(const GemvArgs& g) {
+  B1Mat m;
+  m.w = g.w; m.wscales = g.wscales; m.zeros = g.zeros; m.out = g.out; m.tile_end = g.L.n_tiles;
+  return m;
 }
 
 }  // namespace
@@ -569,8 +610,9 @@ int dispatch_b1(const GemvArgs& g, const __half* act, cudaStream_t s, bool pdl) 
 // shared-memory plan (the caller then uses the per-tile kernel).
 int bl_gemv_b1_launch(const GemvArgs& g, int scale_dtype, cudaStream_t s, bool pdl) {
   if (g.L.n_sg != 1) return BITLUT_ELAYOUT;
-  return scale_dtype == BITLUT_DT_F16 ? dispatch_b1<__half, false>(g, nullptr, s, pdl)
-                                      : dispatch_b1<float, false>(g, nullptr, s, pdl);
+  const B1Mat m = single_mat(g);
+  return scale_dtype == BITLUT_DT_F16 ? dispatch_b1<__half, false>(g, &m, 1, nullptr, s, pdl)
+                                      : dispatch_b1<float, false>(g, &m, 1, nullptr, s, pdl);
 }
 
 bool bl_gemv_b1_fused_fits(const bl::LayoutV2& L, bool zeros, int scale_dtype) {
@@ -584,9 +626,21 @@ bool bl_gemv_b1_fused_fits(const bl::LayoutV2& L, bool zeros, int scale_dtype) {
 
 // Table build + lookup in ONE launch for a batch-1 fp16 activation row
 // (fast epilogue): see include/bitlut_b200.h.
+int bl_mpgemv_fused_launch(const void* a, int a_dtype, const uint8_t* wgpu, int m, int k, int bits,
+                           int group_size, const void* wscales, const void* zeros, int scale_dtype, float* out,
+                           int flags, void* stream, const bl::DepSync& dep, int* grid_out);
+
 extern "C" int bitlut_mpgemv_fused(const void* a, int a_dtype, const uint8_t* wgpu, int m, int k, int bits,
                                    int group_size, const void* wscales, const void* zeros, int scale_dtype,
                                    float* out, int flags, void* stream) {
+  const bl::DepSync none = {};
+  return bl_mpgemv_fused_launch(a, a_dtype, wgpu, m, k, bits, group_size, wscales, zeros, scale_dtype, out,
+                                flags, stream, none, nullptr);
+}
+
+int bl_mpgemv_fused_launch(const void* a, int a_dtype, const uint8_t* wgpu, int m, int k, int bits,
+                           int group_size, const void* wscales, const void* zeros, int scale_dtype, float* out,
+                           int flags, void* stream, const bl::DepSync& dep, int* grid_out) {
   bl::LayoutV2 L;
   int rc = bl::make_layout(m, k, bits, group_size, &L);
   if (rc) return rc;
@@ -598,10 +652,59 @@ extern "C" int bitlut_mpgemv_fused(const void* a, int a_dtype, const uint8_t* wg
   GemvArgs g = {};
   g.w = wgpu; g.wscales = wscales; g.zeros = zeros;
   g.out = out; g.L = L;
+  g.dep = dep;
+  g.grid_out = grid_out;
   g.independent = pdl && (flags & BITLUT_FLAG_INDEPENDENT) != 0;
   g.fast = 1;
   g.rows_per_cta = 1; g.n_rows = 1;
   const __half* act = reinterpret_cast<const __half*>(a);
-  return scale_dtype == BITLUT_DT_F16 ? dispatch_b1<__half, true>(g, act, (cudaStream_t)stream, pdl)
-                                      : dispatch_b1<float, true>(g, act, (cudaStream_t)stream, pdl);
+  const B1Mat mt = single_mat(g);
+  return scale_dtype == BITLUT_DT_F16 ? dispatch_b1<__half, true>(g, &mt, 1, act, (cudaStream_t)stream, pdl)
+                                      : dispatch_b1<float, true>(g, &mt, 1, act, (cudaStream_t)stream, pdl);
+}
+
+int bl_mpgemv_multi_launch(const bitlut_mat* mats, int n_mats, int k, int bits, int group_size,
+                           int scale_dtype, const void* tables, const float* tscales, const float* rowsums,
+                           int flags, void* stream, const bl::DepSync& dep, int* grid_out);
+
+// Several matrices sharing one activation row's tables in ONE batch-1 launch
+// (q/k/v, gate/up): see include/bitlut_b200.h.
+extern "C" int bitlut_mpgemv_multi(const bitlut_mat* mats, int n_mats, int k, int bits, int group_size,
+                                   int scale_dtype, const void* tables, const float* tscales,
+                                   const float* rowsums, int flags, void* stream) {
+  const bl::DepSync none = {};
+  return bl_mpgemv_multi_launch(mats, n_mats, k, bits, group_size, scale_dtype, tables, tscales, rowsums,
+                                flags, stream, none, nullptr);
+}
+
+int bl_mpgemv_multi_launch(const bitlut_mat* mats, int n_mats, int k, int bits, int group_size,
+                           int scale_dtype, const void* tables, const float* tscales, const float* rowsums,
+                           int flags, void* stream, const bl::DepSync& dep, int* grid_out) {
+  if (!mats || n_mats < 1 || n_mats > kMaxMats || !tables || !tscales || !rowsums) return BITLUT_EPARAM;
+  if (scale_dtype != BITLUT_DT_F32 && scale_dtype != BITLUT_DT_F16) return BITLUT_EPARAM;
+  if (!(flags & BITLUT_FLAG_FAST_EPILOGUE)) return BITLUT_EPARAM;
+  bl::LayoutV2 L;
+  B1Mat ms[kMaxMats];
+  int tiles = 0;
+  for (int j = 0; j < n_mats; j++) {
+    int rc = bl::make_layout(mats[j].m, k, bits, group_size, &L);
+    if (rc) return rc;
+    if (!mats[j].wgpu || !mats[j].wscales || !mats[j].out) return BITLUT_EPARAM;
+    if ((mats[j].zeros != nullptr) != (mats[0].zeros != nullptr)) return BITLUT_EPARAM;
+    tiles += L.n_tiles;
+    ms[j].w = mats[j].wgpu; ms[j].wscales = mats[j].wscales; ms[j].zeros = mats[j].zeros;
+    ms[j].out = mats[j].out; ms[j].tile_end = tiles;
+  }
+  if (L.n_sg != 1) return BITLUT_ELAYOUT;
+  const bool pdl = (flags & BITLUT_FLAG_PDL) != 0;
+  GemvArgs g = {};
+  g.qtab = reinterpret_cast<const uint8_t*>(tables); g.tscales = tscales; g.rowsums = rowsums;
+  g.L = L;
+  g.dep = dep;
+  g.grid_out = grid_out;
+  g.independent = pdl && (flags & BITLUT_FLAG_INDEPENDENT) != 0;
+  g.fast = 1;
+  g.rows_per_cta = 1; g.n_rows = 1;
+  return scale_dtype == BITLUT_DT_F16 ? dispatch_b1<__half, false>(g, ms, n_mats, nullptr, (cudaStream_t)stream, pdl)
+                                      : dispatch_b1<float, false>(g, ms, n_mats, nullptr, (cudaStream_t)stream, pdl);
 }

@@ -24,6 +24,8 @@ struct GemvArgs {
   int rows_per_cta;          // activation rows processed per CTA (weights loaded once)
   int n_rows;
   bl::LayoutV2 L;
+  bl::DepSync dep;           // op-list counters (n_wait == 0 and done == null otherwise)
+  int* grid_out;             // host: receives the launch's CTA count (op-list executor), or null
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {

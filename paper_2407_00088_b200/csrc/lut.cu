@@ -112,14 +112,45 @@ constexpr int kLutThreads = 256;
 template <int MODE, typename AT>
 __global__ void __launch_bounds__(kLutThreads)
 build_lut_kernel(const AT* __restrict__ a, int k, int gs, void* __restrict__ tables,
-                 float* __restrict__ tscales, float* __restrict__ rowsums, int independent) {
+                 float* __restrict__ tscales, float* __restrict__ rowsums, int independent,
+                 const bl::DepSync dep) {
   bl::pdl_launch_dependents();
-  if (!independent) bl::pdl_wait();     // activations come from the previous kernel
+  if (dep.counted) bl::dep_wait(dep);
+  else if (!independent) bl::pdl_wait();   // activations come from the previous kernel
   __shared__ __align__(16) float sa[kLutThreads * 4];
   __shared__ float red[kLutThreads / 32];
   lutk::lut_block<MODE, AT>(a, k, gs, tables, tscales, rowsums, blockIdx.y, blockIdx.x * kLutThreads,
                             sa, red);
+  bl::dep_signal(dep);
   if (independent) bl::pdl_wait();      // keep stream completion order
+}
+
+// ---- several table builds in one launch (op lists: every activation row a
+// layer's GEMVs read) ----
+constexpr int kMaxLutJobs = 8;
+struct LutJobs {
+  bl::DepSync dep;
+  int n_jobs, independent;
+  bitlut_lut_job job[kMaxLutJobs];
+  int block_end[kMaxLutJobs];          // cumulative blocks (ceil(KG/256) * n per job)
+};
+
+template <int MODE, typename AT>
+__global__ void __launch_bounds__(kLutThreads) build_lut_multi_kernel(const __grid_constant__ LutJobs J) {
+  bl::pdl_launch_dependents();
+  if (J.dep.counted) bl::dep_wait(J.dep);
+  else if (!J.independent) bl::pdl_wait();
+  __shared__ __align__(16) float sa[kLutThreads * 4];
+  __shared__ float red[kLutThreads / 32];
+  int j = 0;
+  while (j + 1 < J.n_jobs && (int)blockIdx.x >= J.block_end[j]) j++;
+  const int b = blockIdx.x - (j ? J.block_end[j - 1] : 0);
+  const bitlut_lut_job& jb = J.job[j];
+  const int bx = (jb.k / 4 + kLutThreads - 1) / kLutThreads;
+  lutk::lut_block<MODE, AT>(reinterpret_cast<const AT*>(jb.a), jb.k, jb.group_size, jb.tables, jb.tscales,
+                            jb.rowsums, b / bx, (b % bx) * kLutThreads, sa, red);
+  bl::dep_signal(J.dep);
+  if (J.independent) bl::pdl_wait();
 }
 
 inline int grid_1d(int64_t n, int threads) {
@@ -177,10 +208,11 @@ extern "C" int bitlut_row_sums(const void* a, int a_dtype, int n, int k, int gro
 
 int bl_build_lut_launch(const void* a, int a_dtype, int n, int k, int group_size, int mode,
                         void* tables, float* tscales, float* rowsums, cudaStream_t stream, bool pdl,
-                        bool independent) {
+                        bool independent, const bl::DepSync& dep, int* grid_out) {
   const int ind = (pdl && independent) ? 1 : 0;
   const int KG = k / 4;
   dim3 grid((KG + kLutThreads - 1) / kLutThreads, n);
+  if (grid_out) *grid_out = (int)(grid.x * grid.y);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid; cfg.blockDim = dim3(kLutThreads); cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -191,15 +223,15 @@ int bl_build_lut_launch(const void* a, int a_dtype, int n, int k, int group_size
   if (mode == BITLUT_TABLE_Q8) {
     e = a_dtype == BITLUT_DT_F16
             ? cudaLaunchKernelEx(&cfg, build_lut_kernel<BITLUT_TABLE_Q8, __half>, (const __half*)a, k, group_size,
-                                 tables, tscales, rowsums, ind)
+                                 tables, tscales, rowsums, ind, dep)
             : cudaLaunchKernelEx(&cfg, build_lut_kernel<BITLUT_TABLE_Q8, float>, (const float*)a, k, group_size,
-                                 tables, tscales, rowsums, ind);
+                                 tables, tscales, rowsums, ind, dep);
   } else {
     e = a_dtype == BITLUT_DT_F16
             ? cudaLaunchKernelEx(&cfg, build_lut_kernel<BITLUT_TABLE_F16, __half>, (const __half*)a, k, group_size,
-                                 tables, tscales, rowsums, ind)
+                                 tables, tscales, rowsums, ind, dep)
             : cudaLaunchKernelEx(&cfg, build_lut_kernel<BITLUT_TABLE_F16, float>, (const float*)a, k, group_size,
-                                 tables, tscales, rowsums, ind);
+                                 tables, tscales, rowsums, ind, dep);
   }
   return e == cudaSuccess ? BITLUT_OK : BITLUT_EINTERNAL;
 }
@@ -213,7 +245,56 @@ extern "C" int bitlut_build_lut(const void* a, int a_dtype, int n, int k, int gr
   int gpg = group_size / 4;
   if (gpg > 128 || (gpg & (gpg - 1))) return BITLUT_EPARAM;   // CUDA path: power-of-two k-groups per group
   if (n == 0 || k == 0) return BITLUT_OK;
+  const bl::DepSync none = {};
   return bl_build_lut_launch(a, a_dtype, n, k, group_size, mode, tables, tscales, rowsums,
                              (cudaStream_t)stream, (flags & BITLUT_FLAG_PDL) != 0,
-                             (flags & BITLUT_FLAG_INDEPENDENT) != 0);
+                             (flags & BITLUT_FLAG_INDEPENDENT) != 0, none, nullptr);
+}
+
+int bl_build_lut_multi_launch(const bitlut_lut_job* jobs, int n_jobs, int mode, int flags, void* stream,
+                              const bl::DepSync& dep, int* grid_out);
+
+extern "C" int bitlut_build_lut_multi(const bitlut_lut_job* jobs, int n_jobs, int mode, int flags, void* stream) {
+  const bl::DepSync none = {};
+  return bl_build_lut_multi_launch(jobs, n_jobs, mode, flags, stream, none, nullptr);
+}
+
+int bl_build_lut_multi_launch(const bitlut_lut_job* jobs, int n_jobs, int mode, int flags, void* stream,
+                              const bl::DepSync& dep, int* grid_out) {
+  if (!jobs || n_jobs < 1 || n_jobs > kMaxLutJobs) return BITLUT_EPARAM;
+  if (mode != BITLUT_TABLE_Q8 && mode != BITLUT_TABLE_F16) return BITLUT_EPARAM;
+  LutJobs J;
+  J.dep = dep;
+  J.n_jobs = n_jobs;
+  const bool pdl = (flags & BITLUT_FLAG_PDL) != 0;
+  J.independent = pdl && (flags & BITLUT_FLAG_INDEPENDENT) != 0;
+  int blocks = 0;
+  for (int i = 0; i < n_jobs; i++) {
+    const bitlut_lut_job& jb = jobs[i];
+    if (jb.a_dtype != jobs[0].a_dtype) return BITLUT_EPARAM;        // one instantiation per launch
+    if (jb.a_dtype != BITLUT_DT_F32 && jb.a_dtype != BITLUT_DT_F16) return BITLUT_EPARAM;
+    if (jb.n < 1 || jb.k < 4 || jb.group_size < 4) return BITLUT_EPARAM;
+    if (jb.k % jb.group_size != 0 || jb.group_size % 4 != 0) return BITLUT_ELAYOUT;
+    const int gpg = jb.group_size / 4;
+    if (gpg > 128 || (gpg & (gpg - 1))) return BITLUT_EPARAM;
+    blocks += ((jb.k / 4 + kLutThreads - 1) / kLutThreads) * jb.n;
+    J.job[i] = jb;
+    J.block_end[i] = blocks;
+  }
+  if (grid_out) *grid_out = blocks;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks); cfg.blockDim = dim3(kLutThreads); cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr; cfg.numAttrs = 1;
+  const bool f16 = jobs[0].a_dtype == BITLUT_DT_F16;
+  cudaError_t e;
+  if (mode == BITLUT_TABLE_Q8)
+    e = f16 ? cudaLaunchKernelEx(&cfg, build_lut_multi_kernel<BITLUT_TABLE_Q8, __half>, J)
+            : cudaLaunchKernelEx(&cfg, build_lut_multi_kernel<BITLUT_TABLE_Q8, float>, J);
+  else
+    e = f16 ? cudaLaunchKernelEx(&cfg, build_lut_multi_kernel<BITLUT_TABLE_F16, __half>, J)
+            : cudaLaunchKernelEx(&cfg, build_lut_multi_kernel<BITLUT_TABLE_F16, float>, J);
+  return e == cudaSuccess ? BITLUT_OK : BITLUT_EINTERNAL;
 }

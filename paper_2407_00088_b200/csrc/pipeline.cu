@@ -305,6 +305,37 @@ static bool fusable_lookup(const bitlut_pipe_op& s, const bitlut_pipe_op& t) {
   return bl_gemv_b1_fused_fits(L, s.zeros != nullptr, s.scale_dtype);
 }
 
+static bool groupable_tables(const bitlut_pipe_op& a, const bitlut_pipe_op& b) {
+  return a.type == BITLUT_OP_TABLES && b.type == BITLUT_OP_TABLES && a.a_dtype == b.a_dtype;
+}
+
+// Lookups that read the same table op (single dep) and can share one batch-1
+// launch (bitlut_mpgemv_multi): q/k/v, gate/up.
+static bool groupable_lookups(const bitlut_pipe_op& a, const bitlut_pipe_op& b, const bitlut_pipe_op* specs) {
+  if (a.type != BITLUT_OP_LOOKUP || b.type != BITLUT_OP_LOOKUP) return false;
+  if (a.dep[0] < 0 || a.dep[1] >= 0 || a.dep[2] >= 0 || b.dep[0] != a.dep[0] || b.dep[1] >= 0 || b.dep[2] >= 0)
+    return false;
+  if (!(a.flags & BITLUT_FLAG_FAST_EPILOGUE) || !(b.flags & BITLUT_FLAG_FAST_EPILOGUE)) return false;
+  if (a.n != 1 || b.n != 1 || a.k != b.k || a.bits != b.bits || a.group_size != b.group_size) return false;
+  if (a.scale_dtype != b.scale_dtype || (a.zeros != nullptr) != (b.zeros != nullptr)) return false;
+  if (specs[a.dep[0]].type != BITLUT_OP_TABLES) return false;
+  bl::LayoutV2 L;
+  if (bl::make_layout(a.m, a.k, a.bits, a.group_size, &L) || L.n_sg != 1) return false;
+  if (bl::make_layout(b.m, b.k, b.bits, b.group_size, &L) || L.n_sg != 1) return false;
+  return true;
+}
+
+static bool grouping_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("BITLUT_PLAN_NOGROUP");      // diagnostic: 1 disables launch grouping
+    on = (e && atoi(e)) ? 0 : 1;
+  }
+  return on != 0;
+}
+
+constexpr int kMaxGroupTables = 8, kMaxGroupLookups = 4;
+
 extern "C" int bitlut_pipeline_plan_flags(const bitlut_pipe_op* specs, int n_ops, int* flags_out) {
   if (n_ops <= 0 || !specs || !flags_out) return BITLUT_EPARAM;
   for (int i = 0; i < n_ops; i++) {
@@ -313,7 +344,7 @@ extern "C" int bitlut_pipeline_plan_flags(const bitlut_pipe_op* specs, int n_ops
       if (specs[i].dep[d] >= i || specs[i].dep[d] < -1) return BITLUT_EPARAM;
     flags_out[i] = 0;
   }
-  // which table ops can be folded into all of their consumers
+  // 1. which table ops can be folded into all of their consumers
   for (int t = 0; t < n_ops; t++) {
     if (specs[t].type != BITLUT_OP_TABLES || !(specs[t].flags & BITLUT_FLAG_FUSED_TABLES)) continue;
     bool all = true, any = false;
@@ -333,23 +364,50 @@ extern "C" int bitlut_pipeline_plan_flags(const bitlut_pipe_op* specs, int n_ops
         if (specs[i].dep[0] == t) flags_out[i] = BITLUT_FLAG_FUSED_TABLES;
     }
   }
+  // 2. launch groups: consecutive table builds; consecutive lookups over the same tables
+  if (grouping_enabled()) {
+    int lead = -1, size = 0;
+    for (int i = 0; i < n_ops; i++) {
+      if (flags_out[i] == BITLUT_PLAN_SKIP) continue;
+      const bool plain = !(flags_out[i] & BITLUT_FLAG_FUSED_TABLES);
+      bool join = false;
+      if (lead >= 0 && plain && !(flags_out[lead] & BITLUT_FLAG_FUSED_TABLES)) {
+        if (groupable_tables(specs[lead], specs[i])) join = size < kMaxGroupTables;
+        else if (groupable_lookups(specs[lead], specs[i], specs)) join = size < kMaxGroupLookups;
+      }
+      if (join) {
+        flags_out[i] |= BITLUT_PLAN_JOINED;
+        size++;
+      } else {
+        lead = i;
+        size = 1;
+      }
+    }
+  }
+  // 3. launch flags per launch unit (a group runs as one kernel)
   int done_below = 0;            // ops [0, done_below) complete when the next kernel starts
-  for (int i = 0; i < n_ops; i++) {
-    const bitlut_pipe_op& s = specs[i];
-    if (flags_out[i] == BITLUT_PLAN_SKIP) continue;
-    int fl = BITLUT_FLAG_PDL | flags_out[i];
-    const int* deps = (fl & BITLUT_FLAG_FUSED_TABLES) ? specs[s.dep[0]].dep : s.dep;
+  for (int i = 0; i < n_ops;) {
+    if (flags_out[i] == BITLUT_PLAN_SKIP) { i++; continue; }
+    int j = i + 1;
+    while (j < n_ops && flags_out[j] != BITLUT_PLAN_SKIP && (flags_out[j] & BITLUT_PLAN_JOINED)) j++;
     // inputs from before the op list are complete once any kernel of the
     // list has waited (done_below >= 1)
     bool ok = done_below >= 1;
-    for (int d = 0; d < 3; d++)
-      if (deps[d] >= 0) ok = ok && deps[d] < done_below;
-    if (ok) fl |= BITLUT_FLAG_INDEPENDENT;
-    if (s.type == BITLUT_OP_LOOKUP) {
-      if (!ok) done_below = i;    // waits for its predecessor (hence all earlier), then releases
-      fl |= s.flags & BITLUT_FLAG_FAST_EPILOGUE;
+    for (int u = i; u < j; u++) {
+      const bitlut_pipe_op& s = specs[u];
+      const int* deps = (flags_out[u] & BITLUT_FLAG_FUSED_TABLES) ? specs[s.dep[0]].dep : s.dep;
+      for (int d = 0; d < 3; d++)
+        if (deps[d] >= 0) ok = ok && deps[d] < done_below;
     }
-    flags_out[i] = fl;
+    const bool lookup = specs[i].type == BITLUT_OP_LOOKUP;
+    for (int u = i; u < j; u++) {
+      int fl = BITLUT_FLAG_PDL | flags_out[u];
+      if (ok) fl |= BITLUT_FLAG_INDEPENDENT;
+      if (lookup) fl |= specs[u].flags & BITLUT_FLAG_FAST_EPILOGUE;
+      flags_out[u] = fl;
+    }
+    if (lookup && !ok) done_below = i;   // waits for its predecessor (hence all earlier), then releases
+    i = j;
   }
   return BITLUT_OK;
 }
@@ -360,22 +418,188 @@ extern "C" int bitlut_pipeline_launch_ops(const bitlut_pipe_op* specs, int n_ops
   int* flags = n_ops <= 256 ? stack_flags : static_cast<int*>(malloc(sizeof(int) * n_ops));
   if (!flags) return BITLUT_EINTERNAL;
   int rc = bitlut_pipeline_plan_flags(specs, n_ops, flags);
-  for (int i = 0; rc == BITLUT_OK && i < n_ops; i++) {
+  for (int i = 0; rc == BITLUT_OK && i < n_ops;) {
     const bitlut_pipe_op& s = specs[i];
     const int fl = flags[i];
-    if (fl == BITLUT_PLAN_SKIP) continue;
+    if (fl == BITLUT_PLAN_SKIP) { i++; continue; }
+    int j = i + 1;
+    while (j < n_ops && flags[j] != BITLUT_PLAN_SKIP && (flags[j] & BITLUT_PLAN_JOINED)) j++;
+    const int lf = fl & (BITLUT_FLAG_PDL | BITLUT_FLAG_INDEPENDENT | BITLUT_FLAG_FAST_EPILOGUE);
     if (s.type == BITLUT_OP_TABLES) {
-      rc = bitlut_build_lut(s.a, s.a_dtype, s.n, s.k, s.group_size, BITLUT_TABLE_Q8, s.tables,
-                            s.tscales, s.rowsums, fl, stream);
+      if (j - i == 1) {
+        rc = bitlut_build_lut(s.a, s.a_dtype, s.n, s.k, s.group_size, BITLUT_TABLE_Q8, s.tables,
+                              s.tscales, s.rowsums, lf, stream);
+      } else {
+        bitlut_lut_job jobs[kMaxGroupTables];
+        for (int u = i; u < j; u++) {
+          const bitlut_pipe_op& t = specs[u];
+          jobs[u - i] = {t.a, t.a_dtype, t.n, t.k, t.group_size, t.tables, t.tscales, t.rowsums};
+        }
+        rc = bitlut_build_lut_multi(jobs, j - i, BITLUT_TABLE_Q8, lf, stream);
+      }
     } else if (fl & BITLUT_FLAG_FUSED_TABLES) {
       const bitlut_pipe_op& t = specs[s.dep[0]];
       rc = bitlut_mpgemv_fused(t.a, t.a_dtype, s.wgpu, s.m, s.k, s.bits, s.group_size, s.wscales, s.zeros,
-                               s.scale_dtype, s.out, fl & ~BITLUT_FLAG_FUSED_TABLES, stream);
-    } else {
+                               s.scale_dtype, s.out, lf, stream);
+    } else if (j - i == 1) {
       rc = bitlut_mpgemm(s.wgpu, s.m, s.k, s.bits, s.group_size, s.wscales, s.zeros, s.scale_dtype,
-                         s.tables, s.tscales, s.rowsums, BITLUT_TABLE_Q8, s.n, s.out, nullptr, fl, stream);
+                         s.tables, s.tscales, s.rowsums, BITLUT_TABLE_Q8, s.n, s.out, nullptr, lf, stream);
+    } else {
+      bitlut_mat mats[kMaxGroupLookups];
+      for (int u = i; u < j; u++) {
+        const bitlut_pipe_op& t = specs[u];
+        mats[u - i] = {t.wgpu, t.wscales, t.zeros, t.m, t.out};
+      }
+      rc = bitlut_mpgemv_multi(mats, j - i, s.k, s.bits, s.group_size, s.scale_dtype, s.tables, s.tscales,
+                               s.rowsums, lf, stream);
     }
+    i = j;
   }
   if (flags != stack_flags) free(flags);
+  return rc;
+}
+
+// ---------------------------------------------------------------------------
+// Counted variant: every launch unit starts without griddepcontrol.wait and
+// instead waits (one thread, ld.acquire) on the completion counters of the
+// units that produce its inputs; each CTA counts itself into its unit's
+// counter after its last global write (common.cuh DepSync).  No kernel
+// drains the stream: a consumer's CTAs are resident, with their weights
+// already streaming in, when the producer finishes.  Counters are zeroed by
+// a memset at the head of the list (ordered after all earlier stream work,
+// which also makes inputs from before the list complete).  Counted kernels
+// never wait for their stream predecessor; a final join kernel waits until
+// every CTA of the list has counted itself, so the list's stream completion
+// still means "all done".  At most 8 producer launches per launch (else
+// EPARAM: use the PDL variant).  Bitwise identical to the plain launches.
+// ---------------------------------------------------------------------------
+int bl_build_lut_launch(const void* a, int a_dtype, int n, int k, int group_size, int mode, void* tables,
+                        float* tscales, float* rowsums, cudaStream_t stream, bool pdl, bool independent,
+                        const bl::DepSync& dep, int* grid_out);
+int bl_build_lut_multi_launch(const bitlut_lut_job* jobs, int n_jobs, int mode, int flags, void* stream,
+                              const bl::DepSync& dep, int* grid_out);
+int bl_mpgemm_launch(const uint8_t* wgpu, int m, int k, int bits, int group_size, const void* wscales,
+                     const void* zeros, int scale_dtype, const void* tables, const float* tscales,
+                     const float* rowsums, int mode, int n, float* out, int32_t* partials, int flags,
+                     unsigned long long* trace, void* stream, const bl::DepSync& dep, int* grid_out);
+int bl_mpgemv_multi_launch(const bitlut_mat* mats, int n_mats, int k, int bits, int group_size,
+                           int scale_dtype, const void* tables, const float* tscales, const float* rowsums,
+                           int flags, void* stream, const bl::DepSync& dep, int* grid_out);
+int bl_mpgemv_fused_launch(const void* a, int a_dtype, const uint8_t* wgpu, int m, int k, int bits,
+                           int group_size, const void* wscales, const void* zeros, int scale_dtype, float* out,
+                           int flags, void* stream, const bl::DepSync& dep, int* grid_out);
+
+constexpr int kMaxJoinUnits = 1024;
+struct JoinArgs {
+  const unsigned* counters;
+  int n_units;
+  unsigned unit[kMaxJoinUnits];     // counter index of each launch unit
+  unsigned target[kMaxJoinUnits];   // its CTA count
+};
+
+// The list's last launch: completes once every launch unit has counted all
+// of its CTAs (one lane per unit, strided).
+__global__ void join_kernel(const __grid_constant__ JoinArgs J) {
+  for (int i = threadIdx.x; i < J.n_units; i += blockDim.x)
+    while (bl::ld_acquire_u32(J.counters + J.unit[i]) < J.target[i]) __nanosleep(64);
+}
+
+extern "C" int bitlut_pipeline_launch_ops_counted(const bitlut_pipe_op* specs, int n_ops, unsigned* counters,
+                                                  void* stream) {
+  if (n_ops <= 0 || !specs || !counters) return BITLUT_EPARAM;
+  int* flags = static_cast<int*>(malloc(sizeof(int) * n_ops * 3));
+  if (!flags) return BITLUT_EINTERNAL;
+  int* leader = flags + n_ops;        // launch unit (leader op index) of each op, -1 for skipped
+  int* grid = flags + 2 * n_ops;      // CTAs of each unit (at its leader)
+  int rc = bitlut_pipeline_plan_flags(specs, n_ops, flags);
+  if (rc == BITLUT_OK &&
+      cudaMemsetAsync(counters, 0, sizeof(unsigned) * (n_ops + 1), (cudaStream_t)stream) != cudaSuccess)
+    rc = BITLUT_EINTERNAL;
+  JoinArgs* join = static_cast<JoinArgs*>(malloc(sizeof(JoinArgs)));
+  if (!join) rc = BITLUT_EINTERNAL;
+  else { join->counters = counters; join->n_units = 0; }
+  for (int i = 0; i < n_ops; i++) { leader[i] = -1; grid[i] = 0; }
+  for (int i = 0; rc == BITLUT_OK && i < n_ops;) {
+    const bitlut_pipe_op& s = specs[i];
+    const int fl = flags[i];
+    if (fl == BITLUT_PLAN_SKIP) { i++; continue; }
+    int j = i + 1;
+    while (j < n_ops && flags[j] != BITLUT_PLAN_SKIP && (flags[j] & BITLUT_PLAN_JOINED)) j++;
+    for (int u = i; u < j; u++) leader[u] = i;
+    // producer units of every member's (effective) inputs
+    bl::DepSync dep = {};
+    bool overflow = false;
+    for (int u = i; u < j; u++) {
+      const bitlut_pipe_op& m = specs[u];
+      const int* deps = (flags[u] & BITLUT_FLAG_FUSED_TABLES) ? specs[m.dep[0]].dep : m.dep;
+      for (int d = 0; d < 3; d++) {
+        if (deps[d] < 0) continue;
+        const int pu = leader[deps[d]];
+        if (pu < 0) { overflow = true; continue; }
+        bool seen = false;
+        for (int w = 0; w < dep.n_wait; w++) seen = seen || dep.wait_cnt[w] == counters + pu;
+        if (seen) continue;
+        if (dep.n_wait == bl::kMaxDepWaits) { overflow = true; continue; }
+        dep.wait_cnt[dep.n_wait] = counters + pu;
+        dep.wait_target[dep.n_wait] = (unsigned)grid[pu];
+        dep.n_wait++;
+      }
+    }
+    if (overflow) { rc = BITLUT_EPARAM; break; }   // > 8 producer launches: use sync="pdl"
+    const int lf = BITLUT_FLAG_PDL | (fl & BITLUT_FLAG_FAST_EPILOGUE);
+    dep.counted = 1;
+    dep.done = counters + i;
+    dep.total = nullptr;
+    int g = 0;
+    if (s.type == BITLUT_OP_TABLES) {
+      if (j - i == 1) {
+        rc = bl_build_lut_launch(s.a, s.a_dtype, s.n, s.k, s.group_size, BITLUT_TABLE_Q8, s.tables, s.tscales,
+                                 s.rowsums, (cudaStream_t)stream, true, false, dep, &g);
+      } else {
+        bitlut_lut_job jobs[kMaxGroupTables];
+        for (int u = i; u < j; u++) {
+          const bitlut_pipe_op& t = specs[u];
+          jobs[u - i] = {t.a, t.a_dtype, t.n, t.k, t.group_size, t.tables, t.tscales, t.rowsums};
+        }
+        rc = bl_build_lut_multi_launch(jobs, j - i, BITLUT_TABLE_Q8, lf, stream, dep, &g);
+      }
+    } else if (fl & BITLUT_FLAG_FUSED_TABLES) {
+      const bitlut_pipe_op& t = specs[s.dep[0]];
+      rc = bl_mpgemv_fused_launch(t.a, t.a_dtype, s.wgpu, s.m, s.k, s.bits, s.group_size, s.wscales, s.zeros,
+                                  s.scale_dtype, s.out, lf, stream, dep, &g);
+    } else if (j - i == 1) {
+      rc = bl_mpgemm_launch(s.wgpu, s.m, s.k, s.bits, s.group_size, s.wscales, s.zeros, s.scale_dtype, s.tables,
+                            s.tscales, s.rowsums, BITLUT_TABLE_Q8, s.n, s.out, nullptr, lf, nullptr, stream, dep,
+                            &g);
+    } else {
+      bitlut_mat mats[kMaxGroupLookups];
+      for (int u = i; u < j; u++) {
+        const bitlut_pipe_op& t = specs[u];
+        mats[u - i] = {t.wgpu, t.wscales, t.zeros, t.m, t.out};
+      }
+      rc = bl_mpgemv_multi_launch(mats, j - i, s.k, s.bits, s.group_size, s.scale_dtype, s.tables, s.tscales,
+                                  s.rowsums, lf, stream, dep, &g);
+    }
+    grid[i] = g;
+    if (rc == BITLUT_OK && g <= 0) rc = BITLUT_EINTERNAL;
+    if (rc == BITLUT_OK) {
+      if (join->n_units == kMaxJoinUnits) { rc = BITLUT_EPARAM; break; }
+      join->unit[join->n_units] = (unsigned)i;
+      join->target[join->n_units] = (unsigned)g;
+      join->n_units++;
+    }
+    i = j;
+  }
+  if (rc == BITLUT_OK) {     // the list completes when its last CTA has counted itself
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1); cfg.blockDim = dim3(128); cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr; cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, join_kernel, *join) != cudaSuccess) rc = BITLUT_EINTERNAL;
+  }
+  free(join);
+  free(flags);
   return rc;
 }

@@ -55,6 +55,9 @@ def _bind():
                                              ctypes.POINTER(ctypes.c_int)]
     L.bitlut_pipeline_launch_ops.restype = ctypes.c_int
     L.bitlut_pipeline_launch_ops.argtypes = [ctypes.POINTER(PipeOpSpec), ctypes.c_int, ctypes.c_void_p]
+    L.bitlut_pipeline_launch_ops_counted.restype = ctypes.c_int
+    L.bitlut_pipeline_launch_ops_counted.argtypes = [ctypes.POINTER(PipeOpSpec), ctypes.c_int, ctypes.c_void_p,
+                                                     ctypes.c_void_p]
     return L
 
 
@@ -75,11 +78,20 @@ class Pipeline:
     """Records ops, then runs them in one persistent launch."""
 
     EXECUTORS = ("graph", "persistent")
+    SYNCS = ("counters", "pdl")
 
-    def __init__(self, device=None, executor: str = "graph"):
+    def __init__(self, device=None, executor: str = "graph", sync: str = "pdl"):
+        """executor "graph": per-op launches captured in a CUDA graph; their
+        inputs are tracked by programmatic-dependent-launch waits
+        (sync="pdl", default) or by completion counters (sync="counters": no
+        launch drains the stream, but measured slower on B200 -- DESIGN.md
+        §4.6).  executor "persistent": one cooperative launch."""
         if executor not in self.EXECUTORS:
             raise ParameterError(f"executor must be one of {self.EXECUTORS}, got {executor!r}")
+        if sync not in self.SYNCS:
+            raise ParameterError(f"sync must be one of {self.SYNCS}, got {sync!r}")
         self.executor = executor
+        self.sync = sync
         self.device = torch.device(device) if device is not None else torch.device(
             "cuda", torch.cuda.current_device())
         self.specs: list[PipeOpSpec] = []
@@ -185,6 +197,8 @@ class Pipeline:
             self._counters = torch.zeros(2 * n, dtype=torch.int32, device=self.device)
         else:
             self.plan_flags()                       # validates the list before capture
+            if self.sync == "counters":
+                self._counters = torch.zeros(n + 1, dtype=torch.int32, device=self.device)
             side = torch.cuda.Stream(self.device)
             side.wait_stream(torch.cuda.current_stream(self.device))
             with torch.cuda.stream(side):           # one eager pass (module load, first-launch costs)
@@ -197,9 +211,24 @@ class Pipeline:
         return self
 
     def _launch_ops(self, stream: torch.cuda.Stream) -> None:
+        if self.sync == "counters":
+            if self._counters is None:
+                self._counters = torch.zeros(len(self.specs) + 1, dtype=torch.int32, device=self.device)
+            rc = _bind().bitlut_pipeline_launch_ops_counted(self._arr, len(self.specs),
+                                                            ctypes.c_void_p(self._counters.data_ptr()),
+                                                            ctypes.c_void_p(stream.cuda_stream))
+            raise_for_status(rc, "bitlut_pipeline_launch_ops_counted")
+            return
         rc = _bind().bitlut_pipeline_launch_ops(self._arr, len(self.specs),
                                                 ctypes.c_void_p(stream.cuda_stream))
         raise_for_status(rc, "bitlut_pipeline_launch_ops")
+
+    def n_launches(self) -> int:
+        """Kernel launches per run (graph executor: launch units of the plan)."""
+        if self.executor == "persistent":
+            return 1
+        units = sum(1 for f in self.plan_flags() if f != -1 and not (f & N.PLAN_JOINED))
+        return units + (1 if self.sync == "counters" else 0)      # + the join kernel
 
     def run(self, stream: Optional[torch.cuda.Stream] = None) -> None:
         """Enqueue the whole op list on `stream` (default: current stream)."""

@@ -175,3 +175,41 @@ def test_graph_executor_table_fusion_plan():
                         P, P,
                         P, P | F,
                         SKIP, P | FUSED | F, P | FUSED | F | I]
+
+
+def test_graph_executor_launch_grouping_plan():
+    """Consecutive table builds share one launch; consecutive batch-1 fast
+    lookups over the same tables share one launch; a group is INDEPENDENT
+    only if all its members' inputs are complete."""
+    import ctypes
+    from paper_2407_00088_b200.pipeline import PipeOpSpec, _bind
+    T, LK, J = 0, 1, 16
+
+    def tab(k=4096):
+        s = PipeOpSpec()
+        s.type, s.n, s.k, s.group_size, s.a_dtype = T, 1, k, 64, N.DT_F16
+        s.dep[:] = [-1, -1, -1]
+        return s
+
+    def look(dep, m, k=4096, fast=True):
+        s = PipeOpSpec()
+        s.type, s.n, s.k, s.group_size, s.m, s.bits = LK, 1, k, 64, m, 2
+        s.scale_dtype = N.DT_F16
+        s.flags = N.FLAG_FAST_EPILOGUE if fast else 0
+        s.dep[:] = [dep, -1, -1]
+        return s
+
+    # layer-set order: four table builds, then q,k,v | o | gate,up | down
+    ops = [tab(), tab(), tab(), tab(11008),
+           look(0, 4096), look(0, 4096), look(0, 4096), look(1, 4096),
+           look(2, 11008), look(2, 11008), look(3, 4096, k=11008), look(3, 4096, k=11008, fast=False)]
+    arr = (PipeOpSpec * len(ops))(*ops)
+    fl = (ctypes.c_int * len(ops))()
+    assert _bind().bitlut_pipeline_plan_flags(arr, len(ops), fl) == 0
+    P, I, F = N.FLAG_PDL, N.FLAG_INDEPENDENT, N.FLAG_FAST_EPILOGUE
+    assert list(fl) == [P, P | J, P | J, P | J,            # one table launch (first kernel: waits)
+                        P | F, P | F | J, P | F | J,       # q,k,v in one launch, waits for the tables
+                        P | F | I,                         # o (tables complete)
+                        P | F | I, P | F | I | J,          # gate, up
+                        P | F | I,                         # down
+                        P | I]                             # exact epilogue: own launch

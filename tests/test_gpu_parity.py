@@ -367,7 +367,7 @@ def test_independent_launch_chain_matches():
 
 # ---------------------------------------------------------------- pipeline
 
-@pytest.mark.parametrize("executor", ["persistent", "graph"])
+@pytest.mark.parametrize("executor", ["persistent", "graph", "graph-counters"])
 def test_pipeline_matches_per_op_bitwise(executor):
     """Two decoder-like layers (shared-table q/k/v, dependent o, gate/up,
     down) through either pipeline executor == per-op mpgemm, bitwise."""
@@ -386,7 +386,8 @@ def test_pipeline_matches_per_op_bitwise(executor):
         layers.append(L)
     xs = [{nm: torch.randn((1, k), device="cuda", generator=g).half() for nm, k in
            (("attn", 512), ("o", 512), ("mlp", 512), ("down", 1024))} for _ in layers]
-    pl = Pipeline(executor=executor)
+    pl = (Pipeline(executor="graph", sync="counters") if executor == "graph-counters"
+          else Pipeline(executor=executor))
     outs, prev = [], []
     for L, X in zip(layers, xs):
         t = pl.tables(X["attn"], gs, deps=prev)
@@ -400,7 +401,7 @@ def test_pipeline_matches_per_op_bitwise(executor):
         prev = [pl.op_of(yd)]
         outs.append({"q": yq, "k": yk, "v": yv, "o": yo, "gate": yg, "up": yu, "down": yd})
     pl.compile()
-    if executor == "graph":
+    if executor != "persistent":
         F, I = B._native.FLAG_PDL, B._native.FLAG_PDL | B._native.FLAG_INDEPENDENT
         assert pl.plan_flags()[:11] == [F, F, I, I, F, F, F, F, I, F, F]
     for _ in range(3):
@@ -542,3 +543,50 @@ def test_fused_mpgemv_and_graph_fusion():
             for nm, xk in (("q", "attn"), ("k", "attn"), ("v", "attn"), ("o", "o"), ("gate", "mlp"),
                            ("up", "mlp"), ("down", "down")):
                 assert torch.equal(Y[nm], B.mpgemm(X[xk], L[nm], exact_epilogue=False)), nm
+
+
+@pytest.mark.parametrize("sync", ["counters", "pdl"])
+@pytest.mark.parametrize("bits", [1, 2, 4])
+def test_graph_grouped_launches_bitwise(bits, sync):
+    """Layer-set op list (tables one layer ahead): the graph executor groups
+    the table builds (bitlut_build_lut_multi) and the lookups over one table
+    (bitlut_mpgemv_multi); every output == the per-op fast call, bitwise."""
+    from paper_2407_00088_b200 import _native as N
+    from paper_2407_00088_b200.pipeline import Pipeline
+    g = torch.Generator(device="cuda").manual_seed(11 + bits)
+    gs = 64
+    shapes = {"q": (256, 512), "k": (256, 512), "v": (128, 512), "o": (256, 512),
+              "gate": (352, 512), "up": (352, 512), "down": (256, 2048)}
+    groups = [("attn", 512, ["q", "k", "v"]), ("o", 512, ["o"]), ("mlp", 512, ["gate", "up"]),
+              ("down", 2048, ["down"])]
+    layers, xs = [], []
+    for li in range(2):
+        L = {}
+        for nm, (m, k) in shapes.items():
+            q = torch.randint(0, 1 << bits, (m, k), dtype=torch.uint8, device="cuda", generator=g)
+            sc = (torch.randn((m, k // gs), device="cuda", generator=g).abs() * 0.02 + 1e-3).half()
+            z = ((torch.rand((m, k // gs), device="cuda", generator=g) * ((1 << bits) - 1)).half()
+                 if li == 1 else None)
+            L[nm] = B.prepare_weights(B.QuantizedWeights(m=m, k=k, bits=bits, group_size=gs, qvalues=q,
+                                                         scales=sc, zeros=z))
+        layers.append(L)
+        xs.append({gn: torch.randn((1, k), device="cuda", generator=g).half() for gn, k, _ in groups})
+    pl = Pipeline(executor="graph", sync=sync)
+    tabs = [{gn: pl.tables(X[gn], gs) for gn, _, _ in groups} for X in xs]
+    outs = []
+    for L, T in zip(layers, tabs):
+        outs.append({nm: pl.lookup(L[nm], T[gn], fast_epilogue=True) for gn, _, names in groups for nm in names})
+    plan = pl.plan_flags()
+    assert any(f & 16 for f in plan)                      # some launches are grouped
+    pl.compile()
+    for _ in range(2):
+        pl.run()
+        torch.cuda.synchronize()
+        for L, X, Y in zip(layers, xs, outs):
+            for gn, _, names in groups:
+                t = N.build_lut(X[gn], gs, N.TABLE_Q8)
+                for nm in names:
+                    pw = L[nm]
+                    ref, _ = N.lookup(pw.gpu, pw.scales, pw.zeros, *t, pw.m, pw.k, bits, gs, N.TABLE_Q8,
+                                      N.FLAG_PDL | N.FLAG_FAST_EPILOGUE, False)
+                    assert torch.equal(Y[nm], ref), (nm, bits)
