@@ -59,6 +59,11 @@ extern "C" {
  * float combination is a fixed-order parallel reduction instead of the
  * reference's left-to-right chain (deterministic; last-bits differences). */
 #define BITLUT_FLAG_FAST_EPILOGUE 4
+/* With BITLUT_FLAG_FAST_EPILOGUE at batch 1 on 1/2/4-bit weights:
+ * `partials` receives, instead of the per-plane staging values, the exact
+ * integer combination S[m][gq] = sum_p 2^p P_p (shape (1, m, k/gs)) that the
+ * fast kernel scales -- SURVEY §8(c)'s bit-exactness object. */
+#define BITLUT_FLAG_COMBINED_PARTIALS 32
 
 /*
  * GPU weight layout ("layout v2", this library's own; the reference's v1

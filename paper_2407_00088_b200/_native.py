@@ -28,6 +28,7 @@ FLAG_INDEPENDENT = 2
 FLAG_FAST_EPILOGUE = 4
 FLAG_FUSED_TABLES = 8       # table op may fold into its consumers (graph executor)
 PLAN_JOINED = 16            # plan: launched together with the previous op
+FLAG_COMBINED_PARTIALS = 32  # fast batch-1: partials = sum_p 2^p P_p per (channel, group)
 
 _vp, _i = ctypes.c_void_p, ctypes.c_int
 
@@ -158,7 +159,8 @@ def lookup(wgpu: torch.Tensor, wscales: torch.Tensor, zeros: Optional[torch.Tens
     n = tables.shape[0]
     out = torch.empty((n, m), dtype=torch.float32, device=wgpu.device)
     nq = k // group_size
-    partials = (torch.empty((n, bits, m, nq), dtype=torch.int32, device=wgpu.device)
+    pb = 1 if flags & FLAG_COMBINED_PARTIALS else bits
+    partials = (torch.empty((n, pb, m, nq), dtype=torch.int32, device=wgpu.device)
                 if want_partials else torch.empty(0, dtype=torch.int32, device=wgpu.device))
     rc = lib().bitlut_mpgemm(ptr(wgpu), m, k, bits, group_size, ptr(wscales), ptr(zeros),
                              dtype_code(wscales), ptr(tables), ptr(tscales), ptr(rowsums), mode, n,
@@ -194,5 +196,6 @@ def _(wgpu, wscales, zeros, tables, tscales, rowsums, m, k, bits, group_size, mo
       want_partials):
     n = tables.shape[0]
     nq = k // group_size
+    pb = 1 if flags & FLAG_COMBINED_PARTIALS else bits
     return (wgpu.new_empty((n, m), dtype=torch.float32),
-            wgpu.new_empty((n, bits, m, nq) if want_partials else (0,), dtype=torch.int32))
+            wgpu.new_empty((n, pb, m, nq) if want_partials else (0,), dtype=torch.int32))

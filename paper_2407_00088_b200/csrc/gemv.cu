@@ -259,9 +259,12 @@ int bl_mpgemm_launch(const uint8_t* wgpu, int m, int k, int bits, int group_size
     while (r > 1 && (int64_t)L.n_tiles * ((n + r - 1) / r) < 4 * 148) r >>= 1;
     a.rows_per_cta = r;
   }
-  if (mode == BITLUT_TABLE_Q8 && a.fast && !partials && !trace && n == 1 && L.n_sg == 1 && b1_enabled()) {
+  const bool combined = (flags & BITLUT_FLAG_COMBINED_PARTIALS) != 0;
+  if (combined && (!a.fast || mode != BITLUT_TABLE_Q8 || n != 1 || L.n_sg != 1 || trace)) return BITLUT_EPARAM;
+  if (mode == BITLUT_TABLE_Q8 && a.fast && (!partials || combined) && !trace && n == 1 && L.n_sg == 1 &&
+      (b1_enabled() || combined)) {
     rc = bl_gemv_b1_launch(a, scale_dtype, (cudaStream_t)stream, pdl);
-    if (rc != BITLUT_ELAYOUT) return rc;              // else: shape exceeds its smem plan
+    if (rc != BITLUT_ELAYOUT || combined) return rc;  // else: shape exceeds its smem plan
   }
   return scale_dtype == BITLUT_DT_F16 ? dispatch_q8<__half>(a, n, (cudaStream_t)stream, pdl, mode)
                                       : dispatch_q8<float>(a, n, (cudaStream_t)stream, pdl, mode);

@@ -433,6 +433,12 @@ __global__ void __launch_bounds__(256) gemv_b1_kernel(const __grid_constant__ B1
 #pragma unroll
           for (int i = 0; i < NV; i++) S[i] = acc[i];
         }
+        if (p.partials) {                                 // exact integer sums (single-matrix launches)
+          int local;
+          find_mat(a, tile, local);
+#pragma unroll
+          for (int j = 0; j < NCH; j++) p.partials[((int64_t)local * TCH + ch0 + j) * NQ + g] = S[j];
+        }
 #pragma unroll
         for (int j = 0; j < NCH; j++) {
           const int c = ch0 + j;

@@ -590,3 +590,26 @@ def test_graph_grouped_launches_bitwise(bits, sync):
                     ref, _ = N.lookup(pw.gpu, pw.scales, pw.zeros, *t, pw.m, pw.k, bits, gs, N.TABLE_Q8,
                                       N.FLAG_PDL | N.FLAG_FAST_EPILOGUE, False)
                     assert torch.equal(Y[nm], ref), (nm, bits)
+
+
+def test_batch1_fast_integer_sums_exact(small_golden):
+    """the fast batch-1 kernel's integer object -- the exact
+    combination S = sum_p 2^p P_p per (channel, group) -- equals the one
+    formed from the REFERENCE's int32 staging values, bitwise."""
+    from paper_2407_00088_b200 import _native as N
+    n_checked = 0
+    for name, c in small_golden.items():
+        inst = small_inst(c)
+        if inst["bits"] == 3:
+            continue
+        _, pw = make_pw(inst)
+        P = c["partials"].astype(np.int64)               # (bits, n, m, NQ), the reference's
+        for row in range(inst["a"].shape[0]):
+            x = torch.from_numpy(inst["a"][row:row + 1]).cuda()
+            t = N.build_lut(x, inst["group_size"], N.TABLE_Q8)
+            _, S = N.lookup(pw.gpu, pw.scales, pw.zeros, *t, pw.m, pw.k, pw.bits, pw.group_size, N.TABLE_Q8,
+                            N.FLAG_PDL | N.FLAG_FAST_EPILOGUE | N.FLAG_COMBINED_PARTIALS, True)
+            want = sum((1 << p) * P[p, row] for p in range(inst["bits"]))
+            assert np.array_equal(S[0, 0].cpu().numpy().astype(np.int64), want), name
+            n_checked += 1
+    assert n_checked >= 8
