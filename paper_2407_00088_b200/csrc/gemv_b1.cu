@@ -305,7 +305,7 @@ __device__ __forceinline__ void fused_tables(const B1Args& a, uint8_t* smem) {
 }
 
 template <int R, int LG, int BITS, typename ST, bool FUSED>
-__global__ void __launch_bounds__(256) gemv_b1_kernel(const __grid_constant__ B1Args a) {
+__global__ void __launch_bounds__(384) gemv_b1_kernel(const __grid_constant__ B1Args a) {
   const GemvArgs& p = a.g;
   const bl::LayoutV2& L = p.L;
   constexpr int TCH = 32 / BITS;                        // channels per tile
@@ -484,22 +484,24 @@ int sm_count() {
 
 constexpr int kClusterCTAs = 8;
 
-// CTA size: 128 threads, 256 when a tile has more than 128 units (long K).
-int b1_threads(const bl::LayoutV2& L) {
-  static int cap = 0;
-  if (!cap) {
-    const char* e = getenv("BITLUT_B1_THREADS");
-    cap = e ? atoi(e) : 256;
-    if (cap != 128 && cap != 256) cap = 128;
-  }
-  return L.U > 128 ? cap : 128;
+// CTA size.  A dependent launch (its inputs complete only when it starts)
+// wants the shortest per-tile path: as few rounds of units as a <= 384-thread
+// CTA allows, units spread evenly (U = 344 at K = 11008 -> one round of 352
+// threads).  An overlapped (INDEPENDENT) launch wants more resident CTAs:
+// at most 256 threads.  Never fewer than 128.
+int b1_threads(const bl::LayoutV2& L, bool overlapped) {
+  const int cap = overlapped ? 256 : 384;
+  const int rounds = (L.U + cap - 1) / cap;
+  int t = (L.U + rounds - 1) / rounds;
+  t = (t + 31) & ~31;
+  return t < 128 ? 128 : t;
 }
 
 template <int R, int LG, int BITS, typename ST, bool FUSED>
 int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* act, cudaStream_t stream,
               bool pdl) {
   const bl::LayoutV2& L = g.L;
-  const int T = b1_threads(L);
+  const int T = b1_threads(L, g.independent || g.dep.counted);
   if (FUSED && T % (L.gs / 4) != 0) return BITLUT_ELAYOUT;
   if (n_mats < 1 || n_mats > kMaxMats) return BITLUT_EPARAM;
   B1Args a;
@@ -623,7 +625,7 @@ int bl_gemv_b1_launch(const GemvArgs& g, int scale_dtype, cudaStream_t s, bool p
 
 bool bl_gemv_b1_fused_fits(const bl::LayoutV2& L, bool zeros, int scale_dtype) {
   if (L.n_sg != 1) return false;
-  const int T = b1_threads(L);
+  const int T = b1_threads(L, false);
   if (T % (L.gs / 4) != 0) return false;
   const size_t total = scale_dtype == BITLUT_DT_F16 ? b1_plan<__half>(L, zeros, true, T, 1, true).total
                                                     : b1_plan<float>(L, zeros, true, T, 1, true).total;
