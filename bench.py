@@ -351,6 +351,54 @@ def per_shape_table(device, stream, reps, warmup, barrier, peak, world, bits_lis
     return out
 
 
+def gemm_table(device, stream, reps, warmup, barrier, world):
+    """BASELINE configs[3] (prefill mpGEMM): N in {32, 128, 512} activation
+    rows, W4/W2 at 4096x4096 and 11008x4096, gs = 128, int8 tables; one table
+    build per row + the weight-stationary lookup kernel, in a CUDA graph.
+    Work = lookups = b*N*M*K/4.  Bound: the lookups run on register-resident
+    PRMT tables with one IDP.2A (dp2a) per lookup, so the INT pipe is the
+    ceiling -- 64 lookups/clk/SM (IDP.2A measured at 63/clk/SM,
+    tools/microbench/pipes.cu) x 148 SMs x 1.965 GHz = 18.6e12/s; SURVEY
+    8(d)'s LSU figure (32/clk/SM, smem-gather lookups) is reported beside it.
+    Equivalent TOPS = 2*N*M*K / t."""
+    import torch
+    import paper_2407_00088_b200 as B
+    from paper_2407_00088_b200 import _native as N
+    gen = torch.Generator(device=device)
+    gen.manual_seed(5)
+    sms = torch.cuda.get_device_properties(device).multi_processor_count
+    out = {"int_pipe_bound_lookups_per_s": sms * 64 * 1.965e9,
+           "lsu_bound_lookups_per_s": sms * 32 * 1.965e9}
+    for (m, k) in ((4096, 4096), (11008, 4096)):
+        for bits in (4, 2):
+            m_loc = m // world
+            q = torch.randint(0, 1 << bits, (m_loc, k), dtype=torch.uint8, device=device, generator=gen)
+            sc = (torch.randn((m_loc, k // 128), device=device, generator=gen).abs() * 0.02 + 1e-3).half()
+            pw = B.prepare_weights(B.QuantizedWeights(m=m_loc, k=k, bits=bits, group_size=128, qvalues=q,
+                                                      scales=sc))
+            del q
+            for n in (32, 128, 512):
+                a = torch.randn((n, k), device=device, generator=gen).half()
+                for epi in ("exact", "fast"):
+                    fl = N.FLAG_PDL | (N.FLAG_FAST_EPILOGUE if epi == "fast" else 0)
+
+                    def body():
+                        t = N.build_lut(a, 128, N.TABLE_Q8, N.FLAG_PDL)
+                        N.lookup(pw.gpu, pw.scales, None, *t, m_loc, k, bits, 128, N.TABLE_Q8, fl, False)
+                    g = capture(body, stream)
+                    with torch.cuda.stream(stream):
+                        ms = time_graph(g, reps, warmup, barrier)
+                    del g
+                    t = ms * 1e-3
+                    lookups = bits * n * m * (k // 4)
+                    out[f"{m}x{k}_W{bits}_n{n}_{epi}"] = {
+                        "us": round(t * 1e6, 2), "lookups_per_s": float(f"{lookups / t:.4g}"),
+                        "frac_of_int_pipe_bound": round(lookups / t / out["int_pipe_bound_lookups_per_s"], 4),
+                        "equiv_TOPS": round(2 * n * m * k / t / 1e12, 2)}
+            del pw
+    return out
+
+
 # ----------------------------------------------------------------- CPU baseline
 
 def cpu_baseline(layers_host, bits, gs, budget_s, threads):
@@ -405,6 +453,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-shapes", action="store_true")
+    ap.add_argument("--no-gemm", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     bits, gs = 2, 64
@@ -540,6 +589,13 @@ def main():
                                         peak, world)
         per_shape["clocks"] = clk_shapes.summary()
 
+    # ---- prefill mpGEMM (BASELINE configs[3]) ----
+    gemm = None
+    if not args.no_gemm:
+        with ClockSampler(local) as clk_gemm:
+            gemm = gemm_table(device, stream, max(3, args.steps // 5), args.warmup, barrier, world)
+        gemm["clocks"] = clk_gemm.summary()
+
     # ---- e2e: the same step through the public API from HOST buffers: one
     #      H2D of the step's activation rows (pinned), the op list, one D2H of
     #      every GEMV output (pinned), all inside the timed region. ----
@@ -615,6 +671,7 @@ def main():
             "executors": executors_out,
             "lookups_only_graph": lookups_graph,
             "per_shape": per_shape,
+            "mpgemm_prefill": gemm,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "e2e_per_call_api": per_call,
