@@ -188,7 +188,8 @@ int bitlut_mpgemv_fused(const void* a, int a_dtype, const uint8_t* wgpu, int m, 
                         float* out, int flags, void* stream);
 
 /* Several weight matrices that read the same activation row's tables
- * (q/k/v, gate/up) looked up by ONE batch-1 launch (fast epilogue; 1/2/4-bit
+ * (q/k/v, gate/up) looked up by ONE batch-1 launch (fast or, without
+ * BITLUT_FLAG_FAST_EPILOGUE, the reference-order epilogue; 1/2/4-bit
  * weights sharing k, bits, group_size, scale dtype and zero-point presence).
  * tables / tscales / rowsums as produced by bitlut_build_lut (mode Q8, n = 1).
  * Up to 4 matrices.  Returns BITLUT_ELAYOUT for 3-bit weights. */

@@ -46,6 +46,8 @@ struct B1Args {
   B1Mat mats[kMaxMats];
   const __half* act;          // fused variant: fp16 activation row (tables built in-kernel)
   uint32_t sa_off, red_off;   // fused: activation staging (4*T floats) + group-max scratch
+  uint32_t psm_off, terms_off, fin_off;   // exact variant: staging values, products, chain ends
+  int rowlen;                 // exact: floats per channel row of products
   int rounds;                 // unit rounds per tile (units = KG / R)
   int stages;                 // weight pipeline depth: 1 (one tile per CTA) or 2
   int tab_smem;               // tables staged in smem (rounds > 1), else registers
@@ -56,13 +58,17 @@ struct B1Args {
 
 struct B1Plan {
   uint32_t stage_bytes, w_bytes, s_off, s_bytes, z_off, tab_off, ts_off, rs_off, y_off, sa_off, red_off,
-      bar_off, total;
+      psm_off, terms_off, fin_off, bar_off, total;
+  int rowlen;
 };
+
+enum B1Kind { kFast = 0, kFused = 1, kExact = 2 };
 
 __host__ __device__ inline uint32_t al16(size_t x) { return (uint32_t)((x + 15) & ~(size_t)15); }
 
 template <typename ST>
-B1Plan b1_plan(const bl::LayoutV2& L, bool zeros, bool tab_smem, int T, int stages, bool fused = false) {
+B1Plan b1_plan(const bl::LayoutV2& L, bool zeros, bool tab_smem, int T, int stages, int kind = kFast) {
+  const bool fused = kind == kFused, exact = kind == kExact;
   B1Plan s;
   s.w_bytes = (uint32_t)((size_t)L.KG * 16);
   s.s_bytes = (uint32_t)((size_t)L.tile_ch * L.NQ * sizeof(ST));
@@ -76,7 +82,15 @@ B1Plan b1_plan(const bl::LayoutV2& L, bool zeros, bool tab_smem, int T, int stag
   s.y_off = s.rs_off + al16((size_t)L.NQ * 4);
   s.sa_off = s.y_off + al16((size_t)2 * (T / 32) * L.tile_ch * 4);
   s.red_off = s.sa_off + (fused ? al16((size_t)4 * T * 4) : 0);
-  s.bar_off = s.red_off + (fused ? al16((size_t)(T / 32) * 4) : 0);
+  s.psm_off = s.red_off + (fused ? al16((size_t)(T / 32) * 4) : 0);
+  // exact epilogue (reference order): staging values NQ x 33 int32, products
+  // tile_ch x rowlen floats (rowlen/4 odd: conflict-free chain loads), chain ends
+  const int need = (L.bits + 1 + (zeros ? 1 : 0)) * L.NQ;
+  s.rowlen = ((need + 3) / 4) * 4;
+  if (((s.rowlen / 4) & 1) == 0) s.rowlen += 4;
+  s.terms_off = s.psm_off + (exact ? al16((size_t)L.NQ * 33 * 4) : 0);
+  s.fin_off = s.terms_off + (exact ? al16((size_t)L.tile_ch * s.rowlen * 4) : 0);
+  s.bar_off = s.fin_off + (exact ? al16((size_t)3 * 32 * 4) : 0);
   s.total = s.bar_off + 8 * (kMaxStages + 1);
   return s;
 }
@@ -304,8 +318,9 @@ __device__ __forceinline__ void fused_tables(const B1Args& a, uint8_t* smem) {
   cluster_wait();                  // ... and every other slice is in ours
 }
 
-template <int R, int LG, int BITS, typename ST, bool FUSED>
+template <int R, int LG, int BITS, typename ST, int KIND>
 __global__ void __launch_bounds__(384) gemv_b1_kernel(const __grid_constant__ B1Args a) {
+  constexpr bool FUSED = KIND == kFused, EXACT = KIND == kExact;
   const GemvArgs& p = a.g;
   const bl::LayoutV2& L = p.L;
   constexpr int TCH = 32 / BITS;                        // channels per tile
@@ -390,6 +405,46 @@ __global__ void __launch_bounds__(384) gemv_b1_kernel(const __grid_constant__ B1
     for (int rd = 0; rd < a.rounds; rd++) {
       const int u = tid + rd * T;
       const bool live = u < U;
+      if constexpr (EXACT) {
+        // reference epilogue: per-plane staging values (packed stream pairs)
+        int acc[16];
+#pragma unroll
+        for (int i = 0; i < 16; i++) acc[i] = 0;
+        if (live) {
+          const int ub = u >> 5, l = u & 31;
+          const int nu_b = min(32, U - 32 * ub);
+          const int stride = nu_b == 32 ? 512 : nu_b * 16;
+          uint4 tq[R / 2];
+          if (a.tab_smem) {
+            const uint8_t* tb = tab + ub * (32 * R * 8) + l * 16;
+#pragma unroll
+            for (int jp = 0; jp < R / 2; jp++) tq[jp] = *reinterpret_cast<const uint4*>(tb + jp * stride);
+          } else {
+#pragma unroll
+            for (int jp = 0; jp < R / 2; jp++) tq[jp] = tq0[jp];
+          }
+          const uint8_t* wsrc = sb + ub * (32 * R * 16) + l * 16;
+#pragma unroll
+          for (int j = 0; j < R; j++) {
+            const uint4 wr = *reinterpret_cast<const uint4*>(wsrc + j * stride);
+            lookup_kg(wr, (j & 1) ? tq[j >> 1].z : tq[j >> 1].x, (j & 1) ? tq[j >> 1].w : tq[j >> 1].y, acc);
+          }
+        }
+        const int base = transpose_reduce<LG, 16, int>(acc, lane);
+        if (live) {
+          constexpr int NFP = 16 / LG;
+          const int fix = -32767 * (R * LG);
+          int32_t* dst = reinterpret_cast<int32_t*>(smem + a.psm_off) + (u / LG) * 33 + 2 * base;
+#pragma unroll
+          for (int i = 0; i < NFP; i++) {
+            const int v = acc[i] + fix;
+            const int pe = (v << 17) >> 17;
+            dst[2 * i] = pe;
+            dst[2 * i + 1] = (pe - v) >> 15;
+          }
+        }
+        continue;
+      }
       int acc[NACC];
 #pragma unroll
       for (int i = 0; i < NACC; i++) acc[i] = BITS == 1 ? 0 : KGF * R;   // undo A/B's -1 per lookup
@@ -448,6 +503,23 @@ __global__ void __launch_bounds__(384) gemv_b1_kernel(const __grid_constant__ B1
         }
       }
     }
+    if constexpr (EXACT) {
+      __syncthreads();                                  // staging values complete
+      float* terms = reinterpret_cast<float*>(smem + a.terms_off);
+      const int32_t* psm = reinterpret_cast<const int32_t*>(smem + a.psm_off);
+      form_terms<BITS, BITLUT_TABLE_Q8, ST>(p, sraw, zraw, tsm, rsm, psm, terms, a.rowlen, tid, T, 0, 0);
+      __syncthreads();                                  // products complete; stage consumed
+      if (tid == 0) {
+        const int t = tile + S * step;
+        if (t < ntl) issue_stage<ST>(a, t, sb, bar + stage, policy_evict_first());
+      }
+      int local;
+      const int j = find_mat(a, tile, local);
+      chains_and_out(L, terms, reinterpret_cast<float*>(smem + a.fin_off), a.rowlen, has_zeros,
+                     a.mats[j].out + (int64_t)local * TCH);
+      __syncthreads();                                  // psm / terms / fin reusable
+      continue;
+    }
     // ---- cross-group reduction: lanes of this warp, then the warps ----
     const int fb = reduce_lanes<NCH, LG, 32>(y, lane);
     float* yb = ysm + (it & 1) * NW * TCH + warp * TCH;
@@ -497,11 +569,13 @@ int b1_threads(const bl::LayoutV2& L, bool overlapped) {
   return t < 128 ? 128 : t;
 }
 
-template <int R, int LG, int BITS, typename ST, bool FUSED>
+template <int R, int LG, int BITS, typename ST, int KIND>
 int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* act, cudaStream_t stream,
               bool pdl) {
+  constexpr bool FUSED = KIND == kFused;
   const bl::LayoutV2& L = g.L;
-  const int T = b1_threads(L, g.independent || g.dep.counted);
+  // the exact epilogue's serial chains favour one tile per CTA and one round
+  const int T = b1_threads(L, KIND != kExact && (g.independent || g.dep.counted));
   if (FUSED && T % (L.gs / 4) != 0) return BITLUT_ELAYOUT;
   if (n_mats < 1 || n_mats > kMaxMats) return BITLUT_EPARAM;
   B1Args a;
@@ -512,7 +586,7 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
   a.total_tiles = mats[n_mats - 1].tile_end;
   a.rounds = (L.U + T - 1) / T;
   a.tab_smem = FUSED || a.rounds > 1;
-  auto kern = gemv_b1_kernel<R, LG, BITS, ST, FUSED>;
+  auto kern = gemv_b1_kernel<R, LG, BITS, ST, KIND>;
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
@@ -531,18 +605,19 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
   }
   // one stage when every CTA gets a single tile, else double-buffer
   const bool zeros = mats[0].zeros != nullptr;
-  B1Plan s = b1_plan<ST>(L, zeros, a.tab_smem, T, 1, FUSED);
+  B1Plan s = b1_plan<ST>(L, zeros, a.tab_smem, T, 1, KIND);
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, s.total) != cudaSuccess || per_sm < 1)
     return BITLUT_ELAYOUT;
-  const B1Plan s2 = b1_plan<ST>(L, zeros, a.tab_smem, T, 2, FUSED);
+  const B1Plan s2 = b1_plan<ST>(L, zeros, a.tab_smem, T, 2, KIND);
   int per_sm2 = 0;
   if (s2.total > 227 * 1024 ||
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, kern, T, s2.total) != cudaSuccess)
     per_sm2 = 0;
   // two tiles per CTA only where the double-buffered plan still leaves
   // several CTAs per SM (short K); long-K tiles want every CTA they can get
-  int tiles_per_cta = tpc_env > 0 ? tpc_env : (((g.independent || g.dep.counted) && per_sm2 >= 3) ? 2 : 1);
+  int tiles_per_cta = tpc_env > 0 ? tpc_env
+                                  : ((KIND != kExact && (g.independent || g.dep.counted) && per_sm2 >= 3) ? 2 : 1);
   if (tpc_env <= 0 && (a.total_tiles + tiles_per_cta - 1) / tiles_per_cta < sm_count() / 2) tiles_per_cta = 1;
   const int want = (a.total_tiles + tiles_per_cta - 1) / tiles_per_cta;
   // double-buffer when CTAs get several tiles -- by choice (tiles_per_cta)
@@ -556,6 +631,7 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
   a.stage_bytes = s.stage_bytes; a.w_bytes = s.w_bytes; a.s_off = s.s_off; a.s_bytes = s.s_bytes;
   a.z_off = s.z_off; a.tab_off = s.tab_off; a.ts_off = s.ts_off; a.rs_off = s.rs_off;
   a.y_off = s.y_off; a.bar_off = s.bar_off; a.sa_off = s.sa_off; a.red_off = s.red_off;
+  a.psm_off = s.psm_off; a.terms_off = s.terms_off; a.fin_off = s.fin_off; a.rowlen = s.rowlen;
   int grid = sm_count() * per_sm;
   if (grid > want) grid = want;
   const int cs = FUSED ? kClusterCTAs : 1;
@@ -578,29 +654,29 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
   return cudaLaunchKernelEx(&cfg, kern, a) == cudaSuccess ? BITLUT_OK : BITLUT_EINTERNAL;
 }
 
-template <int R, int LG, typename ST, bool FUSED>
+template <int R, int LG, typename ST, int KIND>
 int launch_b1_bits(const GemvArgs& g, const B1Mat* m, int nm, const __half* act, cudaStream_t s, bool pdl) {
   switch (g.L.bits) {
-    case 1: return launch_b1<R, LG, 1, ST, FUSED>(g, m, nm, act, s, pdl);
-    case 2: return launch_b1<R, LG, 2, ST, FUSED>(g, m, nm, act, s, pdl);
-    case 4: return launch_b1<R, LG, 4, ST, FUSED>(g, m, nm, act, s, pdl);
+    case 1: return launch_b1<R, LG, 1, ST, KIND>(g, m, nm, act, s, pdl);
+    case 2: return launch_b1<R, LG, 2, ST, KIND>(g, m, nm, act, s, pdl);
+    case 4: return launch_b1<R, LG, 4, ST, KIND>(g, m, nm, act, s, pdl);
   }
   return BITLUT_EPARAM;
 }
 
-template <typename ST, bool FUSED>
+template <typename ST, int KIND>
 int dispatch_b1(const GemvArgs& g, const B1Mat* m, int nm, const __half* act, cudaStream_t s, bool pdl) {
   const int R = g.L.R, LG = g.L.Lg;
   if (R == 8) {
     switch (LG) {
-      case 1: return launch_b1_bits<8, 1, ST, FUSED>(g, m, nm, act, s, pdl);
-      case 2: return launch_b1_bits<8, 2, ST, FUSED>(g, m, nm, act, s, pdl);
-      case 4: return launch_b1_bits<8, 4, ST, FUSED>(g, m, nm, act, s, pdl);
-      case 8: return launch_b1_bits<8, 8, ST, FUSED>(g, m, nm, act, s, pdl);
-      case 16: return launch_b1_bits<8, 16, ST, FUSED>(g, m, nm, act, s, pdl);
+      case 1: return launch_b1_bits<8, 1, ST, KIND>(g, m, nm, act, s, pdl);
+      case 2: return launch_b1_bits<8, 2, ST, KIND>(g, m, nm, act, s, pdl);
+      case 4: return launch_b1_bits<8, 4, ST, KIND>(g, m, nm, act, s, pdl);
+      case 8: return launch_b1_bits<8, 8, ST, KIND>(g, m, nm, act, s, pdl);
+      case 16: return launch_b1_bits<8, 16, ST, KIND>(g, m, nm, act, s, pdl);
     }
   } else if (R == 4 && LG == 1) {
-    return launch_b1_bits<4, 1, ST, FUSED>(g, m, nm, act, s, pdl);
+    return launch_b1_bits<4, 1, ST, KIND>(g, m, nm, act, s, pdl);
   }
   return BITLUT_EPARAM;
 }
@@ -619,16 +695,19 @@ B1Mat single_mat(const GemvArgs& g) {
 int bl_gemv_b1_launch(const GemvArgs& g, int scale_dtype, cudaStream_t s, bool pdl) {
   if (g.L.n_sg != 1) return BITLUT_ELAYOUT;
   const B1Mat m = single_mat(g);
-  return scale_dtype == BITLUT_DT_F16 ? dispatch_b1<__half, false>(g, &m, 1, nullptr, s, pdl)
-                                      : dispatch_b1<float, false>(g, &m, 1, nullptr, s, pdl);
+  if (g.fast)
+    return scale_dtype == BITLUT_DT_F16 ? dispatch_b1<__half, kFast>(g, &m, 1, nullptr, s, pdl)
+                                        : dispatch_b1<float, kFast>(g, &m, 1, nullptr, s, pdl);
+  return scale_dtype == BITLUT_DT_F16 ? dispatch_b1<__half, kExact>(g, &m, 1, nullptr, s, pdl)
+                                      : dispatch_b1<float, kExact>(g, &m, 1, nullptr, s, pdl);
 }
 
 bool bl_gemv_b1_fused_fits(const bl::LayoutV2& L, bool zeros, int scale_dtype) {
   if (L.n_sg != 1) return false;
   const int T = b1_threads(L, false);
   if (T % (L.gs / 4) != 0) return false;
-  const size_t total = scale_dtype == BITLUT_DT_F16 ? b1_plan<__half>(L, zeros, true, T, 1, true).total
-                                                    : b1_plan<float>(L, zeros, true, T, 1, true).total;
+  const size_t total = scale_dtype == BITLUT_DT_F16 ? b1_plan<__half>(L, zeros, true, T, 1, kFused).total
+                                                    : b1_plan<float>(L, zeros, true, T, 1, kFused).total;
   return total <= 227 * 1024;
 }
 
@@ -667,8 +746,8 @@ int bl_mpgemv_fused_launch(const void* a, int a_dtype, const uint8_t* wgpu, int 
   g.rows_per_cta = 1; g.n_rows = 1;
   const __half* act = reinterpret_cast<const __half*>(a);
   const B1Mat mt = single_mat(g);
-  return scale_dtype == BITLUT_DT_F16 ? dispatch_b1<__half, true>(g, &mt, 1, act, (cudaStream_t)stream, pdl)
-                                      : dispatch_b1<float, true>(g, &mt, 1, act, (cudaStream_t)stream, pdl);
+  return scale_dtype == BITLUT_DT_F16 ? dispatch_b1<__half, kFused>(g, &mt, 1, act, (cudaStream_t)stream, pdl)
+                                      : dispatch_b1<float, kFused>(g, &mt, 1, act, (cudaStream_t)stream, pdl);
 }
 
 int bl_mpgemv_multi_launch(const bitlut_mat* mats, int n_mats, int k, int bits, int group_size,
@@ -690,7 +769,6 @@ int bl_mpgemv_multi_launch(const bitlut_mat* mats, int n_mats, int k, int bits, 
                            int flags, void* stream, const bl::DepSync& dep, int* grid_out) {
   if (!mats || n_mats < 1 || n_mats > kMaxMats || !tables || !tscales || !rowsums) return BITLUT_EPARAM;
   if (scale_dtype != BITLUT_DT_F32 && scale_dtype != BITLUT_DT_F16) return BITLUT_EPARAM;
-  if (!(flags & BITLUT_FLAG_FAST_EPILOGUE)) return BITLUT_EPARAM;
   bl::LayoutV2 L;
   B1Mat ms[kMaxMats];
   int tiles = 0;
@@ -711,8 +789,13 @@ int bl_mpgemv_multi_launch(const bitlut_mat* mats, int n_mats, int k, int bits, 
   g.dep = dep;
   g.grid_out = grid_out;
   g.independent = pdl && (flags & BITLUT_FLAG_INDEPENDENT) != 0;
-  g.fast = 1;
+  g.fast = (flags & BITLUT_FLAG_FAST_EPILOGUE) != 0;
+  g.zeros = mats[0].zeros;                              // presence flag for the epilogue
   g.rows_per_cta = 1; g.n_rows = 1;
-  return scale_dtype == BITLUT_DT_F16 ? dispatch_b1<__half, false>(g, ms, n_mats, nullptr, (cudaStream_t)stream, pdl)
-                                      : dispatch_b1<float, false>(g, ms, n_mats, nullptr, (cudaStream_t)stream, pdl);
+  const cudaStream_t st = (cudaStream_t)stream;
+  if (g.fast)
+    return scale_dtype == BITLUT_DT_F16 ? dispatch_b1<__half, kFast>(g, ms, n_mats, nullptr, st, pdl)
+                                        : dispatch_b1<float, kFast>(g, ms, n_mats, nullptr, st, pdl);
+  return scale_dtype == BITLUT_DT_F16 ? dispatch_b1<__half, kExact>(g, ms, n_mats, nullptr, st, pdl)
+                                      : dispatch_b1<float, kExact>(g, ms, n_mats, nullptr, st, pdl);
 }

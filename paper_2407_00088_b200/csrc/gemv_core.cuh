@@ -458,6 +458,54 @@ __device__ __forceinline__ void prefetch_tables_q8(const GemvArgs& p, int row, u
   }
 }
 
+// Left-to-right chains of the epilogue products, one per channel, each kind
+// in its own warp (warp 0: main sum, warp 1: bias, warp 2: zero points),
+// then out[c] = main - 0.5 * bias (+ zero term) -- the reference's fp32
+// order (_kernels.py:179-191).  All threads of the CTA must call it.
+__device__ __forceinline__ void chains_and_out(const bl::LayoutV2& L, const float* terms, float* fin, int rowlen,
+                                               bool has_zeros, float* out) {
+  const int tid = threadIdx.x;
+  const int tch = L.tile_ch, NQ = L.NQ, bits = L.bits;
+  {
+    const int w = tid >> 5, c = tid & 31;
+    int start = 0, len = 0;
+    bool run = c < tch;
+    if (w == 0) { start = 0; len = bits * NQ; }
+    else if (w == 1) { start = bits * NQ; len = NQ; }
+    else if (w == 2 && has_zeros) { start = (bits + 1) * NQ; len = NQ; }
+    else run = false;
+    if (run) {
+      const float* t = terms + c * rowlen + start;
+      float o = 0.f;
+      int j = 0;
+      if ((start & 3) == 0) {
+        // 16-byte loads (rowlen/4 odd: conflict-free across the 16..32 lanes),
+        // two loads ahead of the serial add chain
+        const float4* t4 = reinterpret_cast<const float4*>(t);
+        const int n4 = len >> 2;
+        float4 a0 = n4 > 0 ? t4[0] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 a1 = n4 > 1 ? t4[1] : a0;
+        for (int q = 0; q < n4; q++) {
+          const float4 cur = a0;
+          a0 = a1;
+          if (q + 2 < n4) a1 = t4[q + 2];
+          o = __fadd_rn(o, cur.x); o = __fadd_rn(o, cur.y);
+          o = __fadd_rn(o, cur.z); o = __fadd_rn(o, cur.w);
+        }
+        j = n4 << 2;
+      }
+      for (; j < len; j++) o = __fadd_rn(o, t[j]);
+      fin[w * 32 + c] = o;
+    }
+  }
+  __syncthreads();
+  if (tid < tch) {
+    float o = __fsub_rn(fin[tid], __fmul_rn(0.5f, fin[32 + tid]));
+    if (has_zeros) o = __fadd_rn(o, fin[64 + tid]);
+    out[tid] = o;
+  }
+}
+
 // Phases 3-5 of one (tile, row): lookups -> exact staging values ->
 // epilogue products -> left-to-right chains -> out.  Requires the tile's
 // weights (TMA variant) and scales in `smem`, tsm / rsm filled, and a
@@ -608,46 +656,8 @@ __device__ __forceinline__ void tile_body(const GemvArgs& p, int tile, int row, 
   __syncthreads();
   TRACE(5);
 
-  // ---- 5. left-to-right chains, one per channel, each kind in its own warp
-  //         (warp 0: main sum, warp 1: bias, warp 2: zero points) ----
-  {
-    const int w = tid >> 5, c = tid & 31;
-    int start = 0, len = 0;
-    bool run = c < tch;
-    if (w == 0) { start = 0; len = bits * NQ; }
-    else if (w == 1) { start = bits * NQ; len = NQ; }
-    else if (w == 2 && has_zeros) { start = (bits + 1) * NQ; len = NQ; }
-    else run = false;
-    if (run) {
-      const float* t = terms + c * rowlen + start;
-      float o = 0.f;
-      int j = 0;
-      if ((start & 3) == 0) {
-        // 16-byte loads (rowlen/4 odd: conflict-free across the 16..32 lanes),
-        // two loads ahead of the serial add chain
-        const float4* t4 = reinterpret_cast<const float4*>(t);
-        const int n4 = len >> 2;
-        float4 a0 = n4 > 0 ? t4[0] : make_float4(0.f, 0.f, 0.f, 0.f);
-        float4 a1 = n4 > 1 ? t4[1] : a0;
-        for (int q = 0; q < n4; q++) {
-          const float4 cur = a0;
-          a0 = a1;
-          if (q + 2 < n4) a1 = t4[q + 2];
-          o = __fadd_rn(o, cur.x); o = __fadd_rn(o, cur.y);
-          o = __fadd_rn(o, cur.z); o = __fadd_rn(o, cur.w);
-        }
-        j = n4 << 2;
-      }
-      for (; j < len; j++) o = __fadd_rn(o, t[j]);
-      fin[w * 32 + c] = o;
-    }
-  }
-  __syncthreads();
-  if (tid < tch) {
-    float o = __fsub_rn(fin[tid], __fmul_rn(0.5f, fin[32 + tid]));
-    if (has_zeros) o = __fadd_rn(o, fin[64 + tid]);
-    p.out[(int64_t)row * L.m + (int64_t)tile * tch + tid] = o;
-  }
+  // ---- 5. left-to-right chains, one per channel ----
+  chains_and_out(L, terms, fin, rowlen, has_zeros, p.out + (int64_t)row * L.m + (int64_t)tile * tch);
 }
 
 }  // namespace blk

@@ -315,7 +315,7 @@ static bool groupable_lookups(const bitlut_pipe_op& a, const bitlut_pipe_op& b, 
   if (a.type != BITLUT_OP_LOOKUP || b.type != BITLUT_OP_LOOKUP) return false;
   if (a.dep[0] < 0 || a.dep[1] >= 0 || a.dep[2] >= 0 || b.dep[0] != a.dep[0] || b.dep[1] >= 0 || b.dep[2] >= 0)
     return false;
-  if (!(a.flags & BITLUT_FLAG_FAST_EPILOGUE) || !(b.flags & BITLUT_FLAG_FAST_EPILOGUE)) return false;
+  if ((a.flags & BITLUT_FLAG_FAST_EPILOGUE) != (b.flags & BITLUT_FLAG_FAST_EPILOGUE)) return false;
   if (a.n != 1 || b.n != 1 || a.k != b.k || a.bits != b.bits || a.group_size != b.group_size) return false;
   if (a.scale_dtype != b.scale_dtype || (a.zeros != nullptr) != (b.zeros != nullptr)) return false;
   if (specs[a.dep[0]].type != BITLUT_OP_TABLES) return false;
