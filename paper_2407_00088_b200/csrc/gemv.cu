@@ -260,8 +260,8 @@ int bl_mpgemm_launch(const uint8_t* wgpu, int m, int k, int bits, int group_size
     a.rows_per_cta = r;
   }
   const bool combined = (flags & BITLUT_FLAG_COMBINED_PARTIALS) != 0;
-  if (combined && (!a.fast || mode != BITLUT_TABLE_Q8 || n != 1 || L.n_sg != 1 || trace)) return BITLUT_EPARAM;
-  if (mode == BITLUT_TABLE_Q8 && (a.fast ? (!partials || combined) : !partials) && !trace && n == 1 &&
+  if (combined && (!a.fast || mode != BITLUT_TABLE_Q8 || L.n_sg != 1 || trace)) return BITLUT_EPARAM;
+  if (mode == BITLUT_TABLE_Q8 && (a.fast ? (!partials || combined) : !partials) && !trace &&
       L.n_sg == 1 && (b1_enabled() || combined)) {
     rc = bl_gemv_b1_launch(a, scale_dtype, (cudaStream_t)stream, pdl);
     if (rc != BITLUT_ELAYOUT || combined) return rc;  // else: shape exceeds its smem plan

@@ -43,6 +43,7 @@ struct B1Mat {
 struct B1Args {
   GemvArgs g;                 // L: the shared layout (k, bits, gs); tables, flags
   int n_mats, total_tiles;
+  int n_rows, rows_per_cta;   // activation rows (mpGEMM): CTA y walks rows [y*rpc, y*rpc + rpc)
   B1Mat mats[kMaxMats];
   const __half* act;          // fused variant: fp16 activation row (tables built in-kernel)
   uint32_t sa_off, red_off;   // fused: activation staging (4*T floats) + group-max scratch
@@ -62,13 +63,17 @@ struct B1Plan {
   int rowlen;
 };
 
-enum B1Kind { kFast = 0, kFused = 1, kExact = 2 };
+// kFastRows / kExactRows: the mpGEMM instantiations (several activation rows
+// per CTA); separate so the batch-1 kernels keep their register budget
+enum B1Kind { kFast = 0, kFused = 1, kExact = 2, kFastRows = 3, kExactRows = 4 };
+__host__ __device__ constexpr bool kind_exact(int k) { return k == kExact || k == kExactRows; }
+__host__ __device__ constexpr bool kind_rows(int k) { return k == kFastRows || k == kExactRows; }
 
 __host__ __device__ inline uint32_t al16(size_t x) { return (uint32_t)((x + 15) & ~(size_t)15); }
 
 template <typename ST>
 B1Plan b1_plan(const bl::LayoutV2& L, bool zeros, bool tab_smem, int T, int stages, int kind = kFast) {
-  const bool fused = kind == kFused, exact = kind == kExact;
+  const bool fused = kind == kFused, exact = kind_exact(kind);
   B1Plan s;
   s.w_bytes = (uint32_t)((size_t)L.KG * 16);
   s.s_bytes = (uint32_t)((size_t)L.tile_ch * L.NQ * sizeof(ST));
@@ -320,7 +325,7 @@ __device__ __forceinline__ void fused_tables(const B1Args& a, uint8_t* smem) {
 
 template <int R, int LG, int BITS, typename ST, int KIND>
 __global__ void __launch_bounds__(384) gemv_b1_kernel(const __grid_constant__ B1Args a) {
-  constexpr bool FUSED = KIND == kFused, EXACT = KIND == kExact;
+  constexpr bool FUSED = KIND == kFused, EXACT = kind_exact(KIND), ROWS = kind_rows(KIND);
   const GemvArgs& p = a.g;
   const bl::LayoutV2& L = p.L;
   constexpr int TCH = 32 / BITS;                        // channels per tile
@@ -369,34 +374,50 @@ __global__ void __launch_bounds__(384) gemv_b1_kernel(const __grid_constant__ B1
           : "memory");
     }
   }
+  const int row0 = ROWS ? blockIdx.y * a.rows_per_cta : 0;
+  const int row1 = ROWS ? min(row0 + a.rows_per_cta, a.n_rows) : 1;
   uint4 tq0[R / 2];
-  if (!FUSED && !a.tab_smem && tid < U) {
-    const int ub = tid >> 5, l = tid & 31;
-    const int nu_b = min(32, U - 32 * ub);
-    const uint8_t* tb = p.qtab + (int64_t)ub * (32 * R * 8) + l * 16;
+  // this thread's unit tables (one round of units per tile) and the row's
+  // table scales / row sums -> smem; rows after the CTA's first reload them
+  auto load_row = [&](int row) {
+    if (!FUSED && !a.tab_smem && tid < U) {
+      const int ub = tid >> 5, l = tid & 31;
+      const int nu_b = min(32, U - 32 * ub);
+      const uint8_t* tb = p.qtab + (int64_t)row * KG * 8 + (int64_t)ub * (32 * R * 8) + l * 16;
 #pragma unroll
-    for (int jp = 0; jp < R / 2; jp++) tq0[jp] = bl::ld_cg_128(tb + jp * nu_b * 16);
-  }
+      for (int jp = 0; jp < R / 2; jp++) tq0[jp] = bl::ld_cg_128(tb + jp * nu_b * 16);
+    }
+    for (int i = tid; i < NQ; i += T) {
+      tsm[i] = bl::ld_cg_f32(p.tscales + (int64_t)row * NQ + i);
+      rsm[i] = bl::ld_cg_f32(p.rowsums + (int64_t)row * NQ + i);
+    }
+  };
   if (FUSED) {
     fused_tables<R>(a, smem);                           // includes the block-wide syncs
   } else {
-    for (int i = tid; i < NQ; i += T) {
-      tsm[i] = bl::ld_cg_f32(p.tscales + i);
-      rsm[i] = bl::ld_cg_f32(p.rowsums + i);
-    }
+    load_row(row0);
   }
   __syncthreads();                                      // barriers initialised, tsm / rsm ready
   if (!FUSED && a.tab_smem) mbar_wait(bar + kMaxStages, 0);
 
   const bool has_zeros = a.mats[0].zeros != nullptr;     // uniform across the matrices
   const float h2 = (float)(2 << (BITS - 1));
-  int it = 0;
+  int it = 0, yit = 0;
   for (int tile = blockIdx.x; tile < ntl; tile += step, it++) {
     const int stage = S == 1 ? 0 : (it & 1);
     uint8_t* sb = smem + stage * a.stage_bytes;
     mbar_wait(bar + stage, (S == 1 ? it : it >> 1) & 1);
     const ST* sraw = reinterpret_cast<const ST*>(sb + a.s_off);
     const ST* zraw = reinterpret_cast<const ST*>(sb + a.z_off);
+  for (int row = row0; row < row1; row++, yit++) {      // mpGEMM: the tile stays in smem
+    if constexpr (ROWS) {
+      if (row != row0 || it > 0) {
+        __syncthreads();                                // previous row done with tsm / rsm
+        load_row(row);
+        __syncthreads();
+      }
+    }
+    const bool last_row = !ROWS || row + 1 == row1;
 
     float y[NCH];
 #pragma unroll
@@ -492,7 +513,8 @@ __global__ void __launch_bounds__(384) gemv_b1_kernel(const __grid_constant__ B1
           int local;
           find_mat(a, tile, local);
 #pragma unroll
-          for (int j = 0; j < NCH; j++) p.partials[((int64_t)local * TCH + ch0 + j) * NQ + g] = S[j];
+          for (int j = 0; j < NCH; j++)
+            p.partials[((int64_t)row * L.m + (int64_t)local * TCH + ch0 + j) * NQ + g] = S[j];
         }
 #pragma unroll
         for (int j = 0; j < NCH; j++) {
@@ -509,35 +531,36 @@ __global__ void __launch_bounds__(384) gemv_b1_kernel(const __grid_constant__ B1
       const int32_t* psm = reinterpret_cast<const int32_t*>(smem + a.psm_off);
       form_terms<BITS, BITLUT_TABLE_Q8, ST>(p, sraw, zraw, tsm, rsm, psm, terms, a.rowlen, tid, T, 0, 0);
       __syncthreads();                                  // products complete; stage consumed
-      if (tid == 0) {
+      if (tid == 0 && last_row) {
         const int t = tile + S * step;
         if (t < ntl) issue_stage<ST>(a, t, sb, bar + stage, policy_evict_first());
       }
       int local;
       const int j = find_mat(a, tile, local);
       chains_and_out(L, terms, reinterpret_cast<float*>(smem + a.fin_off), a.rowlen, has_zeros,
-                     a.mats[j].out + (int64_t)local * TCH);
+                     a.mats[j].out + (int64_t)row * L.m + (int64_t)local * TCH);
       __syncthreads();                                  // psm / terms / fin reusable
       continue;
     }
     // ---- cross-group reduction: lanes of this warp, then the warps ----
     const int fb = reduce_lanes<NCH, LG, 32>(y, lane);
-    float* yb = ysm + (it & 1) * NW * TCH + warp * TCH;
+    float* yb = ysm + (yit & 1) * NW * TCH + warp * TCH;
 #pragma unroll
     for (int j = 0; j < NF; j++) yb[ch0 + fb + j] = y[j];   // lanes holding a duplicate write the same value
     __syncthreads();                                    // stage consumed, ysm complete
-    if (tid == 0) {
+    if (tid == 0 && last_row) {
       const int t = tile + S * step;
       if (t < ntl) issue_stage<ST>(a, t, sb, bar + stage, policy_evict_first());
     }
     if (tid < TCH) {
-      const float* yr = ysm + (it & 1) * NW * TCH + tid;
+      const float* yr = ysm + (yit & 1) * NW * TCH + tid;
       float s = 0.f;
       for (int w = 0; w < NW; w++) s += yr[w * TCH];
       int local;
       const int j = find_mat(a, tile, local);
-      a.mats[j].out[(int64_t)local * TCH + tid] = 0.5f * s;
+      a.mats[j].out[(int64_t)row * L.m + (int64_t)local * TCH + tid] = 0.5f * s;
     }
+  }
   }
   bl::dep_signal(p.dep);
   if (p.independent) bl::pdl_wait();                    // keep stream completion order
@@ -575,7 +598,7 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
   constexpr bool FUSED = KIND == kFused;
   const bl::LayoutV2& L = g.L;
   // the exact epilogue's serial chains favour one tile per CTA and one round
-  const int T = b1_threads(L, KIND != kExact && (g.independent || g.dep.counted));
+  const int T = b1_threads(L, !kind_exact(KIND) && (g.independent || g.dep.counted));
   if (FUSED && T % (L.gs / 4) != 0) return BITLUT_ELAYOUT;
   if (n_mats < 1 || n_mats > kMaxMats) return BITLUT_EPARAM;
   B1Args a;
@@ -586,6 +609,11 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
   a.total_tiles = mats[n_mats - 1].tile_end;
   a.rounds = (L.U + T - 1) / T;
   a.tab_smem = FUSED || a.rounds > 1;
+  const int n_rows = kind_rows(KIND) ? (g.n_rows > 0 ? g.n_rows : 1) : 1;
+  // several activation rows: one round of units (register tables reloaded per row)
+  if (kind_rows(KIND) && (a.rounds > 1 || n_mats > 1)) return BITLUT_ELAYOUT;
+  a.n_rows = n_rows;
+  a.rows_per_cta = n_rows;
   auto kern = gemv_b1_kernel<R, LG, BITS, ST, KIND>;
   static bool configured = false;
   if (!configured) {
@@ -617,7 +645,7 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
   // two tiles per CTA only where the double-buffered plan still leaves
   // several CTAs per SM (short K); long-K tiles want every CTA they can get
   int tiles_per_cta = tpc_env > 0 ? tpc_env
-                                  : ((KIND != kExact && (g.independent || g.dep.counted) && per_sm2 >= 3) ? 2 : 1);
+                                  : ((!kind_exact(KIND) && (g.independent || g.dep.counted) && per_sm2 >= 3) ? 2 : 1);
   if (tpc_env <= 0 && (a.total_tiles + tiles_per_cta - 1) / tiles_per_cta < sm_count() / 2) tiles_per_cta = 1;
   const int want = (a.total_tiles + tiles_per_cta - 1) / tiles_per_cta;
   // double-buffer when CTAs get several tiles -- by choice (tiles_per_cta)
@@ -636,9 +664,25 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
   if (grid > want) grid = want;
   const int cs = FUSED ? kClusterCTAs : 1;
   grid = (grid + cs - 1) / cs * cs;                     // spare CTAs only build their table slice
-  if (g.grid_out) *g.grid_out = grid;
+  int grid_y = 1;
+  if (kind_rows(KIND)) {
+    // mpGEMM: one tile per CTA (weights stay in smem for the CTA's rows);
+    // rows per CTA as large as keeps >= 4 CTAs per SM busy
+    int r = 32;
+    while (r > 1 && (int64_t)a.total_tiles * ((n_rows + r - 1) / r) < 4 * sm_count()) r >>= 1;
+    a.rows_per_cta = r;
+    grid_y = (n_rows + r - 1) / r;
+    if (grid_y > 65535) return BITLUT_ESHAPE;
+    grid = a.total_tiles;
+    a.stages = 1;
+    s = b1_plan<ST>(L, zeros, a.tab_smem, T, 1, KIND);
+    a.stage_bytes = s.stage_bytes; a.tab_off = s.tab_off; a.ts_off = s.ts_off; a.rs_off = s.rs_off;
+    a.y_off = s.y_off; a.bar_off = s.bar_off; a.sa_off = s.sa_off; a.red_off = s.red_off;
+    a.psm_off = s.psm_off; a.terms_off = s.terms_off; a.fin_off = s.fin_off;
+  }
+  if (g.grid_out) *g.grid_out = grid * grid_y;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
+  cfg.gridDim = dim3(grid, grid_y);
   cfg.blockDim = dim3(T);
   cfg.dynamicSmemBytes = s.total;
   cfg.stream = stream;
@@ -695,11 +739,19 @@ B1Mat single_mat(const GemvArgs& g) {
 int bl_gemv_b1_launch(const GemvArgs& g, int scale_dtype, cudaStream_t s, bool pdl) {
   if (g.L.n_sg != 1) return BITLUT_ELAYOUT;
   const B1Mat m = single_mat(g);
+  const bool f16 = scale_dtype == BITLUT_DT_F16;
+  if (g.n_rows > 1) {
+    if (g.fast)
+      return f16 ? dispatch_b1<__half, kFastRows>(g, &m, 1, nullptr, s, pdl)
+                 : dispatch_b1<float, kFastRows>(g, &m, 1, nullptr, s, pdl);
+    return f16 ? dispatch_b1<__half, kExactRows>(g, &m, 1, nullptr, s, pdl)
+               : dispatch_b1<float, kExactRows>(g, &m, 1, nullptr, s, pdl);
+  }
   if (g.fast)
-    return scale_dtype == BITLUT_DT_F16 ? dispatch_b1<__half, kFast>(g, &m, 1, nullptr, s, pdl)
-                                        : dispatch_b1<float, kFast>(g, &m, 1, nullptr, s, pdl);
-  return scale_dtype == BITLUT_DT_F16 ? dispatch_b1<__half, kExact>(g, &m, 1, nullptr, s, pdl)
-                                      : dispatch_b1<float, kExact>(g, &m, 1, nullptr, s, pdl);
+    return f16 ? dispatch_b1<__half, kFast>(g, &m, 1, nullptr, s, pdl)
+               : dispatch_b1<float, kFast>(g, &m, 1, nullptr, s, pdl);
+  return f16 ? dispatch_b1<__half, kExact>(g, &m, 1, nullptr, s, pdl)
+             : dispatch_b1<float, kExact>(g, &m, 1, nullptr, s, pdl);
 }
 
 bool bl_gemv_b1_fused_fits(const bl::LayoutV2& L, bool zeros, int scale_dtype) {
