@@ -18,6 +18,7 @@ ap.add_argument("--gs", type=int, default=64)
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--n", type=int, default=1)
 ap.add_argument("--fast", type=int, default=0)
+ap.add_argument("--indep", type=int, default=0)
 args = ap.parse_args()
 g = torch.Generator(device="cuda").manual_seed(0)
 q = torch.randint(0, 1 << args.bits, (args.m, args.k), dtype=torch.uint8, device="cuda", generator=g)
@@ -28,6 +29,7 @@ a = torch.randn((args.n, args.k), device="cuda", generator=g).half()
 t, ts, rs = N.build_lut(a, args.gs, N.TABLE_Q8)
 for _ in range(args.reps):
     N.lookup(pw.gpu, pw.scales, None, t, ts, rs, pw.m, pw.k, pw.bits, pw.gs if hasattr(pw, "gs") else pw.group_size,
-             N.TABLE_Q8, N.FLAG_PDL | (N.FLAG_FAST_EPILOGUE if args.fast else 0), False)
+             N.TABLE_Q8, N.FLAG_PDL | (N.FLAG_FAST_EPILOGUE if args.fast else 0)
+             | (N.FLAG_INDEPENDENT if args.indep else 0), False)
 torch.cuda.synchronize()
 print("ok")
