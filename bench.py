@@ -298,7 +298,8 @@ def per_shape_table(device, stream, reps, warmup, barrier, peak, world, bits_lis
     from paper_2407_00088_b200 import _native as N
     gen = torch.Generator(device=device)
     gen.manual_seed(99)
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=device)
+    flush = torch.ones(256 * 1024 * 1024, dtype=torch.uint8, device=device)
+    flush_sum = torch.zeros((), dtype=torch.int64, device=device)
     out = {}
     for bits in bits_list:
         res = {}
@@ -330,11 +331,12 @@ def per_shape_table(device, stream, reps, warmup, barrier, peak, world, bits_lis
                     e[mode + "_us"] = round(us, 3)
                     e[mode + "_GBps"] = round(nbytes / (us * 1e-6) / 1e9, 1)
                     e[mode + "_frac_of_peak"] = round(nbytes / (us * 1e-6) / 1e9 / peak, 4)
-                # one launch after an L2 flush (tables prebuilt)
+                # one launch after an L2 flush (tables prebuilt): a 256 MB read
+                # evicts L2 without leaving dirty lines to write back
                 ts_ = []
                 with torch.cuda.stream(stream):
                     for _ in range(5):
-                        flush.fill_(1)
+                        flush_sum.copy_(flush.sum(dtype=torch.int64))
                         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                         e0.record(stream)
                         N.lookup(ws[0], pw.scales, None, *tabs, pw.m, k, bits, gs, N.TABLE_Q8, base, False)
