@@ -33,6 +33,18 @@ BL_DEV int dp2a_hi(uint32_t mult, uint32_t b, int c) {
   return d;
 }
 
+// Unsigned 16-bit multipliers (lo/hi of mult as u16), signed bytes of b.
+BL_DEV int dp2a_lo_u(uint32_t mult, uint32_t b, int c) {
+  int d;
+  asm("dp2a.lo.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(mult), "r"(b), "r"(c));
+  return d;
+}
+BL_DEV int dp2a_hi_u(uint32_t mult, uint32_t b, int c) {
+  int d;
+  asm("dp2a.hi.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(mult), "r"(b), "r"(c));
+  return d;
+}
+
 struct U8x32 { uint32_t w[8]; };
 
 // 256-bit streaming load (sm_100: LDG.E.256): weights are read exactly once.

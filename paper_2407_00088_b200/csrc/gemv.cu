@@ -20,12 +20,16 @@
 //     B = prmt(b, x ^ 0x8)    = s ? b[eff]           : signfill(b[eff])
 // one gets A + B = sigma*Q[eff] - 1 exactly, for every Q in [-127, 127]
 // (checked exhaustively in tests/test_encoding.py).  One prmt does this for
-// four nibbles at once.
+// four nibbles at once.  b is never materialised: prmt(~a, sel) = ~prmt(a,
+// sel) byte for byte (sign-replicate mode included) and ~y = -y - 1, so with
+// Y = prmt(a, x ^ 0x8) the sum is A - Y = sigma*Q[eff] exactly; Y is
+// accumulated with negated multipliers.
 //
-// Accumulation: dp2a.lo/hi (IDP.2A) adds two looked-up bytes into ONE int32
-// with 16-bit multipliers (1, -32768): acc = X - 32768*Y, where X and Y are
-// the partial sums of two streams.  |X| <= 128*gpg < 16384 for gpg <= 128,
-// so X = sext15(acc), Y = (X - acc) >> 15 recover both exactly.
+// Accumulation: dp2a.lo/hi (IDP.2A) adds two looked-up bytes into ONE int32:
+// A with unsigned 16-bit multipliers (1, 32768), Y with signed (-1, -32768),
+// so acc = X + 32768*Y' where X and Y' are the exact partial sums of two
+// streams.  |X| <= 127*gpg < 16384 for gpg <= 128, so X = sext15(acc) and
+// Y' = (acc - X) >> 15 recover both exactly.
 //
 // Per 8 lookups: 3 ALU (shift / xor) + 4 PRMT on the ALU pipe and 8 IDP.2A on
 // the FMA pipe -- both pipes run at 64 lanes/clk/SM on B200 (measured,

@@ -100,39 +100,51 @@ B1Plan b1_plan(const bl::LayoutV2& L, bool zeros, bool tab_smem, int T, int stag
   return s;
 }
 
-// Lookup of one k-group for 32 streams with plane-merging multipliers.
+// Lookup of one k-group for 32 streams with plane-merging multipliers (the
+// A/Y form of gemv_core.cuh lookup_kg: A - Y = sQ exactly, Y enters with the
+// negated multiplier).
 template <int BITS, int NACC>
 __device__ __forceinline__ void lookup_kg_merged(const uint4 w, uint32_t a0, uint32_t a1, int (&acc)[NACC]) {
-  const uint32_t b0 = ~a0, b1 = ~a1;
   const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
   for (int q = 0; q < 4; q++) {
     const uint32_t x = ws[q];
     const uint32_t xx = x ^ 0x88888888u;
-    const uint32_t A0 = bl::prmt(a0, a1, x), B0 = bl::prmt(b0, b1, xx);
-    const uint32_t A1 = bl::prmt(a0, a1, x >> 16), B1 = bl::prmt(b0, b1, xx >> 16);
+    const uint32_t A0 = bl::prmt(a0, a1, x), Y0 = bl::prmt(a0, a1, xx);
+    const uint32_t A1 = bl::prmt(a0, a1, x >> 16), Y1 = bl::prmt(a0, a1, xx >> 16);
     if constexpr (BITS == 4) {
-      // bytes 0..3 of A0/B0 = planes 0..3 of channel 2q; of A1/B1: channel 2q+1
-      constexpr uint32_t M01 = 0x00020001u, M23 = 0x00080004u;
+      // bytes 0..3 of A0/Y0 = planes 0..3 of channel 2q; of A1/Y1: channel 2q+1
+      constexpr uint32_t M01 = 0x00020001u, M23 = 0x00080004u;      // (1, 2), (4, 8)
+      constexpr uint32_t N01 = 0xFFFEFFFFu, N23 = 0xFFF8FFFCu;      // negated
       acc[2 * q] = bl::dp2a_lo(M01, A0, acc[2 * q]);
-      acc[2 * q] = bl::dp2a_lo(M01, B0, acc[2 * q]);
+      acc[2 * q] = bl::dp2a_lo(N01, Y0, acc[2 * q]);
       acc[2 * q] = bl::dp2a_hi(M23, A0, acc[2 * q]);
-      acc[2 * q] = bl::dp2a_hi(M23, B0, acc[2 * q]);
+      acc[2 * q] = bl::dp2a_hi(N23, Y0, acc[2 * q]);
       acc[2 * q + 1] = bl::dp2a_lo(M01, A1, acc[2 * q + 1]);
-      acc[2 * q + 1] = bl::dp2a_lo(M01, B1, acc[2 * q + 1]);
+      acc[2 * q + 1] = bl::dp2a_lo(N01, Y1, acc[2 * q + 1]);
       acc[2 * q + 1] = bl::dp2a_hi(M23, A1, acc[2 * q + 1]);
-      acc[2 * q + 1] = bl::dp2a_hi(M23, B1, acc[2 * q + 1]);
-    } else {
-      // pair i = streams (2i, 2i+1): W2 -> channel i planes (0, 1); W1 -> channels (2i, 2i+1)
-      constexpr uint32_t M = BITS == 2 ? 0x00020001u : kMult;
+      acc[2 * q + 1] = bl::dp2a_hi(N23, Y1, acc[2 * q + 1]);
+    } else if constexpr (BITS == 2) {
+      // pair i = streams (2i, 2i+1) = channel i, planes (0, 1)
+      constexpr uint32_t M = 0x00020001u, Nm = 0xFFFEFFFFu;
       acc[4 * q + 0] = bl::dp2a_lo(M, A0, acc[4 * q + 0]);
-      acc[4 * q + 0] = bl::dp2a_lo(M, B0, acc[4 * q + 0]);
+      acc[4 * q + 0] = bl::dp2a_lo(Nm, Y0, acc[4 * q + 0]);
       acc[4 * q + 1] = bl::dp2a_hi(M, A0, acc[4 * q + 1]);
-      acc[4 * q + 1] = bl::dp2a_hi(M, B0, acc[4 * q + 1]);
+      acc[4 * q + 1] = bl::dp2a_hi(Nm, Y0, acc[4 * q + 1]);
       acc[4 * q + 2] = bl::dp2a_lo(M, A1, acc[4 * q + 2]);
-      acc[4 * q + 2] = bl::dp2a_lo(M, B1, acc[4 * q + 2]);
+      acc[4 * q + 2] = bl::dp2a_lo(Nm, Y1, acc[4 * q + 2]);
       acc[4 * q + 3] = bl::dp2a_hi(M, A1, acc[4 * q + 3]);
-      acc[4 * q + 3] = bl::dp2a_hi(M, B1, acc[4 * q + 3]);
+      acc[4 * q + 3] = bl::dp2a_hi(Nm, Y1, acc[4 * q + 3]);
+    } else {
+      // W1: pair i = channels (2i, 2i+1), packed P_even + 32768 P_odd
+      acc[4 * q + 0] = bl::dp2a_lo_u(kMult, A0, acc[4 * q + 0]);
+      acc[4 * q + 0] = bl::dp2a_lo(kMultNeg, Y0, acc[4 * q + 0]);
+      acc[4 * q + 1] = bl::dp2a_hi_u(kMult, A0, acc[4 * q + 1]);
+      acc[4 * q + 1] = bl::dp2a_hi(kMultNeg, Y0, acc[4 * q + 1]);
+      acc[4 * q + 2] = bl::dp2a_lo_u(kMult, A1, acc[4 * q + 2]);
+      acc[4 * q + 2] = bl::dp2a_lo(kMultNeg, Y1, acc[4 * q + 2]);
+      acc[4 * q + 3] = bl::dp2a_hi_u(kMult, A1, acc[4 * q + 3]);
+      acc[4 * q + 3] = bl::dp2a_hi(kMultNeg, Y1, acc[4 * q + 3]);
     }
   }
 }
@@ -333,7 +345,6 @@ __global__ void __launch_bounds__(384) gemv_b1_kernel(const __grid_constant__ B1
   constexpr int NV = reduced_count<NACC, 1, LG>();      // after the in-group reduction
   constexpr int NCH = BITS == 1 ? 2 * NV : NV;          // float channel values per lane
   constexpr int NF = reduced_count<NCH, LG, 32>();      // after the cross-group reduction
-  constexpr int KGF = BITS == 4 ? 15 : (BITS == 2 ? 3 : -32767);  // per-kg offset of the A/B trick
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int T = blockDim.x, NW = T >> 5;
@@ -454,21 +465,20 @@ __global__ void __launch_bounds__(384) gemv_b1_kernel(const __grid_constant__ B1
         const int base = transpose_reduce<LG, 16, int>(acc, lane);
         if (live) {
           constexpr int NFP = 16 / LG;
-          const int fix = -32767 * (R * LG);
           int32_t* dst = reinterpret_cast<int32_t*>(smem + a.psm_off) + (u / LG) * 33 + 2 * base;
 #pragma unroll
-          for (int i = 0; i < NFP; i++) {
-            const int v = acc[i] + fix;
+          for (int i = 0; i < NFP; i++) {             // v = P_even + 32768 P_odd
+            const int v = acc[i];
             const int pe = (v << 17) >> 17;
             dst[2 * i] = pe;
-            dst[2 * i + 1] = (pe - v) >> 15;
+            dst[2 * i + 1] = (v - pe) >> 15;
           }
         }
         continue;
       }
       int acc[NACC];
 #pragma unroll
-      for (int i = 0; i < NACC; i++) acc[i] = BITS == 1 ? 0 : KGF * R;   // undo A/B's -1 per lookup
+      for (int i = 0; i < NACC; i++) acc[i] = 0;
       if (live) {
         const int ub = u >> 5, l = u & 31;
         const int nu_b = min(32, U - 32 * ub);
@@ -500,10 +510,10 @@ __global__ void __launch_bounds__(384) gemv_b1_kernel(const __grid_constant__ B1
         if constexpr (BITS == 1) {
 #pragma unroll
           for (int i = 0; i < NV; i++) {
-            const int v = acc[i] + KGF * R * LG;
+            const int v = acc[i];                       // P_even + 32768 P_odd
             const int pe = (v << 17) >> 17;
             S[2 * i] = pe;
-            S[2 * i + 1] = (pe - v) >> 15;
+            S[2 * i + 1] = (v - pe) >> 15;
           }
         } else {
 #pragma unroll

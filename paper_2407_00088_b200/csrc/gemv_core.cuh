@@ -7,7 +7,11 @@
 namespace blk {
 
 
-constexpr uint32_t kMult = 0x80000001u;   // int16 pair (lo = 1, hi = -32768)
+// Stream-pair packing: v = P_even + 32768 * P_odd.  The looked-up A bytes go
+// in with unsigned multipliers (1, 32768), the complementary Y bytes (see
+// lookup_kg) with signed (-1, -32768).
+constexpr uint32_t kMult = 0x80000001u;      // u16 pair (lo = 1, hi = 32768)
+constexpr uint32_t kMultNeg = 0x8000FFFFu;   // s16 pair (lo = -1, hi = -32768)
 
 struct GemvArgs {
   const uint8_t* w;
@@ -74,23 +78,28 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 // One k-group of 32 streams: 4 words x (2 selectors + 4 prmt + 8 dp2a).
+// A/B tables: with a = Q - (Q<0) per byte and b = ~a, prmt(a, x) +
+// prmt(b, x ^ 8) = sQ - 1 for every nibble (s = mirror flag, bit 3 of x).
+// Since prmt(~a, sel) = ~prmt(a, sel) byte for byte (sign-replicate mode
+// included) and ~y = -y - 1, the B term is -(Y + 1) with Y = prmt(a, x ^ 8):
+// A - Y = sQ exactly, so the B lookup reuses the A table and enters dp2a
+// with negated multipliers -- no complement, no per-lookup constant.
 __device__ __forceinline__ void lookup_kg(const uint4 w, uint32_t a0, uint32_t a1, int (&acc)[16]) {
-  const uint32_t b0 = ~a0, b1 = ~a1;
   const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
   for (int q = 0; q < 4; q++) {
     const uint32_t x = ws[q];
     const uint32_t xx = x ^ 0x88888888u;
-    const uint32_t A0 = bl::prmt(a0, a1, x), B0 = bl::prmt(b0, b1, xx);
-    const uint32_t A1 = bl::prmt(a0, a1, x >> 16), B1 = bl::prmt(b0, b1, xx >> 16);
-    acc[4 * q + 0] = bl::dp2a_lo(kMult, A0, acc[4 * q + 0]);
-    acc[4 * q + 0] = bl::dp2a_lo(kMult, B0, acc[4 * q + 0]);
-    acc[4 * q + 1] = bl::dp2a_hi(kMult, A0, acc[4 * q + 1]);
-    acc[4 * q + 1] = bl::dp2a_hi(kMult, B0, acc[4 * q + 1]);
-    acc[4 * q + 2] = bl::dp2a_lo(kMult, A1, acc[4 * q + 2]);
-    acc[4 * q + 2] = bl::dp2a_lo(kMult, B1, acc[4 * q + 2]);
-    acc[4 * q + 3] = bl::dp2a_hi(kMult, A1, acc[4 * q + 3]);
-    acc[4 * q + 3] = bl::dp2a_hi(kMult, B1, acc[4 * q + 3]);
+    const uint32_t A0 = bl::prmt(a0, a1, x), Y0 = bl::prmt(a0, a1, xx);
+    const uint32_t A1 = bl::prmt(a0, a1, x >> 16), Y1 = bl::prmt(a0, a1, xx >> 16);
+    acc[4 * q + 0] = bl::dp2a_lo_u(kMult, A0, acc[4 * q + 0]);
+    acc[4 * q + 0] = bl::dp2a_lo(kMultNeg, Y0, acc[4 * q + 0]);
+    acc[4 * q + 1] = bl::dp2a_hi_u(kMult, A0, acc[4 * q + 1]);
+    acc[4 * q + 1] = bl::dp2a_hi(kMultNeg, Y0, acc[4 * q + 1]);
+    acc[4 * q + 2] = bl::dp2a_lo_u(kMult, A1, acc[4 * q + 2]);
+    acc[4 * q + 2] = bl::dp2a_lo(kMultNeg, Y1, acc[4 * q + 2]);
+    acc[4 * q + 3] = bl::dp2a_hi_u(kMult, A1, acc[4 * q + 3]);
+    acc[4 * q + 3] = bl::dp2a_hi(kMultNeg, Y1, acc[4 * q + 3]);
   }
 }
 
@@ -395,7 +404,7 @@ __device__ __forceinline__ void reg_terms(const GemvArgs& p, const int (&acc)[16
   for (int i = 0; i < NF; i++) {
     const int v = acc[i] + fix;
     const int pe = (v << 17) >> 17;
-    const int po = (pe - v) >> 15;
+    const int po = (v - pe) >> 15;
     if (BITS == 1) { S[2 * i] = pe; S[2 * i + 1] = po; }
     else if (BITS == 2) { S[i] = pe + 2 * po; }
     else { if (i & 1) S[i >> 1] += 4 * (pe + 2 * po); else S[i >> 1] = pe + 2 * po; }
@@ -583,7 +592,7 @@ __device__ __forceinline__ void tile_body(const GemvArgs& p, int tile, int row, 
       if (__any_sync(0xffffffffu, live)) base = transpose_reduce<LG, 16, int>(acc, lane);
       if (regepi) {
         if (live) {
-          const int fix = -32767 * (R * LG);
+          const int fix = 0;                  // lookup_kg sums are exact
           const int g = uu / LG;
           switch (bits) {
             case 1: reg_terms<1, NF, ST>(p, acc, fix, base, g, sraw, zraw, tsm, rsm, ysm, ystride, NQ); break;
@@ -595,14 +604,14 @@ __device__ __forceinline__ void tile_body(const GemvArgs& p, int tile, int row, 
         }
       } else if (live) {
         // undo the -1 per lookup of both streams, split each pair
-        const int fix = -32767 * (R * LG);
+        // split each packed pair v = P_even + 32768 P_odd (|P| < 16384)
         int32_t* dst = psm + (size_t)(uu / LG) * pstride + sg * 32 + 2 * base;
 #pragma unroll
         for (int i = 0; i < NF; i++) {
-          const int v = acc[i] + fix;
+          const int v = acc[i];
           const int pe = (v << 17) >> 17;
           dst[2 * i] = pe;
-          dst[2 * i + 1] = (pe - v) >> 15;
+          dst[2 * i + 1] = (v - pe) >> 15;
         }
       }
     } else {

@@ -5,8 +5,11 @@
   A + B == sigma*Q - 1 -- checked exhaustively with a bit-level model of
   `prmt.b32` (default mode: selector bit 3 replicates the selected byte's
   sign);
-* the dp2a packing: two streams in one int32 with multipliers (1, -32768)
-  are recovered exactly for any group of up to 128 k-groups;
+* the A/Y form the kernels use: prmt(~a, sel) == ~prmt(a, sel), so
+  A - prmt(a, x ^ 8) == sigma*Q exactly (the B table is never stored);
+* the dp2a packing: A bytes with unsigned multipliers (1, 32768), Y bytes
+  with signed (-1, -32768) -> two exact stream sums in one int32, recovered
+  for any group of up to 128 k-groups;
 * layout v2 (csrc/layout.cuh): the chunk offset map is a bijection onto
   [0, bits*M*K/8) for every BASELINE shape.
 """
@@ -55,6 +58,30 @@ def test_ab_trick_exhaustive():
                 assert A + B == sigma * Q - 1, (Q, eff, s, A, B)
 
 
+def test_ay_form_exhaustive():
+    """prmt of the complemented table == complement of prmt, for every byte
+    and selector nibble (sign-replicate mode included); hence A - Y = sQ."""
+    for v in range(256):
+        for nib in range(16):
+            words = [(v << (8 * (nib & 3))) & 0xFFFFFFFF] * 2
+            sel = nib
+            lhs = prmt((~words[0]) & 0xFFFFFFFF, (~words[1]) & 0xFFFFFFFF, sel) & 0xFF
+            rhs = (~prmt(words[0], words[1], sel)) & 0xFF
+            assert lhs == rhs, (v, nib)
+    for Q in range(-127, 128):
+        a = encode_a(Q)
+        for eff in range(8):
+            tab_a = [(eff * 37 + j * 11) & 0xFF for j in range(8)]
+            tab_a[eff] = a
+            ta0 = sum(tab_a[i] << (8 * i) for i in range(4))
+            ta1 = sum(tab_a[4 + i] << (8 * i) for i in range(4))
+            for s in (0, 1):
+                x = (s << 3) | eff
+                A = s8(prmt(ta0, ta1, x) & 0xFF)
+                Y = s8(prmt(ta0, ta1, x ^ 0x8) & 0xFF)
+                assert A - Y == (-Q if s else Q), (Q, eff, s)
+
+
 def test_mirror_encoding_matches_reference_flip():
     # x = idx ^ (7 * (idx >> 3)) gives (s, eff) with eff = idx ^ (15*s)
     # restricted to 3 bits (_kernels.py:175-176); the encoding is an involution
@@ -66,25 +93,40 @@ def test_mirror_encoding_matches_reference_flip():
         assert (x ^ (7 * (x >> 3))) == idx
 
 
+def dp2a(mult_lo: int, mult_hi: int, b: int, c: int, half: int) -> int:
+    """dp2a.lo (half = 0) / .hi (half = 1) with integer multipliers and signed bytes of b."""
+    b0 = s8((b >> (16 * half)) & 0xFF)
+    b1 = s8((b >> (16 * half + 8)) & 0xFF)
+    return int(np.int32(c + mult_lo * b0 + mult_hi * b1))
+
+
 @pytest.mark.parametrize("gpg", [4, 8, 16, 32, 64, 128])
 def test_dp2a_pair_packing(gpg):
+    """A bytes with unsigned (1, 32768), Y bytes with signed (-1, -32768):
+    acc = X + 32768 Y' with X, Y' the exact sums of sQ of two streams."""
     rng = np.random.default_rng(gpg)
-    M = -32768
-    for _ in range(2000):
-        # per-lookup contributions A+B in [-128, 126]
-        xe = rng.integers(-128, 127, gpg)
-        xo = rng.integers(-128, 127, gpg)
-        if _ % 3 == 0:
-            xe[:] = -128
-            xo[:] = 126
-        acc = int(np.int32(np.sum(xe) + M * np.sum(xo)))
-        v = acc + (-32767 * gpg)          # add back +1 per lookup on both streams
-        v = int(np.int32(v))
+    for it in range(300):
+        acc, xe, xo = 0, 0, 0
+        for _ in range(gpg):
+            # one byte pair per stream: A and Y with A - Y = sQ in [-127, 127]
+            A = rng.integers(-128, 128, 2)
+            sq = rng.integers(-127, 128, 2) if it % 3 else np.array([-127, 127])
+            Y = A - sq
+            ok = (Y >= -128) & (Y <= 127)
+            A = np.where(ok, A, sq)
+            Y = np.where(ok, Y, 0)
+            wa = (int(A[0]) & 0xFF) | ((int(A[1]) & 0xFF) << 8)
+            wy = (int(Y[0]) & 0xFF) | ((int(Y[1]) & 0xFF) << 8)
+            acc = dp2a(1, 32768, wa, acc, 0)
+            acc = dp2a(-1, -32768, wy, acc, 0)
+            xe += int(A[0] - Y[0])
+            xo += int(A[1] - Y[1])
+        v = acc
         pe = ((v << 17) & 0xFFFFFFFF)
         pe = pe - (1 << 32) if pe & 0x80000000 else pe
         pe >>= 17
-        po = (pe - v) >> 15
-        assert pe == int(np.sum(xe)) + gpg and po == int(np.sum(xo)) + gpg
+        po = (v - pe) >> 15
+        assert pe == xe and po == xo, (pe, xe, po, xo)
 
 
 def chunk_offsets(m, k, bits, gs):
