@@ -45,6 +45,13 @@ BL_DEV int dp2a_hi_u(uint32_t mult, uint32_t b, int c) {
   return d;
 }
 
+// d = c + sum_i a.byte_i * b.byte_i   (signed x signed)
+BL_DEV int dp4a(uint32_t a, uint32_t b, int c) {
+  int d;
+  asm("dp4a.s32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
 struct U8x32 { uint32_t w[8]; };
 
 // 256-bit streaming load (sm_100: LDG.E.256): weights are read exactly once.

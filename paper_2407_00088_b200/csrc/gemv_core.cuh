@@ -13,6 +13,16 @@ namespace blk {
 constexpr uint32_t kMult = 0x80000001u;      // u16 pair (lo = 1, hi = 32768)
 constexpr uint32_t kMultNeg = 0x8000FFFFu;   // s16 pair (lo = -1, hi = -32768)
 
+// One weight matrix of a batch-1 launch over several matrices sharing one
+// activation row's tables (q/k/v, gate/up): tiles numbered matrix after matrix.
+struct StreamMat {
+  const uint8_t* w;
+  const void* wscales;
+  const void* zeros;
+  float* out;
+  int tile_end;               // cumulative tile count up to and including this matrix
+};
+
 struct GemvArgs {
   const uint8_t* w;
   const void* wscales;
