@@ -291,7 +291,12 @@ SHAPES_7B = [("4096x4096", 4096, 4096), ("11008x4096", 11008, 4096), ("4096x1100
 L2_BYTES = 126 * 1024 * 1024
 
 
-def per_shape_table(device, stream, reps, warmup, barrier, peak, world, bits_list=(1, 2, 4), gs=64):
+# group size per bit width at batch 1: W2 g64 (BASELINE configs[1]), W1 g128
+# (configs[2]: 1-bit sign planes), W4 g128 (configs[0] / configs[3])
+GS_OF_BITS = {1: 128, 2: 64, 4: 128}
+
+
+def per_shape_table(device, stream, reps, warmup, barrier, peak, world, bits_list=(1, 2, 4), gs_fixed=None):
     """Per-launch us and GB/s for every 7B shape at W1/W2/W4."""
     import torch
     import paper_2407_00088_b200 as B
@@ -303,7 +308,9 @@ def per_shape_table(device, stream, reps, warmup, barrier, peak, world, bits_lis
     out = {}
     for bits in bits_list:
         res = {}
+        gs_b = gs_fixed or GS_OF_BITS[bits]
         for name, m, k in SHAPES_7B:
+            gs = gs_b
             m_loc = m // world
             q = torch.randint(0, 1 << bits, (m_loc, k), dtype=torch.uint8, device=device, generator=gen)
             sc = (torch.randn((m_loc, k // gs), device=device, generator=gen).abs() * 0.02 + 1e-3).half()
@@ -315,7 +322,7 @@ def per_shape_table(device, stream, reps, warmup, barrier, peak, world, bits_lis
             ws = [pw.gpu] + [pw.gpu.clone() for _ in range(copies - 1)]
             x = torch.randn((1, k), device=device, generator=gen).half()
             tabs = N.build_lut(x, gs, N.TABLE_Q8)
-            entry = {"packed_bytes_per_gpu": nbytes, "launches_rotated": len(ws)}
+            entry = {"packed_bytes_per_gpu": nbytes, "launches_rotated": len(ws), "group_size": gs}
             for epi in ("fast", "exact"):
                 e = {}
                 base = N.FLAG_PDL | (N.FLAG_FAST_EPILOGUE if epi == "fast" else 0)
@@ -350,6 +357,74 @@ def per_shape_table(device, stream, reps, warmup, barrier, peak, world, bits_lis
         out[f"W{bits}"] = res
     del flush
     torch.cuda.empty_cache()
+    return out
+
+
+SHAPES_70B = [("q/o 8192x8192", 8192, 8192, 2), ("k/v 1024x8192", 1024, 8192, 2),
+              ("gate/up 28672x8192", 28672, 8192, 2), ("down 8192x28672", 8192, 28672, 1)]
+
+
+def llama70b_table(device, stream, reps, warmup, barrier, peak):
+    """BASELINE configs[4] on ONE GPU: every Llama-2-70B layer matrix cut to
+    the output-channel shard one rank of a P-GPU tensor-parallel group owns
+    (P = 1, 2, 4, 8; M/P rows), W2/W4 g128, batch 1 (fast epilogue, launches
+    overlapped as in a layer) and batch 8 (mpGEMM rows).  Per-GPU compute
+    time; the all-gather of the output slices is not measurable with one GPU
+    (parallel.py runs it; gloo tests cover it)."""
+    import torch
+    import paper_2407_00088_b200 as B
+    from paper_2407_00088_b200 import _native as N
+    gen = torch.Generator(device=device)
+    gen.manual_seed(70)
+    gs = 128
+    out = {}
+    for bits in (2, 4):
+        for P in (1, 2, 4, 8):
+            layer_us, layer_us8, layer_bytes = 0.0, 0.0, 0
+            rows = {}
+            for name, m, k, count in SHAPES_70B:
+                m_loc = m // P
+                q = torch.randint(0, 1 << bits, (m_loc, k), dtype=torch.uint8, device=device, generator=gen)
+                sc = (torch.randn((m_loc, k // gs), device=device, generator=gen).abs() * 0.02 + 1e-3).half()
+                pw = B.prepare_weights(B.QuantizedWeights(m=m_loc, k=k, bits=bits, group_size=gs, qvalues=q,
+                                                          scales=sc))
+                del q
+                nbytes = pw.packed_bytes
+                copies = max(4, -(-4 * L2_BYTES // nbytes))
+                ws = [pw.gpu] + [pw.gpu.clone() for _ in range(copies - 1)]
+                scs = [pw.scales] + [pw.scales.clone() for _ in range(copies - 1)]
+                e = {"m_per_gpu": m_loc, "k": k, "packed_bytes_per_gpu": nbytes}
+                for nrow in (1, 8):
+                    x = torch.randn((nrow, k), device=device, generator=gen).half()
+                    tabs = N.build_lut(x, gs, N.TABLE_Q8)
+                    fl = N.FLAG_PDL | N.FLAG_FAST_EPILOGUE | (N.FLAG_INDEPENDENT if nrow == 1 else 0)
+
+                    def body(fl=fl, tabs=tabs):
+                        for w, sc_ in zip(ws, scs):
+                            N.lookup(w, sc_, None, *tabs, m_loc, k, bits, gs, N.TABLE_Q8, fl, False)
+                    g = capture(body, stream)
+                    with torch.cuda.stream(stream):
+                        ms = time_graph(g, reps, warmup, barrier)
+                    del g
+                    us = ms * 1e3 / len(ws)
+                    e[f"n{nrow}_us"] = round(us, 3)
+                    e[f"n{nrow}_GBps"] = round(nbytes / (us * 1e-6) / 1e9, 1)
+                    if nrow == 1:
+                        e["n1_frac_of_peak"] = round(nbytes / (us * 1e-6) / 1e9 / peak, 4)
+                    else:
+                        e["n8_equiv_TOPS"] = round(2 * nrow * m_loc * k / (us * 1e-6) / 1e12, 2)
+                layer_us += count * e["n1_us"]
+                layer_us8 += count * e["n8_us"]
+                layer_bytes += count * nbytes
+                rows[name] = e
+                del ws, scs, pw
+                torch.cuda.empty_cache()
+            out[f"W{bits}_tp{P}"] = {
+                "shapes": rows,
+                "layer_us_per_gpu_n1": round(layer_us, 2),
+                "layer_GBps_per_gpu_n1": round(layer_bytes / (layer_us * 1e-6) / 1e9, 1),
+                "layer_us_per_gpu_n8": round(layer_us8, 2),
+                "layer_packed_bytes_per_gpu": layer_bytes}
     return out
 
 
@@ -456,6 +531,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-shapes", action="store_true")
     ap.add_argument("--no-gemm", action="store_true")
+    ap.add_argument("--no-70b", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     bits, gs = 2, 64
@@ -603,6 +679,13 @@ def main():
                                         peak, world)
         per_shape["clocks"] = clk_shapes.summary()
 
+    # ---- Llama-2-70B per-GPU shards (BASELINE configs[4]) ----
+    shards70 = None
+    if not args.no_70b and world == 1:
+        with ClockSampler(local) as clk_70:
+            shards70 = llama70b_table(device, stream, max(3, args.steps // 5), args.warmup, barrier, peak)
+        shards70["clocks"] = clk_70.summary()
+
     # ---- prefill mpGEMM (BASELINE configs[3]) ----
     gemm = None
     if not args.no_gemm:
@@ -714,6 +797,7 @@ def main():
             "lookups_only_graph": lookups_graph,
             "per_shape": per_shape,
             "mpgemm_prefill": gemm,
+            "llama70b_shards": shards70,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "e2e_per_call_api": per_call,

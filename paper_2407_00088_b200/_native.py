@@ -28,7 +28,8 @@ FLAG_INDEPENDENT = 2
 FLAG_FAST_EPILOGUE = 4
 FLAG_FUSED_TABLES = 8       # table op may fold into its consumers (graph executor)
 PLAN_JOINED = 16            # plan: launched together with the previous op
-FLAG_COMBINED_PARTIALS = 32  # fast batch-1: partials = sum_p 2^p P_p per (channel, group)
+FLAG_COMBINED_PARTIALS = 32
+FLAG_STREAM = 64            # fast batch-1: force the streaming kernel (gemv_stream.cu)  # fast batch-1: partials = sum_p 2^p P_p per (channel, group)
 
 _vp, _i = ctypes.c_void_p, ctypes.c_int
 
@@ -49,7 +50,14 @@ _SIGS = {
                              _vp, _vp],
     "bitlut_mpgemm_launches": [_i, _i, _i, _i, _i, _i],
     "bitlut_mpgemv_fused": [_vp, _i, _vp, _i, _i, _i, _i, _vp, _vp, _i, _vp, _i, _vp],
+    "bitlut_mpgemv_multi": [_vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _i, _vp],
 }
+
+
+class BitlutMat(ctypes.Structure):
+    """include/bitlut_b200.h bitlut_mat: one matrix of a grouped batch-1 launch."""
+    _fields_ = [("wgpu", ctypes.c_void_p), ("wscales", ctypes.c_void_p), ("zeros", ctypes.c_void_p),
+                ("m", ctypes.c_int32), ("out", ctypes.c_void_p)]
 
 
 class GpuLayout(ctypes.Structure):
@@ -168,6 +176,24 @@ def lookup(wgpu: torch.Tensor, wscales: torch.Tensor, zeros: Optional[torch.Tens
                              stream_of(wgpu))
     raise_for_status(rc, "bitlut_mpgemm")
     return out, partials
+
+
+def mpgemv_multi(mats, tables: torch.Tensor, tscales: torch.Tensor, rowsums: torch.Tensor, k: int, bits: int,
+                 group_size: int, flags: int) -> list:
+    """Several batch-1 matrices sharing one activation row's tables in ONE
+    launch (bitlut_mpgemv_multi): mats = [(wgpu, wscales, zeros, m), ...];
+    returns one (1, m) f32 output per matrix."""
+    require_cuda(tables, "tables")
+    outs = [torch.empty((1, m), dtype=torch.float32, device=tables.device) for (_, _, _, m) in mats]
+    arr = (BitlutMat * len(mats))()
+    for i, ((w, sc, z, m), o) in enumerate(zip(mats, outs)):
+        arr[i].wgpu, arr[i].wscales = w.data_ptr(), sc.data_ptr()
+        arr[i].zeros = None if z is None else z.data_ptr()
+        arr[i].m, arr[i].out = m, o.data_ptr()
+    rc = lib().bitlut_mpgemv_multi(arr, len(mats), k, bits, group_size, dtype_code(mats[0][1]), ptr(tables),
+                                   ptr(tscales), ptr(rowsums), flags, stream_of(tables))
+    raise_for_status(rc, "bitlut_mpgemv_multi")
+    return outs
 
 
 @torch.library.custom_op("bitlut_b200::mpgemv_fused", mutates_args=())

@@ -254,6 +254,7 @@ int bl_mpgemm_launch(const uint8_t* wgpu, int m, int k, int bits, int group_size
   a.out = out; a.partials = partials; a.trace = trace; a.L = L;
   a.independent = pdl && (flags & BITLUT_FLAG_INDEPENDENT) != 0;
   a.fast = (flags & BITLUT_FLAG_FAST_EPILOGUE) != 0;
+  a.force_stream = (flags & BITLUT_FLAG_STREAM) != 0;
   a.n_rows = n;
   // weight-stationary rows: a CTA keeps its tile in smem for up to 32 rows
   // once there are enough (tile, row-block) CTAs to fill the GPU

@@ -854,6 +854,7 @@ int bl_mpgemv_multi_launch(const bitlut_mat* mats, int n_mats, int k, int bits, 
   g.grid_out = grid_out;
   g.independent = pdl && (flags & BITLUT_FLAG_INDEPENDENT) != 0;
   g.fast = (flags & BITLUT_FLAG_FAST_EPILOGUE) != 0;
+  g.force_stream = (flags & BITLUT_FLAG_STREAM) != 0;
   g.zeros = mats[0].zeros;                              // presence flag for the epilogue
   g.rows_per_cta = 1; g.n_rows = 1;
   const cudaStream_t st = (cudaStream_t)stream;

@@ -40,6 +40,7 @@ struct GemvArgs {
   bl::LayoutV2 L;
   bl::DepSync dep;           // op-list counters (n_wait == 0 and done == null otherwise)
   int* grid_out;             // host: receives the launch's CTA count (op-list executor), or null
+  int force_stream;          // BITLUT_FLAG_STREAM: batch-1 fast lookups through gemv_stream.cu
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {

@@ -548,25 +548,32 @@ int dispatch_s(const GemvArgs& g, const blk::StreamMat* m, int nm, cudaStream_t 
 
 }  // namespace
 
-bool bl_gemv_stream_enabled(int total_tiles, int nsl) {
-  static int on = -1, min_slices = -1;
-  if (on < 0) {
-    const char* e = getenv("BITLUT_STREAM");             // opt-in: 1 enables the streaming kernel
-    on = e ? atoi(e) != 0 : 0;
-    const char* m = getenv("BITLUT_STREAM_MIN_SLICES");  // diagnostic: size threshold
-    min_slices = m ? atoi(m) : 0;
+// Kernel choice for a batch-1 fast launch: forced by BITLUT_FLAG_STREAM, else
+// long-K launches with plenty of slices only: a tile row above 64 KB cannot
+// be double-buffered by gemv_b1_kernel, and >= 4096 slices keep every warp
+// of the streaming kernel busy (bench.py llama70b_shards, 8192x28672:
+// W4 27.1 vs 39.2 us, W2 19.8 vs 20.9 us at 1 GPU; the 1/2- to 1/8-row
+// shards stay on gemv_b1_kernel, which is faster there).
+// BITLUT_STREAM=0/1 in the environment overrides (diagnostic).
+bool bl_gemv_stream_wanted(const bl::LayoutV2& L, int total_tiles, bool force) {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("BITLUT_STREAM");
+    env = e ? atoi(e) : -1;
   }
-  return on != 0 && total_tiles * nsl >= min_slices;
+  if (env >= 0) return env != 0;
+  const int nsl = (L.U + 63) / 64;
+  return force || ((size_t)L.KG * 16 > 65536 && (int64_t)total_tiles * nsl >= 4096);
 }
 
 // Batch-1 fast-epilogue lookups through the streaming kernel.  Returns
-// BITLUT_ELAYOUT when the shape is outside its envelope (the caller then
-// uses gemv_b1_kernel).
+// BITLUT_ELAYOUT when it is not wanted or the shape is outside its envelope
+// (the caller then uses gemv_b1_kernel).
 int bl_gemv_stream_launch(const blk::GemvArgs& g, const blk::StreamMat* mats, int n_mats, int scale_dtype,
                           cudaStream_t s, bool pdl) {
   const bl::LayoutV2& L = g.L;
   if (!g.fast || g.n_rows > 1 || L.n_sg != 1 || n_mats < 1 || n_mats > kMaxMatsS) return BITLUT_ELAYOUT;
-  if (!bl_gemv_stream_enabled(mats[n_mats - 1].tile_end, (L.U + 63) / 64)) return BITLUT_ELAYOUT;
+  if (!bl_gemv_stream_wanted(L, mats[n_mats - 1].tile_end, g.force_stream != 0)) return BITLUT_ELAYOUT;
   return scale_dtype == BITLUT_DT_F16 ? dispatch_s<__half>(g, mats, n_mats, s, pdl)
                                       : dispatch_s<float>(g, mats, n_mats, s, pdl);
 }

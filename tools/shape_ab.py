@@ -19,13 +19,14 @@ ap.add_argument("--gs", type=int, default=64)
 ap.add_argument("--n", type=int, default=1)
 ap.add_argument("--fast", type=int, default=0)
 ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--shapes", default="4096x4096,11008x4096,4096x11008")
 args = ap.parse_args()
 dev = torch.device("cuda", 0)
 g = torch.Generator(device=dev).manual_seed(1)
 print("lib", N.LIB_PATH)
-for (m, k) in ((4096, 4096), (11008, 4096), (4096, 11008)):
+for (m, k) in (tuple(int(v) for v in sh.split("x")) for sh in args.shapes.split(",")):
     nbytes = args.bits * m * k // 8
-    copies = max(8, (600 << 20) // nbytes)
+    copies = max(4, (600 << 20) // nbytes)
     q = torch.randint(0, 1 << args.bits, (m, k), dtype=torch.uint8, device=dev, generator=g)
     s = (torch.randn((m, k // args.gs), device=dev, generator=g).abs() * 0.02 + 1e-3).half()
     pw0 = B.prepare_weights(B.QuantizedWeights(m=m, k=k, bits=args.bits, group_size=args.gs,
