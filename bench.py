@@ -810,11 +810,16 @@ def main():
 
 
 def load_traffic():
-    p = os.path.join(ROOT, "profiles", "gemv_traffic.json")
+    """ncu DRAM bytes (read + write) per lookup launch of the headline step:
+    the four grouped launches of one layer (profiles/r01d_step_gemv_b1_full.json,
+    one `ncu --set full` capture) summed and divided by the layer's 7 GEMVs,
+    the same per-launch unit as roofline.achieved."""
+    p = os.path.join(ROOT, "profiles", "r01d_step_gemv_b1_full.json")
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return d.get("dram_bytes_per_launch")
+        tot = sum(x["dram__bytes_read.sum"] + x["dram__bytes_write.sum"] for x in d["launches"])
+        return round(tot / len(LAYER), 1)
     return None
 
 
