@@ -23,6 +23,8 @@
 
 int bl_gemv_stream_launch(const blk::GemvArgs& g, const blk::StreamMat* mats, int n_mats, int scale_dtype,
                           cudaStream_t s, bool pdl);
+int bl_gemv_pack_launch(const blk::GemvArgs& g, const blk::StreamMat* mats, int n_mats, int scale_dtype,
+                        cudaStream_t s, bool pdl);
 
 namespace {
 
@@ -757,7 +759,9 @@ int bl_gemv_b1_launch(const GemvArgs& g, int scale_dtype, cudaStream_t s, bool p
                : dispatch_b1<float, kExactRows>(g, &m, 1, nullptr, s, pdl);
   }
   if (g.fast) {
-    const int rc = bl_gemv_stream_launch(g, reinterpret_cast<const StreamMat*>(&m), 1, scale_dtype, s, pdl);
+    int rc = bl_gemv_stream_launch(g, reinterpret_cast<const StreamMat*>(&m), 1, scale_dtype, s, pdl);
+    if (rc != BITLUT_ELAYOUT) return rc;
+    rc = bl_gemv_pack_launch(g, reinterpret_cast<const StreamMat*>(&m), 1, scale_dtype, s, pdl);
     if (rc != BITLUT_ELAYOUT) return rc;
     return f16 ? dispatch_b1<__half, kFast>(g, &m, 1, nullptr, s, pdl)
                : dispatch_b1<float, kFast>(g, &m, 1, nullptr, s, pdl);
@@ -859,7 +863,9 @@ int bl_mpgemv_multi_launch(const bitlut_mat* mats, int n_mats, int k, int bits, 
   g.rows_per_cta = 1; g.n_rows = 1;
   const cudaStream_t st = (cudaStream_t)stream;
   if (g.fast) {
-    const int rc = bl_gemv_stream_launch(g, reinterpret_cast<const StreamMat*>(ms), n_mats, scale_dtype, st, pdl);
+    int rc = bl_gemv_stream_launch(g, reinterpret_cast<const StreamMat*>(ms), n_mats, scale_dtype, st, pdl);
+    if (rc != BITLUT_ELAYOUT) return rc;
+    rc = bl_gemv_pack_launch(g, reinterpret_cast<const StreamMat*>(ms), n_mats, scale_dtype, st, pdl);
     if (rc != BITLUT_ELAYOUT) return rc;
   }
   if (g.fast)

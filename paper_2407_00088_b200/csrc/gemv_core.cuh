@@ -65,13 +65,17 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+// try_wait suspend-time hint: a waiting warp sleeps until the phase completes
+// (or this many ns pass) instead of re-issuing the probe -- the spin cost
+// issue slots the lookups of other warps could use
+constexpr uint32_t kSuspendNs = 20000;
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
       "{\n .reg .pred p;\n"
       "BL_WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       " @!p bra BL_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(phase)
+      "r"(phase), "r"(kSuspendNs)
       : "memory");
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -111,6 +115,49 @@ __device__ __forceinline__ void lookup_kg(const uint4 w, uint32_t a0, uint32_t a
     acc[4 * q + 2] = bl::dp2a_lo(kMultNeg, Y1, acc[4 * q + 2]);
     acc[4 * q + 3] = bl::dp2a_hi_u(kMult, A1, acc[4 * q + 3]);
     acc[4 * q + 3] = bl::dp2a_hi(kMultNeg, Y1, acc[4 * q + 3]);
+  }
+}
+
+// Batch-1 fast-path lookup (gemv_stream.cu, gemv_pack.cu): plane-merging
+// accumulators, S_c = sum_p 2^p P_p per channel.
+// One k-group of 32 streams.  A = prmt(a, x), Y = prmt(a, x ^ 8): A - Y = sQ
+// exactly for every nibble (gemv_core.cuh lookup_kg).
+template <int BITS, int NACC>
+__device__ __forceinline__ void lookup_merged(const uint4 w, uint32_t a0, uint32_t a1, int (&acc)[NACC]) {
+  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const uint32_t x = ws[q];
+    const uint32_t xx = x ^ 0x88888888u;
+    if constexpr (BITS == 4) {
+      // nibbles 0..3 = planes 0..3 of channel 2q, nibbles 4..7 of channel 2q+1
+      const uint32_t A0 = bl::prmt(a0, a1, x), Y0 = bl::prmt(a0, a1, xx);
+      const uint32_t A1 = bl::prmt(a0, a1, x >> 16), Y1 = bl::prmt(a0, a1, xx >> 16);
+      acc[2 * q] = bl::dp4a(A0, 0x08040201u, acc[2 * q]);
+      acc[2 * q] = bl::dp4a(Y0, 0xF8FCFEFFu, acc[2 * q]);
+      acc[2 * q + 1] = bl::dp4a(A1, 0x08040201u, acc[2 * q + 1]);
+      acc[2 * q + 1] = bl::dp4a(Y1, 0xF8FCFEFFu, acc[2 * q + 1]);
+    } else if constexpr (BITS == 2) {
+      // byte b of x = channel 4q+b (nibbles: plane 0, plane 1); the selector
+      // [x.b, xx.b] looks up [A_p0, A_p1, Y_p0, Y_p1] in one prmt
+      const uint32_t s01 = bl::prmt(x, xx, 0x5140u), s23 = bl::prmt(x, xx, 0x7362u);
+      acc[4 * q + 0] = bl::dp4a(bl::prmt(a0, a1, s01), 0xFEFF0201u, acc[4 * q + 0]);
+      acc[4 * q + 1] = bl::dp4a(bl::prmt(a0, a1, s01 >> 16), 0xFEFF0201u, acc[4 * q + 1]);
+      acc[4 * q + 2] = bl::dp4a(bl::prmt(a0, a1, s23), 0xFEFF0201u, acc[4 * q + 2]);
+      acc[4 * q + 3] = bl::dp4a(bl::prmt(a0, a1, s23 >> 16), 0xFEFF0201u, acc[4 * q + 3]);
+    } else {
+      // W1: acc[4q+h] = channels (8q+2h, 8q+2h+1) packed P_even + 32768 P_odd
+      const uint32_t A0 = bl::prmt(a0, a1, x), Y0 = bl::prmt(a0, a1, xx);
+      const uint32_t A1 = bl::prmt(a0, a1, x >> 16), Y1 = bl::prmt(a0, a1, xx >> 16);
+      acc[4 * q + 0] = bl::dp2a_lo_u(kMult, A0, acc[4 * q + 0]);
+      acc[4 * q + 0] = bl::dp2a_lo(kMultNeg, Y0, acc[4 * q + 0]);
+      acc[4 * q + 1] = bl::dp2a_hi_u(kMult, A0, acc[4 * q + 1]);
+      acc[4 * q + 1] = bl::dp2a_hi(kMultNeg, Y0, acc[4 * q + 1]);
+      acc[4 * q + 2] = bl::dp2a_lo_u(kMult, A1, acc[4 * q + 2]);
+      acc[4 * q + 2] = bl::dp2a_lo(kMultNeg, Y1, acc[4 * q + 2]);
+      acc[4 * q + 3] = bl::dp2a_hi_u(kMult, A1, acc[4 * q + 3]);
+      acc[4 * q + 3] = bl::dp2a_hi(kMultNeg, Y1, acc[4 * q + 3]);
+    }
   }
 }
 

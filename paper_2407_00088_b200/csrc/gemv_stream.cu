@@ -44,48 +44,6 @@ struct SArgs {
   uint32_t tab_off, ts_off, rs_off, rec_off, cnt_off, wb_off, warp_off, bar_off;
 };
 
-using bl::dp4a;
-
-// One k-group of 32 streams.  A = prmt(a, x), Y = prmt(a, x ^ 8): A - Y = sQ
-// exactly for every nibble (gemv_core.cuh lookup_kg).
-template <int BITS, int NACC>
-__device__ __forceinline__ void lookup_s(const uint4 w, uint32_t a0, uint32_t a1, int (&acc)[NACC]) {
-  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-  for (int q = 0; q < 4; q++) {
-    const uint32_t x = ws[q];
-    const uint32_t xx = x ^ 0x88888888u;
-    if constexpr (BITS == 4) {
-      // nibbles 0..3 = planes 0..3 of channel 2q, nibbles 4..7 of channel 2q+1
-      const uint32_t A0 = bl::prmt(a0, a1, x), Y0 = bl::prmt(a0, a1, xx);
-      const uint32_t A1 = bl::prmt(a0, a1, x >> 16), Y1 = bl::prmt(a0, a1, xx >> 16);
-      acc[2 * q] = dp4a(A0, 0x08040201u, acc[2 * q]);
-      acc[2 * q] = dp4a(Y0, 0xF8FCFEFFu, acc[2 * q]);
-      acc[2 * q + 1] = dp4a(A1, 0x08040201u, acc[2 * q + 1]);
-      acc[2 * q + 1] = dp4a(Y1, 0xF8FCFEFFu, acc[2 * q + 1]);
-    } else if constexpr (BITS == 2) {
-      // byte b of x = channel 4q+b (nibbles: plane 0, plane 1); the selector
-      // [x.b, xx.b] looks up [A_p0, A_p1, Y_p0, Y_p1] in one prmt
-      const uint32_t s01 = bl::prmt(x, xx, 0x5140u), s23 = bl::prmt(x, xx, 0x7362u);
-      acc[4 * q + 0] = dp4a(bl::prmt(a0, a1, s01), 0xFEFF0201u, acc[4 * q + 0]);
-      acc[4 * q + 1] = dp4a(bl::prmt(a0, a1, s01 >> 16), 0xFEFF0201u, acc[4 * q + 1]);
-      acc[4 * q + 2] = dp4a(bl::prmt(a0, a1, s23), 0xFEFF0201u, acc[4 * q + 2]);
-      acc[4 * q + 3] = dp4a(bl::prmt(a0, a1, s23 >> 16), 0xFEFF0201u, acc[4 * q + 3]);
-    } else {
-      // W1: acc[4q+h] = channels (8q+2h, 8q+2h+1) packed P_even + 32768 P_odd
-      const uint32_t A0 = bl::prmt(a0, a1, x), Y0 = bl::prmt(a0, a1, xx);
-      const uint32_t A1 = bl::prmt(a0, a1, x >> 16), Y1 = bl::prmt(a0, a1, xx >> 16);
-      acc[4 * q + 0] = bl::dp2a_lo_u(kMult, A0, acc[4 * q + 0]);
-      acc[4 * q + 0] = bl::dp2a_lo(kMultNeg, Y0, acc[4 * q + 0]);
-      acc[4 * q + 1] = bl::dp2a_hi_u(kMult, A0, acc[4 * q + 1]);
-      acc[4 * q + 1] = bl::dp2a_hi(kMultNeg, Y0, acc[4 * q + 1]);
-      acc[4 * q + 2] = bl::dp2a_lo_u(kMult, A1, acc[4 * q + 2]);
-      acc[4 * q + 2] = bl::dp2a_lo(kMultNeg, Y1, acc[4 * q + 2]);
-      acc[4 * q + 3] = bl::dp2a_hi_u(kMult, A1, acc[4 * q + 3]);
-      acc[4 * q + 3] = bl::dp2a_hi(kMultNeg, Y1, acc[4 * q + 3]);
-    }
-  }
-}
 
 // Fixed-order transpose-reduce of NV floats over the 32 lanes: halving
 // exchanges while more than one value is left, butterfly adds afterwards.
@@ -183,8 +141,8 @@ __device__ __forceinline__ void unit_lookups(const uint8_t* wb, const uint8_t* t
     const uint4 t = *reinterpret_cast<const uint4*>(tb + (j >> 1) * stride);
     const uint4 wa = *reinterpret_cast<const uint4*>(wb + j * stride);
     const uint4 wc = *reinterpret_cast<const uint4*>(wb + (j + 1) * stride);
-    lookup_s<BITS, NACC>(wa, t.x, t.y, acc);
-    lookup_s<BITS, NACC>(wc, t.z, t.w, acc);
+    lookup_merged<BITS, NACC>(wa, t.x, t.y, acc);
+    lookup_merged<BITS, NACC>(wc, t.z, t.w, acc);
   }
 }
 
