@@ -210,6 +210,30 @@ int bitlut_mpgemv_multi(const bitlut_mat* mats, int n_mats, int k, int bits, int
                         int scale_dtype, const void* tables, const float* tscales, const float* rowsums,
                         int flags, void* stream);
 
+/* Tensor-parallel batch-1 lookup with the all-gather fused into the epilogue
+ * (SURVEY §8(e) B200-native upgrade; replaces kernel.py:374-382 mpgemv on
+ * this rank's output-channel shard + parallel.py's NCCL all-gather).  Same
+ * arguments as bitlut_mpgemm at n = 1 with BITLUT_FLAG_FAST_EPILOGUE (the
+ * local (1, m) result also goes to `out`), plus:
+ *   peer_out[q]   (HOST array of n_peers device pointers, q = 0..n_peers-1):
+ *                 the gathered (1, m_total) f32 row of rank q, peer-accessible
+ *                 (symmetric memory / IPC over NVLink); this call writes
+ *                 columns [col_offset, col_offset + m) of every one;
+ *   peer_flags[q] (HOST array of device pointers): rank q's u32 gather flag;
+ *                 the last CTA adds 1 to each with release semantics at
+ *                 system scope after every store of the launch;
+ *   ticket        a zero-initialised u32 of this rank (reset by the kernel).
+ * Rank r's row is complete once its flag reaches epoch * world
+ * (bitlut_gather_wait).  1 <= n_peers <= 8. */
+int bitlut_mpgemv_gather(const uint8_t* wgpu, int m, int k, int bits, int group_size,
+                         const void* wscales, const void* zeros, int scale_dtype, const void* tables,
+                         const float* tscales, const float* rowsums, float* out, int n_peers,
+                         float* const* peer_out, unsigned* const* peer_flags, unsigned* ticket,
+                         int col_offset, int flags, void* stream);
+/* Stream-ordered wait (one thread, ld.acquire.sys) until *flag - target >= 0
+ * as signed 32-bit (wrap-around safe). */
+int bitlut_gather_wait(const unsigned* flag, unsigned target, void* stream);
+
 /* bitlut_mpgemm plus a timeline: `trace` (device, (n * tiles) x 8 u64) gets
  * per-CTA %globaltimer stamps [start, loads issued, after griddepcontrol.wait,
  * tables staged, lookups done, epilogue products done, end] and %smid in

@@ -16,7 +16,7 @@ from typing import Optional
 
 import torch
 
-from .errors import BitLutError, raise_for_status
+from .errors import BitLutError, ParameterError, raise_for_status
 
 LIB_PATH = os.environ.get("BITLUT_B200_LIB") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "_lib", "libbitlut_b200.so")   # env: A/B builds
@@ -51,6 +51,9 @@ _SIGS = {
     "bitlut_mpgemm_launches": [_i, _i, _i, _i, _i, _i],
     "bitlut_mpgemv_fused": [_vp, _i, _vp, _i, _i, _i, _i, _vp, _vp, _i, _vp, _i, _vp],
     "bitlut_mpgemv_multi": [_vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _i, _vp],
+    "bitlut_mpgemv_gather": [_vp, _i, _i, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _i,
+                             _vp],
+    "bitlut_gather_wait": [_vp, ctypes.c_uint32, _vp],
 }
 
 
@@ -194,6 +197,35 @@ def mpgemv_multi(mats, tables: torch.Tensor, tscales: torch.Tensor, rowsums: tor
                                    ptr(tscales), ptr(rowsums), flags, stream_of(tables))
     raise_for_status(rc, "bitlut_mpgemv_multi")
     return outs
+
+
+def mpgemv_gather(wgpu: torch.Tensor, wscales: torch.Tensor, zeros: Optional[torch.Tensor],
+                  tables: torch.Tensor, tscales: torch.Tensor, rowsums: torch.Tensor, m: int, k: int, bits: int,
+                  group_size: int, peer_out_ptrs: list, peer_flag_ptrs: list,
+                  ticket: torch.Tensor, col_offset: int, flags: int) -> torch.Tensor:
+    """bitlut_mpgemv_gather: this rank's batch-1 shard lookup with the
+    all-gather fused into the epilogue.  peer_out_ptrs / peer_flag_ptrs are
+    the device addresses (ints) of every rank's gathered row / flag; returns
+    the local (1, m) f32 result."""
+    require_cuda(wgpu, "packed weights")
+    out = torch.empty((1, m), dtype=torch.float32, device=wgpu.device)
+    n = len(peer_out_ptrs)
+    if n != len(peer_flag_ptrs):
+        raise ParameterError("peer_out_ptrs and peer_flag_ptrs differ in length")
+    outs = (ctypes.c_void_p * n)(*peer_out_ptrs)
+    fls = (ctypes.c_void_p * n)(*peer_flag_ptrs)
+    rc = lib().bitlut_mpgemv_gather(ptr(wgpu), m, k, bits, group_size, ptr(wscales), ptr(zeros),
+                                    dtype_code(wscales), ptr(tables), ptr(tscales), ptr(rowsums), ptr(out), n,
+                                    outs, fls, ptr(ticket), col_offset, flags, stream_of(wgpu))
+    raise_for_status(rc, "bitlut_mpgemv_gather")
+    return out
+
+
+def gather_wait(flag: torch.Tensor, target: int) -> None:
+    """bitlut_gather_wait on the flag's stream."""
+    require_cuda(flag, "gather flag")
+    raise_for_status(lib().bitlut_gather_wait(ptr(flag), target & 0xFFFFFFFF, stream_of(flag)),
+                     "bitlut_gather_wait")
 
 
 @torch.library.custom_op("bitlut_b200::mpgemv_fused", mutates_args=())

@@ -60,6 +60,7 @@ struct B1Args {
   uint32_t stage_bytes;       // per pipeline stage: weights | scales | zeros
   uint32_t w_bytes, s_off, s_bytes, z_off;
   uint32_t tab_off, ts_off, rs_off, y_off, bar_off;
+  GatherArgs gth;             // fused all-gather epilogue (fast kernel), n_peers == 0 otherwise
 };
 
 struct B1Plan {
@@ -484,21 +485,33 @@ __global__ void __launch_bounds__(384) gemv_b1_kernel(const __grid_constant__ B1
         const int ub = u >> 5, l = u & 31;
         const int nu_b = min(32, U - 32 * ub);
         const int stride = nu_b == 32 ? 512 : nu_b * 16;
-        uint4 tq[R / 2];
+        const uint8_t* wsrc = sb + ub * (32 * R * 16) + l * 16;
         if (FUSED || a.tab_smem) {
           const uint8_t* tb = tab + ub * (32 * R * 8) + l * 16;
 #pragma unroll
-          for (int jp = 0; jp < R / 2; jp++) tq[jp] = *reinterpret_cast<const uint4*>(tb + jp * stride);
+          for (int j = 0; j < R; j += 2) {
+            const uint4 t = *reinterpret_cast<const uint4*>(tb + (j >> 1) * stride);
+            const uint4 wa = *reinterpret_cast<const uint4*>(wsrc + j * stride);
+            const uint4 wc = *reinterpret_cast<const uint4*>(wsrc + (j + 1) * stride);
+            lookup_kg_merged<BITS, NACC>(wa, t.x, t.y, acc);
+            lookup_kg_merged<BITS, NACC>(wc, t.z, t.w, acc);
+          }
+        } else if (nu_b == 32) {                        // register tables, full unit block
+#pragma unroll
+          for (int j = 0; j < R; j += 2) {
+            const uint4 wa = *reinterpret_cast<const uint4*>(wsrc + j * 512);
+            const uint4 wc = *reinterpret_cast<const uint4*>(wsrc + (j + 1) * 512);
+            lookup_kg_merged<BITS, NACC>(wa, tq0[j >> 1].x, tq0[j >> 1].y, acc);
+            lookup_kg_merged<BITS, NACC>(wc, tq0[j >> 1].z, tq0[j >> 1].w, acc);
+          }
         } else {
 #pragma unroll
-          for (int jp = 0; jp < R / 2; jp++) tq[jp] = tq0[jp];
-        }
-        const uint8_t* wsrc = sb + ub * (32 * R * 16) + l * 16;
-#pragma unroll
-        for (int j = 0; j < R; j++) {
-          const uint4 wr = *reinterpret_cast<const uint4*>(wsrc + j * stride);
-          lookup_kg_merged<BITS, NACC>(wr, (j & 1) ? tq[j >> 1].z : tq[j >> 1].x,
-                                       (j & 1) ? tq[j >> 1].w : tq[j >> 1].y, acc);
+          for (int j = 0; j < R; j += 2) {
+            const uint4 wa = *reinterpret_cast<const uint4*>(wsrc + j * stride);
+            const uint4 wc = *reinterpret_cast<const uint4*>(wsrc + (j + 1) * stride);
+            lookup_kg_merged<BITS, NACC>(wa, tq0[j >> 1].x, tq0[j >> 1].y, acc);
+            lookup_kg_merged<BITS, NACC>(wc, tq0[j >> 1].z, tq0[j >> 1].w, acc);
+          }
         }
       }
       // sum the LG lanes of each quantization group (exact int32)
@@ -570,8 +583,29 @@ __global__ void __launch_bounds__(384) gemv_b1_kernel(const __grid_constant__ B1
       int local;
       const int j = find_mat(a, tile, local);
       a.mats[j].out[(int64_t)row * L.m + (int64_t)local * TCH + tid] = 0.5f * s;
+      if constexpr (KIND == kFast) {
+        // fused all-gather: the same value into every rank's gathered row
+        for (int q = 0; q < a.gth.n_peers; q++)
+          a.gth.peer_out[q][a.gth.col_offset + local * TCH + tid] = 0.5f * s;
+      }
     }
   }
+  }
+  if constexpr (KIND == kFast) {
+    if (a.gth.n_peers > 0) {
+      __syncthreads();                                  // the CTA's peer stores are issued
+      if (tid == 0) {
+        __threadfence_system();
+        unsigned old;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.gth.ticket) : "memory");
+        if (old == gridDim.x - 1) {                     // last CTA: every store of the grid is ordered before
+          *a.gth.ticket = 0;
+          __threadfence_system();
+          for (int q = 0; q < a.gth.n_peers; q++)
+            asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(a.gth.peer_flag[q]) : "memory");
+        }
+      }
+    }
   }
   bl::dep_signal(p.dep);
   if (p.independent) bl::pdl_wait();                    // keep stream completion order
@@ -615,6 +649,11 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
   B1Args a;
   a.g = g;
   a.act = act;
+  a.gth = GatherArgs{};
+  if (g.gather) {
+    if (KIND != kFast) return BITLUT_EPARAM;
+    a.gth = *g.gather;
+  }
   a.n_mats = n_mats;
   for (int j = 0; j < n_mats; j++) a.mats[j] = mats[j];
   a.total_tiles = mats[n_mats - 1].tile_end;
@@ -759,9 +798,10 @@ int bl_gemv_b1_launch(const GemvArgs& g, int scale_dtype, cudaStream_t s, bool p
                : dispatch_b1<float, kExactRows>(g, &m, 1, nullptr, s, pdl);
   }
   if (g.fast) {
-    int rc = bl_gemv_stream_launch(g, reinterpret_cast<const StreamMat*>(&m), 1, scale_dtype, s, pdl);
+    int rc = BITLUT_ELAYOUT;
+    if (!g.gather) rc = bl_gemv_stream_launch(g, reinterpret_cast<const StreamMat*>(&m), 1, scale_dtype, s, pdl);
     if (rc != BITLUT_ELAYOUT) return rc;
-    rc = bl_gemv_pack_launch(g, reinterpret_cast<const StreamMat*>(&m), 1, scale_dtype, s, pdl);
+    if (!g.gather) rc = bl_gemv_pack_launch(g, reinterpret_cast<const StreamMat*>(&m), 1, scale_dtype, s, pdl);
     if (rc != BITLUT_ELAYOUT) return rc;
     return f16 ? dispatch_b1<__half, kFast>(g, &m, 1, nullptr, s, pdl)
                : dispatch_b1<float, kFast>(g, &m, 1, nullptr, s, pdl);
@@ -873,4 +913,64 @@ int bl_mpgemv_multi_launch(const bitlut_mat* mats, int n_mats, int k, int bits, 
                                         : dispatch_b1<float, kFast>(g, ms, n_mats, nullptr, st, pdl);
   return scale_dtype == BITLUT_DT_F16 ? dispatch_b1<__half, kExact>(g, ms, n_mats, nullptr, st, pdl)
                                       : dispatch_b1<float, kExact>(g, ms, n_mats, nullptr, st, pdl);
+}
+
+// Batch-1 fast lookup of this rank's output-channel shard with the all-gather
+// fused into the epilogue: see include/bitlut_b200.h.
+extern "C" int bitlut_mpgemv_gather(const uint8_t* wgpu, int m, int k, int bits, int group_size,
+                                    const void* wscales, const void* zeros, int scale_dtype, const void* tables,
+                                    const float* tscales, const float* rowsums, float* out, int n_peers,
+                                    float* const* peer_out, unsigned* const* peer_flags, unsigned* ticket,
+                                    int col_offset, int flags, void* stream) {
+  bl::LayoutV2 L;
+  int rc = bl::make_layout(m, k, bits, group_size, &L);
+  if (rc) return rc;
+  if (!wgpu || !wscales || !tables || !tscales || !rowsums || !out || !ticket) return BITLUT_EPARAM;
+  if (n_peers < 1 || n_peers > kMaxPeers || !peer_out || !peer_flags || col_offset < 0) return BITLUT_EPARAM;
+  if (scale_dtype != BITLUT_DT_F32 && scale_dtype != BITLUT_DT_F16) return BITLUT_EPARAM;
+  if (!(flags & BITLUT_FLAG_FAST_EPILOGUE)) return BITLUT_EPARAM;
+  if (L.n_sg != 1) return BITLUT_ELAYOUT;
+  GatherArgs ga = {};
+  ga.n_peers = n_peers;
+  ga.col_offset = col_offset;
+  for (int q = 0; q < n_peers; q++) {
+    if (!peer_out[q] || !peer_flags[q]) return BITLUT_EPARAM;
+    ga.peer_out[q] = peer_out[q];
+    ga.peer_flag[q] = peer_flags[q];
+  }
+  ga.ticket = ticket;
+  const bool pdl = (flags & BITLUT_FLAG_PDL) != 0;
+  GemvArgs g = {};
+  g.w = wgpu; g.wscales = wscales; g.zeros = zeros;
+  g.qtab = reinterpret_cast<const uint8_t*>(tables); g.tscales = tscales; g.rowsums = rowsums;
+  g.out = out; g.L = L;
+  g.independent = pdl && (flags & BITLUT_FLAG_INDEPENDENT) != 0;
+  g.fast = 1;
+  g.rows_per_cta = 1; g.n_rows = 1;
+  g.gather = &ga;
+  const B1Mat mt = single_mat(g);
+  const cudaStream_t st = (cudaStream_t)stream;
+  return scale_dtype == BITLUT_DT_F16 ? dispatch_b1<__half, kFast>(g, &mt, 1, nullptr, st, pdl)
+                                      : dispatch_b1<float, kFast>(g, &mt, 1, nullptr, st, pdl);
+}
+
+namespace {
+__global__ void gather_wait_kernel(const unsigned* flag, unsigned target) {
+  if (threadIdx.x == 0) {
+    unsigned v;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+      if ((int)(v - target) >= 0) break;
+      __nanosleep(100);
+    }
+  }
+}
+}  // namespace
+
+// Stream-ordered wait until this rank's gather flag reaches `target`
+// (wrap-around safe): kernels after it on `stream` see the gathered row.
+extern "C" int bitlut_gather_wait(const unsigned* flag, unsigned target, void* stream) {
+  if (!flag) return BITLUT_EPARAM;
+  gather_wait_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(flag, target);
+  return bl_launch_status();
 }

@@ -23,6 +23,23 @@ struct StreamMat {
   int tile_end;               // cumulative tile count up to and including this matrix
 };
 
+// Fused all-gather epilogue (SURVEY §8(e) "B200-native upgrade"): every
+// output element is also stored into the gathered output buffer of each of
+// n_peers ranks (peer-accessible memory, e.g. torch symmetric memory over
+// NVLink), at column col_offset + channel; after the last CTA of the grid
+// has finished its stores it adds 1 to every peer's flag with release
+// semantics at system scope.  A rank's gathered buffer is complete when its
+// flag reaches (epoch) x world.  `ticket` is a zero-initialised device
+// counter of the caller, reset by the last CTA.
+constexpr int kMaxPeers = 8;
+struct GatherArgs {
+  int n_peers;
+  int col_offset;
+  float* peer_out[kMaxPeers];
+  unsigned* peer_flag[kMaxPeers];
+  unsigned* ticket;
+};
+
 struct GemvArgs {
   const uint8_t* w;
   const void* wscales;
@@ -41,6 +58,7 @@ struct GemvArgs {
   bl::DepSync dep;           // op-list counters (n_wait == 0 and done == null otherwise)
   int* grid_out;             // host: receives the launch's CTA count (op-list executor), or null
   int force_stream;          // BITLUT_FLAG_STREAM: batch-1 fast lookups through gemv_stream.cu
+  const GatherArgs* gather;  // host side: fused all-gather epilogue (batch-1 fast kernel), or null
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {

@@ -117,3 +117,94 @@ def sharded_mpgemm(a, sw: ShardedWeights, group=None, variant="cuda-q8",
     if y.dim() == 1:
         y = y.reshape(1, -1)
     return gather_rows(y, sw.sizes, group)
+
+
+# ---------------------------------------------------------------------------
+# Fused all-gather ("B200-native upgrade"): the lookup kernel's
+# epilogue stores every output element straight into each rank's gathered
+# row over peer memory and signals each rank's flag once per launch
+# (bitlut_mpgemv_gather), so the step has no separate collective launch.
+# A rank's row is complete when its flag reaches epoch * world
+# (bitlut_gather_wait, stream-ordered).
+# ---------------------------------------------------------------------------
+
+def gather_plan(m_total: int, world: int) -> list[tuple[int, int]]:
+    """(col_offset, m_r) of every rank in the gathered row (shard_bounds)."""
+    return [(lo, hi - lo) for lo, hi in (shard_bounds(m_total, r, world) for r in range(world))]
+
+
+class FusedGather:
+    """Peer buffers of the fused all-gather for one rank: the gathered f32
+    row `row` (1, m_total) and u32 `flag` of this rank, the device addresses
+    of every rank's row / flag, a launch ticket and the epoch counter.
+
+    `symmetric(m_total, group)`: production path, one process per GPU;
+    buffers from torch symmetric memory (NVLink peer mappings via the
+    rendezvous handle).  `emulated(m_total, world, device)`: all ranks' buffers
+    on one GPU in one process (the kernel path is identical; used by the
+    single-GPU tests and the CPU-side logic)."""
+
+    def __init__(self, rank: int, world: int, m_total: int, row: torch.Tensor, flag: torch.Tensor,
+                 out_ptrs: list, flag_ptrs: list, keep=None):
+        self.rank, self.world, self.m_total = rank, world, m_total
+        self.row, self.flag = row, flag
+        self.out_ptrs, self.flag_ptrs = out_ptrs, flag_ptrs
+        self.ticket = torch.zeros(1, dtype=torch.int32, device=row.device)
+        self.epoch = 0
+        self._keep = keep                      # keeps peer allocations / handles alive
+
+    @classmethod
+    def emulated(cls, m_total: int, world: int, device) -> list["FusedGather"]:
+        rows = [torch.zeros((1, m_total), dtype=torch.float32, device=device) for _ in range(world)]
+        flags = [torch.zeros(1, dtype=torch.int32, device=device) for _ in range(world)]
+        out_ptrs = [r.data_ptr() for r in rows]
+        flag_ptrs = [f.data_ptr() for f in flags]
+        return [cls(r, world, m_total, rows[r], flags[r], out_ptrs, flag_ptrs, keep=(rows, flags))
+                for r in range(world)]
+
+    @classmethod
+    def symmetric(cls, m_total: int, group=None) -> "FusedGather":
+        import torch.distributed._symmetric_memory as symm_mem
+        group = group or dist.group.WORLD
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        device = torch.device("cuda", torch.cuda.current_device())
+        row = symm_mem.empty((1, m_total), dtype=torch.float32, device=device)
+        flag = symm_mem.empty(1, dtype=torch.int32, device=device)
+        row.zero_()
+        flag.zero_()
+        h_row = symm_mem.rendezvous(row, group.group_name)
+        h_flag = symm_mem.rendezvous(flag, group.group_name)
+        out_ptrs = [int(p) for p in h_row.buffer_ptrs]
+        flag_ptrs = [int(p) for p in h_flag.buffer_ptrs]
+        dist.barrier(group)
+        return cls(rank, world, m_total, row, flag, out_ptrs, flag_ptrs, keep=(h_row, h_flag))
+
+    def launch(self, a_row: torch.Tensor, pw, exact_epilogue: bool = False) -> torch.Tensor:
+        """This rank's shard lookup (batch 1, fast epilogue) writing into
+        every rank's row; returns the local (1, m_r) result.  Does not wait."""
+        from . import _native as N
+        if exact_epilogue:
+            raise ParameterError("the fused all-gather runs the fast epilogue only")
+        col, m_r = gather_plan(self.m_total, self.world)[self.rank]
+        if pw.m != m_r:
+            raise LayoutError(f"shard has {pw.m} channels, rank {self.rank} owns {m_r}")
+        x = a_row.reshape(1, -1)
+        t = N.build_lut(x, pw.group_size, N.TABLE_Q8)
+        y = N.mpgemv_gather(pw.gpu, pw.scales, pw.zeros, *t, pw.m, pw.k, pw.bits, pw.group_size,
+                            self.out_ptrs, self.flag_ptrs, self.ticket, col,
+                            N.FLAG_PDL | N.FLAG_FAST_EPILOGUE)
+        self.epoch += 1
+        return y
+
+    def wait(self) -> torch.Tensor:
+        """Stream-ordered wait for every rank's slice of the current epoch."""
+        from . import _native as N
+        N.gather_wait(self.flag, self.epoch * self.world)
+        return self.row
+
+
+def sharded_mpgemv_fused(a_row, sw: "ShardedWeights", fg: FusedGather) -> torch.Tensor:
+    """Tensor-parallel batch-1 mpGEMV with the all-gather fused into the
+    lookup epilogue: returns this rank's gathered (1, m_total) row."""
+    fg.launch(a_row, sw.local)
+    return fg.wait()

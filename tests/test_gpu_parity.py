@@ -701,3 +701,35 @@ def test_long_k_batch1_fast(bits, gs):
     _, P = N.lookup(pw.gpu, pw.scales, None, *t, m, k, bits, gs, N.TABLE_Q8, N.FLAG_PDL, True)   # exact kernel
     want = sum((1 << p) * P[0, p].long() for p in range(bits))
     assert torch.equal(S1[0, 0].long(), want)
+
+
+@pytest.mark.parametrize("world,bits,gs", [(2, 2, 64), (4, 2, 64), (8, 4, 128), (3, 1, 128)])
+def test_fused_allgather_epilogue_emulated(world, bits, gs):
+    """bitlut_mpgemv_gather with `world` ranks emulated on one GPU (every
+    rank's gathered row and flag local; launches in rank order, so no rank
+    waits on another): after each epoch every rank's row equals the
+    single-GPU fast result bitwise, and the flags count world per epoch."""
+    from paper_2407_00088_b200 import parallel as PP
+    m, k = 1024, 4096
+    g = torch.Generator(device="cuda").manual_seed(world * 10 + bits)
+    q = torch.randint(0, 1 << bits, (m, k), dtype=torch.uint8, device="cuda", generator=g)
+    sc = (torch.randn((m, k // gs), device="cuda", generator=g).abs() * 0.02 + 1e-3).half()
+    qw = B.QuantizedWeights(m=m, k=k, bits=bits, group_size=gs, qvalues=q, scales=sc)
+    full = B.prepare_weights(qw)
+    shards = [B.prepare_weights(PP.shard_quantized_weights(qw, r, world)) for r in range(world)]
+    fgs = PP.FusedGather.emulated(m, world, torch.device("cuda"))
+    for epoch in range(1, 3):
+        x = torch.randn((1, k), device="cuda", generator=g).half()
+        from paper_2407_00088_b200 import _native as N
+        t = N.build_lut(x, gs, N.TABLE_Q8)
+        want, _ = N.lookup(full.gpu, full.scales, None, *t, m, k, bits, gs, N.TABLE_Q8,
+                           N.FLAG_PDL | N.FLAG_FAST_EPILOGUE, False)
+        locs = [fg.launch(x[0], pw) for fg, pw in zip(fgs, shards)]
+        rows = [fg.wait() for fg in fgs]
+        torch.cuda.synchronize()
+        for r in range(world):
+            assert torch.equal(rows[r], want), (r, epoch)
+            col, mr = PP.gather_plan(m, world)[r]
+            assert torch.equal(locs[r], want[:, col:col + mr])
+            assert int(fgs[r].flag.item()) == epoch * world
+            assert int(fgs[r].ticket.item()) == 0

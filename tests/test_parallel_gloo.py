@@ -81,3 +81,17 @@ def test_sharded_mpgemm_world2_bitwise():
     for rank, res in out:
         assert res.pop("error") is None, res
         assert res and all(res.values()), (rank, res)
+
+
+def test_gather_plan_matches_shard_bounds():
+    """Fused all-gather host logic: each rank's column window in the gathered
+    row is its shard_bounds range; windows tile [0, m) in rank order."""
+    from paper_2407_00088_b200 import parallel as PP
+    for m, world in ((4096, 1), (4096, 2), (11008, 4), (28672, 8), (1024, 3), (352, 8)):
+        plan = PP.gather_plan(m, world)
+        assert len(plan) == world
+        pos = 0
+        for r, (col, mr) in enumerate(plan):
+            assert col == pos and (col, col + mr) == PP.shard_bounds(m, r, world)
+            pos += mr
+        assert pos == m
