@@ -61,6 +61,7 @@ struct B1Args {
   uint32_t w_bytes, s_off, s_bytes, z_off;
   uint32_t tab_off, ts_off, rs_off, y_off, bar_off;
   GatherArgs gth;             // fused all-gather epilogue (fast kernel), n_peers == 0 otherwise
+  int ldg_w;                  // fast kernel: weights loaded straight into registers (stage = scales only)
 };
 
 struct B1Plan {
@@ -78,10 +79,11 @@ __host__ __device__ constexpr bool kind_rows(int k) { return k == kFastRows || k
 __host__ __device__ inline uint32_t al16(size_t x) { return (uint32_t)((x + 15) & ~(size_t)15); }
 
 template <typename ST>
-B1Plan b1_plan(const bl::LayoutV2& L, bool zeros, bool tab_smem, int T, int stages, int kind = kFast) {
+B1Plan b1_plan(const bl::LayoutV2& L, bool zeros, bool tab_smem, int T, int stages, int kind = kFast,
+               bool ldg_w = false) {
   const bool fused = kind == kFused, exact = kind_exact(kind);
   B1Plan s;
-  s.w_bytes = (uint32_t)((size_t)L.KG * 16);
+  s.w_bytes = ldg_w ? 0u : (uint32_t)((size_t)L.KG * 16);
   s.s_bytes = (uint32_t)((size_t)L.tile_ch * L.NQ * sizeof(ST));
   s.s_off = al16(s.w_bytes);
   s.z_off = s.s_off + al16(s.s_bytes);
@@ -486,7 +488,31 @@ __global__ void __launch_bounds__(384) gemv_b1_kernel(const __grid_constant__ B1
         const int nu_b = min(32, U - 32 * ub);
         const int stride = nu_b == 32 ? 512 : nu_b * 16;
         const uint8_t* wsrc = sb + ub * (32 * R * 16) + l * 16;
-        if (FUSED || a.tab_smem) {
+        if (KIND == kFast && a.ldg_w) {
+          // weights straight from HBM into registers (the warp reads 512
+          // contiguous bytes per k-step), no shared-memory stage
+          int local;
+          const B1Mat& mt = a.mats[find_mat(a, tile, local)];
+          const uint8_t* gsrc = mt.w + L.sg_row_base(local, 0) + ub * (32 * R * 16) + l * 16;
+          uint4 wv[R];
+#pragma unroll
+          for (int j = 0; j < R; j++) wv[j] = bl::ld_nc_128(gsrc + j * stride);
+          if (a.tab_smem) {
+            const uint8_t* tb = tab + ub * (32 * R * 8) + l * 16;
+#pragma unroll
+            for (int j = 0; j < R; j += 2) {
+              const uint4 t = *reinterpret_cast<const uint4*>(tb + (j >> 1) * stride);
+              lookup_kg_merged<BITS, NACC>(wv[j], t.x, t.y, acc);
+              lookup_kg_merged<BITS, NACC>(wv[j + 1], t.z, t.w, acc);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < R; j += 2) {
+              lookup_kg_merged<BITS, NACC>(wv[j], tq0[j >> 1].x, tq0[j >> 1].y, acc);
+              lookup_kg_merged<BITS, NACC>(wv[j + 1], tq0[j >> 1].z, tq0[j >> 1].w, acc);
+            }
+          }
+        } else if (FUSED || a.tab_smem) {
           const uint8_t* tb = tab + ub * (32 * R * 8) + l * 16;
 #pragma unroll
           for (int j = 0; j < R; j += 2) {
@@ -681,13 +707,21 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
     const char* e = getenv("BITLUT_B1_TILES_PER_CTA");   // diagnostic override
     tpc_env = e ? atoi(e) : 0;
   }
+  static int ldg_env = -1;
+  if (ldg_env < 0) {
+    // diagnostic: weights via registers, no smem stage -- measured slower
+    // (4096^2 W4 overlapped 2.01 vs 1.75 us, W2 on par), off by default
+    const char* e = getenv("BITLUT_B1_LDG");
+    ldg_env = e ? atoi(e) : 0;
+  }
+  a.ldg_w = (KIND == kFast && ldg_env > 0) ? 1 : 0;
   // one stage when every CTA gets a single tile, else double-buffer
   const bool zeros = mats[0].zeros != nullptr;
-  B1Plan s = b1_plan<ST>(L, zeros, a.tab_smem, T, 1, KIND);
+  B1Plan s = b1_plan<ST>(L, zeros, a.tab_smem, T, 1, KIND, a.ldg_w != 0);
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, s.total) != cudaSuccess || per_sm < 1)
     return BITLUT_ELAYOUT;
-  const B1Plan s2 = b1_plan<ST>(L, zeros, a.tab_smem, T, 2, KIND);
+  const B1Plan s2 = b1_plan<ST>(L, zeros, a.tab_smem, T, 2, KIND, a.ldg_w != 0);
   int per_sm2 = 0;
   if (s2.total > 227 * 1024 ||
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, kern, T, s2.total) != cudaSuccess)
