@@ -637,6 +637,137 @@ __global__ void __launch_bounds__(384) gemv_b1_kernel(const __grid_constant__ B1
   if (p.independent) bl::pdl_wait();                    // keep stream completion order
 }
 
+
+// Lean specialisation of the fast batch-1 kernel for its common case: one
+// round of units per tile (thread u = unit u), tables in registers, no zero
+// points, no partials export, no fused gather, weights staged by TMA.  Same
+// arithmetic, same shared-memory plan and launch plan as gemv_b1_kernel
+// (launch_b1 picks it), so outputs are bitwise identical; what it drops is
+// the per-tile cost of the general kernel's mode branches, round / row loops
+// and per-tile reloads: the thread's group, table scale, row sum and smem
+// addresses are fixed for the launch.
+template <int R, int LG, int BITS, typename ST>
+__global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant__ B1Args a) {
+  const GemvArgs& p = a.g;
+  const bl::LayoutV2& L = p.L;
+  constexpr int TCH = 32 / BITS;
+  constexpr int NACC = BITS == 4 ? 8 : 16;
+  constexpr int NV = reduced_count<NACC, 1, LG>();
+  constexpr int NCH = BITS == 1 ? 2 * NV : NV;
+  constexpr int NF = reduced_count<NCH, LG, 32>();
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NW = blockDim.x >> 5;
+  const int NQ = L.NQ, KG = L.KG, U = L.U;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + a.bar_off);
+  float* ysm = reinterpret_cast<float*>(smem + a.y_off);
+  const int ntl = a.total_tiles, step = gridDim.x;
+  const int S = a.stages;
+
+  if (tid == 0) {
+    for (int s = 0; s <= kMaxStages; s++) mbar_init(bar + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint64_t pol = policy_evict_first();
+    for (int s = 0; s < S; s++) {
+      const int t = blockIdx.x + s * step;
+      if (t < ntl) issue_stage<ST>(a, t, smem + s * a.stage_bytes, bar + s, pol);
+    }
+  }
+  if (p.dep.counted) bl::dep_wait(p.dep);
+  else if (!p.independent) bl::pdl_wait();
+  bl::pdl_launch_dependents();
+  // the thread's unit, group and tables: fixed for the launch
+  const int u = tid;
+  const bool live = u < U;
+  const int ub = u >> 5, l = u & 31;
+  const int nu_b = min(32, U - 32 * ub);
+  const int g = u / LG;
+  uint4 tq[R / 2];
+  float ts = 0.f, rs = 0.f;
+  if (live) {
+    const uint8_t* tb = p.qtab + (int64_t)ub * (32 * R * 8) + l * 16;
+#pragma unroll
+    for (int jp = 0; jp < R / 2; jp++) tq[jp] = bl::ld_cg_128(tb + jp * nu_b * 16);
+    ts = bl::ld_cg_f32(p.tscales + g);
+    rs = bl::ld_cg_f32(p.rowsums + g);
+  }
+  const uint32_t woff = (uint32_t)(ub * (32 * R * 16) + l * 16);
+  __syncthreads();                                      // barriers initialised
+  int it = 0;
+  for (int tile = blockIdx.x; tile < ntl; tile += step, it++) {
+    const int stage = S == 1 ? 0 : (it & 1);
+    uint8_t* sb = smem + stage * a.stage_bytes;
+    mbar_wait(bar + stage, (S == 1 ? it : it >> 1) & 1);
+    int acc[NACC];
+#pragma unroll
+    for (int i = 0; i < NACC; i++) acc[i] = 0;
+    if (live) {
+      const uint8_t* wsrc = sb + woff;
+      if (nu_b == 32) {
+#pragma unroll
+        for (int j = 0; j < R; j += 2) {
+          const uint4 wa = *reinterpret_cast<const uint4*>(wsrc + j * 512);
+          const uint4 wc = *reinterpret_cast<const uint4*>(wsrc + (j + 1) * 512);
+          lookup_kg_merged<BITS, NACC>(wa, tq[j >> 1].x, tq[j >> 1].y, acc);
+          lookup_kg_merged<BITS, NACC>(wc, tq[j >> 1].z, tq[j >> 1].w, acc);
+        }
+      } else {
+        const int stride = nu_b * 16;
+#pragma unroll
+        for (int j = 0; j < R; j += 2) {
+          const uint4 wa = *reinterpret_cast<const uint4*>(wsrc + j * stride);
+          const uint4 wc = *reinterpret_cast<const uint4*>(wsrc + (j + 1) * stride);
+          lookup_kg_merged<BITS, NACC>(wa, tq[j >> 1].x, tq[j >> 1].y, acc);
+          lookup_kg_merged<BITS, NACC>(wc, tq[j >> 1].z, tq[j >> 1].w, acc);
+        }
+      }
+    }
+    const int base = reduce_lanes<NACC, 1, LG>(acc, lane);
+    const int ch0 = BITS == 1 ? 2 * base : base;
+    float y[NCH];
+    if (live) {
+      int Sv[NCH];
+      if constexpr (BITS == 1) {
+#pragma unroll
+        for (int i = 0; i < NV; i++) {
+          const int v = acc[i];
+          const int pe = (v << 17) >> 17;
+          Sv[2 * i] = pe;
+          Sv[2 * i + 1] = (v - pe) >> 15;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < NV; i++) Sv[i] = acc[i];
+      }
+      const ST* sp = reinterpret_cast<const ST*>(sb + a.s_off) + ch0 * NQ + g;
+#pragma unroll
+      for (int j = 0; j < NCH; j++) y[j] = bl::to_f32(sp[j * NQ]) * fmaf(ts, (float)Sv[j], -rs);
+    } else {
+#pragma unroll
+      for (int j = 0; j < NCH; j++) y[j] = 0.f;
+    }
+    const int fb = reduce_lanes<NCH, LG, 32>(y, lane);
+    float* yb = ysm + (it & 1) * NW * TCH + warp * TCH;
+#pragma unroll
+    for (int j = 0; j < NF; j++) yb[ch0 + fb + j] = y[j];
+    __syncthreads();                                    // stage consumed, ysm complete
+    if (tid == 0) {
+      const int t = tile + S * step;
+      if (t < ntl) issue_stage<ST>(a, t, sb, bar + stage, policy_evict_first());
+    }
+    if (tid < TCH) {
+      const float* yr = ysm + (it & 1) * NW * TCH + tid;
+      float s = 0.f;
+      for (int w = 0; w < NW; w++) s += yr[w * TCH];
+      int local;
+      const int j = find_mat(a, tile, local);
+      a.mats[j].out[(int64_t)local * TCH + tid] = 0.5f * s;
+    }
+  }
+  bl::dep_signal(p.dep);
+  if (p.independent) bl::pdl_wait();
+}
+
 int sm_count() {
   static int n = 0;
   if (!n) {
@@ -656,7 +787,15 @@ constexpr int kClusterCTAs = 8;
 // threads).  An overlapped (INDEPENDENT) launch wants more resident CTAs:
 // at most 256 threads.  Never fewer than 128.
 int b1_threads(const bl::LayoutV2& L, bool overlapped) {
-  const int cap = overlapped ? 256 : 384;
+  static int cap_env = -1;
+  if (cap_env < 0) {
+    const char* e = getenv("BITLUT_B1_CAP");             // diagnostic: overlapped-launch CTA cap
+    cap_env = e ? atoi(e) : 0;
+  }
+  // one round of units per tile whenever U <= 384: the lean kernel needs it,
+  // and at K = 11008 one round of 352 threads beats two of 176 (4096x11008
+  // overlapped W2 3.38 -> 3.09 us, W4 5.36 -> 4.86 us)
+  const int cap = overlapped ? (cap_env > 0 ? cap_env : 384) : 384;
   const int rounds = (L.U + cap - 1) / cap;
   int t = (L.U + rounds - 1) / rounds;
   t = (t + 31) & ~31;
@@ -690,9 +829,31 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
   if (kind_rows(KIND) && (a.rounds > 1 || n_mats > 1)) return BITLUT_ELAYOUT;
   a.n_rows = n_rows;
   a.rows_per_cta = n_rows;
-  auto kern = gemv_b1_kernel<R, LG, BITS, ST, KIND>;
-  static bool configured = false;
-  if (!configured) {
+  static int ldg_env = -1;
+  if (ldg_env < 0) {
+    // diagnostic: weights via registers, no smem stage -- measured slower
+    // (4096^2 W4 overlapped 2.01 vs 1.75 us, W2 on par), off by default
+    const char* e = getenv("BITLUT_B1_LDG");
+    ldg_env = e ? atoi(e) : 0;
+  }
+  a.ldg_w = (KIND == kFast && ldg_env > 0) ? 1 : 0;
+  static int lean_env = -1;
+  if (lean_env < 0) {
+    const char* e = getenv("BITLUT_B1_LEAN");            // diagnostic: 0 = always the general kernel
+    lean_env = e ? atoi(e) : 1;
+  }
+  const bool lean = KIND == kFast && lean_env != 0 && a.rounds == 1 && !a.tab_smem && !g.partials &&
+                    mats[0].zeros == nullptr && !g.gather && !g.trace && !a.ldg_w;
+  auto kern = lean ? gemv_b1_lean_kernel<R, LG, BITS, ST> : gemv_b1_kernel<R, LG, BITS, ST, KIND>;
+  static bool configured = false, configured_lean = false;
+  if (lean && !configured_lean) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared) != cudaSuccess)
+      return BITLUT_EINTERNAL;
+    configured_lean = true;
+  }
+  if (!lean && !configured) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared) != cudaSuccess)
@@ -707,14 +868,7 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
     const char* e = getenv("BITLUT_B1_TILES_PER_CTA");   // diagnostic override
     tpc_env = e ? atoi(e) : 0;
   }
-  static int ldg_env = -1;
-  if (ldg_env < 0) {
-    // diagnostic: weights via registers, no smem stage -- measured slower
-    // (4096^2 W4 overlapped 2.01 vs 1.75 us, W2 on par), off by default
-    const char* e = getenv("BITLUT_B1_LDG");
-    ldg_env = e ? atoi(e) : 0;
-  }
-  a.ldg_w = (KIND == kFast && ldg_env > 0) ? 1 : 0;
+
   // one stage when every CTA gets a single tile, else double-buffer
   const bool zeros = mats[0].zeros != nullptr;
   B1Plan s = b1_plan<ST>(L, zeros, a.tab_smem, T, 1, KIND, a.ldg_w != 0);
