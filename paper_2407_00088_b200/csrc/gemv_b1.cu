@@ -882,8 +882,20 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
     per_sm2 = 0;
   // two tiles per CTA only where the double-buffered plan still leaves
   // several CTAs per SM (short K); long-K tiles want every CTA they can get
+  static int tpc_ovl = -1, tpc_dep = -1;
+  if (tpc_ovl < 0) {
+    const char* e1 = getenv("BITLUT_B1_TPC_OVL");         // diagnostic: tiles per CTA, overlapped launches
+    const char* e2 = getenv("BITLUT_B1_TPC_DEP");         // ... dependent launches
+    tpc_ovl = e1 ? atoi(e1) : 0;
+    tpc_dep = e2 ? atoi(e2) : 0;
+  }
+  const bool ovl = g.independent || g.dep.counted;
   int tiles_per_cta = tpc_env > 0 ? tpc_env
-                                  : ((!kind_exact(KIND) && (g.independent || g.dep.counted) && per_sm2 >= 3) ? 2 : 1);
+                                  : ((!kind_exact(KIND) && ovl && per_sm2 >= 3) ? 2 : 1);
+  if (tpc_env <= 0 && !kind_exact(KIND)) {
+    if (ovl && tpc_ovl > 0 && per_sm2 >= 1) tiles_per_cta = tpc_ovl;
+    if (!ovl && tpc_dep > 0 && per_sm2 >= 1) tiles_per_cta = tpc_dep;
+  }
   if (tpc_env <= 0 && (a.total_tiles + tiles_per_cta - 1) / tiles_per_cta < sm_count() / 2) tiles_per_cta = 1;
   const int want = (a.total_tiles + tiles_per_cta - 1) / tiles_per_cta;
   // double-buffer when CTAs get several tiles -- by choice (tiles_per_cta)
