@@ -768,6 +768,122 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
   if (p.independent) bl::pdl_wait();
 }
 
+
+// Lean mpGEMM rows kernel (kFastRows common case: one unit round, register
+// tables, no zeros / partials): the tile is staged once and stays in shared
+// memory while the CTA walks its rows; per row the thread's tables, table
+// scale and row sum are prefetched one row ahead (registers, from L2), and
+// one barrier per row publishes the cross-warp partial sums (double-buffered).
+// Bitwise equal to gemv_b1_kernel<kFastRows>.
+template <int R, int LG, int BITS, typename ST>
+__global__ void __launch_bounds__(384) gemv_b1_rows_lean_kernel(const __grid_constant__ B1Args a) {
+  const GemvArgs& p = a.g;
+  const bl::LayoutV2& L = p.L;
+  constexpr int TCH = 32 / BITS;
+  constexpr int NACC = BITS == 4 ? 8 : 16;
+  constexpr int NV = reduced_count<NACC, 1, LG>();
+  constexpr int NCH = BITS == 1 ? 2 * NV : NV;
+  constexpr int NF = reduced_count<NCH, LG, 32>();
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NW = blockDim.x >> 5;
+  const int NQ = L.NQ, KG = L.KG, U = L.U;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + a.bar_off);
+  float* ysm = reinterpret_cast<float*>(smem + a.y_off);
+  const int tile = blockIdx.x;
+  const int row0 = blockIdx.y * a.rows_per_cta;
+  const int row1 = min(row0 + a.rows_per_cta, a.n_rows);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    issue_stage<ST>(a, tile, smem, bar, policy_evict_first());
+  }
+  if (p.dep.counted) bl::dep_wait(p.dep);
+  else if (!p.independent) bl::pdl_wait();
+  bl::pdl_launch_dependents();
+  const int u = tid;
+  const bool live = u < U;
+  const int ub = u >> 5, l = u & 31;
+  const int nu_b = min(32, U - 32 * ub);
+  const int g = u / LG;
+  const uint8_t* tb0 = p.qtab + (int64_t)ub * (32 * R * 8) + l * 16;
+  uint4 tq[R / 2], tn[R / 2];
+  float ts = 0.f, rs = 0.f, tsn = 0.f, rsn = 0.f;
+  auto fetch = [&](int row, uint4 (&t)[R / 2], float& s1, float& s2) {
+    if (live && row < row1) {
+      const uint8_t* tb = tb0 + (int64_t)row * KG * 8;
+#pragma unroll
+      for (int jp = 0; jp < R / 2; jp++) t[jp] = bl::ld_cg_128(tb + jp * nu_b * 16);
+      s1 = bl::ld_cg_f32(p.tscales + (int64_t)row * NQ + g);
+      s2 = bl::ld_cg_f32(p.rowsums + (int64_t)row * NQ + g);
+    }
+  };
+  fetch(row0, tq, ts, rs);
+  __syncthreads();                                      // barrier initialised
+  mbar_wait(bar, 0);
+  const uint8_t* wsrc = smem + (uint32_t)(ub * (32 * R * 16) + l * 16);
+  int local;
+  const int mj = find_mat(a, tile, local);
+  float* outp = a.mats[mj].out + (int64_t)local * TCH;
+  const int stride = nu_b * 16;
+  for (int row = row0, it = 0; row < row1; row++, it++) {
+    fetch(row + 1, tn, tsn, rsn);                       // next row's tables stream in meanwhile
+    int acc[NACC];
+#pragma unroll
+    for (int i = 0; i < NACC; i++) acc[i] = 0;
+    if (live) {
+#pragma unroll
+      for (int j = 0; j < R; j += 2) {
+        const uint4 wa = *reinterpret_cast<const uint4*>(wsrc + j * stride);
+        const uint4 wc = *reinterpret_cast<const uint4*>(wsrc + (j + 1) * stride);
+        lookup_kg_merged<BITS, NACC>(wa, tq[j >> 1].x, tq[j >> 1].y, acc);
+        lookup_kg_merged<BITS, NACC>(wc, tq[j >> 1].z, tq[j >> 1].w, acc);
+      }
+    }
+    const int base = reduce_lanes<NACC, 1, LG>(acc, lane);
+    const int ch0 = BITS == 1 ? 2 * base : base;
+    float y[NCH];
+    if (live) {
+      int Sv[NCH];
+      if constexpr (BITS == 1) {
+#pragma unroll
+        for (int i = 0; i < NV; i++) {
+          const int v = acc[i];
+          const int pe = (v << 17) >> 17;
+          Sv[2 * i] = pe;
+          Sv[2 * i + 1] = (v - pe) >> 15;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < NV; i++) Sv[i] = acc[i];
+      }
+      const ST* sp = reinterpret_cast<const ST*>(smem + a.s_off) + ch0 * NQ + g;
+#pragma unroll
+      for (int j = 0; j < NCH; j++) y[j] = bl::to_f32(sp[j * NQ]) * fmaf(ts, (float)Sv[j], -rs);
+    } else {
+#pragma unroll
+      for (int j = 0; j < NCH; j++) y[j] = 0.f;
+    }
+    const int fb = reduce_lanes<NCH, LG, 32>(y, lane);
+    float* yb = ysm + (it & 1) * NW * TCH + warp * TCH;
+#pragma unroll
+    for (int j = 0; j < NF; j++) yb[ch0 + fb + j] = y[j];
+    __syncthreads();                                    // this row's partials complete
+    if (tid < TCH) {
+      const float* yr = ysm + (it & 1) * NW * TCH + tid;
+      float sum = 0.f;
+      for (int w = 0; w < NW; w++) sum += yr[w * TCH];
+      outp[(int64_t)row * L.m + tid] = 0.5f * sum;
+    }
+#pragma unroll
+    for (int jp = 0; jp < R / 2; jp++) tq[jp] = tn[jp];
+    ts = tsn;
+    rs = rsn;
+  }
+  bl::dep_signal(p.dep);
+  if (p.independent) bl::pdl_wait();
+}
+
 int sm_count() {
   static int n = 0;
   if (!n) {
@@ -842,10 +958,20 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
     const char* e = getenv("BITLUT_B1_LEAN");            // diagnostic: 0 = always the general kernel
     lean_env = e ? atoi(e) : 1;
   }
-  const bool lean = KIND == kFast && lean_env != 0 && a.rounds == 1 && !a.tab_smem && !g.partials &&
-                    mats[0].zeros == nullptr && !g.gather && !g.trace && !a.ldg_w;
-  auto kern = lean ? gemv_b1_lean_kernel<R, LG, BITS, ST> : gemv_b1_kernel<R, LG, BITS, ST, KIND>;
-  static bool configured = false, configured_lean = false;
+  const bool lean_common = lean_env != 0 && a.rounds == 1 && !a.tab_smem && !g.partials &&
+                           mats[0].zeros == nullptr && !g.gather && !g.trace && !a.ldg_w;
+  const bool lean = KIND == kFast && lean_common;
+  const bool lean_rows = KIND == kFastRows && lean_common && n_mats == 1;
+  auto kern = lean ? gemv_b1_lean_kernel<R, LG, BITS, ST>
+                   : (lean_rows ? gemv_b1_rows_lean_kernel<R, LG, BITS, ST> : gemv_b1_kernel<R, LG, BITS, ST, KIND>);
+  static bool configured = false, configured_lean = false, configured_rows = false;
+  if (lean_rows && !configured_rows) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared) != cudaSuccess)
+      return BITLUT_EINTERNAL;
+    configured_rows = true;
+  }
   if (lean && !configured_lean) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -853,7 +979,7 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
       return BITLUT_EINTERNAL;
     configured_lean = true;
   }
-  if (!lean && !configured) {
+  if (!lean && !lean_rows && !configured) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared) != cudaSuccess)
