@@ -659,7 +659,7 @@ def main():
         how = (f"1 persistent launch per step ({args.layers * 11} ops), algorithmic bytes = "
                f"sum bits*M*K/8 = {total_bytes} per launch, CUDA events over {args.steps} launches")
     else:
-        kernel_name = "gemv_b1_kernel" if best_fast else "gemv_kernel"
+        kernel_name = "gemv_b1_lean_kernel" if best_fast else "gemv_kernel"
         achieved = local_bytes / (ms_look * 1e-3) / 1e9
         how = (f"{n_look} lookup launches/graph replay (the step's lookups with tables prebuilt, "
                f"same flags, {'fast' if best_fast else 'exact'} epilogue), algorithmic bytes = "
@@ -814,7 +814,7 @@ def load_traffic():
     the four grouped launches of one layer (profiles/r01d_step_gemv_b1_full.json,
     one `ncu --set full` capture) summed and divided by the layer's 7 GEMVs,
     the same per-launch unit as roofline.achieved."""
-    p = os.path.join(ROOT, "profiles", "r01d_step_gemv_b1_full.json")
+    p = os.path.join(ROOT, "profiles", "r01e_step_gemv_b1_full.json")
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
