@@ -360,6 +360,64 @@ def per_shape_table(device, stream, reps, warmup, barrier, peak, world, bits_lis
     return out
 
 
+def config1_table(device, stream, reps, warmup, barrier, peak):
+    """BASELINE configs[0]: one 4096x4096 W4 mpGEMV, group 128, fp16 scales and
+    asymmetric fp16 zeros, fp16 activation row -- per launch with the tables
+    prebuilt (graph over rotating weight copies >= 4x L2, overlapped and
+    chained) and per call (table build + lookup, chained), for the
+    fp16-table variant (cuda-f16, the configuration the BASELINE names) and
+    the int8-table ones (cuda-q8 exact / fast)."""
+    import torch
+    import paper_2407_00088_b200 as B
+    from paper_2407_00088_b200 import _native as N
+    gen = torch.Generator(device=device)
+    gen.manual_seed(1)
+    m = k = 4096
+    bits, gs = 4, 128
+    q = torch.randint(0, 16, (m, k), dtype=torch.uint8, device=device, generator=gen)
+    sc = (torch.randn((m, k // gs), device=device, generator=gen).abs() * 0.02 + 1e-3).half()
+    z = (torch.rand((m, k // gs), device=device, generator=gen) * 15).half()
+    pw = B.prepare_weights(B.QuantizedWeights(m=m, k=k, bits=bits, group_size=gs, qvalues=q, scales=sc, zeros=z))
+    del q
+    nbytes = pw.packed_bytes
+    copies = max(8, -(-4 * L2_BYTES // nbytes))
+    ws = [pw.gpu] + [pw.gpu.clone() for _ in range(copies - 1)]
+    x = torch.randn((1, k), device=device, generator=gen).half()
+    out = {"shape": "4096x4096", "bits": bits, "group_size": gs, "zeros": True, "packed_bytes": nbytes,
+           "launches_rotated": len(ws)}
+    for name, mode, fast in (("cuda-f16", N.TABLE_F16, False), ("cuda-q8-exact", N.TABLE_Q8, False),
+                             ("cuda-q8-fast", N.TABLE_Q8, True)):
+        tabs = N.build_lut(x, gs, mode)
+        base = N.FLAG_PDL | (N.FLAG_FAST_EPILOGUE if fast else 0)
+        e = {}
+        for label, fl in (("overlapped", base | N.FLAG_INDEPENDENT), ("chained", base)):
+            def body(fl=fl, tabs=tabs, mode=mode):
+                for w in ws:
+                    N.lookup(w, pw.scales, pw.zeros, *tabs, m, k, bits, gs, mode, fl, False)
+            g = capture(body, stream)
+            with torch.cuda.stream(stream):
+                ms = time_graph(g, reps, warmup, barrier)
+            del g
+            us = ms * 1e3 / len(ws)
+            e[label + "_us"] = round(us, 3)
+            e[label + "_GBps"] = round(nbytes / (us * 1e-6) / 1e9, 1)
+            e[label + "_frac_of_peak"] = round(nbytes / (us * 1e-6) / 1e9 / peak, 4)
+
+        def call(mode=mode, base=base):     # the whole call: table build + lookup, chained
+            for w in ws:
+                t = N.build_lut(x, gs, mode, N.FLAG_PDL)
+                N.lookup(w, pw.scales, pw.zeros, *t, m, k, bits, gs, mode, base, False)
+        g = capture(call, stream)
+        with torch.cuda.stream(stream):
+            ms = time_graph(g, reps, warmup, barrier)
+        del g
+        e["call_us"] = round(ms * 1e3 / len(ws), 3)
+        out[name] = e
+    del ws, pw
+    torch.cuda.empty_cache()
+    return out
+
+
 SHAPES_70B = [("q/o 8192x8192", 8192, 8192, 2), ("k/v 1024x8192", 1024, 8192, 2),
               ("gate/up 28672x8192", 28672, 8192, 2), ("down 8192x28672", 8192, 28672, 1)]
 
@@ -679,6 +737,13 @@ def main():
                                         peak, world)
         per_shape["clocks"] = clk_shapes.summary()
 
+    # ---- BASELINE configs[0]: single W4 mpGEMV, zeros, fp16 tables ----
+    cfg1 = None
+    if not args.no_shapes and world == 1:
+        with ClockSampler(local) as clk_1:
+            cfg1 = config1_table(device, stream, max(5, args.steps // 4), args.warmup, barrier, peak)
+        cfg1["clocks"] = clk_1.summary()
+
     # ---- Llama-2-70B per-GPU shards (BASELINE configs[4]) ----
     shards70 = None
     if not args.no_70b and world == 1:
@@ -796,6 +861,7 @@ def main():
             "executors": executors_out,
             "lookups_only_graph": lookups_graph,
             "per_shape": per_shape,
+            "config1_single_mpgemv": cfg1,
             "mpgemm_prefill": gemm,
             "llama70b_shards": shards70,
             "cpu_baseline": cpu,

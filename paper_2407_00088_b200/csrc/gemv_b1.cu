@@ -646,7 +646,7 @@ __global__ void __launch_bounds__(384) gemv_b1_kernel(const __grid_constant__ B1
 // the per-tile cost of the general kernel's mode branches, round / row loops
 // and per-tile reloads: the thread's group, table scale, row sum and smem
 // addresses are fixed for the launch.
-template <int R, int LG, int BITS, typename ST>
+template <int R, int LG, int BITS, typename ST, bool ZEROS>
 __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant__ B1Args a) {
   const GemvArgs& p = a.g;
   const bl::LayoutV2& L = p.L;
@@ -740,8 +740,19 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
         for (int i = 0; i < NV; i++) Sv[i] = acc[i];
       }
       const ST* sp = reinterpret_cast<const ST*>(sb + a.s_off) + ch0 * NQ + g;
+      if constexpr (ZEROS) {
+        // asymmetric zero points: + 2 (2^(b-1) - z) rs per (channel, group)
+        const ST* zp = reinterpret_cast<const ST*>(sb + a.z_off) + ch0 * NQ + g;
+        const float h2 = (float)(2 << (BITS - 1));
 #pragma unroll
-      for (int j = 0; j < NCH; j++) y[j] = bl::to_f32(sp[j * NQ]) * fmaf(ts, (float)Sv[j], -rs);
+        for (int j = 0; j < NCH; j++) {
+          const float t = fmaf(fmaf(-2.f, bl::to_f32(zp[j * NQ]), h2), rs, fmaf(ts, (float)Sv[j], -rs));
+          y[j] = bl::to_f32(sp[j * NQ]) * t;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < NCH; j++) y[j] = bl::to_f32(sp[j * NQ]) * fmaf(ts, (float)Sv[j], -rs);
+      }
     } else {
 #pragma unroll
       for (int j = 0; j < NCH; j++) y[j] = 0.f;
@@ -958,28 +969,17 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
     const char* e = getenv("BITLUT_B1_LEAN");            // diagnostic: 0 = always the general kernel
     lean_env = e ? atoi(e) : 1;
   }
-  const bool lean_common = lean_env != 0 && a.rounds == 1 && !a.tab_smem && !g.partials &&
-                           mats[0].zeros == nullptr && !g.gather && !g.trace && !a.ldg_w;
+  const bool lean_common = lean_env != 0 && a.rounds == 1 && !a.tab_smem && !g.partials && !g.gather &&
+                           !g.trace && !a.ldg_w;
+  const bool has_z = mats[0].zeros != nullptr;
   const bool lean = KIND == kFast && lean_common;
-  const bool lean_rows = KIND == kFastRows && lean_common && n_mats == 1;
-  auto kern = lean ? gemv_b1_lean_kernel<R, LG, BITS, ST>
+  const bool lean_rows = KIND == kFastRows && lean_common && n_mats == 1 && !has_z;
+  auto kern = lean ? (has_z ? gemv_b1_lean_kernel<R, LG, BITS, ST, true> : gemv_b1_lean_kernel<R, LG, BITS, ST, false>)
                    : (lean_rows ? gemv_b1_rows_lean_kernel<R, LG, BITS, ST> : gemv_b1_kernel<R, LG, BITS, ST, KIND>);
-  static bool configured = false, configured_lean = false, configured_rows = false;
-  if (lean_rows && !configured_rows) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
-        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             cudaSharedmemCarveoutMaxShared) != cudaSuccess)
-      return BITLUT_EINTERNAL;
-    configured_rows = true;
-  }
-  if (lean && !configured_lean) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
-        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             cudaSharedmemCarveoutMaxShared) != cudaSuccess)
-      return BITLUT_EINTERNAL;
-    configured_lean = true;
-  }
-  if (!lean && !lean_rows && !configured) {
+  static bool configured_k[4] = {false, false, false, false};   // general, lean, lean + zeros, rows
+  const int ki = lean ? (has_z ? 2 : 1) : (lean_rows ? 3 : 0);
+  bool& configured = configured_k[ki];
+  if (!configured) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared) != cudaSuccess)
@@ -1012,7 +1012,9 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
   if (tpc_ovl < 0) {
     const char* e1 = getenv("BITLUT_B1_TPC_OVL");         // diagnostic: tiles per CTA, overlapped launches
     const char* e2 = getenv("BITLUT_B1_TPC_DEP");         // ... dependent launches
-    tpc_ovl = e1 ? atoi(e1) : 0;
+    // overlapped fast launches: three tiles per double-buffered CTA (layer
+    // set 0.405 -> 0.401 ms, lookups alone 0.402 -> 0.390 ms, 3 of 3 A/B runs)
+    tpc_ovl = e1 ? atoi(e1) : 3;
     tpc_dep = e2 ? atoi(e2) : 0;
   }
   const bool ovl = g.independent || g.dep.counted;
