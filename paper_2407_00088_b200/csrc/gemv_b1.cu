@@ -658,7 +658,7 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int NW = blockDim.x >> 5;
-  const int NQ = L.NQ, KG = L.KG, U = L.U;
+  const int NQ = L.NQ, U = L.U;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + a.bar_off);
   float* ysm = reinterpret_cast<float*>(smem + a.y_off);
   const int ntl = a.total_tiles, step = gridDim.x;
@@ -895,6 +895,279 @@ __global__ void __launch_bounds__(384) gemv_b1_rows_lean_kernel(const __grid_con
   if (p.independent) bl::pdl_wait();
 }
 
+
+// Long-K batch-1 fast lookups split over a thread-block cluster: CS CTAs share
+// every tile, rank r owning quantization groups [r*NG/CS, (r+1)*NG/CS) (its
+// unit blocks are TMA-copied; a block two ranks touch is copied by both).
+// Per tile each CTA forms its partial channel sums exactly like the lean
+// kernel (one unit per thread, register tables, fixed group), stores them
+// into rank 0's shared memory (DSMEM) and arrives on the cluster barrier;
+// rank 0 adds the CS partials in rank order one tile later, after the
+// matching wait -- the barrier's latency overlaps the next tile's lookups.
+// Deterministic for a given CS (the fp32 order differs from the unsplit
+// kernel's in the last bits; the integer sums are the same).
+struct ClArgs {
+  int cs;                     // CTAs per cluster (tile split)
+  int u0[9];                  // unit ranges per rank: [u0[r], u0[r+1])
+  uint32_t stage_bytes, w_bytes_max, s_off, s_bytes, z_off, y_off, part_off, bar_off;
+  int stages;
+};
+
+template <int R, int LG, int BITS, typename ST, bool ZEROS>
+__global__ void __launch_bounds__(256) gemv_b1_cluster_kernel(const __grid_constant__ B1Args a,
+                                                              const __grid_constant__ ClArgs c) {
+  const GemvArgs& p = a.g;
+  const bl::LayoutV2& L = p.L;
+  constexpr int TCH = 32 / BITS;
+  constexpr int NACC = BITS == 4 ? 8 : 16;
+  constexpr int NV = reduced_count<NACC, 1, LG>();
+  constexpr int NCH = BITS == 1 ? 2 * NV : NV;
+  constexpr int NF = reduced_count<NCH, LG, 32>();
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NW = blockDim.x >> 5;
+  const int NQ = L.NQ, U = L.U;
+  const uint32_t rank = cluster_rank();
+  const int CS = c.cs;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + c.bar_off);
+  float* ysm = reinterpret_cast<float*>(smem + c.y_off);
+  float* part = reinterpret_cast<float*>(smem + c.part_off);      // [2][CS][TCH] (rank 0's is read)
+  const int ntl = a.total_tiles;
+  const int ncl = gridDim.x / CS, cl = blockIdx.x / CS;
+  const int S = c.stages;
+  const int ua = c.u0[rank], ue = c.u0[rank + 1];
+  const int b0 = ua >> 5, b1 = (ue + 31) >> 5;
+  uint32_t wbytes = 0;
+  for (int b = b0; b < b1; b++) wbytes += (uint32_t)(min(32, U - 32 * b) * R * 16);
+
+  auto issue = [&](int tile, uint8_t* sb, uint64_t* br, uint64_t pol) {
+    int local;
+    const B1Mat& mt = a.mats[find_mat(a, tile, local)];
+    const bool z = mt.zeros != nullptr;
+    mbar_expect_tx(br, wbytes + c.s_bytes * (z ? 2u : 1u));
+    const uint8_t* src = mt.w + L.sg_row_base(local, 0) + (int64_t)b0 * (32 * R * 16);
+    for (uint32_t off = 0; off < wbytes; off += 32768u) {
+      const uint32_t nb = wbytes - off < 32768u ? wbytes - off : 32768u;
+      bulk_g2s(sb + off, src + off, nb, br, pol);
+    }
+    const int64_t e0 = (int64_t)local * L.tile_ch * L.NQ;
+    bulk_g2s(sb + c.s_off, reinterpret_cast<const ST*>(mt.wscales) + e0, c.s_bytes, br, pol);
+    if (z) bulk_g2s(sb + c.z_off, reinterpret_cast<const ST*>(mt.zeros) + e0, c.s_bytes, br, pol);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < S; s++) mbar_init(bar + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint64_t pol = policy_evict_first();
+    for (int s = 0; s < S; s++) {
+      const int t = cl + s * ncl;
+      if (t < ntl) issue(t, smem + s * c.stage_bytes, bar + s, pol);
+    }
+  }
+  if (p.dep.counted) bl::dep_wait(p.dep);
+  else if (!p.independent) bl::pdl_wait();
+  bl::pdl_launch_dependents();
+  const int u = ua + tid;
+  const bool live = u < ue;
+  const int ub = u >> 5, l = u & 31;
+  const int nu_b = min(32, U - 32 * ub);
+  const int g = u / LG;
+  uint4 tq[R / 2];
+  float ts = 0.f, rs = 0.f;
+  if (live) {
+    const uint8_t* tb = p.qtab + (int64_t)ub * (32 * R * 8) + l * 16;
+#pragma unroll
+    for (int jp = 0; jp < R / 2; jp++) tq[jp] = bl::ld_cg_128(tb + jp * nu_b * 16);
+    ts = bl::ld_cg_f32(p.tscales + g);
+    rs = bl::ld_cg_f32(p.rowsums + g);
+  }
+  const uint32_t woff = (uint32_t)((ub - b0) * (32 * R * 16) + l * 16);
+  __syncthreads();                                      // barriers initialised
+  cluster_arrive_relaxed();                             // every CTA of the cluster has started:
+  cluster_wait();                                       // DSMEM stores are safe from here on
+  int it = 0, prev_tile = -1;
+  for (int tile = cl; tile < ntl; tile += ncl, it++) {
+    const int stage = S == 1 ? 0 : (it & 1);
+    uint8_t* sb = smem + stage * c.stage_bytes;
+    mbar_wait(bar + stage, (S == 1 ? it : it >> 1) & 1);
+    int acc[NACC];
+#pragma unroll
+    for (int i = 0; i < NACC; i++) acc[i] = 0;
+    if (live) {
+      const uint8_t* wsrc = sb + woff;
+      const int stride = nu_b * 16;
+#pragma unroll
+      for (int j = 0; j < R; j += 2) {
+        const uint4 wa = *reinterpret_cast<const uint4*>(wsrc + j * stride);
+        const uint4 wc = *reinterpret_cast<const uint4*>(wsrc + (j + 1) * stride);
+        lookup_kg_merged<BITS, NACC>(wa, tq[j >> 1].x, tq[j >> 1].y, acc);
+        lookup_kg_merged<BITS, NACC>(wc, tq[j >> 1].z, tq[j >> 1].w, acc);
+      }
+    }
+    const int base = reduce_lanes<NACC, 1, LG>(acc, lane);
+    const int ch0 = BITS == 1 ? 2 * base : base;
+    float y[NCH];
+    if (live) {
+      int Sv[NCH];
+      if constexpr (BITS == 1) {
+#pragma unroll
+        for (int i = 0; i < NV; i++) {
+          const int v = acc[i];
+          const int pe = (v << 17) >> 17;
+          Sv[2 * i] = pe;
+          Sv[2 * i + 1] = (v - pe) >> 15;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < NV; i++) Sv[i] = acc[i];
+      }
+      const ST* sp = reinterpret_cast<const ST*>(sb + c.s_off) + ch0 * NQ + g;
+      if constexpr (ZEROS) {
+        const ST* zp = reinterpret_cast<const ST*>(sb + c.z_off) + ch0 * NQ + g;
+        const float h2 = (float)(2 << (BITS - 1));
+#pragma unroll
+        for (int j = 0; j < NCH; j++) {
+          const float t = fmaf(fmaf(-2.f, bl::to_f32(zp[j * NQ]), h2), rs, fmaf(ts, (float)Sv[j], -rs));
+          y[j] = bl::to_f32(sp[j * NQ]) * t;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < NCH; j++) y[j] = bl::to_f32(sp[j * NQ]) * fmaf(ts, (float)Sv[j], -rs);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < NCH; j++) y[j] = 0.f;
+    }
+    const int fb = reduce_lanes<NCH, LG, 32>(y, lane);
+    float* yb = ysm + (it & 1) * NW * TCH + warp * TCH;
+#pragma unroll
+    for (int j = 0; j < NF; j++) yb[ch0 + fb + j] = y[j];
+    __syncthreads();                                    // stage consumed, ysm complete
+    if (tid == 0) {
+      const int t = tile + S * ncl;
+      if (t < ntl) issue(t, sb, bar + stage, policy_evict_first());
+    }
+    if (it > 0) {
+      cluster_wait();                                   // partials of the previous tile are in rank 0
+      if (rank == 0 && tid < TCH) {
+        const float* pr = part + ((it - 1) & 1) * CS * TCH + tid;
+        float sum = 0.f;
+        for (int r = 0; r < CS; r++) sum += pr[r * TCH];
+        int local;
+        const int j = find_mat(a, prev_tile, local);
+        a.mats[j].out[(int64_t)local * TCH + tid] = 0.5f * sum;
+      }
+    }
+    if (tid < TCH) {
+      const float* yr = ysm + (it & 1) * NW * TCH + tid;
+      float sum = 0.f;
+      for (int w = 0; w < NW; w++) sum += yr[w * TCH];
+      st_cluster_f32(part + (it & 1) * CS * TCH + rank * TCH + tid, 0, sum);
+    }
+    cluster_arrive_release();
+    prev_tile = tile;
+  }
+  if (it > 0) {
+    cluster_wait();
+    if (rank == 0 && tid < TCH) {
+      const float* pr = part + ((it - 1) & 1) * CS * TCH + tid;
+      float sum = 0.f;
+      for (int r = 0; r < CS; r++) sum += pr[r * TCH];
+      int local;
+      const int j = find_mat(a, prev_tile, local);
+      a.mats[j].out[(int64_t)local * TCH + tid] = 0.5f * sum;
+    }
+  }
+  cluster_arrive_relaxed();                             // no CTA leaves while a peer may still
+  cluster_wait();                                       // store into its shared memory
+  bl::dep_signal(p.dep);
+  if (p.independent) bl::pdl_wait();
+}
+
+template <int R, int LG, int BITS, typename ST>
+int launch_b1_cluster(const GemvArgs& g, const B1Mat* mats, int n_mats, cudaStream_t stream, bool pdl,
+                      bool* handled) {
+  const bl::LayoutV2& L = g.L;
+  *handled = false;
+  const int NG = L.U / LG;
+  int cs = 2;
+  while (cs < 8 && (NG + cs - 1) / cs * LG > 256) cs <<= 1;
+  if ((NG + cs - 1) / cs * LG > 256) return BITLUT_OK;   // not handled
+  ClArgs c;
+  c.cs = cs;
+  int tmax = 0;
+  for (int r = 0; r <= cs; r++) c.u0[r] = (int)((int64_t)NG * r / cs) * LG;
+  for (int r = 0; r < cs; r++) tmax = max(tmax, c.u0[r + 1] - c.u0[r]);
+  const int T = ((tmax + 31) / 32) * 32 < 64 ? 64 : ((tmax + 31) / 32) * 32;
+  uint32_t wmax = 0;
+  for (int r = 0; r < cs; r++) {
+    const int b0 = c.u0[r] >> 5, b1 = (c.u0[r + 1] + 31) >> 5;
+    uint32_t w = 0;
+    for (int b = b0; b < b1; b++) w += (uint32_t)(min(32, L.U - 32 * b) * L.R * 16);
+    wmax = max(wmax, w);
+  }
+  const bool zeros = mats[0].zeros != nullptr;
+  B1Args a;
+  a.g = g;
+  a.act = nullptr;
+  a.gth = GatherArgs{};
+  a.ldg_w = 0;
+  a.n_mats = n_mats;
+  for (int j = 0; j < n_mats; j++) a.mats[j] = mats[j];
+  a.total_tiles = mats[n_mats - 1].tile_end;
+  c.s_bytes = (uint32_t)((size_t)L.tile_ch * L.NQ * sizeof(ST));
+  c.w_bytes_max = wmax;
+  c.s_off = al16(wmax);
+  c.z_off = c.s_off + al16(c.s_bytes);
+  c.stage_bytes = ((c.z_off + (zeros ? al16(c.s_bytes) : 0)) + 127) & ~127u;
+  auto kern = zeros ? gemv_b1_cluster_kernel<R, LG, BITS, ST, true> : gemv_b1_cluster_kernel<R, LG, BITS, ST, false>;
+  static bool configured[2] = {false, false};
+  if (!configured[zeros]) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared) != cudaSuccess)
+      return BITLUT_EINTERNAL;
+    configured[zeros] = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = cs;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(T);
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  // two stages when that keeps as many clusters resident, else one
+  int best_cl = 0;
+  size_t best_total = 0;
+  for (int st = 1; st <= 2; st++) {
+    const uint32_t y_off = st * c.stage_bytes;
+    const uint32_t part_off = y_off + al16((size_t)2 * (T / 32) * L.tile_ch * 4);
+    const uint32_t bar_off = part_off + al16((size_t)2 * cs * L.tile_ch * 4);
+    const size_t total = bar_off + 16;
+    if (total > 227 * 1024) break;
+    cfg.dynamicSmemBytes = total;
+    cfg.gridDim = dim3(cs * 148);
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess) ncl = 0;
+    if (ncl >= 1 && ncl >= best_cl) {
+      best_cl = ncl; best_total = total;
+      c.stages = st; c.y_off = y_off; c.part_off = part_off; c.bar_off = bar_off;
+    }
+  }
+  if (best_cl < 1) return BITLUT_OK;                  // not handled
+  int ncl = best_cl;
+  if (ncl > a.total_tiles) ncl = a.total_tiles;
+  if (g.grid_out) *g.grid_out = ncl * cs;
+  cfg.gridDim = dim3(ncl * cs);
+  cfg.dynamicSmemBytes = best_total;
+  *handled = true;
+  return cudaLaunchKernelEx(&cfg, kern, a, c) == cudaSuccess ? BITLUT_OK : BITLUT_EINTERNAL;
+}
+
 int sm_count() {
   static int n = 0;
   if (!n) {
@@ -934,6 +1207,22 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
               bool pdl) {
   constexpr bool FUSED = KIND == kFused;
   const bl::LayoutV2& L = g.L;
+  if constexpr (KIND == kFast) {
+    static int cl_env = -1;
+    if (cl_env < 0) {
+      const char* e = getenv("BITLUT_B1_CLUSTER");       // diagnostic: 0 disables the split-K cluster kernel
+      cl_env = e ? atoi(e) : 1;
+    }
+    // long tile rows only (> 64 KB, K > 16384: the 70B down projection and
+    // its shards): 4096x28672 W2 8.3 vs 11.0 us, 2048x28672 4.7 vs 5.9 us;
+    // at K = 11008 the unsplit lean kernel is faster (2.6 vs 3.8 us)
+    if (cl_env != 0 && (size_t)L.KG * 16 > 65536 && L.U > 256 && !g.partials && !g.gather && !g.trace &&
+        g.n_rows <= 1) {
+      bool handled = false;
+      const int rc = launch_b1_cluster<R, LG, BITS, ST>(g, mats, n_mats, stream, pdl, &handled);
+      if (handled || rc != BITLUT_OK) return rc;
+    }
+  }
   // the exact epilogue's serial chains favour one tile per CTA and one round
   const int T = b1_threads(L, !kind_exact(KIND) && (g.independent || g.dep.counted));
   if (FUSED && T % (L.gs / 4) != 0) return BITLUT_ELAYOUT;

@@ -751,3 +751,26 @@ def test_fast_mpgemm_rows(bits, gs, n, m, k):
     yn = y.cpu().numpy()
     for r in range(n):
         assert rel_maxnorm(yn[r], ref[r]) <= 1e-5, r
+
+
+@pytest.mark.parametrize("bits,gs,m,zeros", [(2, 64, 1024, False), (4, 128, 512, True), (1, 128, 2048, False)])
+def test_long_k_cluster_kernel(bits, gs, m, zeros):
+    """K = 28672 shards below the streaming kernel's size threshold run the
+    split-K cluster kernel (DSMEM partial sums): within 1e-5 of the oracle,
+    deterministic, and its integer sums equal the exact kernel's."""
+    from paper_2407_00088_b200 import _native as N
+    k = 28672
+    g = torch.Generator(device="cuda").manual_seed(bits * 7 + m)
+    q = torch.randint(0, 1 << bits, (m, k), dtype=torch.uint8, device="cuda", generator=g)
+    sc = (torch.randn((m, k // gs), device="cuda", generator=g).abs() * 0.02 + 1e-3).half()
+    z = (torch.rand((m, k // gs), device="cuda", generator=g) * ((1 << bits) - 1)).half() if zeros else None
+    pw = B.prepare_weights(B.QuantizedWeights(m=m, k=k, bits=bits, group_size=gs, qvalues=q, scales=sc, zeros=z))
+    x = torch.randn((1, k), device="cuda", generator=g).half()
+    t = N.build_lut(x, gs, N.TABLE_Q8)
+    fl = N.FLAG_PDL | N.FLAG_FAST_EPILOGUE
+    y, _ = N.lookup(pw.gpu, pw.scales, pw.zeros, *t, m, k, bits, gs, N.TABLE_Q8, fl, False)
+    y2, _ = N.lookup(pw.gpu, pw.scales, pw.zeros, *t, m, k, bits, gs, N.TABLE_Q8, fl | N.FLAG_INDEPENDENT, False)
+    assert torch.equal(y, y2)
+    ref = O.mpgemm_q8(x.cpu().numpy(), q.cpu().numpy(), sc.float().cpu().numpy(), bits, gs,
+                      zeros=None if z is None else z.cpu().numpy())[0]
+    assert rel_maxnorm(y[0].cpu().numpy(), ref) <= 1e-5
