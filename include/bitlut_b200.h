@@ -65,10 +65,10 @@ extern "C" {
  * fast kernel scales -- SURVEY §8(c)'s bit-exactness object. */
 #define BITLUT_FLAG_COMBINED_PARTIALS 32
 /* With BITLUT_FLAG_FAST_EPILOGUE at batch 1: use the streaming kernel
- * (per-warp weight rings, whole quantization groups per lane) regardless of
- * the shape.  Without it the library picks that kernel only for long-K
- * shapes (tile rows above 64 KB, K > 16384), where it is the faster one.
- * Same exact integer sums; the fp32 combination order differs. */
+ * (per-warp weight rings, whole quantization groups per lane; an
+ * alternative the library no longer picks by itself -- the split-K cluster
+ * kernel is faster on long K).  Same exact integer sums; the fp32
+ * combination order differs. */
 #define BITLUT_FLAG_STREAM 64
 
 /*

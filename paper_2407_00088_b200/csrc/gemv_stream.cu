@@ -506,22 +506,20 @@ int dispatch_s(const GemvArgs& g, const blk::StreamMat* m, int nm, cudaStream_t 
 
 }  // namespace
 
-// Kernel choice for a batch-1 fast launch: forced by BITLUT_FLAG_STREAM, else
-// long-K launches with plenty of slices only: a tile row above 64 KB cannot
-// be double-buffered by gemv_b1_kernel, and >= 4096 slices keep every warp
-// of the streaming kernel busy (bench.py llama70b_shards, 8192x28672:
-// W4 27.1 vs 39.2 us, W2 19.8 vs 20.9 us at 1 GPU; the 1/2- to 1/8-row
-// shards stay on gemv_b1_kernel, which is faster there).
-// BITLUT_STREAM=0/1 in the environment overrides (diagnostic).
+// Kernel choice for a batch-1 fast launch: only when forced by
+// BITLUT_FLAG_STREAM (or BITLUT_STREAM=1 in the environment).  It used to be
+// the automatic choice for long-K launches; the split-K cluster kernel
+// (gemv_b1.cu) now beats it there too (8192x28672 W2 15.0 vs 19.8 us, W4
+// 24.3 vs 26.7 us overlapped).
 bool bl_gemv_stream_wanted(const bl::LayoutV2& L, int total_tiles, bool force) {
+  (void)L; (void)total_tiles;
   static int env = -2;
   if (env == -2) {
     const char* e = getenv("BITLUT_STREAM");
     env = e ? atoi(e) : -1;
   }
   if (env >= 0) return env != 0;
-  const int nsl = (L.U + 63) / 64;
-  return force || ((size_t)L.KG * 16 > 65536 && (int64_t)total_tiles * nsl >= 4096);
+  return force;
 }
 
 // Batch-1 fast-epilogue lookups through the streaming kernel.  Returns

@@ -680,12 +680,12 @@ def test_stream_kernel_vs_oracle(bits, gs, zeros, m, k, n_mats):
 
 @pytest.mark.parametrize("bits,gs", [(2, 64), (4, 128)])
 def test_long_k_batch1_fast(bits, gs):
-    """K = 28672 (Llama-2-70B down projection): the library routes fast
-    batch-1 calls to the streaming kernel; output within 1e-5 of the oracle
-    and its integer sums equal those formed from the exact kernel's per-plane
-    staging values."""
+    """K = 28672 (Llama-2-70B down projection): fast batch-1 calls (the
+    split-K cluster kernel) within 1e-5 of the oracle; exact path bitwise;
+    the combined integer sums (gemv_b1_kernel) equal those formed from the
+    exact kernel's per-plane staging values."""
     from paper_2407_00088_b200 import _native as N
-    m, k = 4800, 28672                         # >= 4096 slices: the auto path picks it
+    m, k = 4800, 28672
     g = torch.Generator(device="cuda").manual_seed(28672 + bits)
     q = torch.randint(0, 1 << bits, (m, k), dtype=torch.uint8, device="cuda", generator=g)
     sc = (torch.randn((m, k // gs), device="cuda", generator=g).abs() * 0.02 + 1e-3).half()
