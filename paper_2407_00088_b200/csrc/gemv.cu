@@ -266,6 +266,12 @@ int bl_mpgemm_launch(const uint8_t* wgpu, int m, int k, int bits, int group_size
   }
   const bool combined = (flags & BITLUT_FLAG_COMBINED_PARTIALS) != 0;
   if (combined && (!a.fast || mode != BITLUT_TABLE_Q8 || L.n_sg != 1 || trace)) return BITLUT_EPARAM;
+  if (mode == BITLUT_TABLE_F16 && a.fast && n == 1 && !partials && !trace && L.n_sg == 1 && b1_enabled()) {
+    a.f16_tables = 1;                                  // lean batch-1 kernel, fp16-table mode
+    rc = bl_gemv_b1_launch(a, scale_dtype, (cudaStream_t)stream, pdl);
+    a.f16_tables = 0;
+    if (rc != BITLUT_ELAYOUT) return rc;
+  }
   if (mode == BITLUT_TABLE_Q8 && (a.fast ? (!partials || combined) : !partials) && !trace &&
       L.n_sg == 1 && (b1_enabled() || combined)) {
     rc = bl_gemv_b1_launch(a, scale_dtype, (cudaStream_t)stream, pdl);

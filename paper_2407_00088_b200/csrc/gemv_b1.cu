@@ -646,7 +646,12 @@ __global__ void __launch_bounds__(384) gemv_b1_kernel(const __grid_constant__ B1
 // the per-tile cost of the general kernel's mode branches, round / row loops
 // and per-tile reloads: the thread's group, table scale, row sum and smem
 // addresses are fixed for the launch.
-template <int R, int LG, int BITS, typename ST, bool ZEROS>
+// F16: fp16 tables (cuda-f16): 16 B per k-group in registers, per-stream
+// fp32 accumulators (add.f32.f16), planes merged in fp32 (S = sum_p 2^p P_p,
+// powers of two: exact scaling) before the group reduction; no table scale
+// (y = ws * (S - rs) [+ zero term], out = 0.5 * sum, scalar-real semantics
+// _kernels.py:101-137 regrouped, tolerance-tested).
+template <int R, int LG, int BITS, typename ST, bool ZEROS, bool F16 = false>
 __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant__ B1Args a) {
   const GemvArgs& p = a.g;
   const bl::LayoutV2& L = p.L;
@@ -682,13 +687,19 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
   const int ub = u >> 5, l = u & 31;
   const int nu_b = min(32, U - 32 * ub);
   const int g = u / LG;
-  uint4 tq[R / 2];
+  uint4 tq[F16 ? R : R / 2];
   float ts = 0.f, rs = 0.f;
   if (live) {
-    const uint8_t* tb = p.qtab + (int64_t)ub * (32 * R * 8) + l * 16;
+    if constexpr (F16) {
+      const uint8_t* tb = p.qtab + (int64_t)ub * (32 * R * 16) + l * 16;
 #pragma unroll
-    for (int jp = 0; jp < R / 2; jp++) tq[jp] = bl::ld_cg_128(tb + jp * nu_b * 16);
-    ts = bl::ld_cg_f32(p.tscales + g);
+      for (int j = 0; j < R; j++) tq[j] = bl::ld_cg_128(tb + j * nu_b * 16);
+    } else {
+      const uint8_t* tb = p.qtab + (int64_t)ub * (32 * R * 8) + l * 16;
+#pragma unroll
+      for (int jp = 0; jp < R / 2; jp++) tq[jp] = bl::ld_cg_128(tb + jp * nu_b * 16);
+      ts = bl::ld_cg_f32(p.tscales + g);
+    }
     rs = bl::ld_cg_f32(p.rowsums + g);
   }
   const uint32_t woff = (uint32_t)(ub * (32 * R * 16) + l * 16);
@@ -698,6 +709,50 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
     const int stage = S == 1 ? 0 : (it & 1);
     uint8_t* sb = smem + stage * a.stage_bytes;
     mbar_wait(bar + stage, (S == 1 ? it : it >> 1) & 1);
+    float y[NCH];
+    int ch0;
+    if constexpr (F16) {
+      float fa[32];
+#pragma unroll
+      for (int i = 0; i < 32; i++) fa[i] = 0.f;
+      if (live) {
+        const uint8_t* wsrc = sb + woff;
+        const int stride = nu_b == 32 ? 512 : nu_b * 16;
+#pragma unroll
+        for (int j = 0; j < R; j++)
+          lookup_kg_f16(*reinterpret_cast<const uint4*>(wsrc + j * stride), tq[j], fa);
+      }
+      // streams are channel-major (c * BITS + p): merge the planes, exact 2^p
+      constexpr int NCHAN = 32 / BITS;
+      float sc[NCHAN];
+#pragma unroll
+      for (int c = 0; c < NCHAN; c++) {
+        float v = fa[c * BITS];
+#pragma unroll
+        for (int q = 1; q < BITS; q++) v = fmaf((float)(1 << q), fa[c * BITS + q], v);
+        sc[c] = v;
+      }
+      const int basef = reduce_lanes<NCHAN, 1, LG>(sc, lane);
+      ch0 = basef;
+      constexpr int NVF = reduced_count<NCHAN, 1, LG>();
+      static_assert(NVF == NCH, "fp16 mode: channel counts agree");
+      if (live) {
+        const ST* sp = reinterpret_cast<const ST*>(sb + a.s_off) + ch0 * NQ + g;
+        if constexpr (ZEROS) {
+          const ST* zp = reinterpret_cast<const ST*>(sb + a.z_off) + ch0 * NQ + g;
+          const float h2 = (float)(2 << (BITS - 1));
+#pragma unroll
+          for (int j = 0; j < NCH; j++)
+            y[j] = bl::to_f32(sp[j * NQ]) * fmaf(fmaf(-2.f, bl::to_f32(zp[j * NQ]), h2), rs, sc[j] - rs);
+        } else {
+#pragma unroll
+          for (int j = 0; j < NCH; j++) y[j] = bl::to_f32(sp[j * NQ]) * (sc[j] - rs);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < NCH; j++) y[j] = 0.f;
+      }
+    } else {
     int acc[NACC];
 #pragma unroll
     for (int i = 0; i < NACC; i++) acc[i] = 0;
@@ -723,8 +778,7 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
       }
     }
     const int base = reduce_lanes<NACC, 1, LG>(acc, lane);
-    const int ch0 = BITS == 1 ? 2 * base : base;
-    float y[NCH];
+    ch0 = BITS == 1 ? 2 * base : base;
     if (live) {
       int Sv[NCH];
       if constexpr (BITS == 1) {
@@ -756,6 +810,7 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
     } else {
 #pragma unroll
       for (int j = 0; j < NCH; j++) y[j] = 0.f;
+    }
     }
     const int fb = reduce_lanes<NCH, LG, 32>(y, lane);
     float* yb = ysm + (it & 1) * NW * TCH + warp * TCH;
@@ -1217,7 +1272,7 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
     // its shards): 4096x28672 W2 8.3 vs 11.0 us, 2048x28672 4.7 vs 5.9 us;
     // at K = 11008 the unsplit lean kernel is faster (2.6 vs 3.8 us)
     if (cl_env != 0 && (size_t)L.KG * 16 > 65536 && L.U > 256 && !g.partials && !g.gather && !g.trace &&
-        g.n_rows <= 1) {
+        g.n_rows <= 1 && !g.f16_tables) {
       bool handled = false;
       const int rc = launch_b1_cluster<R, LG, BITS, ST>(g, mats, n_mats, stream, pdl, &handled);
       if (handled || rc != BITLUT_OK) return rc;
@@ -1262,11 +1317,16 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
                            !g.trace && !a.ldg_w;
   const bool has_z = mats[0].zeros != nullptr;
   const bool lean = KIND == kFast && lean_common;
-  const bool lean_rows = KIND == kFastRows && lean_common && n_mats == 1 && !has_z;
-  auto kern = lean ? (has_z ? gemv_b1_lean_kernel<R, LG, BITS, ST, true> : gemv_b1_lean_kernel<R, LG, BITS, ST, false>)
+  const bool lean_rows = KIND == kFastRows && lean_common && n_mats == 1 && !has_z && !g.f16_tables;
+  if (g.f16_tables && !lean) return BITLUT_ELAYOUT;     // fp16 tables: the lean kernel or gemv_kernel
+  const bool f16 = g.f16_tables != 0;
+  auto kern = lean ? (f16 ? (has_z ? gemv_b1_lean_kernel<R, LG, BITS, ST, true, true>
+                                   : gemv_b1_lean_kernel<R, LG, BITS, ST, false, true>)
+                          : (has_z ? gemv_b1_lean_kernel<R, LG, BITS, ST, true>
+                                   : gemv_b1_lean_kernel<R, LG, BITS, ST, false>))
                    : (lean_rows ? gemv_b1_rows_lean_kernel<R, LG, BITS, ST> : gemv_b1_kernel<R, LG, BITS, ST, KIND>);
-  static bool configured_k[4] = {false, false, false, false};   // general, lean, lean + zeros, rows
-  const int ki = lean ? (has_z ? 2 : 1) : (lean_rows ? 3 : 0);
+  static bool configured_k[6] = {false, false, false, false, false, false};
+  const int ki = lean ? (has_z ? 2 : 1) + (f16 ? 3 : 0) : (lean_rows ? 3 : 0);
   bool& configured = configured_k[ki];
   if (!configured) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
@@ -1416,9 +1476,10 @@ int bl_gemv_b1_launch(const GemvArgs& g, int scale_dtype, cudaStream_t s, bool p
   }
   if (g.fast) {
     int rc = BITLUT_ELAYOUT;
-    if (!g.gather) rc = bl_gemv_stream_launch(g, reinterpret_cast<const StreamMat*>(&m), 1, scale_dtype, s, pdl);
+    const bool alt = !g.gather && !g.f16_tables;
+    if (alt) rc = bl_gemv_stream_launch(g, reinterpret_cast<const StreamMat*>(&m), 1, scale_dtype, s, pdl);
     if (rc != BITLUT_ELAYOUT) return rc;
-    if (!g.gather) rc = bl_gemv_pack_launch(g, reinterpret_cast<const StreamMat*>(&m), 1, scale_dtype, s, pdl);
+    if (alt) rc = bl_gemv_pack_launch(g, reinterpret_cast<const StreamMat*>(&m), 1, scale_dtype, s, pdl);
     if (rc != BITLUT_ELAYOUT) return rc;
     return f16 ? dispatch_b1<__half, kFast>(g, &m, 1, nullptr, s, pdl)
                : dispatch_b1<float, kFast>(g, &m, 1, nullptr, s, pdl);

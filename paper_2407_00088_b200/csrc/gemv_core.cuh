@@ -58,6 +58,7 @@ struct GemvArgs {
   bl::DepSync dep;           // op-list counters (n_wait == 0 and done == null otherwise)
   int* grid_out;             // host: receives the launch's CTA count (op-list executor), or null
   int force_stream;          // BITLUT_FLAG_STREAM: batch-1 fast lookups through gemv_stream.cu
+  int f16_tables;            // BITLUT_TABLE_F16 (batch-1 fast lean kernel only; 0 = int8 tables)
   const GatherArgs* gather;  // host side: fused all-gather epilogue (batch-1 fast kernel), or null
 };
 

@@ -774,3 +774,29 @@ def test_long_k_cluster_kernel(bits, gs, m, zeros):
     ref = O.mpgemm_q8(x.cpu().numpy(), q.cpu().numpy(), sc.float().cpu().numpy(), bits, gs,
                       zeros=None if z is None else z.cpu().numpy())[0]
     assert rel_maxnorm(y[0].cpu().numpy(), ref) <= 1e-5
+
+
+def test_f16_fast_batch1_lean(config_golden):
+    """fp16 tables, batch 1, fast epilogue (the lean kernel's fp16 mode):
+    BASELINE config 1 within 1e-3 of the reference (scalar-real + zero
+    correction), equal to the reference-order fp16 path within 1e-5, and
+    deterministic; plus W2 / W1 shapes against the exact fp16 path."""
+    inst = W.config1()
+    g = config_golden[inst["name"]]
+    _, pw = make_pw(inst)
+    yf = B.mpgemm(inst["a"], pw, variant="cuda-f16", exact_epilogue=False)[0]
+    ye = B.mpgemm(inst["a"], pw, variant="cuda-f16")[0]
+    rs = O.row_sums(inst["a"].astype(np.float32), inst["group_size"])
+    ref = (g["y_scalar-real"][0] + O.zero_correction(inst["scales"], inst["zeros"], 4, rs[0])).astype(np.float32)
+    assert rel_maxnorm(yf, ref) <= 1e-3, rel_maxnorm(yf, ref)
+    assert rel_maxnorm(yf, ye) <= 1e-5, rel_maxnorm(yf, ye)
+    assert np.array_equal(yf, B.mpgemm(inst["a"], pw, variant="cuda-f16", exact_epilogue=False)[0])
+    gen = torch.Generator(device="cuda").manual_seed(16)
+    for bits, gs, m, k in ((2, 64, 512, 4096), (1, 128, 1024, 4096), (4, 64, 256, 11008), (2, 32, 352, 2048)):
+        q = torch.randint(0, 1 << bits, (m, k), dtype=torch.uint8, device="cuda", generator=gen)
+        sc = (torch.randn((m, k // gs), device="cuda", generator=gen).abs() * 0.02 + 1e-3).half()
+        pw2 = B.prepare_weights(B.QuantizedWeights(m=m, k=k, bits=bits, group_size=gs, qvalues=q, scales=sc))
+        x = torch.randn((1, k), device="cuda", generator=gen).half()
+        a = B.mpgemm(x, pw2, variant="cuda-f16", exact_epilogue=False)
+        b = B.mpgemm(x, pw2, variant="cuda-f16")
+        assert rel_maxnorm(a.cpu().numpy(), b.cpu().numpy()) <= 1e-5, (bits, gs, m, k)
