@@ -477,13 +477,57 @@ def llama70b_table(device, stream, reps, warmup, barrier, peak):
                 rows[name] = e
                 del ws, scs, pw
                 torch.cuda.empty_cache()
+            # the whole per-GPU layer as a decode step issues it: q,k,v in one
+            # launch (one activation row), o, gate+up in one launch, down;
+            # overlapped launches, rotating weight sets >= 4x L2
+            lay = _llama70b_layer_graph(device, stream, reps, warmup, barrier, bits, gs, P, gen)
             out[f"W{bits}_tp{P}"] = {
                 "shapes": rows,
                 "layer_us_per_gpu_n1": round(layer_us, 2),
                 "layer_GBps_per_gpu_n1": round(layer_bytes / (layer_us * 1e-6) / 1e9, 1),
+                "layer_grouped_us_per_gpu_n1": lay["us"],
+                "layer_grouped_GBps_per_gpu_n1": round(layer_bytes / (lay["us"] * 1e-6) / 1e9, 1),
+                "layer_grouped_frac_of_peak": round(layer_bytes / (lay["us"] * 1e-6) / 1e9 / peak, 4),
+                "layer_grouped_launches": lay["launches"],
                 "layer_us_per_gpu_n8": round(layer_us8, 2),
                 "layer_packed_bytes_per_gpu": layer_bytes}
     return out
+
+
+def _llama70b_layer_graph(device, stream, reps, warmup, barrier, bits, gs, P, gen):
+    """One 70B layer shard per GPU (tp P) as 4 grouped batch-1 launches."""
+    import torch
+    import paper_2407_00088_b200 as B
+    from paper_2407_00088_b200 import _native as N
+
+    def make(m, k):
+        q = torch.randint(0, 1 << bits, (m, k), dtype=torch.uint8, device=device, generator=gen)
+        sc = (torch.randn((m, k // gs), device=device, generator=gen).abs() * 0.02 + 1e-3).half()
+        return B.prepare_weights(B.QuantizedWeights(m=m, k=k, bits=bits, group_size=gs, qvalues=q, scales=sc))
+    shapes = {"q": (8192, 8192), "k": (1024, 8192), "v": (1024, 8192), "o": (8192, 8192),
+              "gate": (28672, 8192), "up": (28672, 8192), "down": (8192, 28672)}
+    one = sum(bits * (m // P) * k // 8 for m, k in shapes.values())
+    n_sets = max(2, -(-4 * L2_BYTES // one))
+    sets = [{nm: make(m // P, k) for nm, (m, k) in shapes.items()} for _ in range(n_sets)]
+    xs = {kk: torch.randn((1, kk), device=device, generator=gen).half() for kk in (8192, 28672)}
+    tabs = {kk: N.build_lut(x, gs, N.TABLE_Q8) for kk, x in xs.items()}
+    fl = N.FLAG_PDL | N.FLAG_FAST_EPILOGUE | N.FLAG_INDEPENDENT
+
+    def body():
+        for L in sets:
+            N.mpgemv_multi([(L[n].gpu, L[n].scales, None, L[n].m) for n in ("q", "k", "v")], *tabs[8192],
+                           8192, bits, gs, fl)
+            N.lookup(L["o"].gpu, L["o"].scales, None, *tabs[8192], L["o"].m, 8192, bits, gs, N.TABLE_Q8, fl, False)
+            N.mpgemv_multi([(L[n].gpu, L[n].scales, None, L[n].m) for n in ("gate", "up")], *tabs[8192],
+                           8192, bits, gs, fl)
+            N.lookup(L["down"].gpu, L["down"].scales, None, *tabs[28672], L["down"].m, 28672, bits, gs,
+                     N.TABLE_Q8, fl, False)
+    g = capture(body, stream)
+    with torch.cuda.stream(stream):
+        ms = time_graph(g, reps, warmup, barrier)
+    del g, sets
+    torch.cuda.empty_cache()
+    return {"us": round(ms * 1e3 / n_sets, 3), "launches": 4}
 
 
 def gemm_table(device, stream, reps, warmup, barrier, world):
