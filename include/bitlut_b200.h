@@ -210,6 +210,27 @@ int bitlut_mpgemv_multi(const bitlut_mat* mats, int n_mats, int k, int bits, int
                         int scale_dtype, const void* tables, const float* tscales, const float* rowsums,
                         int flags, void* stream);
 
+/* Several batch-1 matrices with DIFFERENT activation rows (each its own
+ * tables from bitlut_build_lut, mode Q8, n = 1) in one launch -- e.g. the
+ * q,k,v,o,gate,up lookups of a layer set whose tables are all complete:
+ * fewer, larger launches.  Fast epilogue only; matrices share k, bits,
+ * group_size, scale dtype and zero-point presence; up to 8.  Outputs equal
+ * the per-matrix bitlut_mpgemm calls bitwise.  Returns BITLUT_ELAYOUT when
+ * the shape needs a kernel without per-matrix tables (callers then launch
+ * the matrices separately). */
+typedef struct {
+  const uint8_t* wgpu;
+  const void* wscales;
+  const void* zeros;        /* or NULL (all or none) */
+  int m;
+  float* out;               /* (1, m) f32 */
+  const void* tables;       /* this matrix's activation row: (1, k/4*8) int8 kernel format */
+  const float* tscales;     /* (1, k/gs) */
+  const float* rowsums;     /* (1, k/gs) */
+} bitlut_mat_tab;
+int bitlut_mpgemv_multi_tab(const bitlut_mat_tab* mats, int n_mats, int k, int bits, int group_size,
+                            int scale_dtype, int flags, void* stream);
+
 /* Tensor-parallel batch-1 lookup with the all-gather fused into the epilogue
  * (SURVEY §8(e) B200-native upgrade; replaces kernel.py:374-382 mpgemv on
  * this rank's output-channel shard + parallel.py's NCCL all-gather).  Same

@@ -54,6 +54,7 @@ _SIGS = {
     "bitlut_mpgemv_gather": [_vp, _i, _i, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _i,
                              _vp],
     "bitlut_gather_wait": [_vp, ctypes.c_uint32, _vp],
+    "bitlut_mpgemv_multi_tab": [_vp, _i, _i, _i, _i, _i, _i, _vp],
 }
 
 
@@ -61,6 +62,13 @@ class BitlutMat(ctypes.Structure):
     """include/bitlut_b200.h bitlut_mat: one matrix of a grouped batch-1 launch."""
     _fields_ = [("wgpu", ctypes.c_void_p), ("wscales", ctypes.c_void_p), ("zeros", ctypes.c_void_p),
                 ("m", ctypes.c_int32), ("out", ctypes.c_void_p)]
+
+
+class BitlutMatTab(ctypes.Structure):
+    """include/bitlut_b200.h bitlut_mat_tab: one matrix with its own tables."""
+    _fields_ = [("wgpu", ctypes.c_void_p), ("wscales", ctypes.c_void_p), ("zeros", ctypes.c_void_p),
+                ("m", ctypes.c_int32), ("out", ctypes.c_void_p), ("tables", ctypes.c_void_p),
+                ("tscales", ctypes.c_void_p), ("rowsums", ctypes.c_void_p)]
 
 
 class GpuLayout(ctypes.Structure):
@@ -196,6 +204,24 @@ def mpgemv_multi(mats, tables: torch.Tensor, tscales: torch.Tensor, rowsums: tor
     rc = lib().bitlut_mpgemv_multi(arr, len(mats), k, bits, group_size, dtype_code(mats[0][1]), ptr(tables),
                                    ptr(tscales), ptr(rowsums), flags, stream_of(tables))
     raise_for_status(rc, "bitlut_mpgemv_multi")
+    return outs
+
+
+def mpgemv_multi_tab(mats, k: int, bits: int, group_size: int, flags: int) -> list:
+    """bitlut_mpgemv_multi_tab: batch-1 matrices with their own tables in one
+    launch; mats = [(wgpu, wscales, zeros, m, tables, tscales, rowsums), ...]
+    (fast epilogue).  Returns one (1, m) f32 output per matrix."""
+    dev = mats[0][0].device
+    outs = [torch.empty((1, m), dtype=torch.float32, device=dev) for (_, _, _, m, _, _, _) in mats]
+    arr = (BitlutMatTab * len(mats))()
+    for i, ((w, sc, z, m, t, ts, rs), o) in enumerate(zip(mats, outs)):
+        arr[i].wgpu, arr[i].wscales = w.data_ptr(), sc.data_ptr()
+        arr[i].zeros = None if z is None else z.data_ptr()
+        arr[i].m, arr[i].out = m, o.data_ptr()
+        arr[i].tables, arr[i].tscales, arr[i].rowsums = t.data_ptr(), ts.data_ptr(), rs.data_ptr()
+    rc = lib().bitlut_mpgemv_multi_tab(arr, len(mats), k, bits, group_size, dtype_code(mats[0][1]), flags,
+                                       stream_of(mats[0][0]))
+    raise_for_status(rc, "bitlut_mpgemv_multi_tab")
     return outs
 
 

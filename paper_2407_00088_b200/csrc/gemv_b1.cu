@@ -32,7 +32,7 @@ using namespace blk;
 
 constexpr int kMaxStages = 2;
 
-constexpr int kMaxMats = 4;
+constexpr int kMaxMats = 8;
 
 // One weight matrix of a (multi-matrix) launch: matrices that share the
 // activation tables (q/k/v, gate/up) are looked up by one launch whose tiles
@@ -43,6 +43,9 @@ struct B1Mat {                // layout-identical to blk::StreamMat (gemv_stream
   const void* zeros;
   float* out;
   int tile_end;               // cumulative tile count up to and including this matrix
+  const uint8_t* qtab;        // per-matrix tables (lean kernel, partitioned launch), or null
+  const float* tscales;
+  const float* rowsums;
 };
 
 struct B1Args {
@@ -62,6 +65,8 @@ struct B1Args {
   uint32_t tab_off, ts_off, rs_off, y_off, bar_off;
   GatherArgs gth;             // fused all-gather epilogue (fast kernel), n_peers == 0 otherwise
   int ldg_w;                  // fast kernel: weights loaded straight into registers (stage = scales only)
+  int partition;              // lean kernel: CTAs [cta_begin[j], cta_begin[j+1]) serve matrix j only
+  int cta_begin[kMaxMats + 1];
 };
 
 struct B1Plan {
@@ -666,15 +671,33 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
   const int NQ = L.NQ, U = L.U;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + a.bar_off);
   float* ysm = reinterpret_cast<float*>(smem + a.y_off);
-  const int ntl = a.total_tiles, step = gridDim.x;
   const int S = a.stages;
+  // tiles of this CTA: all matrices strided by the grid, or (partitioned
+  // launch) the CTA's own matrix strided by that matrix's CTAs -- then the
+  // matrix's own tables, when it has them
+  int t_first = blockIdx.x, step = gridDim.x, ntl = a.total_tiles;
+  const uint8_t* qtab = p.qtab;
+  const float* tsc = p.tscales;
+  const float* rsum = p.rowsums;
+  if (a.partition) {
+    int pj = 0;
+    while (pj + 1 < a.n_mats && (int)blockIdx.x >= a.cta_begin[pj + 1]) pj++;
+    t_first = (pj ? a.mats[pj - 1].tile_end : 0) + ((int)blockIdx.x - a.cta_begin[pj]);
+    step = a.cta_begin[pj + 1] - a.cta_begin[pj];
+    ntl = a.mats[pj].tile_end;
+    if (a.mats[pj].qtab) {
+      qtab = a.mats[pj].qtab;
+      tsc = a.mats[pj].tscales;
+      rsum = a.mats[pj].rowsums;
+    }
+  }
 
   if (tid == 0) {
     for (int s = 0; s <= kMaxStages; s++) mbar_init(bar + s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     const uint64_t pol = policy_evict_first();
     for (int s = 0; s < S; s++) {
-      const int t = blockIdx.x + s * step;
+      const int t = t_first + s * step;
       if (t < ntl) issue_stage<ST>(a, t, smem + s * a.stage_bytes, bar + s, pol);
     }
   }
@@ -691,21 +714,21 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
   float ts = 0.f, rs = 0.f;
   if (live) {
     if constexpr (F16) {
-      const uint8_t* tb = p.qtab + (int64_t)ub * (32 * R * 16) + l * 16;
+      const uint8_t* tb = qtab + (int64_t)ub * (32 * R * 16) + l * 16;
 #pragma unroll
       for (int j = 0; j < R; j++) tq[j] = bl::ld_cg_128(tb + j * nu_b * 16);
     } else {
-      const uint8_t* tb = p.qtab + (int64_t)ub * (32 * R * 8) + l * 16;
+      const uint8_t* tb = qtab + (int64_t)ub * (32 * R * 8) + l * 16;
 #pragma unroll
       for (int jp = 0; jp < R / 2; jp++) tq[jp] = bl::ld_cg_128(tb + jp * nu_b * 16);
-      ts = bl::ld_cg_f32(p.tscales + g);
+      ts = bl::ld_cg_f32(tsc + g);
     }
-    rs = bl::ld_cg_f32(p.rowsums + g);
+    rs = bl::ld_cg_f32(rsum + g);
   }
   const uint32_t woff = (uint32_t)(ub * (32 * R * 16) + l * 16);
   __syncthreads();                                      // barriers initialised
   int it = 0;
-  for (int tile = blockIdx.x; tile < ntl; tile += step, it++) {
+  for (int tile = t_first; tile < ntl; tile += step, it++) {
     const int stage = S == 1 ? 0 : (it & 1);
     uint8_t* sb = smem + stage * a.stage_bytes;
     mbar_wait(bar + stage, (S == 1 ? it : it >> 1) & 1);
@@ -1389,6 +1412,23 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
   a.psm_off = s.psm_off; a.terms_off = s.terms_off; a.fin_off = s.fin_off; a.rowlen = s.rowlen;
   int grid = sm_count() * per_sm;
   if (grid > want) grid = want;
+  a.partition = 0;
+  if (g.mixed_tables) {
+    if (!lean) return BITLUT_ELAYOUT;                   // per-matrix tables: the lean kernel only
+    // CTAs per matrix in proportion to its tiles (>= 1, <= its tiles); a CTA
+    // then serves one matrix and loads that matrix's tables once
+    const int G = grid < n_mats ? n_mats : grid;
+    a.partition = 1;
+    a.cta_begin[0] = 0;
+    for (int j = 0; j < n_mats; j++) {
+      const int nj = mats[j].tile_end - (j ? mats[j - 1].tile_end : 0);
+      int cj = (int)(((int64_t)G * nj + a.total_tiles / 2) / a.total_tiles);
+      if (cj < 1) cj = 1;
+      if (cj > nj) cj = nj;
+      a.cta_begin[j + 1] = a.cta_begin[j] + cj;
+    }
+    grid = a.cta_begin[n_mats];
+  }
   const int cs = FUSED ? kClusterCTAs : 1;
   grid = (grid + cs - 1) / cs * cs;                     // spare CTAs only build their table slice
   int grid_y = 1;
@@ -1651,4 +1691,66 @@ extern "C" int bitlut_gather_wait(const unsigned* flag, unsigned target, void* s
   if (!flag) return BITLUT_EPARAM;
   gather_wait_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(flag, target);
   return bl_launch_status();
+}
+
+// Shapes whose batch-1 fast launches run the lean kernel (one unit round,
+// no split-K): the op-list planner groups lookups with different tables only
+// for these (pipeline.cu).
+bool bl_mixed_tables_ok(const bl::LayoutV2& L) {
+  static int lean_env = -1;
+  if (lean_env < 0) {
+    const char* e = getenv("BITLUT_B1_LEAN");
+    lean_env = e ? atoi(e) : 1;
+  }
+  return lean_env != 0 && L.n_sg == 1 && L.U <= 384 && (size_t)L.KG * 16 <= 65536 && L.bits != 3;
+}
+
+int bl_mpgemv_multi_tab_launch(const bitlut_mat_tab* mats, int n_mats, int k, int bits, int group_size,
+                               int scale_dtype, int flags, void* stream, const bl::DepSync& dep, int* grid_out);
+
+// Several batch-1 matrices, each with its OWN activation tables, in one launch
+// (fast epilogue): see include/bitlut_b200.h.
+extern "C" int bitlut_mpgemv_multi_tab(const bitlut_mat_tab* mats, int n_mats, int k, int bits, int group_size,
+                                       int scale_dtype, int flags, void* stream) {
+  const bl::DepSync none = {};
+  return bl_mpgemv_multi_tab_launch(mats, n_mats, k, bits, group_size, scale_dtype, flags, stream, none, nullptr);
+}
+
+int bl_mpgemv_multi_tab_launch(const bitlut_mat_tab* mats, int n_mats, int k, int bits, int group_size,
+                               int scale_dtype, int flags, void* stream, const bl::DepSync& dep, int* grid_out) {
+  if (!mats || n_mats < 1 || n_mats > kMaxMats) return BITLUT_EPARAM;
+  if (scale_dtype != BITLUT_DT_F32 && scale_dtype != BITLUT_DT_F16) return BITLUT_EPARAM;
+  if (!(flags & BITLUT_FLAG_FAST_EPILOGUE)) return BITLUT_EPARAM;
+  bl::LayoutV2 L;
+  B1Mat ms[kMaxMats];
+  int tiles = 0;
+  for (int j = 0; j < n_mats; j++) {
+    int rc = bl::make_layout(mats[j].m, k, bits, group_size, &L);
+    if (rc) return rc;
+    if (!mats[j].wgpu || !mats[j].wscales || !mats[j].out || !mats[j].tables || !mats[j].tscales ||
+        !mats[j].rowsums)
+      return BITLUT_EPARAM;
+    if ((mats[j].zeros != nullptr) != (mats[0].zeros != nullptr)) return BITLUT_EPARAM;
+    tiles += L.n_tiles;
+    ms[j].w = mats[j].wgpu; ms[j].wscales = mats[j].wscales; ms[j].zeros = mats[j].zeros;
+    ms[j].out = mats[j].out; ms[j].tile_end = tiles;
+    ms[j].qtab = reinterpret_cast<const uint8_t*>(mats[j].tables);
+    ms[j].tscales = mats[j].tscales;
+    ms[j].rowsums = mats[j].rowsums;
+  }
+  if (L.n_sg != 1) return BITLUT_ELAYOUT;
+  const bool pdl = (flags & BITLUT_FLAG_PDL) != 0;
+  GemvArgs g = {};
+  g.qtab = ms[0].qtab; g.tscales = ms[0].tscales; g.rowsums = ms[0].rowsums;
+  g.L = L;
+  g.independent = pdl && (flags & BITLUT_FLAG_INDEPENDENT) != 0;
+  g.fast = 1;
+  g.zeros = mats[0].zeros;
+  g.rows_per_cta = 1; g.n_rows = 1;
+  g.mixed_tables = 1;
+  g.dep = dep;
+  g.grid_out = grid_out;
+  const cudaStream_t st = (cudaStream_t)stream;
+  return scale_dtype == BITLUT_DT_F16 ? dispatch_b1<__half, kFast>(g, ms, n_mats, nullptr, st, pdl)
+                                      : dispatch_b1<float, kFast>(g, ms, n_mats, nullptr, st, pdl);
 }

@@ -21,6 +21,10 @@ struct StreamMat {
   const void* zeros;
   float* out;
   int tile_end;               // cumulative tile count up to and including this matrix
+  // per-matrix activation tables (bitlut_mpgemv_multi_tab), or null: the launch's
+  const uint8_t* qtab;
+  const float* tscales;
+  const float* rowsums;
 };
 
 // Fused all-gather epilogue (SURVEY §8(e) "B200-native upgrade"): every
@@ -59,6 +63,7 @@ struct GemvArgs {
   int* grid_out;             // host: receives the launch's CTA count (op-list executor), or null
   int force_stream;          // BITLUT_FLAG_STREAM: batch-1 fast lookups through gemv_stream.cu
   int f16_tables;            // BITLUT_TABLE_F16 (batch-1 fast lean kernel only; 0 = int8 tables)
+  int mixed_tables;          // matrices carry their own tables (bitlut_mpgemv_multi_tab): lean kernel only
   const GatherArgs* gather;  // host side: fused all-gather epilogue (batch-1 fast kernel), or null
 };
 

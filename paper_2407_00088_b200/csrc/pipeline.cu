@@ -311,10 +311,22 @@ static bool groupable_tables(const bitlut_pipe_op& a, const bitlut_pipe_op& b) {
 
 // Lookups that read the same table op (single dep) and can share one batch-1
 // launch (bitlut_mpgemv_multi): q/k/v, gate/up.
+bool bl_mixed_tables_ok(const bl::LayoutV2& L);   // gemv_b1.cu
+
+// Two lookups can share a launch when they read the same tables (any
+// epilogue), or -- fast epilogue, lean-kernel shapes -- different tables
+// (bitlut_mpgemv_multi_tab: one launch for e.g. q,k,v,o,gate,up of a layer).
 static bool groupable_lookups(const bitlut_pipe_op& a, const bitlut_pipe_op& b, const bitlut_pipe_op* specs) {
   if (a.type != BITLUT_OP_LOOKUP || b.type != BITLUT_OP_LOOKUP) return false;
-  if (a.dep[0] < 0 || a.dep[1] >= 0 || a.dep[2] >= 0 || b.dep[0] != a.dep[0] || b.dep[1] >= 0 || b.dep[2] >= 0)
+  if (a.dep[0] < 0 || a.dep[1] >= 0 || a.dep[2] >= 0 || b.dep[0] < 0 || b.dep[1] >= 0 || b.dep[2] >= 0)
     return false;
+  if (specs[b.dep[0]].type != BITLUT_OP_TABLES) return false;
+  if (b.dep[0] != a.dep[0]) {
+    if (!(a.flags & BITLUT_FLAG_FAST_EPILOGUE) || !(b.flags & BITLUT_FLAG_FAST_EPILOGUE)) return false;
+    bl::LayoutV2 La;
+    if (bl::make_layout(a.m, a.k, a.bits, a.group_size, &La) || !bl_mixed_tables_ok(La)) return false;
+    if (specs[a.dep[0]].n != 1 || specs[b.dep[0]].n != 1) return false;
+  }
   if ((a.flags & BITLUT_FLAG_FAST_EPILOGUE) != (b.flags & BITLUT_FLAG_FAST_EPILOGUE)) return false;
   if (a.n != 1 || b.n != 1 || a.k != b.k || a.bits != b.bits || a.group_size != b.group_size) return false;
   if (a.scale_dtype != b.scale_dtype || (a.zeros != nullptr) != (b.zeros != nullptr)) return false;
@@ -334,7 +346,7 @@ static bool grouping_enabled() {
   return on != 0;
 }
 
-constexpr int kMaxGroupTables = 8, kMaxGroupLookups = 4;
+constexpr int kMaxGroupTables = 8, kMaxGroupLookups = 8;
 
 extern "C" int bitlut_pipeline_plan_flags(const bitlut_pipe_op* specs, int n_ops, int* flags_out) {
   if (n_ops <= 0 || !specs || !flags_out) return BITLUT_EPARAM;
@@ -445,13 +457,32 @@ extern "C" int bitlut_pipeline_launch_ops(const bitlut_pipe_op* specs, int n_ops
       rc = bitlut_mpgemm(s.wgpu, s.m, s.k, s.bits, s.group_size, s.wscales, s.zeros, s.scale_dtype,
                          s.tables, s.tscales, s.rowsums, BITLUT_TABLE_Q8, s.n, s.out, nullptr, lf, stream);
     } else {
-      bitlut_mat mats[kMaxGroupLookups];
-      for (int u = i; u < j; u++) {
-        const bitlut_pipe_op& t = specs[u];
-        mats[u - i] = {t.wgpu, t.wscales, t.zeros, t.m, t.out};
+      bool same = true;
+      for (int u = i + 1; u < j; u++) same = same && specs[u].dep[0] == s.dep[0];
+      if (same) {
+        bitlut_mat mats[kMaxGroupLookups];
+        for (int u = i; u < j; u++) {
+          const bitlut_pipe_op& t = specs[u];
+          mats[u - i] = {t.wgpu, t.wscales, t.zeros, t.m, t.out};
+        }
+        rc = bitlut_mpgemv_multi(mats, j - i, s.k, s.bits, s.group_size, s.scale_dtype, s.tables, s.tscales,
+                                 s.rowsums, lf, stream);
+      } else {
+        bitlut_mat_tab mats[kMaxGroupLookups];
+        for (int u = i; u < j; u++) {
+          const bitlut_pipe_op& t = specs[u];
+          mats[u - i] = {t.wgpu, t.wscales, t.zeros, t.m, t.out, t.tables, t.tscales, t.rowsums};
+        }
+        rc = bitlut_mpgemv_multi_tab(mats, j - i, s.k, s.bits, s.group_size, s.scale_dtype, lf, stream);
+        if (rc == BITLUT_ELAYOUT) {                     // shape outside the lean kernel: one launch each
+          rc = BITLUT_OK;
+          for (int u = i; rc == BITLUT_OK && u < j; u++) {
+            const bitlut_pipe_op& t = specs[u];
+            rc = bitlut_mpgemm(t.wgpu, t.m, t.k, t.bits, t.group_size, t.wscales, t.zeros, t.scale_dtype,
+                               t.tables, t.tscales, t.rowsums, BITLUT_TABLE_Q8, t.n, t.out, nullptr, lf, stream);
+          }
+        }
       }
-      rc = bitlut_mpgemv_multi(mats, j - i, s.k, s.bits, s.group_size, s.scale_dtype, s.tables, s.tscales,
-                               s.rowsums, lf, stream);
     }
     i = j;
   }
@@ -482,6 +513,8 @@ int bl_mpgemm_launch(const uint8_t* wgpu, int m, int k, int bits, int group_size
                      const void* zeros, int scale_dtype, const void* tables, const float* tscales,
                      const float* rowsums, int mode, int n, float* out, int32_t* partials, int flags,
                      unsigned long long* trace, void* stream, const bl::DepSync& dep, int* grid_out);
+int bl_mpgemv_multi_tab_launch(const bitlut_mat_tab* mats, int n_mats, int k, int bits, int group_size,
+                               int scale_dtype, int flags, void* stream, const bl::DepSync& dep, int* grid_out);
 int bl_mpgemv_multi_launch(const bitlut_mat* mats, int n_mats, int k, int bits, int group_size,
                            int scale_dtype, const void* tables, const float* tscales, const float* rowsums,
                            int flags, void* stream, const bl::DepSync& dep, int* grid_out);
@@ -572,13 +605,25 @@ extern "C" int bitlut_pipeline_launch_ops_counted(const bitlut_pipe_op* specs, i
                             s.tscales, s.rowsums, BITLUT_TABLE_Q8, s.n, s.out, nullptr, lf, nullptr, stream, dep,
                             &g);
     } else {
-      bitlut_mat mats[kMaxGroupLookups];
-      for (int u = i; u < j; u++) {
-        const bitlut_pipe_op& t = specs[u];
-        mats[u - i] = {t.wgpu, t.wscales, t.zeros, t.m, t.out};
+      bool same = true;
+      for (int u = i + 1; u < j; u++) same = same && specs[u].dep[0] == s.dep[0];
+      if (same) {
+        bitlut_mat mats[kMaxGroupLookups];
+        for (int u = i; u < j; u++) {
+          const bitlut_pipe_op& t = specs[u];
+          mats[u - i] = {t.wgpu, t.wscales, t.zeros, t.m, t.out};
+        }
+        rc = bl_mpgemv_multi_launch(mats, j - i, s.k, s.bits, s.group_size, s.scale_dtype, s.tables, s.tscales,
+                                    s.rowsums, lf, stream, dep, &g);
+      } else {
+        bitlut_mat_tab mats[kMaxGroupLookups];
+        for (int u = i; u < j; u++) {
+          const bitlut_pipe_op& t = specs[u];
+          mats[u - i] = {t.wgpu, t.wscales, t.zeros, t.m, t.out, t.tables, t.tscales, t.rowsums};
+        }
+        rc = bl_mpgemv_multi_tab_launch(mats, j - i, s.k, s.bits, s.group_size, s.scale_dtype, lf, stream, dep,
+                                        &g);
       }
-      rc = bl_mpgemv_multi_launch(mats, j - i, s.k, s.bits, s.group_size, s.scale_dtype, s.tables, s.tscales,
-                                  s.rowsums, lf, stream, dep, &g);
     }
     grid[i] = g;
     if (rc == BITLUT_OK && g <= 0) rc = BITLUT_EINTERNAL;

@@ -179,8 +179,9 @@ def test_graph_executor_table_fusion_plan():
 
 def test_graph_executor_launch_grouping_plan():
     """Consecutive table builds share one launch; consecutive batch-1 fast
-    lookups over the same tables share one launch; a group is INDEPENDENT
-    only if all its members' inputs are complete."""
+    lookups with equal K share one launch (same tables, or their own tables
+    through bitlut_mpgemv_multi_tab); a group is INDEPENDENT only if all its
+    members' inputs are complete."""
     import ctypes
     from paper_2407_00088_b200.pipeline import PipeOpSpec, _bind
     T, LK, J = 0, 1, 16
@@ -208,8 +209,8 @@ def test_graph_executor_launch_grouping_plan():
     assert _bind().bitlut_pipeline_plan_flags(arr, len(ops), fl) == 0
     P, I, F = N.FLAG_PDL, N.FLAG_INDEPENDENT, N.FLAG_FAST_EPILOGUE
     assert list(fl) == [P, P | J, P | J, P | J,            # one table launch (first kernel: waits)
-                        P | F, P | F | J, P | F | J,       # q,k,v in one launch, waits for the tables
-                        P | F | I,                         # o (tables complete)
-                        P | F | I, P | F | I | J,          # gate, up
-                        P | F | I,                         # down
+                        P | F, P | F | J, P | F | J,       # q,k,v,o,gate,up (K = 4096, fast, three
+                        P | F | J,                         # different tables) in ONE launch, which
+                        P | F | J, P | F | J,              # waits for the table launch
+                        P | F | I,                         # down (K = 11008): tables complete
                         P | I]                             # exact epilogue: own launch

@@ -800,3 +800,45 @@ def test_f16_fast_batch1_lean(config_golden):
         a = B.mpgemm(x, pw2, variant="cuda-f16", exact_epilogue=False)
         b = B.mpgemm(x, pw2, variant="cuda-f16")
         assert rel_maxnorm(a.cpu().numpy(), b.cpu().numpy()) <= 1e-5, (bits, gs, m, k)
+
+
+@pytest.mark.parametrize("bits,gs", [(2, 64), (4, 128), (1, 128)])
+def test_multi_tab_launch_bitwise(bits, gs):
+    """bitlut_mpgemv_multi_tab (matrices with their own activation tables in
+    one launch, CTAs partitioned among them): every output == the per-matrix
+    fast call, bitwise; the graph executor groups q,k,v,o,gate,up of a layer
+    set (different tables) into one launch and matches per-op calls."""
+    from paper_2407_00088_b200 import _native as N
+    from paper_2407_00088_b200.pipeline import Pipeline
+    g = torch.Generator(device="cuda").manual_seed(bits * 3 + gs)
+    k = 4096
+    ms = (4096, 1024, 1024, 4096, 11008 // 32 * 32, 2048)
+    pws, tabs = [], []
+    for m in ms:
+        q = torch.randint(0, 1 << bits, (m, k), dtype=torch.uint8, device="cuda", generator=g)
+        sc = (torch.randn((m, k // gs), device="cuda", generator=g).abs() * 0.02 + 1e-3).half()
+        pws.append(B.prepare_weights(B.QuantizedWeights(m=m, k=k, bits=bits, group_size=gs, qvalues=q, scales=sc)))
+        tabs.append(N.build_lut(torch.randn((1, k), device="cuda", generator=g).half(), gs, N.TABLE_Q8))
+    fl = N.FLAG_PDL | N.FLAG_FAST_EPILOGUE
+    outs = N.mpgemv_multi_tab([(p.gpu, p.scales, None, p.m, *t) for p, t in zip(pws, tabs)], k, bits, gs, fl)
+    for p, t, o in zip(pws, tabs, outs):
+        ref, _ = N.lookup(p.gpu, p.scales, None, *t, p.m, k, bits, gs, N.TABLE_Q8, fl, False)
+        assert torch.equal(o, ref)
+    # graph executor: one layer set of two layers, tables first (lookahead)
+    xs = [[torch.randn((1, k), device="cuda", generator=g).half() for _ in range(3)] for _ in range(2)]
+    pl = Pipeline(executor="graph")
+    ts = [[pl.tables(x, gs) for x in row] for row in xs]
+    ys = []
+    for L in range(2):
+        names = ("q", "k", "v", "o", "gate", "up")
+        tix = (0, 0, 0, 1, 2, 2)
+        ys.append([pl.lookup(pws[i], ts[L][tix[i]], fast_epilogue=True) for i in range(6)])
+    plan = pl.plan_flags()
+    assert any(f & 16 for f in plan)
+    pl.compile()
+    pl.run()
+    torch.cuda.synchronize()
+    for L in range(2):
+        for i, tx in enumerate((0, 0, 0, 1, 2, 2)):
+            ref = B.mpgemm(xs[L][tx], pws[i], exact_epilogue=False)
+            assert torch.equal(ys[L][i].reshape(ref.shape), ref), (L, i)
