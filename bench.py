@@ -924,7 +924,7 @@ def load_traffic():
     the four grouped launches of one layer (profiles/r01d_step_gemv_b1_full.json,
     one `ncu --set full` capture) summed and divided by the layer's 7 GEMVs,
     the same per-launch unit as roofline.achieved."""
-    p = os.path.join(ROOT, "profiles", "r01e_step_gemv_b1_full.json")
+    p = os.path.join(ROOT, "profiles", "r01g_step_gemv_b1_full.json")
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
