@@ -30,7 +30,8 @@ for bits in bitsl:
         a = torch.randn((1, k), device="cuda", generator=g).half()
         t = N.build_lut(a, 64, N.TABLE_Q8)
         for fast in epis:
-            fl = N.FLAG_PDL | (N.FLAG_FAST_EPILOGUE if fast else 0)
+            fl = N.FLAG_PDL | (N.FLAG_FAST_EPILOGUE if fast else 0) | \
+                (N.FLAG_INDEPENDENT if os.environ.get("BIGM_INDEP") == "1" else 0)
             torch.cuda.synchronize()
             with torch.cuda.stream(st):
                 for _ in range(3):
