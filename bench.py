@@ -885,6 +885,10 @@ def main():
             cpu = {"value": round(gbps, 4), "unit": "GB/s", "cores": threads, "kind": "port",
                    "sample": f"1 Llama-2-7B W2 layer (7 vector-q8 mpGEMV incl. table build) x "
                              f"{reps} reps = {secs:.1f}s on {threads} threads ({model})"}
+            # also one thread (the reference's default threads=1)
+            g1, r1, s1 = cpu_baseline(hl, bits, gs, min(3.0, args.cpu_budget), 1)
+            cpu["single_thread"] = {"value": round(g1, 4), "unit": "GB/s", "cores": 1,
+                                    "sample": f"same layer x {r1} reps = {s1:.1f}s on 1 thread"}
         except Exception as e:  # report, never fake
             cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "port",
                    "sample": f"unavailable: {e}"}
