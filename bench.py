@@ -699,6 +699,7 @@ def main():
     with ClockSampler(local) as clk:
         if world == 1:
             for name, ex, fast, chain, sync in (
+                    ("layer_set_batch_fast", "batch", True, False, "pdl"),
                     ("layer_set_graph_fast", "graph", True, False, "pdl"),
                     ("layer_set_graph_exact", "graph", False, False, "pdl"),
                     ("layer_set_graph_fast_counters", "graph", True, False, "counters"),

@@ -159,6 +159,16 @@ typedef struct {
 } bitlut_lut_job;
 int bitlut_build_lut_multi(const bitlut_lut_job* jobs, int n_jobs, int mode, int flags, void* stream);
 
+/* Any number of table builds in ONE launch, the job list in DEVICE memory
+ * (e.g. every activation row of an independent layer set).  Each job is
+ * exactly a bitlut_build_lut call (one dtype for the list).
+ * bitlut_build_lut_batch_encode (host) validates the HOST copy of the jobs
+ * and writes block_end[j] = cumulative CTA count through job j; the caller
+ * copies jobs and block_end to device memory and passes those copies. */
+int bitlut_build_lut_batch_encode(const bitlut_lut_job* jobs, int n_jobs, int* block_end, int* total_blocks);
+int bitlut_build_lut_batch(const bitlut_lut_job* dev_jobs, const int* dev_block_end, int n_jobs,
+                           int total_blocks, int a_dtype, int mode, int flags, void* stream);
+
 /* ---------------- lookup-accumulate (kernel.py / _kernels.py) ---------------- */
 
 /* mpgemm  kernel.py:280-371 with _kernels.gemv_q8_vector :141-192 (mode Q8)
@@ -230,6 +240,31 @@ typedef struct {
 } bitlut_mat_tab;
 int bitlut_mpgemv_multi_tab(const bitlut_mat_tab* mats, int n_mats, int k, int bits, int group_size,
                             int scale_dtype, int flags, void* stream);
+
+/* Any number of independent batch-1 mpgemv calls of one k (each its own
+ * activation row and int8 tables: a layer set) in ONE launch, fast epilogue;
+ * replaces that many kernel.py:374-382 mpgemv calls.  The descriptors live
+ * in DEVICE memory: bitlut_mpgemv_batch_encode (host) validates the host copy
+ * and fills tile_end (cumulative tiles) and *total_tiles; the caller copies
+ * the array to the device.  Every CTA streams one contiguous tile range of
+ * the concatenated matrices.  Outputs equal the per-matrix bitlut_mpgemm
+ * calls (fast epilogue) bitwise.  Scales of one dtype; no zero points;
+ * shapes the lean batch-1 kernel takes (bits 1/2/4, one unit round), else
+ * BITLUT_ELAYOUT. */
+typedef struct {
+  const uint8_t* wgpu;
+  const void* wscales;
+  float* out;               /* (1, m) f32 */
+  const void* tables;       /* (1, k/4*8) int8 kernel format */
+  const float* tscales;     /* (1, k/gs) */
+  const float* rowsums;     /* (1, k/gs) */
+  int m;
+  int tile_end;             /* filled by bitlut_mpgemv_batch_encode */
+} bitlut_batch_mat;
+int bitlut_mpgemv_batch_encode(bitlut_batch_mat* mats, int n_mats, int k, int bits, int group_size,
+                               int* total_tiles);
+int bitlut_mpgemv_batch(const bitlut_batch_mat* dev_mats, int n_mats, int total_tiles, int k, int bits,
+                        int group_size, int scale_dtype, int flags, void* stream);
 
 /* Tensor-parallel batch-1 lookup with the all-gather fused into the epilogue
  * (SURVEY §8(e) B200-native upgrade; replaces kernel.py:374-382 mpgemv on

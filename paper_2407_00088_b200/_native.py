@@ -55,6 +55,10 @@ _SIGS = {
                              _vp],
     "bitlut_gather_wait": [_vp, ctypes.c_uint32, _vp],
     "bitlut_mpgemv_multi_tab": [_vp, _i, _i, _i, _i, _i, _i, _vp],
+    "bitlut_mpgemv_batch_encode": [_vp, _i, _i, _i, _i, _vp],
+    "bitlut_mpgemv_batch": [_vp, _i, _i, _i, _i, _i, _i, _i, _vp],
+    "bitlut_build_lut_batch_encode": [_vp, _i, _vp, _vp],
+    "bitlut_build_lut_batch": [_vp, _vp, _i, _i, _i, _i, _i, _vp],
 }
 
 
@@ -69,6 +73,88 @@ class BitlutMatTab(ctypes.Structure):
     _fields_ = [("wgpu", ctypes.c_void_p), ("wscales", ctypes.c_void_p), ("zeros", ctypes.c_void_p),
                 ("m", ctypes.c_int32), ("out", ctypes.c_void_p), ("tables", ctypes.c_void_p),
                 ("tscales", ctypes.c_void_p), ("rowsums", ctypes.c_void_p)]
+
+
+class BitlutBatchMat(ctypes.Structure):
+    """include/bitlut_b200.h bitlut_batch_mat: one GEMV of a batched launch
+    (device-resident descriptor array)."""
+    _fields_ = [("wgpu", ctypes.c_void_p), ("wscales", ctypes.c_void_p), ("out", ctypes.c_void_p),
+                ("tables", ctypes.c_void_p), ("tscales", ctypes.c_void_p), ("rowsums", ctypes.c_void_p),
+                ("m", ctypes.c_int32), ("tile_end", ctypes.c_int32)]
+
+
+class BitlutLutJob(ctypes.Structure):
+    """include/bitlut_b200.h bitlut_lut_job: one table build."""
+    _fields_ = [("a", ctypes.c_void_p), ("a_dtype", ctypes.c_int32), ("n", ctypes.c_int32),
+                ("k", ctypes.c_int32), ("group_size", ctypes.c_int32), ("tables", ctypes.c_void_p),
+                ("tscales", ctypes.c_void_p), ("rowsums", ctypes.c_void_p)]
+
+
+def _to_device_bytes(arr, device) -> torch.Tensor:
+    host = torch.frombuffer(bytearray(bytes(arr)), dtype=torch.uint8)
+    return host.to(device)
+
+
+class LookupBatch:
+    """Encoded bitlut_mpgemv_batch launch: independent batch-1 fast GEMVs of
+    one (k, bits, group_size, scale dtype), each with its own int8 tables.
+    `arr`: ctypes array of BitlutBatchMat (host); copied to `device`."""
+
+    def __init__(self, arr, k: int, bits: int, group_size: int, scale_dtype: int, device):
+        tt = ctypes.c_int(0)
+        raise_for_status(lib().bitlut_mpgemv_batch_encode(arr, len(arr), k, bits, group_size, ctypes.byref(tt)),
+                         "bitlut_mpgemv_batch_encode")
+        self.n, self.total_tiles = len(arr), tt.value
+        self.k, self.bits, self.group_size, self.scale_dtype = k, bits, group_size, scale_dtype
+        self.dev = _to_device_bytes(arr, device)
+
+    @classmethod
+    def from_tensors(cls, mats, k: int, bits: int, group_size: int) -> "LookupBatch":
+        """mats = [(wgpu, wscales, m, out (1, m) f32, tables, tscales, rowsums), ...]"""
+        arr = (BitlutBatchMat * len(mats))()
+        for i, (w, sc, m, out, t, ts, rs) in enumerate(mats):
+            arr[i].wgpu, arr[i].wscales, arr[i].out = w.data_ptr(), sc.data_ptr(), out.data_ptr()
+            arr[i].tables, arr[i].tscales, arr[i].rowsums = t.data_ptr(), ts.data_ptr(), rs.data_ptr()
+            arr[i].m = m
+        b = cls(arr, k, bits, group_size, dtype_code(mats[0][1]), mats[0][0].device)
+        b.keep = [x for mt in mats for x in mt if isinstance(x, torch.Tensor)]
+        return b
+
+    def launch(self, flags: int, stream) -> None:
+        rc = lib().bitlut_mpgemv_batch(ptr(self.dev), self.n, self.total_tiles, self.k, self.bits, self.group_size,
+                                       self.scale_dtype, flags, ctypes.c_void_p(stream.cuda_stream))
+        raise_for_status(rc, "bitlut_mpgemv_batch")
+
+
+class TableBatch:
+    """Encoded bitlut_build_lut_batch launch.  `arr`: ctypes array of
+    BitlutLutJob (host, one activation dtype); copied to `device`."""
+
+    def __init__(self, arr, mode: int, device):
+        ends = (ctypes.c_int * len(arr))()
+        tb = ctypes.c_int(0)
+        raise_for_status(lib().bitlut_build_lut_batch_encode(arr, len(arr), ends, ctypes.byref(tb)),
+                         "bitlut_build_lut_batch_encode")
+        self.n, self.total_blocks, self.mode, self.a_dtype = len(arr), tb.value, mode, arr[0].a_dtype
+        self.dev_jobs = _to_device_bytes(arr, device)
+        self.dev_ends = _to_device_bytes(ends, device)
+
+    @classmethod
+    def from_tensors(cls, jobs, mode: int) -> "TableBatch":
+        """jobs = [(a (n, k), group_size, tables, tscales, rowsums), ...]"""
+        arr = (BitlutLutJob * len(jobs))()
+        for i, (a, gs, t, ts, rs) in enumerate(jobs):
+            arr[i].a, arr[i].a_dtype = a.data_ptr(), dtype_code(a)
+            arr[i].n, arr[i].k, arr[i].group_size = a.shape[0], a.shape[1], gs
+            arr[i].tables, arr[i].tscales, arr[i].rowsums = t.data_ptr(), ts.data_ptr(), rs.data_ptr()
+        b = cls(arr, mode, jobs[0][0].device)
+        b.keep = [x for jb in jobs for x in jb if isinstance(x, torch.Tensor)]
+        return b
+
+    def launch(self, flags: int, stream) -> None:
+        rc = lib().bitlut_build_lut_batch(ptr(self.dev_jobs), ptr(self.dev_ends), self.n, self.total_blocks,
+                                          self.a_dtype, self.mode, flags, ctypes.c_void_p(stream.cuda_stream))
+        raise_for_status(rc, "bitlut_build_lut_batch")
 
 
 class GpuLayout(ctypes.Structure):

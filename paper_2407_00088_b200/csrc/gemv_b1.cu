@@ -858,6 +858,169 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
 }
 
 
+// Batched lean kernel: any number of independent batch-1 GEMVs of one K,
+// each with its own tables (a layer set), in ONE launch.  The matrices'
+// descriptors live in device memory (bitlut_batch_mat, tile_end cumulative);
+// CTA b walks the contiguous tile range [b*T/G, (b+1)*T/G) of the
+// concatenated tile list, so every CTA streams the same number of tiles and
+// the launch has a single tail.  The thread's tables, table scale and row sum
+// are reloaded (L2) when the range crosses into the next matrix.  Per tile the
+// arithmetic is gemv_b1_lean_kernel<.., ZEROS=false, F16=false>'s, so outputs
+// are bitwise identical to per-matrix fast-epilogue launches.
+__device__ __forceinline__ void issue_stage_batch(const B1Args& a, const bitlut_batch_mat& mt, int local,
+                                                  uint8_t* sb, uint64_t* bar, uint64_t pol, int st_size) {
+  const bl::LayoutV2& L = a.g.L;
+  mbar_expect_tx(bar, a.w_bytes + a.s_bytes);
+  const uint8_t* src = mt.wgpu + L.sg_row_base(local, 0);
+  for (uint32_t off = 0; off < a.w_bytes; off += 32768u) {
+    const uint32_t nb = a.w_bytes - off < 32768u ? a.w_bytes - off : 32768u;
+    bulk_g2s(sb + off, src + off, nb, bar, pol);
+  }
+  const int64_t e0 = (int64_t)local * L.tile_ch * L.NQ;
+  bulk_g2s(sb + a.s_off, reinterpret_cast<const uint8_t*>(mt.wscales) + e0 * st_size, a.s_bytes, bar, pol);
+}
+
+template <int R, int LG, int BITS, typename ST>
+__global__ void __launch_bounds__(384) gemv_b1_batch_kernel(const __grid_constant__ B1Args a,
+                                                             const bitlut_batch_mat* __restrict__ dm,
+                                                             int n_mats) {
+  const GemvArgs& p = a.g;
+  const bl::LayoutV2& L = p.L;
+  constexpr int TCH = 32 / BITS;
+  constexpr int NACC = BITS == 4 ? 8 : 16;
+  constexpr int NV = reduced_count<NACC, 1, LG>();
+  constexpr int NCH = BITS == 1 ? 2 * NV : NV;
+  constexpr int NF = reduced_count<NCH, LG, 32>();
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NW = blockDim.x >> 5;
+  const int NQ = L.NQ, U = L.U;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + a.bar_off);
+  float* ysm = reinterpret_cast<float*>(smem + a.y_off);
+  const int T = a.total_tiles, G = gridDim.x;
+  const int t0 = (int)((int64_t)blockIdx.x * T / G), t1 = (int)((int64_t)(blockIdx.x + 1) * T / G);
+  // matrix holding t0 = number of matrices ending at or before it
+  int j0 = 0;
+  for (int base = 0; base < n_mats; base += blockDim.x) {
+    const int i = base + tid;
+    j0 += __syncthreads_count(i < n_mats && dm[i].tile_end <= t0);
+  }
+  if (t0 >= t1) {                                       // more CTAs than tiles
+    if (!p.independent) bl::pdl_wait();
+    bl::pdl_launch_dependents();
+    if (p.independent) bl::pdl_wait();
+    return;
+  }
+  // issue cursor (thread 0): the matrix of the next tile to stage
+  int ji = j0, ji_begin = 0, ji_end = 0;
+  if (tid == 0) {
+    for (int s = 0; s <= kMaxStages; s++) mbar_init(bar + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint64_t pol = policy_evict_first();
+    ji_begin = ji ? dm[ji - 1].tile_end : 0;
+    ji_end = dm[ji].tile_end;
+    for (int s = 0; s < 2; s++) {
+      const int t = t0 + s;
+      if (t >= t1) break;
+      while (t >= ji_end) { ji++; ji_begin = ji_end; ji_end = dm[ji].tile_end; }
+      issue_stage_batch(a, dm[ji], t - ji_begin, smem + s * a.stage_bytes, bar + s, pol, (int)sizeof(ST));
+    }
+  }
+  if (!p.independent) bl::pdl_wait();
+  bl::pdl_launch_dependents();
+  const int u = tid;
+  const bool live = u < U;
+  const int ub = u >> 5, l = u & 31;
+  const int nu_b = min(32, U - 32 * ub);
+  const int g = u / LG;
+  int jc = j0;
+  int jc_begin = jc ? dm[jc - 1].tile_end : 0, jc_end = dm[jc].tile_end;
+  float* outp = dm[jc].out;
+  uint4 tq[R / 2];
+  float ts = 0.f, rs = 0.f;
+  auto load_tables = [&](const bitlut_batch_mat& mt) {
+    if (live) {
+      const uint8_t* tb = reinterpret_cast<const uint8_t*>(mt.tables) + (int64_t)ub * (32 * R * 8) + l * 16;
+#pragma unroll
+      for (int jp = 0; jp < R / 2; jp++) tq[jp] = bl::ld_cg_128(tb + jp * nu_b * 16);
+      ts = bl::ld_cg_f32(mt.tscales + g);
+      rs = bl::ld_cg_f32(mt.rowsums + g);
+    }
+  };
+  load_tables(dm[jc]);
+  const uint32_t woff = (uint32_t)(ub * (32 * R * 16) + l * 16);
+  __syncthreads();                                      // barriers initialised
+  int it = 0;
+  for (int tile = t0; tile < t1; tile++, it++) {
+    if (tile >= jc_end) {                               // next matrix: its tables and output
+      while (tile >= jc_end) { jc++; jc_begin = jc_end; jc_end = dm[jc].tile_end; }
+      outp = dm[jc].out;
+      load_tables(dm[jc]);
+    }
+    const int stage = it & 1;
+    uint8_t* sb = smem + stage * a.stage_bytes;
+    mbar_wait(bar + stage, (it >> 1) & 1);
+    float y[NCH];
+    int acc[NACC];
+#pragma unroll
+    for (int i = 0; i < NACC; i++) acc[i] = 0;
+    if (live) {
+      const uint8_t* wsrc = sb + woff;
+      const int stride = nu_b == 32 ? 512 : nu_b * 16;
+#pragma unroll
+      for (int j = 0; j < R; j += 2) {
+        const uint4 wa = *reinterpret_cast<const uint4*>(wsrc + j * stride);
+        const uint4 wc = *reinterpret_cast<const uint4*>(wsrc + (j + 1) * stride);
+        lookup_kg_merged<BITS, NACC>(wa, tq[j >> 1].x, tq[j >> 1].y, acc);
+        lookup_kg_merged<BITS, NACC>(wc, tq[j >> 1].z, tq[j >> 1].w, acc);
+      }
+    }
+    const int base = reduce_lanes<NACC, 1, LG>(acc, lane);
+    const int ch0 = BITS == 1 ? 2 * base : base;
+    if (live) {
+      int Sv[NCH];
+      if constexpr (BITS == 1) {
+#pragma unroll
+        for (int i = 0; i < NV; i++) {
+          const int v = acc[i];
+          const int pe = (v << 17) >> 17;
+          Sv[2 * i] = pe;
+          Sv[2 * i + 1] = (v - pe) >> 15;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < NV; i++) Sv[i] = acc[i];
+      }
+      const ST* sp = reinterpret_cast<const ST*>(sb + a.s_off) + ch0 * NQ + g;
+#pragma unroll
+      for (int j = 0; j < NCH; j++) y[j] = bl::to_f32(sp[j * NQ]) * fmaf(ts, (float)Sv[j], -rs);
+    } else {
+#pragma unroll
+      for (int j = 0; j < NCH; j++) y[j] = 0.f;
+    }
+    const int fb = reduce_lanes<NCH, LG, 32>(y, lane);
+    float* yb = ysm + (it & 1) * NW * TCH + warp * TCH;
+#pragma unroll
+    for (int j = 0; j < NF; j++) yb[ch0 + fb + j] = y[j];
+    __syncthreads();                                    // stage consumed, ysm complete
+    if (tid == 0) {
+      const int t = tile + 2;
+      if (t < t1) {
+        while (t >= ji_end) { ji++; ji_begin = ji_end; ji_end = dm[ji].tile_end; }
+        issue_stage_batch(a, dm[ji], t - ji_begin, sb, bar + stage, policy_evict_first(), (int)sizeof(ST));
+      }
+    }
+    if (tid < TCH) {
+      const float* yr = ysm + (it & 1) * NW * TCH + tid;
+      float s = 0.f;
+      for (int w = 0; w < NW; w++) s += yr[w * TCH];
+      outp[(int64_t)(tile - jc_begin) * TCH + tid] = 0.5f * s;
+    }
+  }
+  if (p.independent) bl::pdl_wait();
+}
+
+
 // Lean mpGEMM rows kernel (kFastRows common case: one unit round, register
 // tables, no zeros / partials): the tile is staged once and stays in shared
 // memory while the CTA walks its rows; per row the thread's tables, table
@@ -1498,7 +1661,126 @@ B1Mat single_mat(const GemvArgs& g) {
   return m;
 }
 
+// Batched lean launch: grid = every resident CTA (two stages each), each CTA
+// one contiguous tile range.
+template <int R, int LG, int BITS, typename ST>
+int launch_batch(const GemvArgs& g, const bitlut_batch_mat* dm, int n_mats, int total_tiles, cudaStream_t stream,
+                 bool pdl) {
+  const bl::LayoutV2& L = g.L;
+  const int T = b1_threads(L, true);
+  if ((L.U + T - 1) / T != 1) return BITLUT_ELAYOUT;
+  auto kern = gemv_b1_batch_kernel<R, LG, BITS, ST>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared) != cudaSuccess)
+      return BITLUT_EINTERNAL;
+    configured = true;
+  }
+  const B1Plan s = b1_plan<ST>(L, false, false, T, 2, kFast);
+  if (s.total > 227 * 1024) return BITLUT_ELAYOUT;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, s.total) != cudaSuccess || per_sm < 1)
+    return BITLUT_ELAYOUT;
+  B1Args a;
+  a.g = g;
+  a.act = nullptr;
+  a.gth = GatherArgs{};
+  a.n_mats = 0;
+  a.total_tiles = total_tiles;
+  a.rounds = 1; a.tab_smem = 0; a.ldg_w = 0; a.partition = 0;
+  a.n_rows = 1; a.rows_per_cta = 1;
+  a.stages = 2;
+  a.stage_bytes = s.stage_bytes; a.w_bytes = s.w_bytes; a.s_off = s.s_off; a.s_bytes = s.s_bytes;
+  a.z_off = s.z_off; a.tab_off = s.tab_off; a.ts_off = s.ts_off; a.rs_off = s.rs_off;
+  a.y_off = s.y_off; a.bar_off = s.bar_off; a.sa_off = s.sa_off; a.red_off = s.red_off;
+  a.psm_off = s.psm_off; a.terms_off = s.terms_off; a.fin_off = s.fin_off; a.rowlen = s.rowlen;
+  int grid = sm_count() * per_sm;
+  if (grid > total_tiles) grid = total_tiles;
+  if (g.grid_out) *g.grid_out = grid;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(T);
+  cfg.dynamicSmemBytes = s.total;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a, dm, n_mats) == cudaSuccess ? BITLUT_OK : BITLUT_EINTERNAL;
+}
+
+template <int R, int LG, typename ST>
+int launch_batch_bits(const GemvArgs& g, const bitlut_batch_mat* dm, int n, int tt, cudaStream_t s, bool pdl) {
+  switch (g.L.bits) {
+    case 1: return launch_batch<R, LG, 1, ST>(g, dm, n, tt, s, pdl);
+    case 2: return launch_batch<R, LG, 2, ST>(g, dm, n, tt, s, pdl);
+    case 4: return launch_batch<R, LG, 4, ST>(g, dm, n, tt, s, pdl);
+  }
+  return BITLUT_ELAYOUT;
+}
+
+template <typename ST>
+int dispatch_batch(const GemvArgs& g, const bitlut_batch_mat* dm, int n, int tt, cudaStream_t s, bool pdl) {
+  const int R = g.L.R, LG = g.L.Lg;
+  if (R == 8) {
+    switch (LG) {
+      case 1: return launch_batch_bits<8, 1, ST>(g, dm, n, tt, s, pdl);
+      case 2: return launch_batch_bits<8, 2, ST>(g, dm, n, tt, s, pdl);
+      case 4: return launch_batch_bits<8, 4, ST>(g, dm, n, tt, s, pdl);
+      case 8: return launch_batch_bits<8, 8, ST>(g, dm, n, tt, s, pdl);
+      case 16: return launch_batch_bits<8, 16, ST>(g, dm, n, tt, s, pdl);
+    }
+  } else if (R == 4 && LG == 1) {
+    return launch_batch_bits<4, 1, ST>(g, dm, n, tt, s, pdl);
+  }
+  return BITLUT_ELAYOUT;
+}
+
 }  // namespace
+
+// Host-side check and tile numbering of a batched launch (see the header).
+extern "C" int bitlut_mpgemv_batch_encode(bitlut_batch_mat* mats, int n_mats, int k, int bits, int group_size,
+                                          int* total_tiles) {
+  if (!mats || n_mats < 1 || !total_tiles) return BITLUT_EPARAM;
+  int64_t tiles = 0;
+  for (int j = 0; j < n_mats; j++) {
+    bl::LayoutV2 L;
+    const int rc = bl::make_layout(mats[j].m, k, bits, group_size, &L);
+    if (rc) return rc;
+    if (!mats[j].wgpu || !mats[j].wscales || !mats[j].out || !mats[j].tables || !mats[j].tscales ||
+        !mats[j].rowsums)
+      return BITLUT_EPARAM;
+    if (L.n_sg != 1 || L.bits == 3 || L.U > 384) return BITLUT_ELAYOUT;
+    tiles += L.n_tiles;
+    if (tiles > (int64_t)1 << 30) return BITLUT_ESHAPE;
+    mats[j].tile_end = (int)tiles;
+  }
+  *total_tiles = (int)tiles;
+  return BITLUT_OK;
+}
+
+extern "C" int bitlut_mpgemv_batch(const bitlut_batch_mat* dev_mats, int n_mats, int total_tiles, int k, int bits,
+                                   int group_size, int scale_dtype, int flags, void* stream) {
+  if (!dev_mats || n_mats < 1 || total_tiles < 1) return BITLUT_EPARAM;
+  if (scale_dtype != BITLUT_DT_F32 && scale_dtype != BITLUT_DT_F16) return BITLUT_EPARAM;
+  if (!(flags & BITLUT_FLAG_FAST_EPILOGUE)) return BITLUT_EPARAM;
+  bl::LayoutV2 L;
+  const int rc = bl::make_layout(32, k, bits, group_size, &L);
+  if (rc) return rc;
+  if (L.n_sg != 1 || L.bits == 3 || L.U > 384) return BITLUT_ELAYOUT;
+  const bool pdl = (flags & BITLUT_FLAG_PDL) != 0;
+  GemvArgs g = {};
+  g.L = L;
+  g.independent = pdl && (flags & BITLUT_FLAG_INDEPENDENT) != 0;
+  g.fast = 1;
+  g.rows_per_cta = 1; g.n_rows = 1;
+  const cudaStream_t st = (cudaStream_t)stream;
+  return scale_dtype == BITLUT_DT_F16 ? dispatch_batch<__half>(g, dev_mats, n_mats, total_tiles, st, pdl)
+                                      : dispatch_batch<float>(g, dev_mats, n_mats, total_tiles, st, pdl);
+}
 
 // Internal entry used by bitlut_mpgemm_traced (gemv.cu) for batch-1 fast
 // calls: returns BITLUT_ELAYOUT when the shape does not fit the kernel's
@@ -1697,12 +1979,14 @@ extern "C" int bitlut_gather_wait(const unsigned* flag, unsigned target, void* s
 // no split-K): the op-list planner groups lookups with different tables only
 // for these (pipeline.cu).
 bool bl_mixed_tables_ok(const bl::LayoutV2& L) {
-  static int lean_env = -1;
+  static int lean_env = -1, mixed_env = -1;
   if (lean_env < 0) {
     const char* e = getenv("BITLUT_B1_LEAN");
     lean_env = e ? atoi(e) : 1;
+    const char* m = getenv("BITLUT_MIXED_TABLES");       // diagnostic: 0 = group same-table lookups only
+    mixed_env = m ? atoi(m) : 1;
   }
-  return lean_env != 0 && L.n_sg == 1 && L.U <= 384 && (size_t)L.KG * 16 <= 65536 && L.bits != 3;
+  return lean_env != 0 && mixed_env != 0 && L.n_sg == 1 && L.U <= 384 && (size_t)L.KG * 16 <= 65536 && L.bits != 3;
 }
 
 int bl_mpgemv_multi_tab_launch(const bitlut_mat_tab* mats, int n_mats, int k, int bits, int group_size,

@@ -153,6 +153,29 @@ __global__ void __launch_bounds__(kLutThreads) build_lut_multi_kernel(const __gr
   if (J.independent) bl::pdl_wait();
 }
 
+// ---- any number of table builds, job list in device memory ----
+template <int MODE, typename AT>
+__global__ void __launch_bounds__(kLutThreads)
+build_lut_batch_kernel(const bitlut_lut_job* __restrict__ jobs, const int* __restrict__ block_end, int n_jobs,
+                       int independent) {
+  __shared__ __align__(16) float sa[kLutThreads * 4];
+  __shared__ float red[kLutThreads / 32];
+  // job of this block = number of jobs ending at or before it
+  int j = 0;
+  for (int base = 0; base < n_jobs; base += kLutThreads) {
+    const int i = base + threadIdx.x;
+    j += __syncthreads_count(i < n_jobs && block_end[i] <= (int)blockIdx.x);
+  }
+  bl::pdl_launch_dependents();
+  if (!independent) bl::pdl_wait();
+  const bitlut_lut_job& jb = jobs[j];
+  const int b = blockIdx.x - (j ? block_end[j - 1] : 0);
+  const int bx = (jb.k / 4 + kLutThreads - 1) / kLutThreads;
+  lutk::lut_block<MODE, AT>(reinterpret_cast<const AT*>(jb.a), jb.k, jb.group_size, jb.tables, jb.tscales,
+                            jb.rowsums, b / bx, (b % bx) * kLutThreads, sa, red);
+  if (independent) bl::pdl_wait();
+}
+
 inline int grid_1d(int64_t n, int threads) {
   int64_t b = (n + threads - 1) / threads;
   const int64_t cap = 148 * 16 * 8;
@@ -296,5 +319,54 @@ int bl_build_lut_multi_launch(const bitlut_lut_job* jobs, int n_jobs, int mode, 
   else
     e = f16 ? cudaLaunchKernelEx(&cfg, build_lut_multi_kernel<BITLUT_TABLE_F16, __half>, J)
             : cudaLaunchKernelEx(&cfg, build_lut_multi_kernel<BITLUT_TABLE_F16, float>, J);
+  return e == cudaSuccess ? BITLUT_OK : BITLUT_EINTERNAL;
+}
+
+extern "C" int bitlut_build_lut_batch_encode(const bitlut_lut_job* jobs, int n_jobs, int* block_end,
+                                             int* total_blocks) {
+  if (!jobs || n_jobs < 1 || !block_end || !total_blocks) return BITLUT_EPARAM;
+  int64_t blocks = 0;
+  for (int i = 0; i < n_jobs; i++) {
+    const bitlut_lut_job& jb = jobs[i];
+    if (jb.a_dtype != jobs[0].a_dtype) return BITLUT_EPARAM;
+    if (jb.a_dtype != BITLUT_DT_F32 && jb.a_dtype != BITLUT_DT_F16) return BITLUT_EPARAM;
+    if (!jb.a || !jb.tables || !jb.rowsums) return BITLUT_EPARAM;
+    if (jb.n < 1 || jb.k < 4 || jb.group_size < 4) return BITLUT_EPARAM;
+    if (jb.k % jb.group_size != 0 || jb.group_size % 4 != 0) return BITLUT_ELAYOUT;
+    const int gpg = jb.group_size / 4;
+    if (gpg > 128 || (gpg & (gpg - 1))) return BITLUT_EPARAM;
+    blocks += (int64_t)((jb.k / 4 + kLutThreads - 1) / kLutThreads) * jb.n;
+    if (blocks > 0x7fffffff) return BITLUT_ESHAPE;
+    block_end[i] = (int)blocks;
+  }
+  *total_blocks = (int)blocks;
+  return BITLUT_OK;
+}
+
+extern "C" int bitlut_build_lut_batch(const bitlut_lut_job* dev_jobs, const int* dev_block_end, int n_jobs,
+                                      int total_blocks, int a_dtype, int mode, int flags, void* stream) {
+  if (!dev_jobs || !dev_block_end || n_jobs < 1 || total_blocks < 1) return BITLUT_EPARAM;
+  if (mode != BITLUT_TABLE_Q8 && mode != BITLUT_TABLE_F16) return BITLUT_EPARAM;
+  if (a_dtype != BITLUT_DT_F32 && a_dtype != BITLUT_DT_F16) return BITLUT_EPARAM;
+  const bool pdl = (flags & BITLUT_FLAG_PDL) != 0;
+  const int ind = (pdl && (flags & BITLUT_FLAG_INDEPENDENT)) ? 1 : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(total_blocks); cfg.blockDim = dim3(kLutThreads); cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr; cfg.numAttrs = 1;
+  const bool f16 = a_dtype == BITLUT_DT_F16;
+  cudaError_t e;
+  if (mode == BITLUT_TABLE_Q8)
+    e = f16 ? cudaLaunchKernelEx(&cfg, build_lut_batch_kernel<BITLUT_TABLE_Q8, __half>, dev_jobs, dev_block_end,
+                                 n_jobs, ind)
+            : cudaLaunchKernelEx(&cfg, build_lut_batch_kernel<BITLUT_TABLE_Q8, float>, dev_jobs, dev_block_end,
+                                 n_jobs, ind);
+  else
+    e = f16 ? cudaLaunchKernelEx(&cfg, build_lut_batch_kernel<BITLUT_TABLE_F16, __half>, dev_jobs, dev_block_end,
+                                 n_jobs, ind)
+            : cudaLaunchKernelEx(&cfg, build_lut_batch_kernel<BITLUT_TABLE_F16, float>, dev_jobs, dev_block_end,
+                                 n_jobs, ind);
   return e == cudaSuccess ? BITLUT_OK : BITLUT_EINTERNAL;
 }

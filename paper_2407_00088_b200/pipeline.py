@@ -8,6 +8,12 @@ replayed.  Two executors run the same list, bitwise identically to calling
   wait), captured into one CUDA graph; a replay is one graph launch.
 * ``"persistent"``: ONE cooperative launch; every CTA walks the op list and
   per-op completion counters replace kernel boundaries.
+* ``"batch"``: for op lists of INDEPENDENT batch-1 calls only (table builds
+  without dependencies, each lookup reading one of them, fast epilogue, int8
+  tables, no zero points: a layer set): every table build in one launch
+  (bitlut_build_lut_batch), then one lookup launch per K
+  (bitlut_mpgemv_batch, each CTA one contiguous tile range over all the
+  matrices); bitwise equal to the graph executor.
 
     pl = Pipeline()
     t = pl.tables(x, group_size=64)                     # op 0
@@ -77,7 +83,7 @@ class TableRef(OpRef):
 class Pipeline:
     """Records ops, then runs them in one persistent launch."""
 
-    EXECUTORS = ("graph", "persistent")
+    EXECUTORS = ("graph", "persistent", "batch")
     SYNCS = ("counters", "pdl")
 
     def __init__(self, device=None, executor: str = "graph", sync: str = "pdl"):
@@ -187,7 +193,9 @@ class Pipeline:
         if n == 0:
             raise ParameterError("empty pipeline")
         self._arr = (PipeOpSpec * n)(*self.specs)
-        if self.executor == "persistent":
+        if self.executor == "batch":
+            self._compile_batch()
+        elif self.executor == "persistent":
             nbytes = L.bitlut_pipeline_table_bytes(n)
             host = torch.empty(nbytes, dtype=torch.uint8)
             rc = L.bitlut_pipeline_encode(self._arr, n, ctypes.c_void_p(host.data_ptr()), nbytes)
@@ -210,6 +218,48 @@ class Pipeline:
             self._graph = g
         return self
 
+    def _compile_batch(self) -> None:
+        """Validate an independent op list and encode the batched launches."""
+        jobs, groups = [], {}
+        for i, s in enumerate(self.specs):
+            if s.type == OP_TABLES:
+                if any(d >= 0 for d in s.dep):
+                    raise ParameterError("batch executor: table builds must not depend on other ops")
+                j = N.BitlutLutJob()
+                j.a, j.a_dtype, j.n, j.k, j.group_size = s.a, s.a_dtype, s.n, s.k, s.group_size
+                j.tables, j.tscales, j.rowsums = s.tables, s.tscales, s.rowsums
+                jobs.append(j)
+                continue
+            if s.dep[0] < 0 or s.dep[1] >= 0 or s.dep[2] >= 0 or self.specs[s.dep[0]].type != OP_TABLES:
+                raise ParameterError("batch executor: each lookup must depend on exactly its table build")
+            if not (s.flags & N.FLAG_FAST_EPILOGUE) or s.n != 1 or s.zeros:
+                raise ParameterError("batch executor: batch-1 fast-epilogue lookups without zero points only")
+            m = N.BitlutBatchMat()
+            m.wgpu, m.wscales, m.out, m.m = s.wgpu, s.wscales, s.out, s.m
+            m.tables, m.tscales, m.rowsums = s.tables, s.tscales, s.rowsums
+            groups.setdefault((s.k, s.bits, s.group_size, s.scale_dtype), []).append(m)
+        if not jobs or len({j.a_dtype for j in jobs}) != 1:
+            raise ParameterError("batch executor: table builds of one activation dtype")
+        self._tbatch = N.TableBatch((N.BitlutLutJob * len(jobs))(*jobs), N.TABLE_Q8, self.device)
+        self._lbatches = [N.LookupBatch((N.BitlutBatchMat * len(ms))(*ms), k, bits, gs, sd, self.device)
+                          for (k, bits, gs, sd), ms in groups.items()]
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(side):
+            self._launch_batch(side)
+        side.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            self._launch_batch(side)
+        self._graph = g
+
+    def _launch_batch(self, stream: torch.cuda.Stream) -> None:
+        self._tbatch.launch(N.FLAG_PDL, stream)
+        for i, lb in enumerate(self._lbatches):
+            # the first lookup launch waits for the tables; later ones start
+            # after it passed that wait, so their tables are complete
+            lb.launch(N.FLAG_PDL | N.FLAG_FAST_EPILOGUE | (N.FLAG_INDEPENDENT if i else 0), stream)
+
     def _launch_ops(self, stream: torch.cuda.Stream) -> None:
         if self.sync == "counters":
             if self._counters is None:
@@ -227,6 +277,10 @@ class Pipeline:
         """Kernel launches per run (graph executor: launch units of the plan)."""
         if self.executor == "persistent":
             return 1
+        if self.executor == "batch":
+            if self._arr is None:
+                self.compile()
+            return 1 + len(self._lbatches)
         units = sum(1 for f in self.plan_flags() if f != -1 and not (f & N.PLAN_JOINED))
         return units + (1 if self.sync == "counters" else 0)      # + the join kernel
 
@@ -235,7 +289,7 @@ class Pipeline:
         if self._arr is None:
             self.compile()
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
-        if self.executor == "graph":
+        if self.executor in ("graph", "batch"):
             with torch.cuda.stream(st):
                 self._graph.replay()
             return
@@ -249,6 +303,11 @@ class Pipeline:
         """Graph executor without the graph: launch the op list directly."""
         if self._arr is None:
             self._arr = (PipeOpSpec * len(self.specs))(*self.specs)
+        if self.executor == "batch":
+            if self._graph is None:
+                self.compile()
+            self._launch_batch(stream if stream is not None else torch.cuda.current_stream(self.device))
+            return
         self._launch_ops(stream if stream is not None else torch.cuda.current_stream(self.device))
 
     @property
