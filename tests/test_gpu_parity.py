@@ -842,3 +842,54 @@ def test_multi_tab_launch_bitwise(bits, gs):
         for i, tx in enumerate((0, 0, 0, 1, 2, 2)):
             ref = B.mpgemm(xs[L][tx], pws[i], exact_epilogue=False)
             assert torch.equal(ys[L][i].reshape(ref.shape), ref), (L, i)
+
+
+@pytest.mark.parametrize("bits,gs,scale_dtype", [(2, 64, torch.float16), (4, 128, torch.float32),
+                                                 (1, 128, torch.float16)])
+def test_batch_executor_bitwise(bits, gs, scale_dtype):
+    """Pipeline(executor="batch"): every table build in one launch
+    (bitlut_build_lut_batch), one bitlut_mpgemv_batch launch per K over
+    device-resident descriptors; outputs == per-call mpgemm (fast epilogue)
+    bitwise, tables == bitlut_build_lut bitwise; matrices of several sizes,
+    two K values, more CTAs than tiles (tiny matrices); dependent op lists
+    rejected."""
+    from paper_2407_00088_b200 import _native as N
+    from paper_2407_00088_b200.pipeline import Pipeline
+    g = torch.Generator(device="cuda").manual_seed(bits * 7 + gs)
+    shapes = [(4096, 4096), (1024, 4096), (32, 4096), (2048, 2816), (64, 2816), (11008 // 32 * 32, 4096)]
+    pws = []
+    for m, k in shapes:
+        q = torch.randint(0, 1 << bits, (m, k), dtype=torch.uint8, device="cuda", generator=g)
+        sc = (torch.randn((m, k // gs), device="cuda", generator=g).abs() * 0.02 + 1e-3).to(scale_dtype)
+        pws.append(B.prepare_weights(B.QuantizedWeights(m=m, k=k, bits=bits, group_size=gs, qvalues=q, scales=sc)))
+    xs = [torch.randn((1, k), device="cuda", generator=g).half() for _, k in shapes]
+    pl = Pipeline(executor="batch")
+    ts = [pl.tables(x, gs) for x in xs]
+    ys = [pl.lookup(p, t, fast_epilogue=True) for p, t in zip(pws, ts)]
+    ys.append(pl.lookup(pws[0], ts[1] if shapes[1][1] == shapes[0][1] else ts[0], fast_epilogue=True))
+    for y in ys:
+        y.fill_(float("nan"))
+    pl.compile()
+    assert pl.n_launches() == 3
+    for _ in range(2):                                  # graph replay is repeatable
+        pl.run()
+        torch.cuda.synchronize()
+        for i, (x, p) in enumerate(zip(xs, pws)):
+            ref = B.mpgemm(x, p, exact_epilogue=False)
+            assert torch.equal(ys[i].reshape(ref.shape), ref), i
+            t_ref = N.build_lut(x, gs, N.TABLE_Q8)
+            for a, b in zip(ts[i].tensors, t_ref):
+                assert torch.equal(a, b), i
+        ref = B.mpgemm(xs[1], pws[0], exact_epilogue=False)
+        assert torch.equal(ys[-1].reshape(ref.shape), ref)
+    # dependencies between ops: not a batch
+    bad = Pipeline(executor="batch")
+    t0 = bad.tables(xs[0], gs)
+    y0 = bad.lookup(pws[0], t0, fast_epilogue=True)
+    bad.tables(xs[0], gs, deps=[bad.op_of(y0)])
+    with pytest.raises(B.ParameterError):
+        bad.compile()
+    exact = Pipeline(executor="batch")
+    exact.lookup(pws[0], exact.tables(xs[0], gs))
+    with pytest.raises(B.ParameterError):
+        exact.compile()
