@@ -749,18 +749,33 @@ def main():
     tabs = [{gname: N.build_lut(A[gname], gs, N.TABLE_Q8) for gname, _, _ in LUT_GROUPS}
             for A in acts]
     torch.cuda.synchronize()
-    g_look = capture(lambda: lookups_only(layers, tabs, fast=best_fast, chain=best.startswith("decode")),
-                     stream)
+    if best == "layer_set_batch_fast":
+        # the batch executor's lookup launches alone (its tables built by one
+        # eager run of the step)
+        pb = pipes[best][0]
+        pb.run(stream)
+        torch.cuda.synchronize()
+        g_look = capture(lambda: pb._launch_lookups(stream), stream)
+        n_look = len(pb._lbatches)
+    else:
+        g_look = capture(lambda: lookups_only(layers, tabs, fast=best_fast, chain=best.startswith("decode")),
+                         stream)
+        n_look = args.layers * len(LAYER)
     with torch.cuda.stream(stream):
         ms_look = time_graph(g_look, args.steps, args.warmup, barrier)
     del g_look
     local_bytes = sum(pw.packed_bytes for L in layers for pw in L.values())
-    n_look = args.layers * len(LAYER)
     peak, peak_src = load_peaks()
     if best.endswith("persistent_fast"):
         kernel_name, achieved = "pipeline_kernel (whole step, 1 launch)", value
         how = (f"1 persistent launch per step ({args.layers * 11} ops), algorithmic bytes = "
                f"sum bits*M*K/8 = {total_bytes} per launch, CUDA events over {args.steps} launches")
+    elif best == "layer_set_batch_fast":
+        kernel_name = "gemv_b1_batch_kernel"
+        achieved = local_bytes / (ms_look * 1e-3) / 1e9
+        how = (f"the step's {n_look} batched lookup launches (one per K: {args.layers} layers' q,k,v,o,gate,up "
+               f"and down; tables prebuilt, same flags) per graph replay, algorithmic bytes = sum bits*M*K/8 "
+               f"= {local_bytes} per replay, CUDA events over {args.steps} replays")
     else:
         kernel_name = "gemv_b1_lean_kernel" if best_fast else "gemv_kernel"
         achieved = local_bytes / (ms_look * 1e-3) / 1e9
@@ -812,10 +827,12 @@ def main():
         # the H2D of chunk c+1 and the D2H of chunk c-1 overlap the lookups of
         # chunk c (two copy streams + events)
         fast_best = "fast" in best
-        n_chunks = 8 if args.layers % 8 == 0 else 1
+        n_chunks = int(os.environ.get("BENCH_E2E_CHUNKS", "4"))
+        n_chunks = n_chunks if n_chunks > 0 and args.layers % n_chunks == 0 else 1
         per = args.layers // n_chunks
+        ex_best = "batch" if best == "layer_set_batch_fast" else "graph"
         chunks = [build_pipeline(layers[c * per:(c + 1) * per], acts[c * per:(c + 1) * per],
-                                 fast=fast_best, executor="graph", chain=best.startswith("decode"))
+                                 fast=fast_best, executor=ex_best, chain=best.startswith("decode"))
                   for c in range(n_chunks)]
         host_in = act_arena.cpu().pin_memory()
         per_act = act_arena.numel() // n_chunks
@@ -849,7 +866,7 @@ def main():
                "h2d_bytes_per_step": int(host_in.numel() * host_in.element_size()),
                "d2h_bytes_per_step": int(sum(h.numel() * h.element_size() for h in host_outs)),
                "ms_per_step": round(ms_e2e, 4),
-               "path": f"pinned host activations -> {n_chunks} x Pipeline(graph, {best}) -> pinned host "
+               "path": f"pinned host activations -> {n_chunks} x Pipeline({ex_best}, {best}) -> pinned host "
                        f"outputs ({args.layers} layers x 7 GEMVs; copies overlap neighbouring chunks), "
                        "CUDA events on the compute stream, which waits for the last D2H"}
     # the per-call drop-in API (reference kernel.py mpgemv: numpy in / numpy out)
@@ -904,7 +921,7 @@ def main():
             "config": cfg,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": load_traffic(), "kernel": kernel_name,
+                         "traffic": load_traffic(kernel_name), "kernel": kernel_name,
                          "peak_source": peak_src, "how": how},
             "executor": best,
             "executors": executors_out,
@@ -924,11 +941,20 @@ def main():
         dist.destroy_process_group()
 
 
-def load_traffic():
-    """ncu DRAM bytes (read + write) per lookup launch of the headline step:
-    the four grouped launches of one layer (profiles/r01d_step_gemv_b1_full.json,
-    one `ncu --set full` capture) summed and divided by the layer's 7 GEMVs,
-    the same per-launch unit as roofline.achieved."""
+def load_traffic(kernel="gemv_b1_lean_kernel"):
+    """ncu DRAM bytes (read + write) per launch of the headline's dominant
+    kernel, from one committed `ncu --set full` capture: the batch
+    executor's two lookup launches (profiles/r01h_batch_full.json, mean per
+    launch, the unit of roofline.achieved), or the graph executor's grouped
+    launches of one layer divided by its 7 GEMVs (r01g_step_gemv_b1_full.json)."""
+    if kernel == "gemv_b1_batch_kernel":
+        p = os.path.join(ROOT, "profiles", "r01h_batch_full.json")
+        if os.path.exists(p):
+            with open(p) as f:
+                d = json.load(f)
+            tot = sum(x["dram__bytes_read.sum"] + x["dram__bytes_write.sum"] for x in d["launches"])
+            return round(tot / len(d["launches"]), 1)
+        return None
     p = os.path.join(ROOT, "profiles", "r01g_step_gemv_b1_full.json")
     if os.path.exists(p):
         with open(p) as f:

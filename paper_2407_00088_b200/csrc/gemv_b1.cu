@@ -919,7 +919,7 @@ __global__ void __launch_bounds__(384) gemv_b1_batch_kernel(const __grid_constan
     const uint64_t pol = policy_evict_first();
     ji_begin = ji ? dm[ji - 1].tile_end : 0;
     ji_end = dm[ji].tile_end;
-    for (int s = 0; s < 2; s++) {
+    for (int s = 0; s < a.stages; s++) {
       const int t = t0 + s;
       if (t >= t1) break;
       while (t >= ji_end) { ji++; ji_begin = ji_end; ji_end = dm[ji].tile_end; }
@@ -957,9 +957,10 @@ __global__ void __launch_bounds__(384) gemv_b1_batch_kernel(const __grid_constan
       outp = dm[jc].out;
       load_tables(dm[jc]);
     }
-    const int stage = it & 1;
+    const int S = a.stages;
+    const int stage = S == 1 ? 0 : (it & 1);
     uint8_t* sb = smem + stage * a.stage_bytes;
-    mbar_wait(bar + stage, (it >> 1) & 1);
+    mbar_wait(bar + stage, (S == 1 ? it : it >> 1) & 1);
     float y[NCH];
     int acc[NACC];
 #pragma unroll
@@ -1004,7 +1005,7 @@ __global__ void __launch_bounds__(384) gemv_b1_batch_kernel(const __grid_constan
     for (int j = 0; j < NF; j++) yb[ch0 + fb + j] = y[j];
     __syncthreads();                                    // stage consumed, ysm complete
     if (tid == 0) {
-      const int t = tile + 2;
+      const int t = tile + S;
       if (t < t1) {
         while (t >= ji_end) { ji++; ji_begin = ji_end; ji_end = dm[ji].tile_end; }
         issue_stage_batch(a, dm[ji], t - ji_begin, sb, bar + stage, policy_evict_first(), (int)sizeof(ST));
@@ -1678,11 +1679,27 @@ int launch_batch(const GemvArgs& g, const bitlut_batch_mat* dm, int n_mats, int 
       return BITLUT_EINTERNAL;
     configured = true;
   }
-  const B1Plan s = b1_plan<ST>(L, false, false, T, 2, kFast);
-  if (s.total > 227 * 1024) return BITLUT_ELAYOUT;
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, s.total) != cudaSuccess || per_sm < 1)
-    return BITLUT_ELAYOUT;
+  // stages: two (double-buffered CTAs), or one when double buffering
+  // leaves <= 2 CTAs per SM and one stage fits twice as many (long K)
+  static int st_env = -1;
+  if (st_env < 0) {
+    const char* e = getenv("BITLUT_BATCH_STAGES");       // diagnostic: force 1 or 2
+    st_env = e ? atoi(e) : 0;
+  }
+  int per_sm = 0, per_sm1 = 0;
+  const B1Plan s2 = b1_plan<ST>(L, false, false, T, 2, kFast);
+  const B1Plan s1 = b1_plan<ST>(L, false, false, T, 1, kFast);
+  if (s2.total > 227 * 1024 ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, s2.total) != cudaSuccess)
+    per_sm = 0;
+  if (s1.total > 227 * 1024 ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm1, kern, T, s1.total) != cudaSuccess)
+    per_sm1 = 0;
+  int stages = 2;
+  if (st_env == 1 || (st_env == 0 && per_sm <= 2 && per_sm1 >= 2 * per_sm) || per_sm < 1) stages = 1;
+  if (stages == 1) per_sm = per_sm1;
+  if (per_sm < 1) return BITLUT_ELAYOUT;
+  const B1Plan s = stages == 2 ? s2 : s1;
   B1Args a;
   a.g = g;
   a.act = nullptr;
@@ -1691,7 +1708,7 @@ int launch_batch(const GemvArgs& g, const bitlut_batch_mat* dm, int n_mats, int 
   a.total_tiles = total_tiles;
   a.rounds = 1; a.tab_smem = 0; a.ldg_w = 0; a.partition = 0;
   a.n_rows = 1; a.rows_per_cta = 1;
-  a.stages = 2;
+  a.stages = stages;
   a.stage_bytes = s.stage_bytes; a.w_bytes = s.w_bytes; a.s_off = s.s_off; a.s_bytes = s.s_bytes;
   a.z_off = s.z_off; a.tab_off = s.tab_off; a.ts_off = s.ts_off; a.rs_off = s.rs_off;
   a.y_off = s.y_off; a.bar_off = s.bar_off; a.sa_off = s.sa_off; a.red_off = s.red_off;

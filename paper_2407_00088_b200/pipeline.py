@@ -255,6 +255,11 @@ class Pipeline:
 
     def _launch_batch(self, stream: torch.cuda.Stream) -> None:
         self._tbatch.launch(N.FLAG_PDL, stream)
+        self._launch_lookups(stream)
+
+    def _launch_lookups(self, stream: torch.cuda.Stream) -> None:
+        """The batch executor's lookup launches only (diagnostic: the tables
+        must be built already)."""
         for i, lb in enumerate(self._lbatches):
             # the first lookup launch waits for the tables; later ones start
             # after it passed that wait, so their tables are complete
