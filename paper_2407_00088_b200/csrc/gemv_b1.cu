@@ -1686,9 +1686,25 @@ int launch_batch(const GemvArgs& g, const bitlut_batch_mat* dm, int n_mats, int 
     const char* e = getenv("BITLUT_BATCH_STAGES");       // diagnostic: force 1 or 2
     st_env = e ? atoi(e) : 0;
   }
+  static int trim_env = -1;
+  if (trim_env < 0) {
+    const char* e = getenv("BITLUT_BATCH_TRIM");         // diagnostic: 0 keeps the lean plan's smem
+    trim_env = e ? atoi(e) : 1;
+  }
+  // the batch kernel keeps table scale and row sum in registers: its plan is
+  // the stages, the cross-warp sums and the barriers (K = 4096 W2: 37.9 ->
+  // 36.5 KB, six CTAs per SM instead of five)
+  auto trim = [&](B1Plan p) {
+    if (!trim_env) return p;
+    p.ts_off = p.rs_off = p.y_off = p.tab_off;
+    p.sa_off = p.y_off + al16((size_t)2 * (T / 32) * L.tile_ch * 4);
+    p.red_off = p.psm_off = p.terms_off = p.fin_off = p.bar_off = p.sa_off;
+    p.total = p.bar_off + 8 * (kMaxStages + 1);
+    return p;
+  };
   int per_sm = 0, per_sm1 = 0;
-  const B1Plan s2 = b1_plan<ST>(L, false, false, T, 2, kFast);
-  const B1Plan s1 = b1_plan<ST>(L, false, false, T, 1, kFast);
+  const B1Plan s2 = trim(b1_plan<ST>(L, false, false, T, 2, kFast));
+  const B1Plan s1 = trim(b1_plan<ST>(L, false, false, T, 1, kFast));
   if (s2.total > 227 * 1024 ||
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, s2.total) != cudaSuccess)
     per_sm = 0;
