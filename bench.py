@@ -715,15 +715,17 @@ def main():
             # tensor-parallel: each rank runs the layer set on its output-channel
             # shards (the same op list as N = 1), then one NCCL all-gather of the
             # step's output arena; the decode chain gathers after every GEMV
-            for fast in (True, False):
-                pl, outs, out_arena = build_pipeline(layers, acts, fast=fast, executor="graph", chain=False)
+            for name, ex, fast in (("layer_set_batch_fast", "batch", True),
+                                   ("layer_set_graph_fast", "graph", True),
+                                   ("layer_set_graph_exact", "graph", False)):
+                pl, outs, out_arena = build_pipeline(layers, acts, fast=fast, executor=ex, chain=False)
                 gathered = torch.empty((world * out_arena.numel(),), dtype=out_arena.dtype, device=device)
+                pipes[name] = (pl, out_arena)
 
                 def ls_step(pl=pl, out_arena=out_arena, gathered=gathered):
                     pl.run(stream)                 # one graph launch
                     dist.all_gather_into_tensor(gathered, out_arena, group=group)
-                executors["layer_set_graph_" + ("fast" if fast else "exact")] = {
-                    "ms": time_runs(ls_step), "launches": pl.n_launches() + 1}
+                executors[name] = {"ms": time_runs(ls_step), "launches": pl.n_launches() + 1}
             for fast in (True, False):
                 g_step = capture(lambda: step_fn(layers, acts, world, group, fast=fast), stream)
                 executors["decode_chain_graph_" + ("fast" if fast else "exact")] = {
