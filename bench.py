@@ -179,24 +179,27 @@ def step_fn(layers, acts, world, group, fast=False):
     return res
 
 
-def build_pipeline(layers, acts, fast=False, executor="persistent", chain=True, sync="pdl", lookahead=None):
+def build_pipeline(layers, acts, fast=False, executor="persistent", chain=True, sync="pdl", lookahead=None,
+                   groups=None):
     """The step as a pipeline.Pipeline op list.  chain=True: the decode
     chain's dependencies -- a layer's qkv table build waits for the previous
     layer's down GEMV, o's for q,k,v, gate/up's for o, down's for gate,up.
     chain=False: the layer set as independent mpGEMV calls (activation rows
     are inputs; BASELINE configs[1]).  Either way every GEMV waits for its
     own table build.  All outputs are views of one f32 arena (one D2H per
-    step).  Returns (pipeline, outputs, out_arena)."""
+    step).  groups: the LUT_GROUPS names to include (layer set only;
+    default all).  Returns (pipeline, outputs, out_arena)."""
     import torch
     from paper_2407_00088_b200.pipeline import Pipeline
+    lut_groups = [gr for gr in LUT_GROUPS if groups is None or gr[0] in groups]
     pl = Pipeline(executor=executor, sync=sync)
-    per_layer = sum(pw.m for pw in layers[0].values())
+    per_layer = sum(layers[0][nm].m for _, _, names in lut_groups for nm in names)
     out_arena = torch.empty((len(layers) * per_layer,), dtype=torch.float32,
                             device=layers[0]["q"].gpu.device)
     prev, outs, off = [], [], 0
     if chain:
         for L, A in zip(layers, acts):
-            for gname, k, names in LUT_GROUPS:
+            for gname, k, names in lut_groups:
                 t = pl.tables(A[gname], L[names[0]].group_size, deps=prev)
                 ys = []
                 for nm in names:
@@ -216,14 +219,14 @@ def build_pipeline(layers, acts, fast=False, executor="persistent", chain=True, 
 
         def tables_of(i):
             return {g: pl.tables(acts[i][g], layers[i][names[0]].group_size)
-                    for g, _, names in LUT_GROUPS}
+                    for g, _, names in lut_groups}
         tabs = {}
         for i in range(D):
             tabs[i] = tables_of(i)
         for i, L in enumerate(layers):
             if i + D < len(layers):
                 tabs[i + D] = tables_of(i + D)
-            for gname, k, names in LUT_GROUPS:
+            for gname, k, names in lut_groups:
                 for nm in names:
                     m = L[nm].m
                     outs.append(pl.lookup(L[nm], tabs[i][gname], fast_epilogue=fast,
@@ -829,47 +832,107 @@ def main():
         # the H2D of chunk c+1 and the D2H of chunk c-1 overlap the lookups of
         # chunk c (two copy streams + events)
         fast_best = "fast" in best
-        n_chunks = int(os.environ.get("BENCH_E2E_CHUNKS", "4"))
-        n_chunks = n_chunks if n_chunks > 0 and args.layers % n_chunks == 0 else 1
-        per = args.layers // n_chunks
-        ex_best = "batch" if best == "layer_set_batch_fast" else "graph"
-        chunks = [build_pipeline(layers[c * per:(c + 1) * per], acts[c * per:(c + 1) * per],
-                                 fast=fast_best, executor=ex_best, chain=best.startswith("decode"))
-                  for c in range(n_chunks)]
-        host_in = act_arena.cpu().pin_memory()
-        per_act = act_arena.numel() // n_chunks
-        host_outs = [torch.empty(ch[2].shape, dtype=ch[2].dtype).pin_memory() for ch in chunks]
-        in_stream, out_stream = torch.cuda.Stream(device), torch.cuda.Stream(device)
-        ev_start, ev_out = torch.cuda.Event(), torch.cuda.Event()
-        ev_in = [torch.cuda.Event() for _ in chunks]
-        ev_done = [torch.cuda.Event() for _ in chunks]
+        ksplit = best == "layer_set_batch_fast" and os.environ.get("BENCH_E2E_MODE", "layers") == "ksplit"
+        if ksplit:
+            # batch executor: the step as two Pipelines by input width -- every
+            # layer's q,k,v,o,gate,up (K = 4096), then every down (K = 11008).
+            # Inputs in two pinned host arenas; the D2H of the first part's
+            # outputs overlaps the down lookups, only the down outputs' D2H
+            # (0.5 MB) trails the compute.
+            kA = sum(k for g_, k, _ in LUT_GROUPS if g_ != "down")
+            kB = sum(k for g_, k, _ in LUT_GROUPS if g_ == "down")
+            dev_in = [torch.empty((args.layers * kA,), dtype=act_arena.dtype, device=device),
+                      torch.empty((args.layers * kB,), dtype=act_arena.dtype, device=device)]
+            acts_e2e = []
+            for i, A in enumerate(acts):
+                d, offA = {}, i * kA
+                for g_, k, _ in LUT_GROUPS:
+                    if g_ == "down":
+                        d[g_] = dev_in[1][i * kB:(i + 1) * kB].view(1, kB)
+                    else:
+                        d[g_] = dev_in[0][offA:offA + k].view(1, k)
+                        offA += k
+                    d[g_].copy_(A[g_])
+                acts_e2e.append(d)
+            parts = [build_pipeline(layers, acts_e2e, fast=True, executor="batch", chain=False,
+                                    groups=[g_ for g_, _, _ in LUT_GROUPS if g_ != "down"]),
+                     build_pipeline(layers, acts_e2e, fast=True, executor="batch", chain=False, groups=["down"])]
+            host_ins = [t.cpu().pin_memory() for t in dev_in]
+            host_outs = [torch.empty(p_[2].shape, dtype=p_[2].dtype).pin_memory() for p_ in parts]
+            in_stream, out_stream = torch.cuda.Stream(device), torch.cuda.Stream(device)
+            ev_start, ev_out = torch.cuda.Event(), torch.cuda.Event()
+            ev_in = [torch.cuda.Event() for _ in parts]
+            ev_done = [torch.cuda.Event() for _ in parts]
+            chunks = parts
+            host_in_bytes = sum(h.numel() * h.element_size() for h in host_ins)
 
-        def e2e_step():
-            ev_start.record(stream)                              # time_runs' events are on `stream`
-            in_stream.wait_event(ev_start)
-            with torch.cuda.stream(in_stream):                   # H2D of chunk c+1 overlaps chunk c
-                for c in range(n_chunks):
-                    act_arena[c * per_act:(c + 1) * per_act].copy_(host_in[c * per_act:(c + 1) * per_act],
-                                                                   non_blocking=True)
-                    ev_in[c].record(in_stream)
-            for c, (pl_c, _, arena_c) in enumerate(chunks):
-                stream.wait_event(ev_in[c])
-                pl_c.run(stream)
-                ev_done[c].record(stream)
-                out_stream.wait_event(ev_done[c])
-                with torch.cuda.stream(out_stream):              # D2H of chunk c overlaps chunk c+1
-                    host_outs[c].copy_(arena_c, non_blocking=True)
-            ev_out.record(out_stream)
-            stream.wait_event(ev_out)                            # the step ends when the last D2H does
+            def e2e_step():
+                ev_start.record(stream)
+                in_stream.wait_event(ev_start)
+                with torch.cuda.stream(in_stream):
+                    for c in range(2):
+                        dev_in[c].copy_(host_ins[c], non_blocking=True)
+                        ev_in[c].record(in_stream)
+                for c, (pl_c, _, arena_c) in enumerate(parts):
+                    stream.wait_event(ev_in[c])
+                    pl_c.run(stream)
+                    ev_done[c].record(stream)
+                    out_stream.wait_event(ev_done[c])
+                    with torch.cuda.stream(out_stream):          # D2H of part 0 overlaps part 1
+                        host_outs[c].copy_(arena_c, non_blocking=True)
+                ev_out.record(out_stream)
+                stream.wait_event(ev_out)
+            split, ex_best, n_chunks = "by K (4096 | 11008)", "batch", 2
+        else:
+            # chunk sizes in layers (BENCH_E2E_SPLIT, comma list summing to
+            # --layers): four equal chunks measured best -- the f32 outputs' D2H
+            # (5.4 MB, ~30 GB/s) must overlap the lookups, and every chunk
+            # boundary costs a drain (1,3,8,8,8,3,1: 0.433 ms; 8,8,8,8: 0.416-0.430;
+            # by K, BENCH_E2E_MODE=ksplit: 0.426)
+            split = [int(x) for x in os.environ.get("BENCH_E2E_SPLIT", "8,8,8,8").split(",") if x]
+            if sum(split) != args.layers or min(split) < 1:
+                split = [args.layers]
+            bounds = [sum(split[:c]) for c in range(len(split) + 1)]
+            n_chunks = len(split)
+            ex_best = "batch" if best == "layer_set_batch_fast" else "graph"
+            chunks = [build_pipeline(layers[bounds[c]:bounds[c + 1]], acts[bounds[c]:bounds[c + 1]],
+                                     fast=fast_best, executor=ex_best, chain=best.startswith("decode"))
+                      for c in range(n_chunks)]
+            host_in = act_arena.cpu().pin_memory()
+            host_in_bytes = host_in.numel() * host_in.element_size()
+            per_layer_act = act_arena.numel() // args.layers
+            host_outs = [torch.empty(ch[2].shape, dtype=ch[2].dtype).pin_memory() for ch in chunks]
+            in_stream, out_stream = torch.cuda.Stream(device), torch.cuda.Stream(device)
+            ev_start, ev_out = torch.cuda.Event(), torch.cuda.Event()
+            ev_in = [torch.cuda.Event() for _ in chunks]
+            ev_done = [torch.cuda.Event() for _ in chunks]
+
+            def e2e_step():
+                ev_start.record(stream)                              # time_runs' events are on `stream`
+                in_stream.wait_event(ev_start)
+                with torch.cuda.stream(in_stream):                   # H2D of chunk c+1 overlaps chunk c
+                    for c in range(n_chunks):
+                        lo, hi = bounds[c] * per_layer_act, bounds[c + 1] * per_layer_act
+                        act_arena[lo:hi].copy_(host_in[lo:hi], non_blocking=True)
+                        ev_in[c].record(in_stream)
+                for c, (pl_c, _, arena_c) in enumerate(chunks):
+                    stream.wait_event(ev_in[c])
+                    pl_c.run(stream)
+                    ev_done[c].record(stream)
+                    out_stream.wait_event(ev_done[c])
+                    with torch.cuda.stream(out_stream):              # D2H of chunk c overlaps chunk c+1
+                        host_outs[c].copy_(arena_c, non_blocking=True)
+                ev_out.record(out_stream)
+                stream.wait_event(ev_out)                            # the step ends when the last D2H does
         ms_e2e = time_runs(e2e_step)
         for c, (_, _, arena_c) in enumerate(chunks):             # the bytes really arrived
             assert torch.equal(host_outs[c], arena_c.cpu())
         e2e = {"value": round(total_bytes / (ms_e2e * 1e-3) / 1e9, 2), "unit": "GB/s",
-               "h2d_bytes_per_step": int(host_in.numel() * host_in.element_size()),
+               "h2d_bytes_per_step": int(host_in_bytes),
                "d2h_bytes_per_step": int(sum(h.numel() * h.element_size() for h in host_outs)),
                "ms_per_step": round(ms_e2e, 4),
-               "path": f"pinned host activations -> {n_chunks} x Pipeline({ex_best}, {best}) -> pinned host "
-                       f"outputs ({args.layers} layers x 7 GEMVs; copies overlap neighbouring chunks), "
+               "path": f"pinned host activations -> {n_chunks} x Pipeline({ex_best}, {best}) (split {split}) -> "
+                       f"pinned host outputs ({args.layers} layers x 7 GEMVs; copies overlap neighbouring chunks), "
                        "CUDA events on the compute stream, which waits for the last D2H"}
     # the per-call drop-in API (reference kernel.py mpgemv: numpy in / numpy out)
     per_call = None
