@@ -637,6 +637,7 @@ def main():
     ap.add_argument("--no-shapes", action="store_true")
     ap.add_argument("--no-gemm", action="store_true")
     ap.add_argument("--no-70b", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     bits, gs = 2, 64
@@ -801,6 +802,36 @@ def main():
             per_shape = per_shape_table(device, stream, max(5, args.steps // 4), args.warmup, barrier,
                                         peak, world)
         per_shape["clocks"] = clk_shapes.summary()
+
+    # ---- the same layer set through the batch executor at W4 g128 and W1
+    #      g128 (north star: >= 70 % of HBM peak for W4/W2/W1 7B shapes at
+    #      batch 1); step = table launch + lookup launches, CUDA events ----
+    bits_sweep = None
+    if not args.no_sweep and world == 1:
+        bits_sweep = {}
+        with ClockSampler(local) as clk_sw:
+            for b_, gs_ in ((4, 128), (1, 128)):
+                L_ = build_layers(args.layers, b_, gs_, rank, world, device, seed=20251020 + b_)
+                pl_, _, _ = build_pipeline(L_, acts, fast=True, executor="batch", chain=False)
+                ms_ = time_runs(lambda: pl_.run(stream))
+                pl_.run(stream)
+                torch.cuda.synchronize()
+                g_ = capture(lambda: pl_._launch_lookups(stream), stream)
+                with torch.cuda.stream(stream):
+                    msl_ = time_graph(g_, args.steps, args.warmup, barrier)
+                bytes_ = packed_bytes_full(args.layers, b_)
+                bits_sweep[f"W{b_}_g{gs_}"] = {
+                    "packed_bytes_per_step": bytes_, "ms_per_step": round(ms_, 5),
+                    "GBps": round(bytes_ / (ms_ * 1e-3) / 1e9, 1),
+                    "frac_of_peak": round(bytes_ / (ms_ * 1e-3) / 1e9 / peak, 4),
+                    "lookups_only_ms": round(msl_, 5),
+                    "lookups_only_GBps": round(bytes_ / (msl_ * 1e-3) / 1e9, 1),
+                    "lookups_only_frac_of_peak": round(bytes_ / (msl_ * 1e-3) / 1e9 / peak, 4),
+                    "launches_per_step": pl_.n_launches()}
+                del g_, pl_, L_
+                torch.cuda.synchronize()
+                torch.cuda.empty_cache()
+        bits_sweep["clocks"] = clk_sw.summary()
 
     # ---- BASELINE configs[0]: single W4 mpGEMV, zeros, fp16 tables ----
     cfg1 = None
@@ -991,6 +1022,7 @@ def main():
             "executor": best,
             "executors": executors_out,
             "lookups_only_graph": lookups_graph,
+            "layer_set_bits_sweep": bits_sweep,
             "per_shape": per_shape,
             "config1_single_mpgemv": cfg1,
             "mpgemm_prefill": gemm,
