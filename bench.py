@@ -624,6 +624,35 @@ def cpu_info():
 
 # ----------------------------------------------------------------- main
 
+def details_path(arg):
+    """Where the detail sections go: --details, else gpurun_out/ when it
+    exists (it travels back from the GPU box), else next to bench.py."""
+    if arg:
+        return arg
+    d = os.path.join(ROOT, "gpurun_out")
+    return os.path.join(d if os.path.isdir(d) else ROOT, "bench_details.json")
+
+
+def emit(line, details, path):
+    """Detail sections to a side file; ONE compact JSON line (< 2 KB) last on
+    stdout, so a driver that keeps only the tail of stdout parses it."""
+    if details is not None:
+        try:
+            with open(path, "w") as f:
+                json.dump(details, f, indent=1)
+            line["details_file"] = os.path.relpath(path, ROOT)
+        except OSError:
+            pass
+    s = json.dumps(line, separators=(",", ":"))
+    for drop in ("summary", "details_file"):
+        if len(s) <= 2000:
+            break
+        line.pop(drop, None)
+        s = json.dumps(line, separators=(",", ":"))
+    sys.stdout.flush()
+    print(s, flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -631,13 +660,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--layers", type=int, default=32)
-    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--cpu-budget", type=float, default=6.0)
+    ap.add_argument("--full", action="store_true",
+                    help="also run the detail sections (per-shape, configs[0], 70B shards, prefill "
+                         "mpGEMM, every executor) into the details file")
+    ap.add_argument("--details", default=None, help="path of the details JSON (default gpurun_out/ or ./)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-shapes", action="store_true")
-    ap.add_argument("--no-gemm", action="store_true")
-    ap.add_argument("--no-70b", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--ref-min-seconds", type=float, default=3.0,
+                    help="reference arm: minimum timed region (s)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     bits, gs = 2, 64
@@ -670,18 +702,10 @@ def main():
     layers = build_layers(args.layers, bits, gs, rank, world, device)
     acts, act_arena = make_acts(args.layers, device)
     stream = torch.cuda.Stream(device)
-
-    # ---- the step through the package's op-list executors (pipeline.py).
-    #      layer_set: the 7 GEMVs per layer as independent mpGEMV calls (the
-    #      BASELINE metric); decode_chain: each table build also waits for the
-    #      previous GEMVs, as in a real decode.  "graph" = per-op kernels
-    #      chained with PDL in one CUDA graph; "persistent" = one cooperative
-    #      launch.  fast = exact int32 sums + fixed-order parallel fp32
-    #      epilogue (<= 1e-5 of the reference); exact = the reference's fp32
-    #      order, bitwise.  `value` = the fastest layer_set executor. ----
+    peak, peak_src = load_peaks()
     total_bytes = packed_bytes_full(args.layers, bits)
-    n_ops = args.layers * (len(LUT_GROUPS) + len(LAYER))
-    executors = {}
+    details = {"config": cfg}
+    summary = {}
 
     def time_runs(run, steps=None):
         steps = steps or args.steps
@@ -691,417 +715,400 @@ def main():
             torch.cuda.synchronize()
             if barrier:
                 barrier()
+            torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             for _ in range(steps):
                 run()
             e1.record(stream)
             torch.cuda.synchronize()
-        return e0.elapsed_time(e1) / steps
-
-    pipes = {}
-    with ClockSampler(local) as clk:
-        if world == 1:
-            for name, ex, fast, chain, sync in (
-                    ("layer_set_batch_fast", "batch", True, False, "pdl"),
-                    ("layer_set_graph_fast", "graph", True, False, "pdl"),
-                    ("layer_set_graph_exact", "graph", False, False, "pdl"),
-                    ("layer_set_graph_fast_counters", "graph", True, False, "counters"),
-                    ("decode_chain_graph_fast", "graph", True, True, "pdl"),
-                    ("decode_chain_graph_exact", "graph", False, True, "pdl"),
-                    ("decode_chain_graph_fast_counters", "graph", True, True, "counters"),
-                    ("decode_chain_persistent_fast", "persistent", True, True, "pdl")):
-                pl, outs, out_arena = build_pipeline(layers, acts, fast=fast, executor=ex, chain=chain,
-                                                     sync=sync)
-                pipes[name] = (pl, out_arena)
-                executors[name] = {"ms": time_runs(lambda: pl.run(stream)), "launches": pl.n_launches()}
-        else:
-            # tensor-parallel: each rank runs the layer set on its output-channel
-            # shards (the same op list as N = 1), then one NCCL all-gather of the
-            # step's output arena; the decode chain gathers after every GEMV
-            for name, ex, fast in (("layer_set_batch_fast", "batch", True),
-                                   ("layer_set_graph_fast", "graph", True),
-                                   ("layer_set_graph_exact", "graph", False)):
-                pl, outs, out_arena = build_pipeline(layers, acts, fast=fast, executor=ex, chain=False)
-                gathered = torch.empty((world * out_arena.numel(),), dtype=out_arena.dtype, device=device)
-                pipes[name] = (pl, out_arena)
-
-                def ls_step(pl=pl, out_arena=out_arena, gathered=gathered):
-                    pl.run(stream)                 # one graph launch
-                    dist.all_gather_into_tensor(gathered, out_arena, group=group)
-                executors[name] = {"ms": time_runs(ls_step), "launches": pl.n_launches() + 1}
-            for fast in (True, False):
-                g_step = capture(lambda: step_fn(layers, acts, world, group, fast=fast), stream)
-                executors["decode_chain_graph_" + ("fast" if fast else "exact")] = {
-                    "ms": time_runs(g_step.replay), "launches": n_ops}
-                del g_step
-    if world > 1:
-        for v in executors.values():
-            t = torch.tensor([v["ms"]], device=device)
+            if barrier:
+                barrier()
+        ms = e0.elapsed_time(e1) / steps
+        if world > 1:                                   # max over ranks
+            t = torch.tensor([ms], device=device)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            v["ms"] = float(t.item())
-    cands = [k for k in executors if k.startswith("layer_set")] or list(executors)
-    best = min(cands, key=lambda k: executors[k]["ms"])
+            ms = float(t.item())
+        return ms
+
+    # ---- the step through the package's op-list executors (pipeline.py).
+    #      layer_set: the 7 GEMVs per layer as independent mpGEMV calls (the
+    #      BASELINE metric); decode_chain: each table build also waits for the
+    #      previous GEMVs, as in a real decode.  `value` = the batch executor
+    #      (one table launch + one lookup launch per K). ----
+    executors, pipes = {}, {}
+    runs = [("layer_set_batch_fast", "batch", True, False, "pdl"),
+            ("decode_chain_graph_fast", "graph", True, True, "pdl")]
+    if args.full:
+        runs += [("layer_set_graph_fast", "graph", True, False, "pdl"),
+                 ("layer_set_graph_exact", "graph", False, False, "pdl"),
+                 ("decode_chain_graph_exact", "graph", False, True, "pdl")]
+    if world > 1:
+        runs = [r for r in runs if not r[3]]            # the decode chain gathers per GEMV: details only
+    gathered = {}
+    with ClockSampler(local) as clk:
+        for name, ex, fast, chain, sync in runs:
+            pl, outs, out_arena = build_pipeline(layers, acts, fast=fast, executor=ex, chain=chain, sync=sync)
+            pipes[name] = (pl, out_arena)
+            if world == 1:
+                executors[name] = {"ms": time_runs(lambda: pl.run(stream)), "launches": pl.n_launches()}
+                continue
+            # tensor parallel: the rank's shard of the layer set, then ONE
+            # NCCL all-gather of the step's output arena (one collective per
+            # step); compute-only and collective-only timed apart as well
+            gat = torch.empty((world * out_arena.numel(),), dtype=out_arena.dtype, device=device)
+            gathered[name] = gat
+
+            def ls_step(pl=pl, out_arena=out_arena, gat=gat):
+                pl.run(stream)
+                dist.all_gather_into_tensor(gat, out_arena, group=group)
+
+            def coll_only(out_arena=out_arena, gat=gat):
+                dist.all_gather_into_tensor(gat, out_arena, group=group)
+            executors[name] = {"ms": time_runs(ls_step), "launches": pl.n_launches(),
+                               "compute_only_ms": time_runs(lambda pl=pl: pl.run(stream)),
+                               "collective_only_ms": time_runs(coll_only),
+                               "gather_bytes_per_rank": out_arena.numel() * out_arena.element_size()}
+    best = "layer_set_batch_fast"
     ms_step = executors[best]["ms"]
     launches_per_step = executors[best]["launches"]
     value = total_bytes / (ms_step * 1e-3) / 1e9
-    executors_out = {k: {"ms_per_step": round(v["ms"], 5),
-                         "GBps": round(total_bytes / (v["ms"] * 1e-3) / 1e9, 2),
-                         "launches_per_step": v["launches"]} for k, v in executors.items()}
-    best_fast = "fast" in best
+    details["executors"] = {k: dict({kk: (round(vv, 5) if isinstance(vv, float) else vv)
+                                     for kk, vv in v.items()},
+                                    GBps=round(total_bytes / (v["ms"] * 1e-3) / 1e9, 2))
+                            for k, v in executors.items()}
+    if "decode_chain_graph_fast" in executors:
+        summary["decode_chain_ms"] = round(executors["decode_chain_graph_fast"]["ms"], 4)
+    if world > 1:
+        summary["compute_only_ms"] = round(executors[best]["compute_only_ms"], 4)
+        summary["collective_only_ms"] = round(executors[best]["collective_only_ms"], 4)
 
-    # ---- the dominant kernel alone: the step's lookups (tables prebuilt,
-    #      same flags and epilogue as the headline executor) ----
-    tabs = [{gname: N.build_lut(A[gname], gs, N.TABLE_Q8) for gname, _, _ in LUT_GROUPS}
-            for A in acts]
+    # ---- the dominant kernel alone: the batch executor's lookup launches
+    #      (tables built by one eager run of the step), same flags ----
+    pb = pipes[best][0]
+    pb.run(stream)
     torch.cuda.synchronize()
-    if best == "layer_set_batch_fast":
-        # the batch executor's lookup launches alone (its tables built by one
-        # eager run of the step)
-        pb = pipes[best][0]
-        pb.run(stream)
-        torch.cuda.synchronize()
-        g_look = capture(lambda: pb._launch_lookups(stream), stream)
-        n_look = len(pb._lbatches)
-    else:
-        g_look = capture(lambda: lookups_only(layers, tabs, fast=best_fast, chain=best.startswith("decode")),
-                         stream)
-        n_look = args.layers * len(LAYER)
-    with torch.cuda.stream(stream):
-        ms_look = time_graph(g_look, args.steps, args.warmup, barrier)
+    g_look = capture(lambda: pb._launch_lookups(stream), stream)
+    n_look = len(pb._lbatches)
+    ms_look = time_graph_max(g_look, args.steps, args.warmup, barrier, stream, world, device)
     del g_look
     local_bytes = sum(pw.packed_bytes for L in layers for pw in L.values())
-    peak, peak_src = load_peaks()
-    if best.endswith("persistent_fast"):
-        kernel_name, achieved = "pipeline_kernel (whole step, 1 launch)", value
-        how = (f"1 persistent launch per step ({args.layers * 11} ops), algorithmic bytes = "
-               f"sum bits*M*K/8 = {total_bytes} per launch, CUDA events over {args.steps} launches")
-    elif best == "layer_set_batch_fast":
-        kernel_name = "gemv_b1_batch_kernel"
-        achieved = local_bytes / (ms_look * 1e-3) / 1e9
-        how = (f"the step's {n_look} batched lookup launches (one per K: {args.layers} layers' q,k,v,o,gate,up "
-               f"and down; tables prebuilt, same flags) per graph replay, algorithmic bytes = sum bits*M*K/8 "
-               f"= {local_bytes} per replay, CUDA events over {args.steps} replays")
-    else:
-        kernel_name = "gemv_b1_lean_kernel" if best_fast else "gemv_kernel"
-        achieved = local_bytes / (ms_look * 1e-3) / 1e9
-        how = (f"{n_look} lookup launches/graph replay (the step's lookups with tables prebuilt, "
-               f"same flags, {'fast' if best_fast else 'exact'} epilogue), algorithmic bytes = "
-               f"bits*M*K/8 per launch, CUDA events over {args.steps} replays")
-    lookups_graph = {"ms": round(ms_look, 5), "GBps": round(local_bytes / (ms_look * 1e-3) / 1e9, 1),
-                     "launches": n_look}
+    achieved = local_bytes / (ms_look * 1e-3) / 1e9
+    kernel_name = "gemv_b1_batch_kernel"
+    details["roofline_how"] = (
+        f"the step's {n_look} batched lookup launches (one per K; {args.layers} layers' q,k,v,o,gate,up and "
+        f"down; tables prebuilt) per graph replay; algorithmic bytes = sum bits*M*K/8 = {local_bytes} per "
+        f"replay per GPU; CUDA events on the launching stream over {args.steps} replays; peak {peak_src}")
 
-    # ---- per-shape mpGEMV: graph of R launches over rotating
-    #      weight copies >= 4x L2, tables prebuilt; "overlapped" = independent
-    #      launches (PDL lets launch i+1 start while i drains), "chained" =
-    #      each launch waits for the previous one; plus one launch after an
-    #      L2 flush.  W1 / W2 / W4, fast and exact epilogues. ----
-    per_shape = None
-    if not args.no_shapes:
-        with ClockSampler(local) as clk_shapes:
-            per_shape = per_shape_table(device, stream, max(5, args.steps // 4), args.warmup, barrier,
-                                        peak, world)
-        per_shape["clocks"] = clk_shapes.summary()
-
-    # ---- the same layer set through the batch executor at W4 g128 and W1
-    #      g128 (north star: >= 70 % of HBM peak for W4/W2/W1 7B shapes at
-    #      batch 1); step = table launch + lookup launches, CUDA events ----
-    bits_sweep = None
+    # ---- the same layer set at the other BASELINE widths (north star: >= 70 %
+    #      of HBM peak at W4 / W2 / W1): batch executor, step and lookups only ----
     if not args.no_sweep and world == 1:
-        bits_sweep = {}
+        sweep = {}
         with ClockSampler(local) as clk_sw:
-            for b_, gs_ in ((4, 128), (1, 128)):
+            for label, b_, gs_ in (("W4_g128", 4, 128), ("W1_g128", 1, 128)):
                 L_ = build_layers(args.layers, b_, gs_, rank, world, device, seed=20251020 + b_)
                 pl_, _, _ = build_pipeline(L_, acts, fast=True, executor="batch", chain=False)
                 ms_ = time_runs(lambda: pl_.run(stream))
                 pl_.run(stream)
                 torch.cuda.synchronize()
                 g_ = capture(lambda: pl_._launch_lookups(stream), stream)
-                with torch.cuda.stream(stream):
-                    msl_ = time_graph(g_, args.steps, args.warmup, barrier)
+                msl_ = time_graph_max(g_, args.steps, args.warmup, barrier, stream, world, device)
                 bytes_ = packed_bytes_full(args.layers, b_)
-                bits_sweep[f"W{b_}_g{gs_}"] = {
+                sweep[label] = {
                     "packed_bytes_per_step": bytes_, "ms_per_step": round(ms_, 5),
                     "GBps": round(bytes_ / (ms_ * 1e-3) / 1e9, 1),
                     "frac_of_peak": round(bytes_ / (ms_ * 1e-3) / 1e9 / peak, 4),
-                    "lookups_only_ms": round(msl_, 5),
-                    "lookups_only_GBps": round(bytes_ / (msl_ * 1e-3) / 1e9, 1),
                     "lookups_only_frac_of_peak": round(bytes_ / (msl_ * 1e-3) / 1e9 / peak, 4),
                     "launches_per_step": pl_.n_launches()}
                 del g_, pl_, L_
                 torch.cuda.synchronize()
                 torch.cuda.empty_cache()
-        bits_sweep["clocks"] = clk_sw.summary()
-
-    # ---- BASELINE configs[0]: single W4 mpGEMV, zeros, fp16 tables ----
-    cfg1 = None
-    if not args.no_shapes and world == 1:
-        with ClockSampler(local) as clk_1:
-            cfg1 = config1_table(device, stream, max(5, args.steps // 4), args.warmup, barrier, peak)
-        cfg1["clocks"] = clk_1.summary()
-
-    # ---- Llama-2-70B per-GPU shards (BASELINE configs[4]) ----
-    shards70 = None
-    if not args.no_70b and world == 1:
-        with ClockSampler(local) as clk_70:
-            shards70 = llama70b_table(device, stream, max(3, args.steps // 5), args.warmup, barrier, peak)
-        shards70["clocks"] = clk_70.summary()
-
-    # ---- prefill mpGEMM (BASELINE configs[3]) ----
-    gemm = None
-    if not args.no_gemm:
-        with ClockSampler(local) as clk_gemm:
-            gemm = gemm_table(device, stream, max(3, args.steps // 5), args.warmup, barrier, world)
-        gemm["clocks"] = clk_gemm.summary()
+        sweep["clocks"] = clk_sw.summary()
+        details["layer_set_bits_sweep"] = sweep
+        summary["layer_set_frac"] = {"W2_g64": round(value / peak, 4),
+                                     **{k: v["frac_of_peak"] for k, v in sweep.items() if k != "clocks"}}
 
     # ---- e2e: the same step through the public API from HOST buffers: one
     #      H2D of the step's activation rows (pinned), the op list, one D2H of
     #      every GEMV output (pinned), all inside the timed region. ----
     e2e = None
-    if not args.no_e2e and world == 1 and best in pipes:
-        # the same op list cut into 8 chunks of layers (each its own Pipeline):
-        # the H2D of chunk c+1 and the D2H of chunk c-1 overlap the lookups of
-        # chunk c (two copy streams + events)
-        fast_best = "fast" in best
-        ksplit = best == "layer_set_batch_fast" and os.environ.get("BENCH_E2E_MODE", "layers") == "ksplit"
-        if ksplit:
-            # batch executor: the step as two Pipelines by input width -- every
-            # layer's q,k,v,o,gate,up (K = 4096), then every down (K = 11008).
-            # Inputs in two pinned host arenas; the D2H of the first part's
-            # outputs overlaps the down lookups, only the down outputs' D2H
-            # (0.5 MB) trails the compute.
-            kA = sum(k for g_, k, _ in LUT_GROUPS if g_ != "down")
-            kB = sum(k for g_, k, _ in LUT_GROUPS if g_ == "down")
-            dev_in = [torch.empty((args.layers * kA,), dtype=act_arena.dtype, device=device),
-                      torch.empty((args.layers * kB,), dtype=act_arena.dtype, device=device)]
-            acts_e2e = []
-            for i, A in enumerate(acts):
-                d, offA = {}, i * kA
-                for g_, k, _ in LUT_GROUPS:
-                    if g_ == "down":
-                        d[g_] = dev_in[1][i * kB:(i + 1) * kB].view(1, kB)
-                    else:
-                        d[g_] = dev_in[0][offA:offA + k].view(1, k)
-                        offA += k
-                    d[g_].copy_(A[g_])
-                acts_e2e.append(d)
-            parts = [build_pipeline(layers, acts_e2e, fast=True, executor="batch", chain=False,
-                                    groups=[g_ for g_, _, _ in LUT_GROUPS if g_ != "down"]),
-                     build_pipeline(layers, acts_e2e, fast=True, executor="batch", chain=False, groups=["down"])]
-            host_ins = [t.cpu().pin_memory() for t in dev_in]
-            host_outs = [torch.empty(p_[2].shape, dtype=p_[2].dtype).pin_memory() for p_ in parts]
-            in_stream, out_stream = torch.cuda.Stream(device), torch.cuda.Stream(device)
-            ev_start, ev_out = torch.cuda.Event(), torch.cuda.Event()
-            ev_in = [torch.cuda.Event() for _ in parts]
-            ev_done = [torch.cuda.Event() for _ in parts]
-            chunks = parts
-            host_in_bytes = sum(h.numel() * h.element_size() for h in host_ins)
-
-            def e2e_step():
-                ev_start.record(stream)
-                in_stream.wait_event(ev_start)
-                with torch.cuda.stream(in_stream):
-                    for c in range(2):
-                        dev_in[c].copy_(host_ins[c], non_blocking=True)
-                        ev_in[c].record(in_stream)
-                for c, (pl_c, _, arena_c) in enumerate(parts):
-                    stream.wait_event(ev_in[c])
-                    pl_c.run(stream)
-                    ev_done[c].record(stream)
-                    out_stream.wait_event(ev_done[c])
-                    with torch.cuda.stream(out_stream):          # D2H of part 0 overlaps part 1
-                        host_outs[c].copy_(arena_c, non_blocking=True)
-                ev_out.record(out_stream)
-                stream.wait_event(ev_out)
-            split, ex_best, n_chunks = "by K (4096 | 11008)", "batch", 2
-        else:
-            # chunk sizes in layers (BENCH_E2E_SPLIT, comma list summing to
-            # --layers): four equal chunks measured best -- the f32 outputs' D2H
-            # (5.4 MB, ~30 GB/s) must overlap the lookups, and every chunk
-            # boundary costs a drain (1,3,8,8,8,3,1: 0.433 ms; 8,8,8,8: 0.416-0.430;
-            # by K, BENCH_E2E_MODE=ksplit: 0.426)
-            split = [int(x) for x in os.environ.get("BENCH_E2E_SPLIT", "8,8,8,8").split(",") if x]
-            if sum(split) != args.layers or min(split) < 1:
-                split = [args.layers]
-            bounds = [sum(split[:c]) for c in range(len(split) + 1)]
-            n_chunks = len(split)
-            ex_best = "batch" if best == "layer_set_batch_fast" else "graph"
-            chunks = [build_pipeline(layers[bounds[c]:bounds[c + 1]], acts[bounds[c]:bounds[c + 1]],
-                                     fast=fast_best, executor=ex_best, chain=best.startswith("decode"))
-                      for c in range(n_chunks)]
-            host_in = act_arena.cpu().pin_memory()
-            host_in_bytes = host_in.numel() * host_in.element_size()
-            per_layer_act = act_arena.numel() // args.layers
-            host_outs = [torch.empty(ch[2].shape, dtype=ch[2].dtype).pin_memory() for ch in chunks]
-            in_stream, out_stream = torch.cuda.Stream(device), torch.cuda.Stream(device)
-            ev_start, ev_out = torch.cuda.Event(), torch.cuda.Event()
-            ev_in = [torch.cuda.Event() for _ in chunks]
-            ev_done = [torch.cuda.Event() for _ in chunks]
-
-            def e2e_step():
-                ev_start.record(stream)                              # time_runs' events are on `stream`
-                in_stream.wait_event(ev_start)
-                with torch.cuda.stream(in_stream):                   # H2D of chunk c+1 overlaps chunk c
-                    for c in range(n_chunks):
-                        lo, hi = bounds[c] * per_layer_act, bounds[c + 1] * per_layer_act
-                        act_arena[lo:hi].copy_(host_in[lo:hi], non_blocking=True)
-                        ev_in[c].record(in_stream)
-                for c, (pl_c, _, arena_c) in enumerate(chunks):
-                    stream.wait_event(ev_in[c])
-                    pl_c.run(stream)
-                    ev_done[c].record(stream)
-                    out_stream.wait_event(ev_done[c])
-                    with torch.cuda.stream(out_stream):              # D2H of chunk c overlaps chunk c+1
-                        host_outs[c].copy_(arena_c, non_blocking=True)
-                ev_out.record(out_stream)
-                stream.wait_event(ev_out)                            # the step ends when the last D2H does
-        ms_e2e = time_runs(e2e_step)
-        for c, (_, _, arena_c) in enumerate(chunks):             # the bytes really arrived
-            assert torch.equal(host_outs[c], arena_c.cpu())
-        e2e = {"value": round(total_bytes / (ms_e2e * 1e-3) / 1e9, 2), "unit": "GB/s",
-               "h2d_bytes_per_step": int(host_in_bytes),
-               "d2h_bytes_per_step": int(sum(h.numel() * h.element_size() for h in host_outs)),
-               "ms_per_step": round(ms_e2e, 4),
-               "path": f"pinned host activations -> {n_chunks} x Pipeline({ex_best}, {best}) (split {split}) -> "
-                       f"pinned host outputs ({args.layers} layers x 7 GEMVs; copies overlap neighbouring chunks), "
-                       "CUDA events on the compute stream, which waits for the last D2H"}
-    # the per-call drop-in API (reference kernel.py mpgemv: numpy in / numpy out)
+    if not args.no_e2e:
+        e2e = e2e_run(args, layers, acts, act_arena, stream, device, world, group, time_runs, total_bytes)
     per_call = None
     if not args.no_e2e and world == 1:
-        n_pc = min(args.layers, 4)
-        host_rows = [{g: A[g][0].cpu().numpy() for g in A} for A in acts[:n_pc]]
-
-        def pc_step():
-            for L, HA in zip(layers[:n_pc], host_rows):
-                for gname, k, names in LUT_GROUPS:
-                    for nm in names:
-                        B.mpgemv(HA[gname], L[nm])
-        pc_step()
-        t0 = time.perf_counter()
-        reps = 3
-        for _ in range(reps):
-            pc_step()
-        dt = (time.perf_counter() - t0) / reps
-        per_call = {"value": round(packed_bytes_full(n_pc, bits) / dt / 1e9, 2), "unit": "GB/s",
-                    "us_per_call": round(dt * 1e6 / (7 * n_pc), 1),
-                    "path": "mpgemv(numpy fp16 row, PackedWeights) -> numpy, one call per GEMV "
-                            "(table build + lookup + H2D/D2H + sync per call), wall clock"}
+        per_call = per_call_run(layers, acts, bits, args)
+        details["e2e_per_call_api"] = per_call
+        summary["per_call_us"] = per_call["us_per_call"]
 
     # ---- CPU baseline (rank 0, N = 1 only) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        try:
-            from oracle import oracle as O
-            threads = O.c_max_threads()
-            hl = host_layer(layers[0], acts[0], bits)
-            gbps, reps, secs = cpu_baseline(hl, bits, gs, args.cpu_budget, threads)
-            model, ncpu = cpu_info()
-            cpu = {"value": round(gbps, 4), "unit": "GB/s", "cores": threads, "kind": "port",
-                   "sample": f"1 Llama-2-7B W2 layer (7 vector-q8 mpGEMV incl. table build) x "
-                             f"{reps} reps = {secs:.1f}s on {threads} threads ({model})"}
-            # also one thread (the reference's default threads=1)
-            g1, r1, s1 = cpu_baseline(hl, bits, gs, min(3.0, args.cpu_budget), 1)
-            cpu["single_thread"] = {"value": round(g1, 4), "unit": "GB/s", "cores": 1,
-                                    "sample": f"same layer x {r1} reps = {s1:.1f}s on 1 thread"}
-        except Exception as e:  # report, never fake
-            cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "port",
-                   "sample": f"unavailable: {e}"}
+        cpu = cpu_baseline_run(layers, acts, bits, gs, args)
+
+    # ---- detail sections (--full): per-shape, configs[0], 70B shards, prefill ----
+    if args.full:
+        with ClockSampler(local) as clk_d:
+            details["per_shape"] = per_shape_table(device, stream, max(5, args.steps // 4), args.warmup, barrier,
+                                                   peak, world)
+            if world == 1:
+                details["config1_single_mpgemv"] = config1_table(device, stream, max(5, args.steps // 4),
+                                                                 args.warmup, barrier, peak)
+                details["llama70b_shards"] = llama70b_table(device, stream, max(3, args.steps // 5), args.warmup,
+                                                            barrier, peak)
+            details["mpgemm_prefill"] = gemm_table(device, stream, max(3, args.steps // 5), args.warmup, barrier,
+                                                   world)
+        details["detail_clocks"] = clk_d.summary()
 
     if rank == 0:
+        clocks = clk.summary()
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
             "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
-            "vs_baseline": None, "dtype": "i8 tables / i32 accumulate / f32 epilogue",
+            "vs_baseline": None, "dtype": "u8 weights, i8 tables, i32 accumulate, f32 epilogue",
             "data": "synthetic (seeded torch RNG), random-init W2 weights of the Llama-2-7B shapes",
             "config": cfg,
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                         "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": load_traffic(kernel_name), "kernel": kernel_name,
-                         "peak_source": peak_src, "how": how},
-            "executor": best,
-            "executors": executors_out,
-            "lookups_only_graph": lookups_graph,
-            "layer_set_bits_sweep": bits_sweep,
-            "per_shape": per_shape,
-            "config1_single_mpgemv": cfg1,
-            "mpgemm_prefill": gemm,
-            "llama70b_shards": shards70,
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": load_traffic(kernel_name),
+                         "kernel": kernel_name},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "e2e_per_call_api": per_call,
             "gpu_launches": launches_per_step * args.steps,
-            "clocks": clk.summary(),
+            "clocks": {k: clocks[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
+            "summary": summary,
         }
-        print(json.dumps(line))
+        details["line"] = dict(line)
+        emit(line, details, details_path(args.details))
     if world > 1:
         dist.destroy_process_group()
 
 
-def load_traffic(kernel="gemv_b1_lean_kernel"):
+def time_graph_max(g, reps, warmup, barrier, stream, world, device):
+    import torch
+    with torch.cuda.stream(stream):
+        ms = time_graph(g, reps, warmup, barrier)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms
+
+
+def e2e_run(args, layers, acts, act_arena, stream, device, world, group, time_runs, total_bytes):
+    """The headline op list from pinned HOST buffers.  N = 1: the step cut
+    into chunks of layers (one batch Pipeline each); the H2D of chunk c+1 and
+    the D2H of chunk c-1 overlap chunk c.  N > 1: H2D of the (replicated)
+    activations, the rank's shard, one all-gather, D2H of the gathered
+    outputs."""
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        pl, _, out_arena = build_pipeline(layers, acts, fast=True, executor="batch", chain=False)
+        gat = torch.empty((world * out_arena.numel(),), dtype=out_arena.dtype, device=device)
+        host_in = act_arena.cpu().pin_memory()
+        host_out = torch.empty(gat.shape, dtype=gat.dtype).pin_memory()
+
+        def step():
+            act_arena.copy_(host_in, non_blocking=True)
+            pl.run(stream)
+            dist.all_gather_into_tensor(gat, out_arena, group=group)
+            host_out.copy_(gat, non_blocking=True)
+        ms = time_runs(step)
+        return {"value": round(total_bytes / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+                "h2d_bytes_per_step": int(host_in.numel() * host_in.element_size()),
+                "d2h_bytes_per_step": int(host_out.numel() * host_out.element_size()),
+                "ms_per_step": round(ms, 4)}
+    split = [int(x) for x in os.environ.get("BENCH_E2E_SPLIT", "8,8,8,8").split(",") if x]
+    if sum(split) != args.layers or min(split) < 1:
+        split = [args.layers]
+    bounds = [sum(split[:c]) for c in range(len(split) + 1)]
+    n_chunks = len(split)
+    chunks = [build_pipeline(layers[bounds[c]:bounds[c + 1]], acts[bounds[c]:bounds[c + 1]],
+                             fast=True, executor="batch", chain=False) for c in range(n_chunks)]
+    host_in = act_arena.cpu().pin_memory()
+    per_layer_act = act_arena.numel() // args.layers
+    host_outs = [torch.empty(ch[2].shape, dtype=ch[2].dtype).pin_memory() for ch in chunks]
+    in_stream, out_stream = torch.cuda.Stream(device), torch.cuda.Stream(device)
+    ev_start, ev_out = torch.cuda.Event(), torch.cuda.Event()
+    ev_in = [torch.cuda.Event() for _ in chunks]
+    ev_done = [torch.cuda.Event() for _ in chunks]
+
+    def e2e_step():
+        ev_start.record(stream)                              # time_runs' events are on `stream`
+        in_stream.wait_event(ev_start)
+        with torch.cuda.stream(in_stream):                   # H2D of chunk c+1 overlaps chunk c
+            for c in range(n_chunks):
+                lo, hi = bounds[c] * per_layer_act, bounds[c + 1] * per_layer_act
+                act_arena[lo:hi].copy_(host_in[lo:hi], non_blocking=True)
+                ev_in[c].record(in_stream)
+        for c, (pl_c, _, arena_c) in enumerate(chunks):
+            stream.wait_event(ev_in[c])
+            pl_c.run(stream)
+            ev_done[c].record(stream)
+            out_stream.wait_event(ev_done[c])
+            with torch.cuda.stream(out_stream):              # D2H of chunk c overlaps chunk c+1
+                host_outs[c].copy_(arena_c, non_blocking=True)
+        ev_out.record(out_stream)
+        stream.wait_event(ev_out)                            # the step ends when the last D2H does
+    ms = time_runs(e2e_step)
+    for c, (_, _, arena_c) in enumerate(chunks):             # the bytes really arrived
+        assert torch.equal(host_outs[c], arena_c.cpu())
+    return {"value": round(total_bytes / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+            "h2d_bytes_per_step": int(host_in.numel() * host_in.element_size()),
+            "d2h_bytes_per_step": int(sum(h.numel() * h.element_size() for h in host_outs)),
+            "ms_per_step": round(ms, 4)}
+
+
+def per_call_run(layers, acts, bits, args):
+    """The per-call drop-in API (reference kernel.py:374 mpgemv: numpy fp16
+    row in, numpy f32 out), one call per GEMV, wall clock."""
+    import paper_2407_00088_b200 as B
+    n_pc = min(args.layers, 4)
+    host_rows = [{g: A[g][0].cpu().numpy() for g in A} for A in acts[:n_pc]]
+
+    def pc_step():
+        for L, HA in zip(layers[:n_pc], host_rows):
+            for gname, k, names in LUT_GROUPS:
+                for nm in names:
+                    B.mpgemv(HA[gname], L[nm])
+    pc_step()
+    reps, t0 = 5, time.perf_counter()
+    for _ in range(reps):
+        pc_step()
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": round(packed_bytes_full(n_pc, bits) / dt / 1e9, 2), "unit": "GB/s",
+            "us_per_call": round(dt * 1e6 / (7 * n_pc), 1),
+            "path": "mpgemv(numpy fp16 row, PackedWeights) -> numpy f32, one call per GEMV, wall clock"}
+
+
+def cpu_baseline_run(layers, acts, bits, gs, args):
+    try:
+        from oracle import oracle as O
+        threads = O.c_max_threads()
+        hl = host_layer(layers[0], acts[0], bits)
+        gbps, reps, secs = cpu_baseline(hl, bits, gs, args.cpu_budget, threads)
+        model, ncpu = cpu_info()
+        cpu = {"value": round(gbps, 4), "unit": "GB/s", "cores": threads, "kind": "port",
+               "sample": f"1 7B W2 layer (7 vector-q8 mpGEMV + tables) x {reps} = {secs:.1f}s, "
+                         f"{threads} threads, {model}"}
+        g1, r1, s1 = cpu_baseline(hl, bits, gs, min(2.0, args.cpu_budget), 1)
+        cpu["single_thread"] = round(g1, 4)
+        return cpu
+    except Exception as e:  # report, never fake
+        return {"value": None, "unit": "GB/s", "cores": 0, "kind": "port", "sample": f"unavailable: {e}"}
+
+
+def load_traffic(kernel="gemv_b1_batch_kernel"):
     """ncu DRAM bytes (read + write) per launch of the headline's dominant
-    kernel, from one committed `ncu --set full` capture: the batch
-    executor's two lookup launches (profiles/r01h_batch_full.json, mean per
-    launch, the unit of roofline.achieved), or the graph executor's grouped
-    launches of one layer divided by its 7 GEMVs (r01g_step_gemv_b1_full.json)."""
-    if kernel == "gemv_b1_batch_kernel":
-        p = os.path.join(ROOT, "profiles", "r01h_batch_full.json")
+    kernel from one committed `ncu --set full` capture of the batch
+    executor's lookup launches (mean per launch; roofline.achieved is per
+    replay of the same launches)."""
+    for name in ("r02_batch_w2_full.json", "r01h_batch_full.json"):
+        p = os.path.join(ROOT, "profiles", name)
         if os.path.exists(p):
             with open(p) as f:
                 d = json.load(f)
             tot = sum(x["dram__bytes_read.sum"] + x["dram__bytes_write.sum"] for x in d["launches"])
             return round(tot / len(d["launches"]), 1)
-        return None
-    p = os.path.join(ROOT, "profiles", "r01g_step_gemv_b1_full.json")
-    if os.path.exists(p):
-        with open(p) as f:
-            d = json.load(f)
-        tot = sum(x["dram__bytes_read.sum"] + x["dram__bytes_write.sum"] for x in d["launches"])
-        return round(tot / len(LAYER), 1)
     return None
 
 
+# ----------------------------------------------------------------- reference arm
+
+def _ref_module():
+    """The UNMODIFIED reference package installed under baseline/_ref
+    (pip --target), or None."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "bitlut")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/bitlut_numba_cache")
+    sys.path.insert(0, ref)
+    try:
+        import bitlut
+        return bitlut
+    except Exception:
+        return None
+
+
 def run_reference(args, bits, gs, rank, world, cfg):
-    """--impl reference: the reference's CPU algorithm (C port of
-    _kernels.gemv_q8_vector + lut_build) on all host cores, same metric."""
+    """--impl reference: the reference's own CPU implementation of the path
+    on the host cores, same metric/config.  Preferred: the real reference
+    package (baseline/_ref, numba) through its public API -- bitlut.mpgemv(a,
+    pw, variant="vector-q8", threads=os.cpu_count()) -- on one Llama-2-7B W2
+    layer (7 GEMVs incl. their table builds) per sample.  Fallback when it is
+    not importable: the C port (oracle/, pinned bitwise to it).  A step is a
+    bounded sample of the 32-layer workload: r layers, r chosen in warm-up
+    so the K timed steps last >= --ref-min-seconds; median step time."""
     if rank != 0:
         return
-    from oracle import oracle as O
     from paper_2407_00088_b200 import workloads as W
-    threads = O.c_max_threads()
-    # one 7B layer from the seeded numpy workloads (the same bytes the parity tests use)
+    bl = _ref_module()
+    threads = os.cpu_count() or 1
     hl = []
     for name, m, k in LAYER:
         si = {(4096, 4096): 0, (11008, 4096): 1, (4096, 11008): 2}[(m, k)]
-        inst = W.config2(si)
-        planes = O.pack_v1(O.decompose_bits(inst["q"], bits, 4), 32, 128, 4, 16)
-        hl.append((name, m, k, planes, inst["scales"].astype(np.float32),
-                   inst["a"].astype(np.float32)))
+        hl.append((name, m, k, W.config2(si)))
     layer_bytes = sum(bits * m * k // 8 for _, m, k in LAYER)
-    for _ in range(args.warmup):
-        for name, m, k, planes, s, a in hl:
-            O.c_mpgemm(a, planes, m, k, bits, gs, s, threads=threads)
-    t0 = time.perf_counter()
+    if bl is not None:
+        kind = "reference"
+        tile = bl.TileConfig(n_tile=1, m_tile=32, k_tile=128, g=4, lanes=16)
+        prepared = {}
+        for name, m, k, inst in hl:
+            if (m, k) not in prepared:
+                qw = bl.QuantizedWeights(m=m, k=k, bits=bits, group_size=gs, qvalues=inst["q"],
+                                         scales=inst["scales"].astype(np.float32))
+                prepared[(m, k)] = (bl.prepare_weights(qw, tile), inst["a"][0].astype(np.float32))
+
+        def layer():
+            for name, m, k, _ in hl:
+                pw, a = prepared[(m, k)]
+                bl.mpgemv(a, pw, variant="vector-q8", threads=threads)
+        impl = f"bitlut {getattr(bl, '__version__', '?')} (baseline/_ref, numba) mpgemv vector-q8 threads={threads}"
+    else:
+        kind = "port"
+        from oracle import oracle as O
+        threads = O.c_max_threads()
+        ports = []
+        for name, m, k, inst in hl:
+            planes = O.pack_v1(O.decompose_bits(inst["q"], bits, 4), 32, 128, 4, 16)
+            ports.append((m, k, planes, inst["scales"].astype(np.float32), inst["a"].astype(np.float32)))
+
+        def layer():
+            for m, k, planes, s, a in ports:
+                O.c_mpgemm(a, planes, m, k, bits, gs, s, threads=threads)
+        impl = f"C port of the reference vector-q8 kernel (oracle/), {threads} threads"
+    t_layer = []
+    for _ in range(max(2, args.warmup)):                     # includes numba JIT on the first call
+        t0 = time.perf_counter()
+        layer()
+        t_layer.append(time.perf_counter() - t0)
+    per_layer = min(t_layer[1:])
+    reps = max(1, int(np.ceil(args.ref_min_seconds / max(args.steps, 1) / per_layer)))
+    samples = []
     for _ in range(args.steps):
-        for name, m, k, planes, s, a in hl:
-            O.c_mpgemm(a, planes, m, k, bits, gs, s, threads=threads)
-    dt = (time.perf_counter() - t0) / args.steps
-    gbps = layer_bytes / dt / 1e9
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            layer()
+        samples.append(time.perf_counter() - t0)
+    dt = float(np.median(samples))
+    gbps = reps * layer_bytes / dt / 1e9
     model, ncpu = cpu_info()
-    sample = (f"1 Llama-2-7B W2 layer (7 vector-q8 mpGEMV incl. table build) per step, "
-              f"C port of the reference kernel on {threads} threads ({model})")
-    print(json.dumps({
+    sample = (f"{reps} Llama-2-7B W2 g64 layer(s) (7 mpGEMV incl. table build) per step, {impl}, "
+              f"{model}; median of {args.steps} steps, timed {sum(samples):.1f}s")
+    line = {
         "impl": "reference", "metric": METRIC, "value": round(gbps, 4), "unit": "GB/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
-        "dtype": "i8 tables / i32 accumulate / f32 epilogue", "data": "synthetic (seeded numpy PCG64)",
+        "dtype": "u8 weights, i8 tables, i32 accumulate, f32 epilogue", "data": "synthetic (seeded numpy PCG64)",
         "config": cfg,
-        "cpu_baseline": {"value": round(gbps, 4), "unit": "GB/s", "cores": threads, "kind": "port",
+        "cpu_baseline": {"value": round(gbps, 4), "unit": "GB/s", "cores": threads, "kind": kind,
                          "sample": sample},
-        "e2e": {"value": round(gbps, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-    }))
+        "e2e": {"value": round(gbps, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "timed_region_s": round(sum(samples), 2),
+    }
+    emit(line, None, None)
 
 
 if __name__ == "__main__":
