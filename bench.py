@@ -112,8 +112,11 @@ class ClockSampler:
 
 # ----------------------------------------------------------------- workload
 
-def build_layers(n_layers, bits, gs, rank, world, device, seed=20251020):
-    """Packed weights for n_layers 7B layers; this rank's output-channel shard."""
+def build_layers(n_layers, bits, gs, rank, world, device, seed=20251020, encoding="offset"):
+    """Packed weights for n_layers 7B layers; this rank's output-channel
+    shard.  encoding "offset" (the reference's implicit zero), "sign" (1-bit
+    sign planes w = +-s, per-group scale) or "ternary" ({-1,0,+1} in 2
+    planes, one per-tensor scale): BASELINE configs[1] / configs[2]."""
     import torch
     import paper_2407_00088_b200 as B
     gen = torch.Generator(device=device)
@@ -123,12 +126,20 @@ def build_layers(n_layers, bits, gs, rank, world, device, seed=20251020):
     for _ in range(n_layers):
         mats = {}
         for name, m, k in LAYER:
-            q = torch.randint(0, 1 << bits, (m, k), dtype=torch.uint8, device=device, generator=gen)
+            if encoding == "ternary":
+                q = torch.randint(-1, 2, (m, k), dtype=torch.int8, device=device, generator=gen)
+            else:
+                q = torch.randint(0, 1 << bits, (m, k), dtype=torch.uint8, device=device, generator=gen)
             s = (torch.randn((m, k // gs), device=device, generator=gen).abs() * 0.02 + 1e-3).half()
             if world > 1:
                 lo, hi = rank * m // world, (rank + 1) * m // world
                 q, s = q[lo:hi].contiguous(), s[lo:hi].contiguous()
-            qw = B.QuantizedWeights(m=q.shape[0], k=k, bits=bits, group_size=gs, qvalues=q, scales=s)
+            if encoding == "sign":
+                qw = B.QuantizedWeights.sign_planes(q, s, gs)
+            elif encoding == "ternary":
+                qw = B.QuantizedWeights.ternary(q, s[0, 0], gs)
+            else:
+                qw = B.QuantizedWeights(m=q.shape[0], k=k, bits=bits, group_size=gs, qvalues=q, scales=s)
             pw = B.prepare_weights(qw, tile)
             mats[name] = pw
             del q
@@ -805,8 +816,9 @@ def main():
     if not args.no_sweep and world == 1:
         sweep = {}
         with ClockSampler(local) as clk_sw:
-            for label, b_, gs_ in (("W4_g128", 4, 128), ("W1_g128", 1, 128)):
-                L_ = build_layers(args.layers, b_, gs_, rank, world, device, seed=20251020 + b_)
+            for label, b_, gs_, enc_ in (("W4_g128", 4, 128, "offset"), ("W1_g128", 1, 128, "offset"),
+                                         ("W1_sign_g128", 1, 128, "sign"), ("W2_ternary", 2, 128, "ternary")):
+                L_ = build_layers(args.layers, b_, gs_, rank, world, device, seed=20251020 + b_, encoding=enc_)
                 pl_, _, _ = build_pipeline(L_, acts, fast=True, executor="batch", chain=False)
                 ms_ = time_runs(lambda: pl_.run(stream))
                 pl_.run(stream)

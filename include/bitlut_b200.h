@@ -247,24 +247,55 @@ int bitlut_mpgemv_multi_tab(const bitlut_mat_tab* mats, int n_mats, int k, int b
  * in DEVICE memory: bitlut_mpgemv_batch_encode (host) validates the host copy
  * and fills tile_end (cumulative tiles) and *total_tiles; the caller copies
  * the array to the device.  Every CTA streams one contiguous tile range of
- * the concatenated matrices.  Outputs equal the per-matrix bitlut_mpgemm
- * calls (fast epilogue) bitwise.  Scales of one dtype; no zero points;
- * shapes the lean batch-1 kernel takes (bits 1/2/4, one unit round), else
- * BITLUT_ELAYOUT. */
+ * the concatenated matrices (csrc/gemv_batch.cu).  Scales of one dtype, one
+ * weight encoding per launch (BITLUT_W_*); shapes with one unit round per
+ * tile (bits 1/2/4, k/4/R <= 384 units), else BITLUT_ELAYOUT.
+ *
+ * Weight encodings (w = the dequantized weight of code q):
+ *   BITLUT_W_OFFSET   w = s (q - 2^(b-1)): the reference's implicit zero
+ *                     (core.py:121-123, _kernels.py:187-191); zeros NULL
+ *   BITLUT_W_ZEROS    w = s (q - z), z per (channel, group) in `zeros`
+ *                     (BASELINE configs[0]: asymmetric)
+ *   BITLUT_W_SIGN     1-bit sign planes w = s (2q - 1): the table entry is
+ *                     already the signed sum, no row-sum term (configs[2])
+ *   BITLUT_W_TERNARY  2-bit codes q in {0,1,2}, w = s_t (q - 1) with ONE
+ *                     per-tensor scale s_t (`wscales` points at it; no
+ *                     per-group scale stream) (configs[2])
+ * partials (optional, all or none, BITLUT_FLAG_COMBINED_PARTIALS): the exact
+ * int32 S = sum_p 2^p P_p per (channel, group), (m, k/gs) row-major -- the
+ * integer object SURVEY §8(c) pins against the reference's staging values. */
+#define BITLUT_W_OFFSET 0
+#define BITLUT_W_ZEROS 1
+#define BITLUT_W_SIGN 2
+#define BITLUT_W_TERNARY 3
 typedef struct {
   const uint8_t* wgpu;
-  const void* wscales;
+  const void* wscales;      /* (m, k/gs), or 1 value (BITLUT_W_TERNARY) */
+  const void* zeros;        /* (m, k/gs) for BITLUT_W_ZEROS, else NULL */
   float* out;               /* (1, m) f32 */
   const void* tables;       /* (1, k/4*8) int8 kernel format */
   const float* tscales;     /* (1, k/gs) */
   const float* rowsums;     /* (1, k/gs) */
+  int32_t* partials;        /* (m, k/gs) int32, or NULL */
   int m;
   int tile_end;             /* filled by bitlut_mpgemv_batch_encode */
 } bitlut_batch_mat;
 int bitlut_mpgemv_batch_encode(bitlut_batch_mat* mats, int n_mats, int k, int bits, int group_size,
-                               int* total_tiles);
+                               int weight_mode, int* total_tiles);
 int bitlut_mpgemv_batch(const bitlut_batch_mat* dev_mats, int n_mats, int total_tiles, int k, int bits,
-                        int group_size, int scale_dtype, int flags, void* stream);
+                        int group_size, int scale_dtype, int weight_mode, int flags, void* stream);
+
+/* The drop-in call with HOST buffers (replaces kernel.py:280-371 mpgemm /
+ * :374-382 mpgemv as a numpy caller sees them): copies a_host (n, k) f16/f32
+ * to a_dev, builds the tables (or, batch 1 fast epilogue fp16, runs the fused
+ * build + lookup launch), looks up, copies the (n, m) f32 result to out_host
+ * and synchronizes `stream`.  The device scratch (a_dev, tables, tscales,
+ * rowsums, out_dev: sizes as for bitlut_build_lut / bitlut_mpgemm) is the
+ * caller's; flags as bitlut_mpgemm.  csrc/host_api.cu. */
+int bitlut_mpgemm_host(const void* a_host, int a_dtype, int n, int k, const uint8_t* wgpu, int m, int bits,
+                       int group_size, const void* wscales, const void* zeros, int scale_dtype, int mode,
+                       int flags, void* a_dev, void* tables, float* tscales, float* rowsums, float* out_dev,
+                       float* out_host, void* stream);
 
 /* Tensor-parallel batch-1 lookup with the all-gather fused into the epilogue
  * (SURVEY §8(e) B200-native upgrade; replaces kernel.py:374-382 mpgemv on

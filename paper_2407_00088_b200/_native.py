@@ -50,13 +50,15 @@ _SIGS = {
                              _vp, _vp],
     "bitlut_mpgemm_launches": [_i, _i, _i, _i, _i, _i],
     "bitlut_mpgemv_fused": [_vp, _i, _vp, _i, _i, _i, _i, _vp, _vp, _i, _vp, _i, _vp],
+    "bitlut_mpgemm_host": [_vp, _i, _i, _i, _vp, _i, _i, _i, _vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp,
+                           _vp],
     "bitlut_mpgemv_multi": [_vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _i, _vp],
     "bitlut_mpgemv_gather": [_vp, _i, _i, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _i,
                              _vp],
     "bitlut_gather_wait": [_vp, ctypes.c_uint32, _vp],
     "bitlut_mpgemv_multi_tab": [_vp, _i, _i, _i, _i, _i, _i, _vp],
-    "bitlut_mpgemv_batch_encode": [_vp, _i, _i, _i, _i, _vp],
-    "bitlut_mpgemv_batch": [_vp, _i, _i, _i, _i, _i, _i, _i, _vp],
+    "bitlut_mpgemv_batch_encode": [_vp, _i, _i, _i, _i, _i, _vp],
+    "bitlut_mpgemv_batch": [_vp, _i, _i, _i, _i, _i, _i, _i, _i, _vp],
     "bitlut_build_lut_batch_encode": [_vp, _i, _vp, _vp],
     "bitlut_build_lut_batch": [_vp, _vp, _i, _i, _i, _i, _i, _vp],
 }
@@ -78,9 +80,15 @@ class BitlutMatTab(ctypes.Structure):
 class BitlutBatchMat(ctypes.Structure):
     """include/bitlut_b200.h bitlut_batch_mat: one GEMV of a batched launch
     (device-resident descriptor array)."""
-    _fields_ = [("wgpu", ctypes.c_void_p), ("wscales", ctypes.c_void_p), ("out", ctypes.c_void_p),
-                ("tables", ctypes.c_void_p), ("tscales", ctypes.c_void_p), ("rowsums", ctypes.c_void_p),
+    _fields_ = [("wgpu", ctypes.c_void_p), ("wscales", ctypes.c_void_p), ("zeros", ctypes.c_void_p),
+                ("out", ctypes.c_void_p), ("tables", ctypes.c_void_p), ("tscales", ctypes.c_void_p),
+                ("rowsums", ctypes.c_void_p), ("partials", ctypes.c_void_p),
                 ("m", ctypes.c_int32), ("tile_end", ctypes.c_int32)]
+
+
+# weight encodings of the batch executor (bitlut_b200.h BITLUT_W_*)
+W_OFFSET, W_ZEROS, W_SIGN, W_TERNARY = 0, 1, 2, 3
+W_MODES = {"offset": W_OFFSET, "zeros": W_ZEROS, "sign": W_SIGN, "ternary": W_TERNARY}
 
 
 class BitlutLutJob(ctypes.Structure):
@@ -100,29 +108,38 @@ class LookupBatch:
     one (k, bits, group_size, scale dtype), each with its own int8 tables.
     `arr`: ctypes array of BitlutBatchMat (host); copied to `device`."""
 
-    def __init__(self, arr, k: int, bits: int, group_size: int, scale_dtype: int, device):
+    def __init__(self, arr, k: int, bits: int, group_size: int, scale_dtype: int, device, weight_mode: int = W_OFFSET):
         tt = ctypes.c_int(0)
-        raise_for_status(lib().bitlut_mpgemv_batch_encode(arr, len(arr), k, bits, group_size, ctypes.byref(tt)),
-                         "bitlut_mpgemv_batch_encode")
+        raise_for_status(lib().bitlut_mpgemv_batch_encode(arr, len(arr), k, bits, group_size, weight_mode,
+                                                          ctypes.byref(tt)), "bitlut_mpgemv_batch_encode")
         self.n, self.total_tiles = len(arr), tt.value
         self.k, self.bits, self.group_size, self.scale_dtype = k, bits, group_size, scale_dtype
+        self.weight_mode = weight_mode
+        self.partials = bool(arr[0].partials)          # all or none (checked by the encoder)
         self.dev = _to_device_bytes(arr, device)
 
     @classmethod
-    def from_tensors(cls, mats, k: int, bits: int, group_size: int) -> "LookupBatch":
-        """mats = [(wgpu, wscales, m, out (1, m) f32, tables, tscales, rowsums), ...]"""
+    def from_tensors(cls, mats, k: int, bits: int, group_size: int, weight_mode: int = W_OFFSET) -> "LookupBatch":
+        """mats = [(wgpu, wscales, m, out (1, m) f32, tables, tscales, rowsums[, zeros[, partials]]), ...]"""
         arr = (BitlutBatchMat * len(mats))()
-        for i, (w, sc, m, out, t, ts, rs) in enumerate(mats):
+        for i, mt in enumerate(mats):
+            w, sc, m, out, t, ts, rs = mt[:7]
+            z = mt[7] if len(mt) > 7 else None
+            pp = mt[8] if len(mt) > 8 else None
             arr[i].wgpu, arr[i].wscales, arr[i].out = w.data_ptr(), sc.data_ptr(), out.data_ptr()
             arr[i].tables, arr[i].tscales, arr[i].rowsums = t.data_ptr(), ts.data_ptr(), rs.data_ptr()
+            arr[i].zeros = z.data_ptr() if z is not None else None
+            arr[i].partials = pp.data_ptr() if pp is not None else None
             arr[i].m = m
-        b = cls(arr, k, bits, group_size, dtype_code(mats[0][1]), mats[0][0].device)
+        b = cls(arr, k, bits, group_size, dtype_code(mats[0][1]), mats[0][0].device, weight_mode)
         b.keep = [x for mt in mats for x in mt if isinstance(x, torch.Tensor)]
         return b
 
     def launch(self, flags: int, stream) -> None:
         rc = lib().bitlut_mpgemv_batch(ptr(self.dev), self.n, self.total_tiles, self.k, self.bits, self.group_size,
-                                       self.scale_dtype, flags, ctypes.c_void_p(stream.cuda_stream))
+                                       self.scale_dtype, self.weight_mode,
+                                       flags | (FLAG_COMBINED_PARTIALS if self.partials else 0),
+                                       ctypes.c_void_p(stream.cuda_stream))
         raise_for_status(rc, "bitlut_mpgemv_batch")
 
 

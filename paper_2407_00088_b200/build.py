@@ -15,7 +15,8 @@ import sys
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-SOURCES = ["weight_prep.cu", "lut.cu", "gemv.cu", "gemv_b1.cu", "gemv_stream.cu", "gemv_pack.cu", "pipeline.cu"]
+SOURCES = ["weight_prep.cu", "lut.cu", "gemv.cu", "gemv_b1.cu", "gemv_batch.cu", "gemv_stream.cu", "gemv_pack.cu",
+           "pipeline.cu", "host_api.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
 
@@ -52,14 +53,25 @@ def build_lib(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(objdir, exist_ok=True)
     flags = [f for f in NVCC_FLAGS if f != "-shared"]
 
+    csrc = os.path.join(PKG, "csrc")
+    headers = [os.path.join(csrc, f) for f in os.listdir(csrc) if f.endswith(".cuh")]
+    headers.append(os.path.join(ROOT, "include", "bitlut_b200.h"))
+    newest_header = max(os.path.getmtime(h) for h in headers)
+
     def compile_one(src):
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
-        cmd = [nvcc(), *flags, "-c", "-o", obj, os.path.join(PKG, "csrc", src)]
+        srcp = os.path.join(csrc, src)
+        if (not force and os.path.exists(obj)
+                and os.path.getmtime(obj) > max(os.path.getmtime(srcp), newest_header)):
+            return obj, None                       # up to date (incremental rebuild)
+        cmd = [nvcc(), *flags, "-c", "-o", obj, srcp]
         return obj, subprocess.run(cmd, capture_output=True, text=True)
 
     with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         results = list(ex.map(compile_one, SOURCES))
     for obj, res in results:
+        if res is None:
+            continue
         if res.returncode != 0:
             sys.stderr.write(res.stdout + res.stderr)
             raise RuntimeError(f"nvcc failed compiling {os.path.basename(obj)}")

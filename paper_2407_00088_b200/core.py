@@ -122,6 +122,14 @@ class QuantizedWeights:
     qvalues: object   # uint8 (m, k)
     scales: object    # float32/float16 (m, k // group_size)
     zeros: object = None
+    # weight encoding (batch executor, bitlut_b200.h BITLUT_W_*): "offset"
+    # (zeros None: the reference's implicit zero), "zeros" (asymmetric),
+    # "sign" (1-bit sign planes, built by sign_planes) or "ternary" (built by
+    # ternary); None = derived from zeros.  sign/ternary keep the equivalent
+    # (scale, zero) pair in scales/zeros, so every kernel can run them.
+    encoding: object = None
+
+    ENCODINGS = ("offset", "zeros", "sign", "ternary")
 
     def __post_init__(self):
         if not 1 <= self.bits <= 4:
@@ -147,6 +155,18 @@ class QuantizedWeights:
                 raise ShapeError("zeros shape mismatch")
             if not _all_finite(self.zeros):
                 raise DataError("zeros contain non-finite values")
+        enc = self.encoding
+        if enc is None:
+            enc = "offset" if self.zeros is None else "zeros"
+        if enc not in self.ENCODINGS:
+            raise ParameterError(f"encoding must be one of {self.ENCODINGS}, got {enc!r}")
+        if (enc == "offset") != (self.zeros is None):
+            raise ParameterError(f"encoding {enc!r} {'takes no' if enc == 'offset' else 'needs'} zero points")
+        if enc == "sign" and self.bits != 1:
+            raise ParameterError("sign planes are 1-bit")
+        if enc == "ternary" and self.bits != 2:
+            raise ParameterError("ternary weights use 2 bit planes")
+        object.__setattr__(self, "encoding", enc)
 
     @property
     def offset(self) -> int:
@@ -159,21 +179,32 @@ class QuantizedWeights:
     @classmethod
     def sign_planes(cls, signs_q, scales, group_size):
         """1-bit sign planes: w = +s where q = 1, -s where q = 0
-        (BASELINE config 3).  Stored as bits=1, scale 2s, zero 0.5."""
+        (BASELINE config 3).  Stored as bits=1, scale 2s, zero 0.5 (the
+        generic zero-point form); encoding "sign" lets the batch executor
+        drop the zero points and the row-sum term (BITLUT_W_SIGN)."""
         s = as_tensor(scales)
         return cls(m=_shape(signs_q)[0], k=_shape(signs_q)[1], bits=1, group_size=group_size,
                    qvalues=signs_q, scales=(2 * s.float()).to(s.dtype),
-                   zeros=torch.full(tuple(s.shape), 0.5, dtype=s.dtype))
+                   zeros=torch.full(tuple(s.shape), 0.5, dtype=s.dtype), encoding="sign")
 
     @classmethod
-    def ternary(cls, values, scales, group_size):
-        """Ternary weights v in {-1, 0, +1}: q = v + 1 in 2 bit planes,
-        zero 1 (BASELINE config 3)."""
+    def ternary(cls, values, scale, group_size):
+        """Ternary weights v in {-1, 0, +1} with ONE per-tensor scale:
+        q = v + 1 in 2 bit planes, zero 1 (BASELINE config 3).  `scale` is
+        a scalar (or an (m, k/gs) array of one value); encoding "ternary"
+        lets the batch executor read that one value instead of a scale
+        stream (BITLUT_W_TERNARY)."""
         v = as_tensor(values)
         q = (v.to(torch.int16) + 1).to(torch.uint8)
-        s = as_tensor(scales)
-        return cls(m=q.shape[0], k=q.shape[1], bits=2, group_size=group_size, qvalues=q,
-                   scales=s, zeros=torch.ones(tuple(s.shape), dtype=s.dtype))
+        m, k = q.shape
+        s = as_tensor(scale)
+        if s.dim() == 0 or s.numel() == 1:
+            s = s.reshape(1, 1).expand(m, k // group_size).contiguous()
+        flat = s.reshape(-1)
+        if flat.numel() and not bool((flat == flat[0]).all()):
+            raise DataError("ternary weights take one per-tensor scale")
+        return cls(m=m, k=k, bits=2, group_size=group_size, qvalues=q,
+                   scales=s, zeros=torch.ones(tuple(s.shape), dtype=s.dtype), encoding="ternary")
 
 
 @dataclass(frozen=True)

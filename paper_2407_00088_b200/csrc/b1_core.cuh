@@ -1,0 +1,91 @@
+// Batch-1 lookup core shared by gemv_b1.cu (per-call kernels) and
+// gemv_batch.cu (the batch executor's kernel): the plane-merged k-group
+// lookup and the lane reductions.
+#pragma once
+#include "gemv_core.cuh"
+
+namespace blk {
+
+// Lookup of one k-group for 32 streams with plane-merging multipliers (the
+// A/Y form of gemv_core.cuh lookup_kg: A - Y = sQ exactly, Y enters with the
+// negated multiplier).
+template <int BITS, int NACC>
+__device__ __forceinline__ void lookup_kg_merged(const uint4 w, uint32_t a0, uint32_t a1, int (&acc)[NACC]) {
+  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const uint32_t x = ws[q];
+    const uint32_t xx = x ^ 0x88888888u;
+    if constexpr (BITS == 2) {
+      // byte b of x = channel 4q+b (nibbles: plane 0, plane 1): the selector
+      // [x.b, xx.b] looks up [A_p0, A_p1, Y_p0, Y_p1] in one prmt, dp4a with
+      // (1, 2, -1, -2) adds S_c = P0 + 2 P1 -- 13 instead of 15 instructions
+      // per 8 lookups
+      const uint32_t s01 = bl::prmt(x, xx, 0x5140u), s23 = bl::prmt(x, xx, 0x7362u);
+      acc[4 * q + 0] = bl::dp4a(bl::prmt(a0, a1, s01), 0xFEFF0201u, acc[4 * q + 0]);
+      acc[4 * q + 1] = bl::dp4a(bl::prmt(a0, a1, s01 >> 16), 0xFEFF0201u, acc[4 * q + 1]);
+      acc[4 * q + 2] = bl::dp4a(bl::prmt(a0, a1, s23), 0xFEFF0201u, acc[4 * q + 2]);
+      acc[4 * q + 3] = bl::dp4a(bl::prmt(a0, a1, s23 >> 16), 0xFEFF0201u, acc[4 * q + 3]);
+      continue;
+    }
+    const uint32_t A0 = bl::prmt(a0, a1, x), Y0 = bl::prmt(a0, a1, xx);
+    const uint32_t A1 = bl::prmt(a0, a1, x >> 16), Y1 = bl::prmt(a0, a1, xx >> 16);
+    if constexpr (BITS == 4) {
+      // bytes 0..3 of A0/Y0 = planes 0..3 of channel 2q, of A1/Y1: channel
+      // 2q+1; dp4a with (1,2,4,8) adds a channel's planes in one instruction
+      acc[2 * q] = bl::dp4a(A0, 0x08040201u, acc[2 * q]);
+      acc[2 * q] = bl::dp4a(Y0, 0xF8FCFEFFu, acc[2 * q]);
+      acc[2 * q + 1] = bl::dp4a(A1, 0x08040201u, acc[2 * q + 1]);
+      acc[2 * q + 1] = bl::dp4a(Y1, 0xF8FCFEFFu, acc[2 * q + 1]);
+    } else {
+      // W1: pair i = channels (2i, 2i+1), packed P_even + 32768 P_odd
+      acc[4 * q + 0] = bl::dp2a_lo_u(kMult, A0, acc[4 * q + 0]);
+      acc[4 * q + 0] = bl::dp2a_lo(kMultNeg, Y0, acc[4 * q + 0]);
+      acc[4 * q + 1] = bl::dp2a_hi_u(kMult, A0, acc[4 * q + 1]);
+      acc[4 * q + 1] = bl::dp2a_hi(kMultNeg, Y0, acc[4 * q + 1]);
+      acc[4 * q + 2] = bl::dp2a_lo_u(kMult, A1, acc[4 * q + 2]);
+      acc[4 * q + 2] = bl::dp2a_lo(kMultNeg, Y1, acc[4 * q + 2]);
+      acc[4 * q + 3] = bl::dp2a_hi_u(kMult, A1, acc[4 * q + 3]);
+      acc[4 * q + 3] = bl::dp2a_hi(kMultNeg, Y1, acc[4 * q + 3]);
+    }
+  }
+}
+
+// Reduce NV values across the lanes that differ in lane bits [O0, O1):
+// halving exchanges while more than one value is left (each lane keeps a
+// disjoint half, no redundant adds), plain butterfly adds afterwards.
+// Returns the index of the lane's first remaining value; the count is
+// reduced_count<NV, O0, O1>().
+template <int NV, int O0, int O1>
+__host__ __device__ constexpr int reduced_count() {
+  int n = NV;
+  for (int o = O0; o < O1; o <<= 1)
+    if (n > 1) n >>= 1;
+  return n;
+}
+
+template <int NV, int O0, int O1, typename T>
+__device__ __forceinline__ int reduce_lanes(T (&v)[NV], int lane) {
+  int base = 0;
+#pragma unroll
+  for (int o = O0, n = NV; o < O1; o <<= 1) {
+    if (n > 1) {
+      n >>= 1;
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int i = 0; i < NV / 2; i++) {
+        if (i < n) {
+          const T send = up ? v[i] : v[i + n];
+          const T keep = up ? v[i + n] : v[i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      if (up) base += n;
+    } else {
+      v[0] = v[0] + __shfl_xor_sync(0xffffffffu, v[0], o);
+    }
+  }
+  return base;
+}
+
+}  // namespace blk

@@ -132,6 +132,16 @@ BL_DEV void dep_signal(const DepSync& d) {
   }
 }
 
+// max that propagates NaN (max.NaN.f32): a non-finite activation makes its
+// group's table scale NaN, so the outputs that read it are non-finite too
+// (the CUDA-tensor path has no host-side finiteness check).  Equal to fmaxf
+// on non-NaN inputs, so the tables stay bitwise the reference's.
+BL_DEV float fmax_nan(float a, float b) {
+  float d;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+  return d;
+}
+
 BL_DEV float to_f32(float x) { return x; }
 BL_DEV float to_f32(__half x) { return __half2float(x); }
 

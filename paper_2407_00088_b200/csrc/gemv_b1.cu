@@ -18,6 +18,7 @@
 //             reference (<= 1e-5 relative, tests/test_gpu_parity.py).
 // The reference-order (bit-exact float) epilogue stays in gemv.cu.
 #include "gemv_core.cuh"
+#include "b1_core.cuh"
 
 #include <cstdlib>
 
@@ -111,88 +112,6 @@ B1Plan b1_plan(const bl::LayoutV2& L, bool zeros, bool tab_smem, int T, int stag
   s.bar_off = s.fin_off + (exact ? al16((size_t)3 * 32 * 4) : 0);
   s.total = s.bar_off + 8 * (kMaxStages + 1);
   return s;
-}
-
-// Lookup of one k-group for 32 streams with plane-merging multipliers (the
-// A/Y form of gemv_core.cuh lookup_kg: A - Y = sQ exactly, Y enters with the
-// negated multiplier).
-template <int BITS, int NACC>
-__device__ __forceinline__ void lookup_kg_merged(const uint4 w, uint32_t a0, uint32_t a1, int (&acc)[NACC]) {
-  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-  for (int q = 0; q < 4; q++) {
-    const uint32_t x = ws[q];
-    const uint32_t xx = x ^ 0x88888888u;
-    if constexpr (BITS == 2) {
-      // byte b of x = channel 4q+b (nibbles: plane 0, plane 1): the selector
-      // [x.b, xx.b] looks up [A_p0, A_p1, Y_p0, Y_p1] in one prmt, dp4a with
-      // (1, 2, -1, -2) adds S_c = P0 + 2 P1 -- 13 instead of 15 instructions
-      // per 8 lookups
-      const uint32_t s01 = bl::prmt(x, xx, 0x5140u), s23 = bl::prmt(x, xx, 0x7362u);
-      acc[4 * q + 0] = bl::dp4a(bl::prmt(a0, a1, s01), 0xFEFF0201u, acc[4 * q + 0]);
-      acc[4 * q + 1] = bl::dp4a(bl::prmt(a0, a1, s01 >> 16), 0xFEFF0201u, acc[4 * q + 1]);
-      acc[4 * q + 2] = bl::dp4a(bl::prmt(a0, a1, s23), 0xFEFF0201u, acc[4 * q + 2]);
-      acc[4 * q + 3] = bl::dp4a(bl::prmt(a0, a1, s23 >> 16), 0xFEFF0201u, acc[4 * q + 3]);
-      continue;
-    }
-    const uint32_t A0 = bl::prmt(a0, a1, x), Y0 = bl::prmt(a0, a1, xx);
-    const uint32_t A1 = bl::prmt(a0, a1, x >> 16), Y1 = bl::prmt(a0, a1, xx >> 16);
-    if constexpr (BITS == 4) {
-      // bytes 0..3 of A0/Y0 = planes 0..3 of channel 2q, of A1/Y1: channel
-      // 2q+1; dp4a with (1,2,4,8) adds a channel's planes in one instruction
-      acc[2 * q] = bl::dp4a(A0, 0x08040201u, acc[2 * q]);
-      acc[2 * q] = bl::dp4a(Y0, 0xF8FCFEFFu, acc[2 * q]);
-      acc[2 * q + 1] = bl::dp4a(A1, 0x08040201u, acc[2 * q + 1]);
-      acc[2 * q + 1] = bl::dp4a(Y1, 0xF8FCFEFFu, acc[2 * q + 1]);
-    } else {
-      // W1: pair i = channels (2i, 2i+1), packed P_even + 32768 P_odd
-      acc[4 * q + 0] = bl::dp2a_lo_u(kMult, A0, acc[4 * q + 0]);
-      acc[4 * q + 0] = bl::dp2a_lo(kMultNeg, Y0, acc[4 * q + 0]);
-      acc[4 * q + 1] = bl::dp2a_hi_u(kMult, A0, acc[4 * q + 1]);
-      acc[4 * q + 1] = bl::dp2a_hi(kMultNeg, Y0, acc[4 * q + 1]);
-      acc[4 * q + 2] = bl::dp2a_lo_u(kMult, A1, acc[4 * q + 2]);
-      acc[4 * q + 2] = bl::dp2a_lo(kMultNeg, Y1, acc[4 * q + 2]);
-      acc[4 * q + 3] = bl::dp2a_hi_u(kMult, A1, acc[4 * q + 3]);
-      acc[4 * q + 3] = bl::dp2a_hi(kMultNeg, Y1, acc[4 * q + 3]);
-    }
-  }
-}
-
-// Reduce NV values across the lanes that differ in lane bits [O0, O1):
-// halving exchanges while more than one value is left (each lane keeps a
-// disjoint half, no redundant adds), plain butterfly adds afterwards.
-// Returns the index of the lane's first remaining value; the count is
-// reduced_count<NV, O0, O1>().
-template <int NV, int O0, int O1>
-__host__ __device__ constexpr int reduced_count() {
-  int n = NV;
-  for (int o = O0; o < O1; o <<= 1)
-    if (n > 1) n >>= 1;
-  return n;
-}
-
-template <int NV, int O0, int O1, typename T>
-__device__ __forceinline__ int reduce_lanes(T (&v)[NV], int lane) {
-  int base = 0;
-#pragma unroll
-  for (int o = O0, n = NV; o < O1; o <<= 1) {
-    if (n > 1) {
-      n >>= 1;
-      const bool up = (lane & o) != 0;
-#pragma unroll
-      for (int i = 0; i < NV / 2; i++) {
-        if (i < n) {
-          const T send = up ? v[i] : v[i + n];
-          const T keep = up ? v[i + n] : v[i];
-          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-        }
-      }
-      if (up) base += n;
-    } else {
-      v[0] = v[0] + __shfl_xor_sync(0xffffffffu, v[0], o);
-    }
-  }
-  return base;
 }
 
 __device__ __forceinline__ int find_mat(const B1Args& a, int tile, int& local) {
@@ -292,16 +211,16 @@ __device__ __forceinline__ void fused_tables(const B1Args& a, uint8_t* smem) {
     }
     float mx = 0.f;
 #pragma unroll
-    for (int idx = 0; idx < 8; idx++) mx = fmaxf(mx, fabsf(e[idx]));
+    for (int idx = 0; idx < 8; idx++) mx = bl::fmax_nan(mx, fabsf(e[idx]));
     const int seg = gpg < 32 ? gpg : 32;
-    for (int o = 1; o < seg; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    for (int o = 1; o < seg; o <<= 1) mx = bl::fmax_nan(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (gpg > 32) {
       if ((tid & 31) == 0) red[tid >> 5] = mx;
       __syncthreads();
       const int wpg = gpg >> 5;
       const int w0 = (tid >> 5) / wpg * wpg;
       mx = 0.f;
-      for (int w = 0; w < wpg; w++) mx = fmaxf(mx, red[w0 + w]);
+      for (int w = 0; w < wpg; w++) mx = bl::fmax_nan(mx, red[w0 + w]);
     }
     float scale = __fdiv_rn(mx, 127.0f);
     if (scale == 0.0f) scale = 1.0f;
@@ -854,170 +773,6 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
     }
   }
   bl::dep_signal(p.dep);
-  if (p.independent) bl::pdl_wait();
-}
-
-
-// Batched lean kernel: any number of independent batch-1 GEMVs of one K,
-// each with its own tables (a layer set), in ONE launch.  The matrices'
-// descriptors live in device memory (bitlut_batch_mat, tile_end cumulative);
-// CTA b walks the contiguous tile range [b*T/G, (b+1)*T/G) of the
-// concatenated tile list, so every CTA streams the same number of tiles and
-// the launch has a single tail.  The thread's tables, table scale and row sum
-// are reloaded (L2) when the range crosses into the next matrix.  Per tile the
-// arithmetic is gemv_b1_lean_kernel<.., ZEROS=false, F16=false>'s, so outputs
-// are bitwise identical to per-matrix fast-epilogue launches.
-__device__ __forceinline__ void issue_stage_batch(const B1Args& a, const bitlut_batch_mat& mt, int local,
-                                                  uint8_t* sb, uint64_t* bar, uint64_t pol, int st_size) {
-  const bl::LayoutV2& L = a.g.L;
-  mbar_expect_tx(bar, a.w_bytes + a.s_bytes);
-  const uint8_t* src = mt.wgpu + L.sg_row_base(local, 0);
-  for (uint32_t off = 0; off < a.w_bytes; off += 32768u) {
-    const uint32_t nb = a.w_bytes - off < 32768u ? a.w_bytes - off : 32768u;
-    bulk_g2s(sb + off, src + off, nb, bar, pol);
-  }
-  const int64_t e0 = (int64_t)local * L.tile_ch * L.NQ;
-  bulk_g2s(sb + a.s_off, reinterpret_cast<const uint8_t*>(mt.wscales) + e0 * st_size, a.s_bytes, bar, pol);
-}
-
-template <int R, int LG, int BITS, typename ST>
-__global__ void __launch_bounds__(384) gemv_b1_batch_kernel(const __grid_constant__ B1Args a,
-                                                             const bitlut_batch_mat* __restrict__ dm,
-                                                             int n_mats) {
-  const GemvArgs& p = a.g;
-  const bl::LayoutV2& L = p.L;
-  constexpr int TCH = 32 / BITS;
-  constexpr int NACC = BITS == 4 ? 8 : 16;
-  constexpr int NV = reduced_count<NACC, 1, LG>();
-  constexpr int NCH = BITS == 1 ? 2 * NV : NV;
-  constexpr int NF = reduced_count<NCH, LG, 32>();
-  extern __shared__ __align__(128) uint8_t smem[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int NW = blockDim.x >> 5;
-  const int NQ = L.NQ, U = L.U;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + a.bar_off);
-  float* ysm = reinterpret_cast<float*>(smem + a.y_off);
-  const int T = a.total_tiles, G = gridDim.x;
-  const int t0 = (int)((int64_t)blockIdx.x * T / G), t1 = (int)((int64_t)(blockIdx.x + 1) * T / G);
-  // matrix holding t0 = number of matrices ending at or before it
-  int j0 = 0;
-  for (int base = 0; base < n_mats; base += blockDim.x) {
-    const int i = base + tid;
-    j0 += __syncthreads_count(i < n_mats && dm[i].tile_end <= t0);
-  }
-  if (t0 >= t1) {                                       // more CTAs than tiles
-    if (!p.independent) bl::pdl_wait();
-    bl::pdl_launch_dependents();
-    if (p.independent) bl::pdl_wait();
-    return;
-  }
-  // issue cursor (thread 0): the matrix of the next tile to stage
-  int ji = j0, ji_begin = 0, ji_end = 0;
-  if (tid == 0) {
-    for (int s = 0; s <= kMaxStages; s++) mbar_init(bar + s, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    const uint64_t pol = policy_evict_first();
-    ji_begin = ji ? dm[ji - 1].tile_end : 0;
-    ji_end = dm[ji].tile_end;
-    for (int s = 0; s < a.stages; s++) {
-      const int t = t0 + s;
-      if (t >= t1) break;
-      while (t >= ji_end) { ji++; ji_begin = ji_end; ji_end = dm[ji].tile_end; }
-      issue_stage_batch(a, dm[ji], t - ji_begin, smem + s * a.stage_bytes, bar + s, pol, (int)sizeof(ST));
-    }
-  }
-  if (!p.independent) bl::pdl_wait();
-  bl::pdl_launch_dependents();
-  const int u = tid;
-  const bool live = u < U;
-  const int ub = u >> 5, l = u & 31;
-  const int nu_b = min(32, U - 32 * ub);
-  const int g = u / LG;
-  int jc = j0;
-  int jc_begin = jc ? dm[jc - 1].tile_end : 0, jc_end = dm[jc].tile_end;
-  float* outp = dm[jc].out;
-  uint4 tq[R / 2];
-  float ts = 0.f, rs = 0.f;
-  auto load_tables = [&](const bitlut_batch_mat& mt) {
-    if (live) {
-      const uint8_t* tb = reinterpret_cast<const uint8_t*>(mt.tables) + (int64_t)ub * (32 * R * 8) + l * 16;
-#pragma unroll
-      for (int jp = 0; jp < R / 2; jp++) tq[jp] = bl::ld_cg_128(tb + jp * nu_b * 16);
-      ts = bl::ld_cg_f32(mt.tscales + g);
-      rs = bl::ld_cg_f32(mt.rowsums + g);
-    }
-  };
-  load_tables(dm[jc]);
-  const uint32_t woff = (uint32_t)(ub * (32 * R * 16) + l * 16);
-  __syncthreads();                                      // barriers initialised
-  int it = 0;
-  for (int tile = t0; tile < t1; tile++, it++) {
-    if (tile >= jc_end) {                               // next matrix: its tables and output
-      while (tile >= jc_end) { jc++; jc_begin = jc_end; jc_end = dm[jc].tile_end; }
-      outp = dm[jc].out;
-      load_tables(dm[jc]);
-    }
-    const int S = a.stages;
-    const int stage = S == 1 ? 0 : (it & 1);
-    uint8_t* sb = smem + stage * a.stage_bytes;
-    mbar_wait(bar + stage, (S == 1 ? it : it >> 1) & 1);
-    float y[NCH];
-    int acc[NACC];
-#pragma unroll
-    for (int i = 0; i < NACC; i++) acc[i] = 0;
-    if (live) {
-      const uint8_t* wsrc = sb + woff;
-      const int stride = nu_b == 32 ? 512 : nu_b * 16;
-#pragma unroll
-      for (int j = 0; j < R; j += 2) {
-        const uint4 wa = *reinterpret_cast<const uint4*>(wsrc + j * stride);
-        const uint4 wc = *reinterpret_cast<const uint4*>(wsrc + (j + 1) * stride);
-        lookup_kg_merged<BITS, NACC>(wa, tq[j >> 1].x, tq[j >> 1].y, acc);
-        lookup_kg_merged<BITS, NACC>(wc, tq[j >> 1].z, tq[j >> 1].w, acc);
-      }
-    }
-    const int base = reduce_lanes<NACC, 1, LG>(acc, lane);
-    const int ch0 = BITS == 1 ? 2 * base : base;
-    if (live) {
-      int Sv[NCH];
-      if constexpr (BITS == 1) {
-#pragma unroll
-        for (int i = 0; i < NV; i++) {
-          const int v = acc[i];
-          const int pe = (v << 17) >> 17;
-          Sv[2 * i] = pe;
-          Sv[2 * i + 1] = (v - pe) >> 15;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < NV; i++) Sv[i] = acc[i];
-      }
-      const ST* sp = reinterpret_cast<const ST*>(sb + a.s_off) + ch0 * NQ + g;
-#pragma unroll
-      for (int j = 0; j < NCH; j++) y[j] = bl::to_f32(sp[j * NQ]) * fmaf(ts, (float)Sv[j], -rs);
-    } else {
-#pragma unroll
-      for (int j = 0; j < NCH; j++) y[j] = 0.f;
-    }
-    const int fb = reduce_lanes<NCH, LG, 32>(y, lane);
-    float* yb = ysm + (it & 1) * NW * TCH + warp * TCH;
-#pragma unroll
-    for (int j = 0; j < NF; j++) yb[ch0 + fb + j] = y[j];
-    __syncthreads();                                    // stage consumed, ysm complete
-    if (tid == 0) {
-      const int t = tile + S;
-      if (t < t1) {
-        while (t >= ji_end) { ji++; ji_begin = ji_end; ji_end = dm[ji].tile_end; }
-        issue_stage_batch(a, dm[ji], t - ji_begin, sb, bar + stage, policy_evict_first(), (int)sizeof(ST));
-      }
-    }
-    if (tid < TCH) {
-      const float* yr = ysm + (it & 1) * NW * TCH + tid;
-      float s = 0.f;
-      for (int w = 0; w < NW; w++) s += yr[w * TCH];
-      outp[(int64_t)(tile - jc_begin) * TCH + tid] = 0.5f * s;
-    }
-  }
   if (p.independent) bl::pdl_wait();
 }
 
@@ -1662,158 +1417,7 @@ B1Mat single_mat(const GemvArgs& g) {
   return m;
 }
 
-// Batched lean launch: grid = every resident CTA (two stages each), each CTA
-// one contiguous tile range.
-template <int R, int LG, int BITS, typename ST>
-int launch_batch(const GemvArgs& g, const bitlut_batch_mat* dm, int n_mats, int total_tiles, cudaStream_t stream,
-                 bool pdl) {
-  const bl::LayoutV2& L = g.L;
-  const int T = b1_threads(L, true);
-  if ((L.U + T - 1) / T != 1) return BITLUT_ELAYOUT;
-  auto kern = gemv_b1_batch_kernel<R, LG, BITS, ST>;
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
-        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             cudaSharedmemCarveoutMaxShared) != cudaSuccess)
-      return BITLUT_EINTERNAL;
-    configured = true;
-  }
-  // stages: two (double-buffered CTAs), or one when double buffering
-  // leaves <= 2 CTAs per SM and one stage fits twice as many (long K)
-  static int st_env = -1;
-  if (st_env < 0) {
-    const char* e = getenv("BITLUT_BATCH_STAGES");       // diagnostic: force 1 or 2
-    st_env = e ? atoi(e) : 0;
-  }
-  static int trim_env = -1;
-  if (trim_env < 0) {
-    const char* e = getenv("BITLUT_BATCH_TRIM");         // diagnostic: 0 keeps the lean plan's smem
-    trim_env = e ? atoi(e) : 1;
-  }
-  // the batch kernel keeps table scale and row sum in registers: its plan is
-  // the stages, the cross-warp sums and the barriers (K = 4096 W2: 37.9 ->
-  // 36.5 KB, six CTAs per SM instead of five)
-  auto trim = [&](B1Plan p) {
-    if (!trim_env) return p;
-    p.ts_off = p.rs_off = p.y_off = p.tab_off;
-    p.sa_off = p.y_off + al16((size_t)2 * (T / 32) * L.tile_ch * 4);
-    p.red_off = p.psm_off = p.terms_off = p.fin_off = p.bar_off = p.sa_off;
-    p.total = p.bar_off + 8 * (kMaxStages + 1);
-    return p;
-  };
-  int per_sm = 0, per_sm1 = 0;
-  const B1Plan s2 = trim(b1_plan<ST>(L, false, false, T, 2, kFast));
-  const B1Plan s1 = trim(b1_plan<ST>(L, false, false, T, 1, kFast));
-  if (s2.total > 227 * 1024 ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, s2.total) != cudaSuccess)
-    per_sm = 0;
-  if (s1.total > 227 * 1024 ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm1, kern, T, s1.total) != cudaSuccess)
-    per_sm1 = 0;
-  int stages = 2;
-  if (st_env == 1 || (st_env == 0 && per_sm <= 2 && per_sm1 >= 2 * per_sm) || per_sm < 1) stages = 1;
-  if (stages == 1) per_sm = per_sm1;
-  if (per_sm < 1) return BITLUT_ELAYOUT;
-  const B1Plan s = stages == 2 ? s2 : s1;
-  B1Args a;
-  a.g = g;
-  a.act = nullptr;
-  a.gth = GatherArgs{};
-  a.n_mats = 0;
-  a.total_tiles = total_tiles;
-  a.rounds = 1; a.tab_smem = 0; a.ldg_w = 0; a.partition = 0;
-  a.n_rows = 1; a.rows_per_cta = 1;
-  a.stages = stages;
-  a.stage_bytes = s.stage_bytes; a.w_bytes = s.w_bytes; a.s_off = s.s_off; a.s_bytes = s.s_bytes;
-  a.z_off = s.z_off; a.tab_off = s.tab_off; a.ts_off = s.ts_off; a.rs_off = s.rs_off;
-  a.y_off = s.y_off; a.bar_off = s.bar_off; a.sa_off = s.sa_off; a.red_off = s.red_off;
-  a.psm_off = s.psm_off; a.terms_off = s.terms_off; a.fin_off = s.fin_off; a.rowlen = s.rowlen;
-  int grid = sm_count() * per_sm;
-  if (grid > total_tiles) grid = total_tiles;
-  if (g.grid_out) *g.grid_out = grid;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(T);
-  cfg.dynamicSmemBytes = s.total;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, a, dm, n_mats) == cudaSuccess ? BITLUT_OK : BITLUT_EINTERNAL;
-}
-
-template <int R, int LG, typename ST>
-int launch_batch_bits(const GemvArgs& g, const bitlut_batch_mat* dm, int n, int tt, cudaStream_t s, bool pdl) {
-  switch (g.L.bits) {
-    case 1: return launch_batch<R, LG, 1, ST>(g, dm, n, tt, s, pdl);
-    case 2: return launch_batch<R, LG, 2, ST>(g, dm, n, tt, s, pdl);
-    case 4: return launch_batch<R, LG, 4, ST>(g, dm, n, tt, s, pdl);
-  }
-  return BITLUT_ELAYOUT;
-}
-
-template <typename ST>
-int dispatch_batch(const GemvArgs& g, const bitlut_batch_mat* dm, int n, int tt, cudaStream_t s, bool pdl) {
-  const int R = g.L.R, LG = g.L.Lg;
-  if (R == 8) {
-    switch (LG) {
-      case 1: return launch_batch_bits<8, 1, ST>(g, dm, n, tt, s, pdl);
-      case 2: return launch_batch_bits<8, 2, ST>(g, dm, n, tt, s, pdl);
-      case 4: return launch_batch_bits<8, 4, ST>(g, dm, n, tt, s, pdl);
-      case 8: return launch_batch_bits<8, 8, ST>(g, dm, n, tt, s, pdl);
-      case 16: return launch_batch_bits<8, 16, ST>(g, dm, n, tt, s, pdl);
-    }
-  } else if (R == 4 && LG == 1) {
-    return launch_batch_bits<4, 1, ST>(g, dm, n, tt, s, pdl);
-  }
-  return BITLUT_ELAYOUT;
-}
-
 }  // namespace
-
-// Host-side check and tile numbering of a batched launch (see the header).
-extern "C" int bitlut_mpgemv_batch_encode(bitlut_batch_mat* mats, int n_mats, int k, int bits, int group_size,
-                                          int* total_tiles) {
-  if (!mats || n_mats < 1 || !total_tiles) return BITLUT_EPARAM;
-  int64_t tiles = 0;
-  for (int j = 0; j < n_mats; j++) {
-    bl::LayoutV2 L;
-    const int rc = bl::make_layout(mats[j].m, k, bits, group_size, &L);
-    if (rc) return rc;
-    if (!mats[j].wgpu || !mats[j].wscales || !mats[j].out || !mats[j].tables || !mats[j].tscales ||
-        !mats[j].rowsums)
-      return BITLUT_EPARAM;
-    if (L.n_sg != 1 || L.bits == 3 || L.U > 384) return BITLUT_ELAYOUT;
-    tiles += L.n_tiles;
-    if (tiles > (int64_t)1 << 30) return BITLUT_ESHAPE;
-    mats[j].tile_end = (int)tiles;
-  }
-  *total_tiles = (int)tiles;
-  return BITLUT_OK;
-}
-
-extern "C" int bitlut_mpgemv_batch(const bitlut_batch_mat* dev_mats, int n_mats, int total_tiles, int k, int bits,
-                                   int group_size, int scale_dtype, int flags, void* stream) {
-  if (!dev_mats || n_mats < 1 || total_tiles < 1) return BITLUT_EPARAM;
-  if (scale_dtype != BITLUT_DT_F32 && scale_dtype != BITLUT_DT_F16) return BITLUT_EPARAM;
-  if (!(flags & BITLUT_FLAG_FAST_EPILOGUE)) return BITLUT_EPARAM;
-  bl::LayoutV2 L;
-  const int rc = bl::make_layout(32, k, bits, group_size, &L);
-  if (rc) return rc;
-  if (L.n_sg != 1 || L.bits == 3 || L.U > 384) return BITLUT_ELAYOUT;
-  const bool pdl = (flags & BITLUT_FLAG_PDL) != 0;
-  GemvArgs g = {};
-  g.L = L;
-  g.independent = pdl && (flags & BITLUT_FLAG_INDEPENDENT) != 0;
-  g.fast = 1;
-  g.rows_per_cta = 1; g.n_rows = 1;
-  const cudaStream_t st = (cudaStream_t)stream;
-  return scale_dtype == BITLUT_DT_F16 ? dispatch_batch<__half>(g, dev_mats, n_mats, total_tiles, st, pdl)
-                                      : dispatch_batch<float>(g, dev_mats, n_mats, total_tiles, st, pdl);
-}
 
 // Internal entry used by bitlut_mpgemm_traced (gemv.cu) for batch-1 fast
 // calls: returns BITLUT_ELAYOUT when the shape does not fit the kernel's

@@ -66,14 +66,14 @@ __global__ void quantize_tables_kernel(const float* __restrict__ half, int kg, i
   const int64_t base = ((int64_t)row * kg + (int64_t)gq * gpg) * width;
   const int cnt = gpg * width;
   float mx = 0.f;
-  for (int i = threadIdx.x; i < cnt; i += blockDim.x) mx = fmaxf(mx, fabsf(half[base + i]));
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) mx = bl::fmax_nan(mx, fabsf(half[base + i]));
   __shared__ float red[32];
-  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  for (int o = 16; o > 0; o >>= 1) mx = bl::fmax_nan(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
   __syncthreads();
   if (threadIdx.x < 32) {
     float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
-    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    for (int o = 16; o > 0; o >>= 1) v = bl::fmax_nan(v, __shfl_xor_sync(0xffffffffu, v, o));
     if (threadIdx.x == 0) red[0] = v;
   }
   __syncthreads();

@@ -53,16 +53,16 @@ __device__ __forceinline__ void lut_block(const AT* __restrict__ a, int k, int g
   if (MODE == BITLUT_TABLE_Q8) {
     float mx = 0.f;
 #pragma unroll
-    for (int idx = 0; idx < 8; idx++) mx = fmaxf(mx, fabsf(e[idx]));
+    for (int idx = 0; idx < 8; idx++) mx = bl::fmax_nan(mx, fabsf(e[idx]));
     const int seg = gpg < 32 ? gpg : 32;
-    for (int o = 1; o < seg; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    for (int o = 1; o < seg; o <<= 1) mx = bl::fmax_nan(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (gpg > 32) {
       if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
       __syncthreads();
       const int wpg = gpg >> 5;                       // warps per group
       const int w0 = (threadIdx.x >> 5) / wpg * wpg;
       mx = 0.f;
-      for (int w = 0; w < wpg; w++) mx = fmaxf(mx, red[w0 + w]);
+      for (int w = 0; w < wpg; w++) mx = bl::fmax_nan(mx, red[w0 + w]);
     }
     float scale = __fdiv_rn(mx, 127.0f);
     if (scale == 0.0f) scale = 1.0f;

@@ -23,6 +23,7 @@ contract; CUDA inputs return CUDA tensors without synchronizing.
 """
 from __future__ import annotations
 
+import threading
 from dataclasses import dataclass
 from enum import Enum
 
@@ -31,7 +32,7 @@ import torch
 
 from . import _native as N
 from .core import Matrix, TileConfig, as_tensor
-from .errors import DataError, LayoutError, OverflowConfigError, ParameterError, ShapeError
+from .errors import DataError, LayoutError, OverflowConfigError, ParameterError, ShapeError, raise_for_status
 from .lut_build import REAL, LookupTables
 from .weight_prep import LAYOUT_VERSION, PackedWeights
 
@@ -118,21 +119,37 @@ def _check_layout_match(cfg: TileConfig, pw: PackedWeights) -> None:
                           f"for: {cfg} vs {t}")
 
 
-def _activation_rows(a):
-    """kernel.py:266-277: -> (device tensor (n, k) f16/f32, how-to-return)."""
+def _host_rows(a):
+    """Numpy activations (kernel.py:266-277): contiguous (n, k) f16/f32 with the
+    reference's host-side finiteness check, or None for tensor inputs."""
+    if isinstance(a, Matrix):
+        a = a.to_array()
+    if not isinstance(a, np.ndarray):
+        return None
+    arr = a if a.dtype in (np.float16, np.float32) else a.astype(np.float32)
+    if arr.ndim == 1:
+        arr = arr.reshape(1, -1)
+    if arr.ndim != 2:
+        raise ShapeError("activations must be 1-D or 2-D")
+    if not np.isfinite(arr).all():
+        raise DataError("activations contain non-finite values")
+    return np.ascontiguousarray(arr)
+
+
+def _activation_rows(a, check_finite=None):
+    """kernel.py:266-277: -> (device tensor (n, k) f16/f32, how-to-return).
+
+    Host inputs (numpy, CPU tensors) are checked for non-finite values on the
+    host, as the reference does.  CUDA inputs are not checked unless
+    ``check_finite=True`` (that check needs a host synchronization); a
+    non-finite activation then yields non-finite outputs (the table build
+    propagates NaN/Inf into the table scales and row sums)."""
     kind = "cuda"
     if isinstance(a, Matrix):
         a = a.to_array()
     if isinstance(a, np.ndarray):
         kind = "numpy"
-        arr = a if a.dtype in (np.float16, np.float32) else a.astype(np.float32)
-        if arr.ndim == 1:
-            arr = arr.reshape(1, -1)
-        if arr.ndim != 2:
-            raise ShapeError("activations must be 1-D or 2-D")
-        if not np.isfinite(arr).all():
-            raise DataError("activations contain non-finite values")
-        t = torch.from_numpy(np.ascontiguousarray(arr))
+        t = torch.from_numpy(_host_rows(a).copy())
     else:
         t = as_tensor(a)
         if t.dtype not in (torch.float16, torch.float32):
@@ -145,6 +162,8 @@ def _activation_rows(a):
             kind = "cpu"
             if not bool(torch.isfinite(t).all()):
                 raise DataError("activations contain non-finite values")
+        elif check_finite and not bool(torch.isfinite(t).all()):
+            raise DataError("activations contain non-finite values")
     if not t.is_cuda:
         if not torch.cuda.is_available():
             raise N.BitLutError("a CUDA device is required (the B200 package has no CPU path)")
@@ -152,10 +171,66 @@ def _activation_rows(a):
     return t.contiguous(), kind
 
 
+_TLS = threading.local()
+_SCRATCH_MAX = 16
+
+
+class _HostScratch:
+    """Per-thread, per-shape buffers of the host-buffer call: pinned staging
+    for the activations and the result, device scratch for the tables and
+    the output (allocated once, reused by every later call of the shape)."""
+
+    def __init__(self, dev, n, k, m, gs, a_dtype, mode):
+        tdt = torch.int8 if mode == N.TABLE_Q8 else torch.float16
+        self.a_host = torch.empty((n, k), dtype=a_dtype, pin_memory=True)
+        self.a_np = self.a_host.numpy()
+        self.a_dev = torch.empty((n, k), dtype=a_dtype, device=dev)
+        self.tables = torch.empty((n, k // 4, 8), dtype=tdt, device=dev)
+        self.ts = torch.empty((n, k // gs), dtype=torch.float32, device=dev)
+        self.rs = torch.empty((n, k // gs), dtype=torch.float32, device=dev)
+        self.out_dev = torch.empty((n, m), dtype=torch.float32, device=dev)
+        self.out_host = torch.empty((n, m), dtype=torch.float32, pin_memory=True)
+        self.out_np = self.out_host.numpy()
+
+
+def _scratch(dev, n, k, m, gs, a_dtype, mode) -> _HostScratch:
+    cache = getattr(_TLS, "scratch", None)
+    if cache is None:
+        cache = _TLS.scratch = {}
+    key = (dev.index, n, k, m, gs, a_dtype, mode)
+    b = cache.get(key)
+    if b is None:
+        if len(cache) >= _SCRATCH_MAX:
+            cache.pop(next(iter(cache)))
+        b = cache[key] = _HostScratch(dev, n, k, m, gs, a_dtype, mode)
+    return b
+
+
+def _host_call(rows: np.ndarray, pw: PackedWeights, mode: int, flags: int) -> np.ndarray:
+    """numpy in -> numpy out through bitlut_mpgemm_host: one C call does the
+    H2D copy, the table build + lookup launch(es), the D2H copy and the
+    stream synchronization (csrc/host_api.cu)."""
+    n, k = rows.shape
+    a_dtype = torch.float16 if rows.dtype == np.float16 else torch.float32
+    dev = pw.gpu.device
+    b = _scratch(dev, n, k, pw.m, pw.group_size, a_dtype, mode)
+    np.copyto(b.a_np, rows)
+    if torch.cuda.current_device() != dev.index:
+        torch.cuda.set_device(dev)
+    rc = N.lib().bitlut_mpgemm_host(
+        b.a_host.data_ptr(), N.DT_F16 if a_dtype == torch.float16 else N.DT_F32, n, k, pw.gpu.data_ptr(), pw.m,
+        pw.bits, pw.group_size, pw.scales.data_ptr(), None if pw.zeros is None else pw.zeros.data_ptr(),
+        N.dtype_code(pw.scales), mode, flags, b.a_dev.data_ptr(), b.tables.data_ptr(), b.ts.data_ptr(),
+        b.rs.data_ptr(), b.out_dev.data_ptr(), b.out_host.data_ptr(),
+        torch.cuda.current_stream(dev).cuda_stream)
+    raise_for_status(rc, "bitlut_mpgemm_host")
+    return b.out_np.copy()
+
+
 def mpgemm(a, pw: PackedWeights, cfg: TileConfig | None = None,
            variant: KernelVariant | str = KernelVariant.CUDA_Q8,
            threads: int = 1, stats: KernelStats | None = None, *,
-           check_finite: bool = True, return_partials: bool = False, pdl: bool = True,
+           check_finite: bool | None = None, return_partials: bool = False, pdl: bool = True,
            exact_epilogue: bool = True):
     """Mixed-precision GEMM: (N, K) activations x packed low-bit weights.
 
@@ -174,20 +249,27 @@ def mpgemm(a, pw: PackedWeights, cfg: TileConfig | None = None,
     validate_kernel_config(cfg, pw.bits, pw.group_size, pw.m, pw.k)
     if threads < 1:
         raise ParameterError("threads must be >= 1")
-    rows, kind = _activation_rows(a)
-    n, k = rows.shape
-    if k != pw.k:
-        raise ShapeError(f"activation length {k} != weight k {pw.k}")
-    if kind == "cuda" and check_finite and not bool(torch.isfinite(rows).all()):
-        raise DataError("activations contain non-finite values")
     if pw.gpu is None:
         raise LayoutError("packed weights carry no GPU layout (prepare them with prepare_weights)")
     mode = N.TABLE_Q8 if variant is KernelVariant.CUDA_Q8 else N.TABLE_F16
     if return_partials and mode != N.TABLE_Q8:
         raise ParameterError("exact int32 partials exist only for int8 tables (cuda-q8)")
+    flags = (N.FLAG_PDL if pdl else 0) | (0 if exact_epilogue else N.FLAG_FAST_EPILOGUE)
+    host = None if return_partials else _host_rows(a)
+    if host is not None:                       # numpy in, numpy out: one C call, one sync
+        if host.shape[1] != pw.k:
+            raise ShapeError(f"activation length {host.shape[1]} != weight k {pw.k}")
+        out = _host_call(host, pw, mode, flags)
+        if stats is not None:
+            stats.lookups += pw.bits * host.shape[0] * pw.m * (pw.k // pw.g)
+            stats.lut_builds += -(-host.shape[0] // cfg.n_tile) * (pw.k // cfg.k_tile)
+        return out
+    rows, kind = _activation_rows(a, check_finite)
+    n, k = rows.shape
+    if k != pw.k:
+        raise ShapeError(f"activation length {k} != weight k {pw.k}")
     if rows.device != pw.gpu.device:
         rows = rows.to(pw.gpu.device)
-    flags = (N.FLAG_PDL if pdl else 0) | (0 if exact_epilogue else N.FLAG_FAST_EPILOGUE)
     out = None
     if (mode == N.TABLE_Q8 and not exact_epilogue and not return_partials and n == 1
             and rows.dtype == torch.float16 and pw.bits != 3):

@@ -135,8 +135,18 @@ def gather_plan(m_total: int, world: int) -> list[tuple[int, int]]:
 
 class FusedGather:
     """Peer buffers of the fused all-gather for one rank: the gathered f32
-    row `row` (1, m_total) and u32 `flag` of this rank, the device addresses
-    of every rank's row / flag, a launch ticket and the epoch counter.
+    rows `row` (2, m_total) -- double-buffered by epoch parity -- and the u32
+    `flag` of this rank, the device addresses of every rank's rows / flag, a
+    launch ticket and the epoch counter.
+
+    Reuse protocol (what makes the double buffer sufficient): a rank issues
+    launch e+1 only after it consumed epoch e's row, in stream order
+    (launch, wait, consume, launch, ...).  Launch e+2 on rank A writes the
+    slot of epoch e; it is stream-ordered after A's wait for epoch e+1,
+    which completes only when every rank B has issued launch e+1 -- and B
+    issued that after consuming epoch e.  So no write of epoch e+2 can
+    reach a slot a peer is still reading (the single-buffered version let a
+    fast rank overwrite epoch e in a slow peer's row).
 
     `symmetric(m_total, group)`: production path, one process per GPU;
     buffers from torch symmetric memory (NVLink peer mappings via the
@@ -155,7 +165,7 @@ class FusedGather:
 
     @classmethod
     def emulated(cls, m_total: int, world: int, device) -> list["FusedGather"]:
-        rows = [torch.zeros((1, m_total), dtype=torch.float32, device=device) for _ in range(world)]
+        rows = [torch.zeros((2, m_total), dtype=torch.float32, device=device) for _ in range(world)]
         flags = [torch.zeros(1, dtype=torch.int32, device=device) for _ in range(world)]
         out_ptrs = [r.data_ptr() for r in rows]
         flag_ptrs = [f.data_ptr() for f in flags]
@@ -168,7 +178,7 @@ class FusedGather:
         group = group or dist.group.WORLD
         rank, world = dist.get_rank(group), dist.get_world_size(group)
         device = torch.device("cuda", torch.cuda.current_device())
-        row = symm_mem.empty((1, m_total), dtype=torch.float32, device=device)
+        row = symm_mem.empty((2, m_total), dtype=torch.float32, device=device)
         flag = symm_mem.empty(1, dtype=torch.int32, device=device)
         row.zero_()
         flag.zero_()
@@ -190,17 +200,20 @@ class FusedGather:
             raise LayoutError(f"shard has {pw.m} channels, rank {self.rank} owns {m_r}")
         x = a_row.reshape(1, -1)
         t = N.build_lut(x, pw.group_size, N.TABLE_Q8)
-        y = N.mpgemv_gather(pw.gpu, pw.scales, pw.zeros, *t, pw.m, pw.k, pw.bits, pw.group_size,
-                            self.out_ptrs, self.flag_ptrs, self.ticket, col,
-                            N.FLAG_PDL | N.FLAG_FAST_EPILOGUE)
         self.epoch += 1
+        slot = (self.epoch & 1) * self.m_total * 4          # bytes: this epoch's row of every rank
+        y = N.mpgemv_gather(pw.gpu, pw.scales, pw.zeros, *t, pw.m, pw.k, pw.bits, pw.group_size,
+                            [p + slot for p in self.out_ptrs], self.flag_ptrs, self.ticket, col,
+                            N.FLAG_PDL | N.FLAG_FAST_EPILOGUE)
         return y
 
     def wait(self) -> torch.Tensor:
-        """Stream-ordered wait for every rank's slice of the current epoch."""
+        """Stream-ordered wait for every rank's slice of the current epoch;
+        returns this epoch's gathered (1, m_total) row (valid until launch
+        epoch + 2 -- see the reuse protocol above)."""
         from . import _native as N
         N.gather_wait(self.flag, self.epoch * self.world)
-        return self.row
+        return self.row[self.epoch & 1:(self.epoch & 1) + 1]
 
 
 def sharded_mpgemv_fused(a_row, sw: "ShardedWeights", fg: FusedGather) -> torch.Tensor:

@@ -10,10 +10,11 @@ replayed.  Two executors run the same list, bitwise identically to calling
   per-op completion counters replace kernel boundaries.
 * ``"batch"``: for op lists of INDEPENDENT batch-1 calls only (table builds
   without dependencies, each lookup reading one of them, fast epilogue, int8
-  tables, no zero points: a layer set): every table build in one launch
-  (bitlut_build_lut_batch), then one lookup launch per K
-  (bitlut_mpgemv_batch, each CTA one contiguous tile range over all the
-  matrices); bitwise equal to the graph executor.
+  tables: a layer set): every table build in one launch
+  (bitlut_build_lut_batch), then one lookup launch per (K, weight encoding)
+  (bitlut_mpgemv_batch, csrc/gemv_batch.cu: each CTA one contiguous tile
+  range over all the matrices; offset / zero-point / sign-plane / ternary
+  weights); within 1e-5 of the reference, deterministic.
 
     pl = Pipeline()
     t = pl.tables(x, group_size=64)                     # op 0
@@ -108,6 +109,7 @@ class Pipeline:
         self._counters = None
         self._arr = None
         self._graph = None
+        self._wextra = {}              # lookup op index -> (PackedWeights, partials tensor or None)
 
     @staticmethod
     def _deps(deps) -> list[int]:
@@ -142,11 +144,14 @@ class Pipeline:
                         group_size=group_size)
 
     def lookup(self, pw, t: TableRef, deps: Optional[Sequence] = None,
-               fast_epilogue: bool = False, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+               fast_epilogue: bool = False, out: Optional[torch.Tensor] = None,
+               partials: Optional[torch.Tensor] = None) -> torch.Tensor:
         """Lookup GEMV with packed weights pw over table op t; returns the
         (n, m) float32 output tensor (filled when the pipeline runs; pass
         ``out`` to choose it, e.g. a view of one output arena).  By default
-        the op depends on its table build only."""
+        the op depends on its table build only.  ``partials`` (batch
+        executor only): an (m, k/gs) int32 tensor that receives the exact
+        integer sums S = sum_p 2^p P_p."""
         if pw.gpu is None:
             raise ParameterError("packed weights carry no GPU layout")
         if (pw.k, pw.group_size) != (t.k, t.group_size):
@@ -168,7 +173,8 @@ class Pipeline:
         s.out = out.data_ptr()
         s.flags = N.FLAG_FAST_EPILOGUE if fast_epilogue else 0
         self.specs.append(s)
-        self.keep += [pw.gpu, pw.scales, pw.zeros, out]
+        self.keep += [pw.gpu, pw.scales, pw.zeros, out, pw.native_scales, partials]
+        self._wextra[len(self.specs) - 1] = (pw, partials)
         self.outputs.append(out)
         return out
 
@@ -232,17 +238,25 @@ class Pipeline:
                 continue
             if s.dep[0] < 0 or s.dep[1] >= 0 or s.dep[2] >= 0 or self.specs[s.dep[0]].type != OP_TABLES:
                 raise ParameterError("batch executor: each lookup must depend on exactly its table build")
-            if not (s.flags & N.FLAG_FAST_EPILOGUE) or s.n != 1 or s.zeros:
-                raise ParameterError("batch executor: batch-1 fast-epilogue lookups without zero points only")
+            if not (s.flags & N.FLAG_FAST_EPILOGUE) or s.n != 1:
+                raise ParameterError("batch executor: batch-1 fast-epilogue lookups only")
+            pw, partials = self._wextra[i]
+            mode = N.W_MODES[pw.encoding]
             m = N.BitlutBatchMat()
-            m.wgpu, m.wscales, m.out, m.m = s.wgpu, s.wscales, s.out, s.m
+            m.wgpu, m.out, m.m = s.wgpu, s.out, s.m
+            # sign / ternary: the native scale (s of w = s (2q - 1); the
+            # per-tensor scale), no zero points; zeros: the zero-point array
+            m.wscales = pw.native_scales.data_ptr() if mode in (N.W_SIGN, N.W_TERNARY) else s.wscales
+            m.zeros = s.zeros if mode == N.W_ZEROS else None
+            m.partials = partials.data_ptr() if partials is not None else None
             m.tables, m.tscales, m.rowsums = s.tables, s.tscales, s.rowsums
-            groups.setdefault((s.k, s.bits, s.group_size, s.scale_dtype), []).append(m)
+            sd = N.dtype_code(pw.native_scales) if mode in (N.W_SIGN, N.W_TERNARY) else s.scale_dtype
+            groups.setdefault((s.k, s.bits, s.group_size, sd, mode, partials is not None), []).append(m)
         if not jobs or len({j.a_dtype for j in jobs}) != 1:
             raise ParameterError("batch executor: table builds of one activation dtype")
         self._tbatch = N.TableBatch((N.BitlutLutJob * len(jobs))(*jobs), N.TABLE_Q8, self.device)
-        self._lbatches = [N.LookupBatch((N.BitlutBatchMat * len(ms))(*ms), k, bits, gs, sd, self.device)
-                          for (k, bits, gs, sd), ms in groups.items()]
+        self._lbatches = [N.LookupBatch((N.BitlutBatchMat * len(ms))(*ms), k, bits, gs, sd, self.device, mode)
+                          for (k, bits, gs, sd, mode, _), ms in groups.items()]
         side = torch.cuda.Stream(self.device)
         side.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(side):

@@ -68,6 +68,10 @@ class PackedWeights:
     zeros: Optional[torch.Tensor] = None
     gpu: Optional[torch.Tensor] = field(default=None, compare=False)
     layout_version: int = LAYOUT_VERSION
+    # QuantizedWeights.encoding; native_scales: what the batch executor reads
+    # for it (sign: s of w = s (2q - 1); ternary: the one per-tensor scale)
+    encoding: str = "offset"
+    native_scales: Optional[torch.Tensor] = field(default=None, compare=False)
 
     def __post_init__(self):
         expected = self.m * (self.k // self.g) // indices_per_byte(self.g)
@@ -76,6 +80,8 @@ class PackedWeights:
                              f"(bits={self.bits}, plane_bytes={expected})")
         if tuple(self.scales.shape) != (self.m, self.k // self.group_size):
             raise ShapeError("scales shape mismatch")
+        if self.encoding == "offset" and self.zeros is not None:
+            object.__setattr__(self, "encoding", "zeros")
 
     @property
     def plane_bytes(self) -> int:
@@ -153,7 +159,7 @@ def gpu_layout_ok(m: int, k: int, bits: int, g: int, group_size: int) -> bool:
 
 
 def pack_and_permute(planes: list[BitPlane], tile: TileConfig, scales, group_size: int,
-                     zeros=None) -> PackedWeights:
+                     zeros=None, encoding=None) -> PackedWeights:
     """weight_prep.py:214-246: v1 planes (byte-identical to the reference)
     plus the layout-v2 operand for the CUDA kernel."""
     if not planes:
@@ -184,8 +190,14 @@ def pack_and_permute(planes: list[BitPlane], tile: TileConfig, scales, group_siz
     if s.dtype not in (torch.float32, torch.float16):
         s = s.float()
     z = None if zeros is None else to_device(zeros, dev, s.dtype)
+    enc = encoding or ("offset" if z is None else "zeros")
+    native = None
+    if enc == "sign":           # generic form (2s, 1/2) -> s (exact halving)
+        native = (s.float() * 0.5).to(s.dtype).contiguous()
+    elif enc == "ternary":      # the one per-tensor scale
+        native = s.reshape(-1)[:1].clone()
     return PackedWeights(m=m, k=k, bits=bits, g=g, group_size=group_size, tile=tile, planes=v1,
-                         scales=s, zeros=z, gpu=gpu)
+                         scales=s, zeros=z, gpu=gpu, encoding=enc, native_scales=native)
 
 
 def unpack_planes(pw: PackedWeights) -> list[BitPlane]:
@@ -201,7 +213,7 @@ def unpack_planes(pw: PackedWeights) -> list[BitPlane]:
 def prepare_weights(qw: QuantizedWeights, tile: TileConfig = DEFAULT_TILE, device=None) -> PackedWeights:
     """weight_prep.py:260-263: decompose, pack (v1), repack (v2) -- all on the GPU."""
     planes = decompose_bits(qw, tile.g, device=device)
-    return pack_and_permute(planes, tile, qw.scales, qw.group_size, zeros=qw.zeros)
+    return pack_and_permute(planes, tile, qw.scales, qw.group_size, zeros=qw.zeros, encoding=qw.encoding)
 
 
 def from_v1(pw: PackedWeights) -> PackedWeights:
@@ -210,4 +222,4 @@ def from_v1(pw: PackedWeights) -> PackedWeights:
     if pw.gpu is not None:
         return pw
     planes = unpack_planes(pw)
-    return pack_and_permute(planes, pw.tile, pw.scales, pw.group_size, zeros=pw.zeros)
+    return pack_and_permute(planes, pw.tile, pw.scales, pw.group_size, zeros=pw.zeros, encoding=pw.encoding)

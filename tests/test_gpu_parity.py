@@ -727,6 +727,8 @@ def test_fused_allgather_epilogue_emulated(world, bits, gs):
         locs = [fg.launch(x[0], pw) for fg, pw in zip(fgs, shards)]
         rows = [fg.wait() for fg in fgs]
         torch.cuda.synchronize()
+        ref = O.mpgemm_q8(x.cpu().numpy(), q.cpu().numpy(), sc.float().cpu().numpy(), bits, gs)[0]
+        assert rel_maxnorm(rows[0][0].cpu().numpy(), ref) <= 1e-5      # the gathered row vs the oracle
         for r in range(world):
             assert torch.equal(rows[r], want), (r, epoch)
             col, mr = PP.gather_plan(m, world)[r]

@@ -1,0 +1,280 @@
+"""GPU parity on every BASELINE config and mode the bench reports, against
+the committed golden vectors the REAL reference produced
+(oracle/make_golden.py) -- the fixtures round 1 left unused:
+
+* configs[3] prefill at N = 32 / 128 / 512 (W4, W2; 4096x4096, 11008x4096):
+  exact epilogue bitwise (sampled rows + sha256 of all rows), fast epilogue
+  within 1e-5 (max-norm), fp16 tables (N = 32) within 1e-3 of scalar-real;
+* configs[4] batch 8 (the four 70B shapes, W2/W4): bitwise + sha256;
+* the batch executor's kernel (csrc/gemv_batch.cu): its exact integer sums
+  S = sum_p 2^p P_p on the three configs[1] shapes equal the reference's
+  staging values combined, bitwise (P pinned by sha256 to the reference);
+  configs[0] (zero points), configs[2] sign planes and ternary weights
+  through its native encodings within 1e-5 of the reference + the zero
+  correction.
+"""
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2407_00088_b200 as B
+from paper_2407_00088_b200 import _native as N
+from paper_2407_00088_b200 import workloads as W
+from paper_2407_00088_b200.pipeline import Pipeline
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(arr) -> str:
+    return hashlib.sha256(np.ascontiguousarray(arr).tobytes()).hexdigest()
+
+
+def rel_maxnorm(y, ref):
+    return float(np.abs(np.asarray(y, np.float64) - ref).max() / np.abs(ref).max())
+
+
+def make_pw(inst):
+    qw = B.QuantizedWeights(m=inst["q"].shape[0], k=inst["q"].shape[1], bits=inst["bits"],
+                            group_size=inst["group_size"], qvalues=inst["q"], scales=inst["scales"],
+                            zeros=inst.get("zeros"))
+    return B.prepare_weights(qw, B.TileConfig(n_tile=1, m_tile=32, k_tile=128, g=4, lanes=16))
+
+
+# ---------------------------------------------------------------- configs[3]
+
+@pytest.mark.parametrize("n", [32, 128, 512])
+@pytest.mark.parametrize("bits", [4, 2])
+@pytest.mark.parametrize("si", [0, 1])
+def test_config4_prefill_all_n(config_golden, n, bits, si):
+    inst = W.config4(n, bits, si)
+    g = config_golden[inst["name"]]
+    pw = make_pw(inst)
+    a = torch.from_numpy(inst["a"]).cuda()
+    y = B.mpgemm(a, pw).cpu().numpy()                         # reference-order epilogue
+    assert np.array_equal(y[g["rows"]], g["y_vector-q8_rows"])
+    assert sha(y) == g["meta"]["sha_y_vector-q8"]
+    yf = B.mpgemm(a, pw, exact_epilogue=False).cpu().numpy()  # the bench's prefill path
+    for r, row in zip(g["rows"], g["y_vector-q8_rows"]):
+        assert rel_maxnorm(yf[r], row) <= 1e-5, (r, rel_maxnorm(yf[r], row))
+    for r in range(0, n, max(1, n // 16)):                    # every row against the exact path
+        assert rel_maxnorm(yf[r], y[r]) <= 1e-5, r
+
+
+@pytest.mark.parametrize("bits", [4, 2])
+@pytest.mark.parametrize("si", [0, 1])
+def test_config4_fp16_tables(config_golden, bits, si):
+    """fp16 tables (cuda-f16) on configs[3] at N = 32 against the reference's
+    fp32-table scalar-real rows: max|dy| <= 1e-3 max|y| per row."""
+    inst = W.config4(32, bits, si)
+    g = config_golden[inst["name"]]
+    pw = make_pw(inst)
+    a = torch.from_numpy(inst["a"]).cuda()
+    for exact in (True, False):
+        y = B.mpgemm(a, pw, variant="cuda-f16", exact_epilogue=exact).cpu().numpy()
+        for r, row in zip(g["rows"], g["y_scalar-real_rows"]):
+            assert rel_maxnorm(y[r], row) <= 1e-3, (exact, r, rel_maxnorm(y[r], row))
+
+
+# ---------------------------------------------------------------- configs[4] batch 8
+
+@pytest.mark.parametrize("si", [0, 1, 2, 3])
+@pytest.mark.parametrize("bits", [2, 4])
+def test_config5_batch8(config_golden, si, bits):
+    inst = W.config5(si, bits, 8)
+    g = config_golden[inst["name"]]
+    pw = make_pw(inst)
+    a = torch.from_numpy(inst["a"]).cuda()
+    y = B.mpgemm(a, pw).cpu().numpy()
+    assert np.array_equal(y[g["rows"]], g["y_vector-q8_rows"])
+    assert sha(y) == g["meta"]["sha_y_vector-q8"]
+    yf = B.mpgemm(a, pw, exact_epilogue=False).cpu().numpy()
+    for r in range(8):
+        assert rel_maxnorm(yf[r], y[r]) <= 1e-5, r
+
+
+# ---------------------------------------------------------------- batch executor kernel
+
+def _batch_run(items, partials=False):
+    """items = [(PackedWeights, fp16 activation row (1, k))]: one batch
+    Pipeline; returns (outputs, partials or None)."""
+    pl = Pipeline(executor="batch")
+    outs, parts = [], []
+    for pw, x in items:
+        t = pl.tables(x, pw.group_size)
+        p = (torch.full((pw.m, pw.k // pw.group_size), -(1 << 30), dtype=torch.int32, device="cuda")
+             if partials else None)
+        outs.append(pl.lookup(pw, t, fast_epilogue=True, partials=p))
+        parts.append(p)
+    pl.compile()
+    pl.run()
+    torch.cuda.synchronize()
+    return outs, (parts if partials else None)
+
+
+def test_batch_kernel_integer_sums_config2(config_golden):
+    """configs[1] (the headline workload) through the batch executor: the
+    exported S = sum_p 2^p P_p equals the reference's staging values P
+    combined, bitwise, on all three 7B shapes (P from the exact kernel,
+    pinned to the reference by sha256 and the stored head)."""
+    items, wants, refs = [], [], []
+    for si in range(3):
+        inst = W.config2(si)
+        g = config_golden[inst["name"]]
+        pw = make_pw(inst)
+        _, P = B.mpgemm(inst["a"], pw, return_partials=True)           # (1, bits, m, NQ)
+        Pr = P.transpose(1, 0, 2, 3)
+        assert sha(Pr) == g["meta"]["sha_partials"]                     # == the reference's P
+        assert np.array_equal(Pr[:, :, :64, :], g["partials_head"])
+        wants.append(sum((1 << p) * P[0, p].astype(np.int64) for p in range(inst["bits"])))
+        refs.append(g["y_vector-q8"][0])
+        items.append((pw, torch.from_numpy(inst["a"]).cuda()))
+    outs, parts = _batch_run(items, partials=True)
+    for y, S, want, ref in zip(outs, parts, wants, refs):
+        assert np.array_equal(S.cpu().numpy().astype(np.int64), want)
+        assert rel_maxnorm(y[0].cpu().numpy(), ref) <= 1e-5
+
+
+def test_batch_kernel_zeros_config1(config_golden):
+    """configs[0] (W4 g128, asymmetric fp16 zeros) through the batch
+    executor's zero-point encoding: within 1e-5 of the reference's vector-q8
+    + the oracle's zero correction; bitwise equal to the per-call fast
+    lookup (same per-tile arithmetic)."""
+    inst = W.config1()
+    g = config_golden[inst["name"]]
+    pw = make_pw(inst)
+    assert pw.encoding == "zeros"
+    x = torch.from_numpy(inst["a"]).cuda()
+    outs, _ = _batch_run([(pw, x)])
+    rs = O.row_sums(inst["a"].astype(np.float32), inst["group_size"])
+    ref = (g["y_vector-q8"][0] + O.zero_correction(inst["scales"], inst["zeros"], 4, rs[0])).astype(np.float32)
+    assert rel_maxnorm(outs[0][0].cpu().numpy(), ref) <= 1e-5
+    t = N.build_lut(x, inst["group_size"], N.TABLE_Q8)
+    y1, _ = N.lookup(pw.gpu, pw.scales, pw.zeros, *t, pw.m, pw.k, 4, inst["group_size"], N.TABLE_Q8,
+                     N.FLAG_PDL | N.FLAG_FAST_EPILOGUE, False)
+    assert torch.equal(outs[0], y1)
+
+
+def _config3_native(inst, kind):
+    """configs[2] instance -> QuantizedWeights with the native encoding."""
+    if kind == "sign":
+        s = (inst["scales"].astype(np.float32) * 0.5).astype(np.float16)      # the instance stores 2s
+        return B.QuantizedWeights.sign_planes(inst["q"], s, inst["group_size"])
+    v = inst["q"].astype(np.int8) - 1
+    return B.QuantizedWeights.ternary(v, inst["scales"][0, 0], inst["group_size"])
+
+
+@pytest.mark.parametrize("kind", ["sign", "ternary"])
+def test_batch_kernel_config3_native_encodings(config_golden, kind):
+    """configs[2]: 1-bit sign planes (no zero points, no row-sum term) and
+    ternary weights (one per-tensor scale, no scale stream) through the
+    batch executor, all three 7B shapes in one op list: within 1e-5 of the
+    reference (vector-q8 + the zero correction of the equivalent
+    (scale, zero) form); exact integer sums == the exact kernel's."""
+    items, refs, Ps = [], [], []
+    for si in range(3):
+        inst = W.config3(si, kind)
+        g = config_golden[inst["name"]]
+        qw = _config3_native(inst, kind)
+        assert qw.encoding == kind
+        # the native form describes the same weights as the instance's (scale, zero)
+        assert np.array_equal(qw.scales.cpu().numpy() if isinstance(qw.scales, torch.Tensor) else qw.scales,
+                              inst["scales"])
+        pw = B.prepare_weights(qw)
+        items.append((pw, torch.from_numpy(inst["a"]).cuda()))
+        rs = O.row_sums(inst["a"].astype(np.float32), inst["group_size"])
+        refs.append((g["y_vector-q8"][0] + O.zero_correction(inst["scales"], inst["zeros"], inst["bits"],
+                                                               rs[0])).astype(np.float32))
+        _, P = B.mpgemm(inst["a"], make_pw(inst), return_partials=True)
+        Ps.append(sum((1 << p) * P[0, p].astype(np.int64) for p in range(inst["bits"])))
+    outs, parts = _batch_run(items, partials=True)
+    for y, S, ref, want in zip(outs, parts, refs, Ps):
+        assert rel_maxnorm(y[0].cpu().numpy(), ref) <= 1e-5, rel_maxnorm(y[0].cpu().numpy(), ref)
+        assert np.array_equal(S.cpu().numpy().astype(np.int64), want)
+    # deterministic across replays
+    outs2, _ = _batch_run(items)
+    for a_, b_ in zip(outs, outs2):
+        assert torch.equal(a_, b_)
+
+
+def test_batch_kernel_mixed_encodings_one_list():
+    """One op list mixing offset / zero-point / sign / ternary weights of two
+    K values: one lookup launch per (K, encoding); every output within 1e-5
+    of the oracle for the equivalent (scale, zero) weights."""
+    g = torch.Generator(device="cuda").manual_seed(77)
+    items, refs = [], []
+    for kind, bits, m, k in (("offset", 2, 512, 4096), ("zeros", 4, 256, 4096), ("sign", 1, 1024, 4096),
+                             ("ternary", 2, 512, 4096), ("offset", 2, 256, 11008), ("sign", 1, 512, 11008),
+                             ("ternary", 2, 256, 11008)):
+        gs = 64 if kind == "offset" else 128
+        x = torch.randn((1, k), device="cuda", generator=g).half()
+        sc = (torch.randn((m, k // gs), device="cuda", generator=g).abs() * 0.02 + 1e-3).half()
+        if kind == "sign":
+            q = torch.randint(0, 2, (m, k), dtype=torch.uint8, device="cuda", generator=g)
+            qw = B.QuantizedWeights.sign_planes(q, sc, gs)
+        elif kind == "ternary":
+            v = torch.randint(-1, 2, (m, k), dtype=torch.int8, device="cuda", generator=g)
+            qw = B.QuantizedWeights.ternary(v, sc[0, 0], gs)
+        else:
+            q = torch.randint(0, 1 << bits, (m, k), dtype=torch.uint8, device="cuda", generator=g)
+            z = (torch.rand((m, k // gs), device="cuda", generator=g) * ((1 << bits) - 1)).half() \
+                if kind == "zeros" else None
+            qw = B.QuantizedWeights(m=m, k=k, bits=bits, group_size=gs, qvalues=q, scales=sc, zeros=z)
+        pw = B.prepare_weights(qw)
+        items.append((pw, x))
+        zz = None if qw.zeros is None else qw.zeros.float().cpu().numpy()
+        refs.append(O.mpgemm_q8(x.cpu().numpy(), qw.qvalues.cpu().numpy(), qw.scales.float().cpu().numpy(),
+                                qw.bits, gs, zeros=zz)[0])
+    outs, _ = _batch_run(items)
+    for (pw, _), y, ref in zip(items, outs, refs):
+        assert rel_maxnorm(y[0].cpu().numpy(), ref) <= 1e-5, (pw.encoding, pw.bits, pw.k)
+
+
+# ---------------------------------------------------------------- drop-in call paths
+
+def test_nonfinite_cuda_input_propagates_without_sync():
+    """CUDA-tensor activations are not checked on the host (that needs a
+    synchronization): a NaN / Inf activation makes every output of its row
+    non-finite (NaN-propagating group max in the table build); numpy inputs
+    keep the reference's DataError; check_finite=True restores it for CUDA."""
+    inst = W.small_instance(5, 256, 1024, 2, 64, n=3)
+    pw = make_pw(inst)
+    a = torch.from_numpy(inst["a"]).cuda()
+    a[1, 17] = float("nan")
+    a[2, 900] = float("inf")
+    for exact in (True, False):
+        for variant in ("cuda-q8", "cuda-f16"):
+            y = B.mpgemm(a, pw, exact_epilogue=exact, variant=variant)
+            assert bool(torch.isfinite(y[0]).all())
+            assert not bool(torch.isfinite(y[1]).any()), (exact, variant)
+            assert not bool(torch.isfinite(y[2]).any()), (exact, variant)
+    y1 = B.mpgemm(a[1:2].half(), pw, exact_epilogue=False)            # batch 1, fused build + lookup
+    assert not bool(torch.isfinite(y1).any())
+    with pytest.raises(B.DataError):
+        B.mpgemm(a, pw, check_finite=True)
+    with pytest.raises(B.DataError):
+        B.mpgemm(a.cpu().numpy(), pw)
+
+
+@pytest.mark.parametrize("dtype", [np.float16, np.float32])
+@pytest.mark.parametrize("n", [1, 3])
+def test_host_buffer_call_path(config_golden, dtype, n):
+    """numpy in -> numpy out through bitlut_mpgemm_host (one C call: H2D,
+    tables, lookup, D2H, sync): bitwise the reference's vector-q8 output on
+    configs[1]; repeated calls (scratch reuse) and row subsets agree."""
+    inst = W.config2(0)
+    g = config_golden[inst["name"]]
+    pw = make_pw(inst)
+    a = np.repeat(inst["a"], n, axis=0).astype(dtype)
+    for _ in range(3):
+        y = B.mpgemm(a, pw)
+        assert isinstance(y, np.ndarray) and y.shape == (n, 4096)
+        for r in range(n):
+            assert np.array_equal(y[r], g["y_vector-q8"][0])
+    yv = B.mpgemv(a[0], pw)
+    assert np.array_equal(yv, g["y_vector-q8"][0])
+    yf = B.mpgemv(a[0], pw, exact_epilogue=False)
+    assert rel_maxnorm(yf, g["y_vector-q8"][0]) <= 1e-5
