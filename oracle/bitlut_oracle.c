@@ -14,6 +14,12 @@
  *   _kernels.py:85-138    gemv_real       (scalar-real, fp32 tables)
  *   kernel.py:254-263     M-block slicing over threads (OpenMP here; outputs
  *                         are independent of the thread count).
+ *   _kernels.py:20-82     quantize_groups (core.py:227-262 quantize_weights),
+ *                         with numba's types: the products x*l and sum(x*l)
+ *                         in float64 (float32 * int64 promotes), sum(l*l) in
+ *                         float32, candidate scores in float64, round() half
+ *                         to even -- pinned by sha256 to the reference's own
+ *                         output (tests/golden/nmse.json).
  * The v1 layout comes from weight_prep.py:193-246 (pack it with the numpy
  * oracle or the CUDA bitlut_pack_v1).
  */
@@ -238,4 +244,76 @@ int orc_max_threads(void) {
 #else
   return 1;
 #endif
+}
+
+/* _kernels.py:20-82: one group per row of x (ng, gs); q_out (ng, gs) u8,
+ * d_out (ng) f32. */
+int orc_quantize_groups(const float* x, int64_t ng, int gs, int half, int nstep, uint8_t* q_out,
+                        float* d_out, int threads) {
+#ifdef _OPENMP
+  int nt = threads > 0 ? threads : omp_get_max_threads();
+#else
+  int nt = 1;
+  (void)threads;
+#endif
+#pragma omp parallel for num_threads(nt) schedule(static)
+  for (int64_t gi = 0; gi < ng; gi++) {
+    const float* xr = x + gi * gs;
+    uint8_t* qr = q_out + gi * gs;
+    float amax = 0.0f, smax = 0.0f;
+    for (int j = 0; j < gs; j++) {
+      const float ax = fabsf(xr[j]);
+      if (ax > amax) {
+        amax = ax;
+        smax = xr[j];
+      }
+    }
+    if (amax == 0.0f) {
+      d_out[gi] = 0.0f;
+      for (int j = 0; j < gs; j++) qr[j] = (uint8_t)half;
+      continue;
+    }
+    const float inv = (float)(-half) / smax;
+    if (nstep == 0) {
+      const float d = smax / (float)(-half);
+      for (int j = 0; j < gs; j++) {
+        long l = lrintf(xr[j] * inv);
+        if (l < -half) l = -half;
+        if (l > half - 1) l = half - 1;
+        qr[j] = (uint8_t)(l + half);
+      }
+      d_out[gi] = d;
+      continue;
+    }
+    double best_score = -1.0;
+    float best_inv = inv;
+    for (int t = -nstep; t <= nstep; t++) {
+      const float cand = ((float)(-half) + 0.1f * (float)t) / smax;
+      double sumlx = 0.0;
+      float suml2 = 0.0f;
+      for (int j = 0; j < gs; j++) {
+        long l = lrintf(xr[j] * cand);
+        if (l < -half) l = -half;
+        if (l > half - 1) l = half - 1;
+        sumlx += (double)xr[j] * (double)l;
+        suml2 += (float)(l * l);
+      }
+      if (suml2 > 0.0f && sumlx * sumlx > best_score * (double)suml2) {
+        best_score = sumlx * sumlx / (double)suml2;
+        best_inv = cand;
+      }
+    }
+    double sumlx = 0.0;
+    float suml2 = 0.0f;
+    for (int j = 0; j < gs; j++) {
+      long l = lrintf(xr[j] * best_inv);
+      if (l < -half) l = -half;
+      if (l > half - 1) l = half - 1;
+      qr[j] = (uint8_t)(l + half);
+      sumlx += (double)xr[j] * (double)l;
+      suml2 += (float)(l * l);
+    }
+    d_out[gi] = suml2 > 0.0f ? (float)(sumlx / (double)suml2) : 0.0f;
+  }
+  return 0;
 }

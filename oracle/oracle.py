@@ -428,5 +428,22 @@ def c_mpgemm(a, planes_v1, m, k, bits, group_size, wscales, mode="vector-q8",
     return out
 
 
+def c_quantize_weights(w: np.ndarray, bits: int, group_size: int, refine: bool = True, threads: int = 0):
+    """core.py:227-262 quantize_weights via the C port of _kernels.py:20-82:
+    -> (q (M, K) uint8, scales (M, K/gs) float32)."""
+    import ctypes
+    P = ctypes.c_void_p
+    w = np.ascontiguousarray(w, dtype=F32)
+    m, k = w.shape
+    ng = m * k // group_size
+    q = np.empty((m, k), dtype=np.uint8)
+    d = np.empty((m, k // group_size), dtype=F32)
+    fn = c_lib().orc_quantize_groups
+    fn.argtypes = [P, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, ctypes.c_int]
+    fn(w.ctypes.data_as(P), ng, group_size, 1 << (bits - 1), 9 if refine else 0, q.ctypes.data_as(P),
+       d.ctypes.data_as(P), int(threads))
+    return q, d
+
+
 def c_max_threads() -> int:
     return int(c_lib().orc_max_threads())

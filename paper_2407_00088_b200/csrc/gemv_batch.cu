@@ -28,8 +28,15 @@
 // the tile carries no scale stream at all.)
 //
 // Per tile the CTA-wide barrier publishes the cross-warp sums and frees the
-// stage; thread 0 refills it and warp 0 adds the cross-warp sums (measured:
-// rotating both over the warps was 3-4 % slower on every width).
+// stage; thread 0 refills it and warp 0 adds the cross-warp sums.  Measured
+// and not kept (same-box A/B, 32-layer 7B layer sets):
+// rotating the refill and the final sums over the warps (-3 %); a producer
+// warp with full/empty mbarriers instead of the CTA barrier (-2..-10 %: the
+// extra warp costs a CTA per SM); a leader warp waiting on an "empty"
+// mbarrier while the others run ahead (-1 %); the integer lane reduction
+// through shared memory (W1 -2 %); two units per thread (-2..-5 %: half the
+// resident warps).  The kernel is issue-bound at ~2.6 (W2) / ~3.0 (W1)
+// warp-instructions per 4-weight lookup.
 #include "b1_core.cuh"
 
 #include <cstdlib>
@@ -49,6 +56,8 @@ struct BatchArgs {
 };
 
 __host__ __device__ inline uint32_t al16(size_t x) { return (uint32_t)((x + 15) & ~(size_t)15); }
+
+
 
 template <typename ST, int MODE>
 __device__ __forceinline__ void issue_tile(const BatchArgs& a, const bitlut_batch_mat& mt, int local, uint8_t* sb,
@@ -116,7 +125,9 @@ __global__ void __launch_bounds__(384) gemv_batch_kernel(const __grid_constant__
   // issue cursor (thread 0): the matrix of the next tile to stage
   int ji = jc, ji_begin = jc_begin, ji_end = jc_end;
   if (tid == 0) {
-    for (int s = 0; s < kStagesMax; s++) mbar_init(bar + s, 1);
+    for (int s = 0; s < kStagesMax; s++) {
+      mbar_init(bar + s, 1);                            // the stage's TMA bytes landed
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     const uint64_t pol = policy_evict_first();
     for (int s = 0; s < S; s++) {
@@ -128,7 +139,7 @@ __global__ void __launch_bounds__(384) gemv_batch_kernel(const __grid_constant__
   }
   if (!a.independent) bl::pdl_wait();
   bl::pdl_launch_dependents();
-  const int u = tid;
+  const int u = tid;                                    // thread u looks up unit u
   const bool live = u < U;
   const int ub = u >> 5, l = u & 31;
   const int nu_b = min(32, U - 32 * ub);
@@ -229,6 +240,7 @@ __global__ void __launch_bounds__(384) gemv_batch_kernel(const __grid_constant__
       const int t = tile + S;
       if (t < t1) {
         advance(dm, n_mats, t, ji, ji_begin, ji_end);
+        // the warps' generic writes (smem lane reduction) before the async-proxy refill
         issue_tile<ST, MODE>(a, dm[ji], t - ji_begin, sb, bar + stage, policy_evict_first());
       }
     }

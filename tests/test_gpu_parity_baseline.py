@@ -278,3 +278,45 @@ def test_host_buffer_call_path(config_golden, dtype, n):
     assert np.array_equal(yv, g["y_vector-q8"][0])
     yf = B.mpgemv(a[0], pw, exact_epilogue=False)
     assert rel_maxnorm(yf, g["y_vector-q8"][0]) <= 1e-5
+
+
+# ---------------------------------------------------------------- NMSE acceptance (criterion C2)
+
+TABLE4_BANDS = {(4096, 4096): (1.5e-3, 7e-3), (11008, 4096): (3.46e-3 / 2, 3.46e-3 * 2),
+                (4096, 11008): (4.15e-3 / 2, 4.15e-3 * 2)}      # pkg/tests/test_acceptance.py:21-26
+
+
+def test_nmse_acceptance_through_cuda_path():
+    """The reference's NMSE criterion (pkg/tests/test_acceptance.py:61-82,
+    :121-138) run through the CUDA path: the reference's own quantized
+    weights (C port, sha256-pinned), cuda-q8 mpgemv -> output bitwise the
+    reference's vector-q8, NMSE equal to the recorded 6.892e-3 / 6.598e-3 /
+    7.012e-3 (pkg/test_output.txt:220) and inside the criterion's bands;
+    the fast epilogue and fp16 tables inside the bands too."""
+    import json
+    import os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "nmse.json")))
+    for row in gold["shapes"]:
+        m, k = row["m"], row["k"]
+        rng = np.random.default_rng(0)
+        w = rng.standard_normal((m, k), dtype=np.float32)
+        a = rng.standard_normal(k, dtype=np.float32)
+        q, d = O.c_quantize_weights(w, 4, 32)
+        assert sha(q) == row["sha_q"] and sha(d) == row["sha_scales"]
+        # reference_gemm (oracle.py:26-42): float32, ascending k
+        wt = np.ascontiguousarray(w.T)
+        y = np.zeros(m, dtype=np.float32)
+        for kk in range(k):
+            y += a[kk] * wt[kk]
+        assert sha(y.reshape(1, -1)) == row["sha_y_ref"]
+        pw = B.prepare_weights(B.QuantizedWeights(m=m, k=k, bits=4, group_size=32, qvalues=q, scales=d))
+        out = B.mpgemv(a, pw)
+        assert sha(out.reshape(1, -1)) == row["sha_y_vector_q8"]
+        nmse = float(((y - out) ** 2).sum()) / float((y ** 2).sum())
+        assert nmse == row["nmse_vector_q8"], (nmse, row["nmse_vector_q8"])
+        lo, hi = TABLE4_BANDS[(m, k)]
+        assert lo <= nmse <= hi
+        for kw in ({"exact_epilogue": False}, {"variant": "cuda-f16"}):
+            o2 = B.mpgemv(a, pw, **kw)
+            n2 = float(((y - o2) ** 2).sum()) / float((y ** 2).sum())
+            assert lo <= n2 <= hi and abs(n2 - nmse) <= 0.01 * nmse, (kw, n2, nmse)

@@ -111,3 +111,26 @@ def test_known_answers():
     z = O.mirror_consolidate(O.precompute_lut(np.zeros(8, np.float32), 4))
     qz, tz = O.quantize_tables(z, 4, 8)
     assert np.all(tz == 1.0) and np.all(qz == 0)
+
+
+def _table4_inputs(m, k):
+    """pkg/tests/test_acceptance.py:65-68: w, a from default_rng(0)."""
+    rng = np.random.default_rng(0)
+    w = rng.standard_normal((m, k), dtype=np.float32)
+    a = rng.standard_normal(k, dtype=np.float32)
+    return w, a
+
+
+def test_c_quantizer_pinned_to_reference():
+    """The C restatement of the reference's group quantizer (_kernels.py:20-82)
+    reproduces its codes and scales bit for bit on the Table-4 shapes of the
+    NMSE criterion (sha256 from oracle/make_golden_nmse.py)."""
+    import hashlib
+    import json
+    import os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "nmse.json")))
+    for row in gold["shapes"]:
+        w, _ = _table4_inputs(row["m"], row["k"])
+        q, d = O.c_quantize_weights(w, row["bits"], row["group_size"])
+        assert hashlib.sha256(q.tobytes()).hexdigest() == row["sha_q"], (row["m"], row["k"])
+        assert hashlib.sha256(d.tobytes()).hexdigest() == row["sha_scales"], (row["m"], row["k"])
