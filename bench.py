@@ -8,9 +8,10 @@ tables (bit-exact vs the reference's vector-q8), fp16 activations ~N(0,1).
 A STEP = one pass over L layers (default 32 = the whole 7B model, 1.62 GB of
 packed weights > 126 MB L2, so no L2 flush is needed): per layer 4 table
 builds (qkv / o / gate-up / down inputs) + 7 lookup GEMVs, run through the
-package's op-list executors (pipeline.Pipeline: "graph" = per-op kernels
-chained with programmatic dependent launch in one CUDA graph, "persistent" =
-one cooperative launch); the fastest is the headline, all are reported.
+package's op-list executors (pipeline.Pipeline: "batch" = every table build
+in one launch + one lookup launch per K -- the headline; "graph" = per-op
+kernels chained with programmatic dependent launch in one CUDA graph, also
+the dependent decode chain).
 
 value  = packed-weight bytes (bits*M*K/8, the reference's weight_bytes,
          cli.py:153) per step / device time, GB/s, all ranks aggregated.
@@ -190,7 +191,7 @@ def step_fn(layers, acts, world, group, fast=False):
     return res
 
 
-def build_pipeline(layers, acts, fast=False, executor="persistent", chain=True, sync="pdl", lookahead=None,
+def build_pipeline(layers, acts, fast=False, executor="graph", chain=True, sync="pdl", lookahead=None,
                    groups=None):
     """The step as a pipeline.Pipeline op list.  chain=True: the decode
     chain's dependencies -- a layer's qkv table build waits for the previous

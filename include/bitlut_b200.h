@@ -64,12 +64,6 @@ extern "C" {
  * integer combination S[m][gq] = sum_p 2^p P_p (shape (1, m, k/gs)) that the
  * fast kernel scales -- SURVEY §8(c)'s bit-exactness object. */
 #define BITLUT_FLAG_COMBINED_PARTIALS 32
-/* With BITLUT_FLAG_FAST_EPILOGUE at batch 1: use the streaming kernel
- * (per-warp weight rings, whole quantization groups per lane; an
- * alternative the library no longer picks by itself -- the split-K cluster
- * kernel is faster on long K).  Same exact integer sums; the fp32
- * combination order differs. */
-#define BITLUT_FLAG_STREAM 64
 
 /*
  * GPU weight layout ("layout v2", this library's own; the reference's v1
@@ -331,12 +325,11 @@ int bitlut_mpgemm_traced(const uint8_t* wgpu, int m, int k, int bits, int group_
                          int mode, int n, float* out, int32_t* partials, int flags,
                          unsigned long long* trace, void* stream);
 
-/* ---------------- persistent pipeline (this library's executor) ----------------
- * A whole op list -- table builds and lookup GEMVs, e.g. every projection of
- * every decoder layer of a batch-1 decode step -- runs in ONE cooperative
- * launch.  Each op names up to three earlier ops it depends on; completion
- * counters in global memory replace kernel boundaries.  Per-op arithmetic is
- * identical to bitlut_build_lut (mode Q8) + bitlut_mpgemm (mode Q8). */
+/* ---------------- op lists (this library's executors) ----------------
+ * A list of table builds and lookup GEMVs -- e.g. every projection of every
+ * decoder layer of a batch-1 decode step.  Each op names up to three earlier
+ * ops it depends on.  Per-op arithmetic is identical to bitlut_build_lut
+ * (mode Q8) + bitlut_mpgemm (mode Q8). */
 #define BITLUT_OP_TABLES 0
 #define BITLUT_OP_LOOKUP 1
 typedef struct {
@@ -358,22 +351,7 @@ typedef struct {
                                = may be folded into its consumers (bitlut_mpgemv_fused) */
 } bitlut_pipe_op;
 
-/* Bytes of the encoded op table for n_ops ops. */
-size_t bitlut_pipeline_table_bytes(int n_ops);
-/* Validate the specs and encode them into `table_host` (caller-allocated,
- * bitlut_pipeline_table_bytes(n_ops) bytes).  All LOOKUP ops must share the
- * group size's kernel configuration and the scale dtype. */
-int bitlut_pipeline_encode(const bitlut_pipe_op* specs, int n_ops, void* table_host, size_t table_bytes);
-/* Run an encoded table: `table_dev` is a device copy of `table_host`;
- * `counters` is device scratch of 2*n_ops uint32 (zeroed by the call). */
-int bitlut_pipeline_launch(const void* table_host, const void* table_dev, unsigned* counters, void* stream);
-/* Diagnostic variant: `trace` gets 4 %globaltimer stamps per (op, unit)
- * [start, dependencies met, inputs staged, done] at (unit_base[op] + unit)*4;
- * unit_base: device int array of per-op unit offsets (tools/pipeline_timeline.py). */
-int bitlut_pipeline_launch_traced(const void* table_host, const void* table_dev, unsigned* counters,
-                                  unsigned long long* trace, const int* unit_base, void* stream);
-
-/* Per-op executor for the same op list: stream-ordered launches of the
+/* Per-op executor: stream-ordered launches of the
  * bitlut_build_lut / bitlut_mpgemm kernels (mode Q8) chained with
  * programmatic dependent launch, for capture into a CUDA graph.  Lookups
  * whose deps are already complete when they start are launched with

@@ -29,7 +29,6 @@ FLAG_FAST_EPILOGUE = 4
 FLAG_FUSED_TABLES = 8       # table op may fold into its consumers (graph executor)
 PLAN_JOINED = 16            # plan: launched together with the previous op
 FLAG_COMBINED_PARTIALS = 32
-FLAG_STREAM = 64            # fast batch-1: force the streaming kernel (gemv_stream.cu)  # fast batch-1: partials = sum_p 2^p P_p per (channel, group)
 
 _vp, _i = ctypes.c_void_p, ctypes.c_int
 
@@ -204,8 +203,7 @@ def lib() -> ctypes.CDLL:
 
 
 def exported_symbols() -> list[str]:
-    return list(_SIGS) + ["bitlut_version", "bitlut_pipeline_table_bytes", "bitlut_pipeline_encode",
-                          "bitlut_pipeline_launch", "bitlut_pipeline_launch_traced",
+    return list(_SIGS) + ["bitlut_version",
                           "bitlut_pipeline_plan_flags", "bitlut_pipeline_launch_ops",
                           "bitlut_build_lut_multi", "bitlut_mpgemv_multi",
                           "bitlut_pipeline_launch_ops_counted"]

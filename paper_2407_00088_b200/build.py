@@ -15,8 +15,7 @@ import sys
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-SOURCES = ["weight_prep.cu", "lut.cu", "gemv.cu", "gemv_b1.cu", "gemv_batch.cu", "gemv_stream.cu", "gemv_pack.cu",
-           "pipeline.cu", "host_api.cu"]
+SOURCES = ["weight_prep.cu", "lut.cu", "gemv.cu", "gemv_b1.cu", "gemv_batch.cu", "pipeline.cu", "host_api.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
 

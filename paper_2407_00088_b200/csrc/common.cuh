@@ -147,6 +147,15 @@ BL_DEV float to_f32(__half x) { return __half2float(x); }
 
 }  // namespace bl
 
+// Host side: the current device's ordinal for per-device once-flags
+// (function attributes and SM counts are per device; one process may drive
+// several GPUs).
+static inline int bl_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d < 0 || d >= 64 ? 0 : d;
+}
+
 // Host-side launch-status helper: every entry point returns one of the
 // BITLUT_* codes; a CUDA launch failure maps to BITLUT_EINTERNAL.
 static inline int bl_launch_status() {

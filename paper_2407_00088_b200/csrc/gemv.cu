@@ -161,7 +161,8 @@ int launch_q8(const GemvArgs& a, int n, cudaStream_t stream, bool pdl) {
   // L1 has little to cache, while the default carveout can leave room for
   // only one CTA of a long-K tile per SM (4096x11008: two waves instead of
   // two co-resident CTAs).
-  static bool configured = false;
+  static bool configured_dev[64] = {};                  // per device
+  bool& configured = configured_dev[bl_device()];
   if (!configured) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -254,7 +255,6 @@ int bl_mpgemm_launch(const uint8_t* wgpu, int m, int k, int bits, int group_size
   a.out = out; a.partials = partials; a.trace = trace; a.L = L;
   a.independent = pdl && (flags & BITLUT_FLAG_INDEPENDENT) != 0;
   a.fast = (flags & BITLUT_FLAG_FAST_EPILOGUE) != 0;
-  a.force_stream = (flags & BITLUT_FLAG_STREAM) != 0;
   a.n_rows = n;
   // weight-stationary rows: a CTA keeps its tile in smem for up to 32 rows
   // once there are enough (tile, row-block) CTAs to fill the GPU

@@ -22,10 +22,6 @@
 
 #include <cstdlib>
 
-int bl_gemv_stream_launch(const blk::GemvArgs& g, const blk::StreamMat* mats, int n_mats, int scale_dtype,
-                          cudaStream_t s, bool pdl);
-int bl_gemv_pack_launch(const blk::GemvArgs& g, const blk::StreamMat* mats, int n_mats, int scale_dtype,
-                        cudaStream_t s, bool pdl);
 
 namespace {
 
@@ -38,7 +34,7 @@ constexpr int kMaxMats = 8;
 // One weight matrix of a (multi-matrix) launch: matrices that share the
 // activation tables (q/k/v, gate/up) are looked up by one launch whose tiles
 // are numbered matrix after matrix.
-struct B1Mat {                // layout-identical to blk::StreamMat (gemv_stream.cu)
+struct B1Mat {
   const uint8_t* w;
   const void* wscales;
   const void* zeros;
@@ -1117,13 +1113,13 @@ int launch_b1_cluster(const GemvArgs& g, const B1Mat* mats, int n_mats, cudaStre
   c.z_off = c.s_off + al16(c.s_bytes);
   c.stage_bytes = ((c.z_off + (zeros ? al16(c.s_bytes) : 0)) + 127) & ~127u;
   auto kern = zeros ? gemv_b1_cluster_kernel<R, LG, BITS, ST, true> : gemv_b1_cluster_kernel<R, LG, BITS, ST, false>;
-  static bool configured[2] = {false, false};
-  if (!configured[zeros]) {
+  static bool configured[64][2] = {};                  // per device
+  if (!configured[bl_device()][zeros]) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared) != cudaSuccess)
       return BITLUT_EINTERNAL;
-    configured[zeros] = true;
+    configured[bl_device()][zeros] = true;
   }
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[2];
@@ -1166,10 +1162,10 @@ int launch_b1_cluster(const GemvArgs& g, const B1Mat* mats, int n_mats, cudaStre
 }
 
 int sm_count() {
-  static int n = 0;
+  static int n_dev[64] = {};                           // per device
+  const int dev = bl_device();
+  int& n = n_dev[dev];
   if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
   }
@@ -1267,9 +1263,9 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
                           : (has_z ? gemv_b1_lean_kernel<R, LG, BITS, ST, true>
                                    : gemv_b1_lean_kernel<R, LG, BITS, ST, false>))
                    : (lean_rows ? gemv_b1_rows_lean_kernel<R, LG, BITS, ST> : gemv_b1_kernel<R, LG, BITS, ST, KIND>);
-  static bool configured_k[6] = {false, false, false, false, false, false};
-  const int ki = lean ? (has_z ? 2 : 1) + (f16 ? 3 : 0) : (lean_rows ? 3 : 0);
-  bool& configured = configured_k[ki];
+  static bool configured_k[64][7] = {};                // per device and kernel variant
+  const int ki = lean ? (has_z ? 2 : 1) + (f16 ? 3 : 0) : (lean_rows ? 6 : 0);
+  bool& configured = configured_k[bl_device()][ki];
   if (!configured) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -1433,16 +1429,9 @@ int bl_gemv_b1_launch(const GemvArgs& g, int scale_dtype, cudaStream_t s, bool p
     return f16 ? dispatch_b1<__half, kExactRows>(g, &m, 1, nullptr, s, pdl)
                : dispatch_b1<float, kExactRows>(g, &m, 1, nullptr, s, pdl);
   }
-  if (g.fast) {
-    int rc = BITLUT_ELAYOUT;
-    const bool alt = !g.gather && !g.f16_tables;
-    if (alt) rc = bl_gemv_stream_launch(g, reinterpret_cast<const StreamMat*>(&m), 1, scale_dtype, s, pdl);
-    if (rc != BITLUT_ELAYOUT) return rc;
-    if (alt) rc = bl_gemv_pack_launch(g, reinterpret_cast<const StreamMat*>(&m), 1, scale_dtype, s, pdl);
-    if (rc != BITLUT_ELAYOUT) return rc;
+  if (g.fast)
     return f16 ? dispatch_b1<__half, kFast>(g, &m, 1, nullptr, s, pdl)
                : dispatch_b1<float, kFast>(g, &m, 1, nullptr, s, pdl);
-  }
   return f16 ? dispatch_b1<__half, kExact>(g, &m, 1, nullptr, s, pdl)
              : dispatch_b1<float, kExact>(g, &m, 1, nullptr, s, pdl);
 }
@@ -1535,16 +1524,9 @@ int bl_mpgemv_multi_launch(const bitlut_mat* mats, int n_mats, int k, int bits, 
   g.grid_out = grid_out;
   g.independent = pdl && (flags & BITLUT_FLAG_INDEPENDENT) != 0;
   g.fast = (flags & BITLUT_FLAG_FAST_EPILOGUE) != 0;
-  g.force_stream = (flags & BITLUT_FLAG_STREAM) != 0;
   g.zeros = mats[0].zeros;                              // presence flag for the epilogue
   g.rows_per_cta = 1; g.n_rows = 1;
   const cudaStream_t st = (cudaStream_t)stream;
-  if (g.fast) {
-    int rc = bl_gemv_stream_launch(g, reinterpret_cast<const StreamMat*>(ms), n_mats, scale_dtype, st, pdl);
-    if (rc != BITLUT_ELAYOUT) return rc;
-    rc = bl_gemv_pack_launch(g, reinterpret_cast<const StreamMat*>(ms), n_mats, scale_dtype, st, pdl);
-    if (rc != BITLUT_ELAYOUT) return rc;
-  }
   if (g.fast)
     return scale_dtype == BITLUT_DT_F16 ? dispatch_b1<__half, kFast>(g, ms, n_mats, nullptr, st, pdl)
                                         : dispatch_b1<float, kFast>(g, ms, n_mats, nullptr, st, pdl);

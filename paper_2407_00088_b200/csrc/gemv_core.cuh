@@ -13,19 +13,6 @@ namespace blk {
 constexpr uint32_t kMult = 0x80000001u;      // u16 pair (lo = 1, hi = 32768)
 constexpr uint32_t kMultNeg = 0x8000FFFFu;   // s16 pair (lo = -1, hi = -32768)
 
-// One weight matrix of a batch-1 launch over several matrices sharing one
-// activation row's tables (q/k/v, gate/up): tiles numbered matrix after matrix.
-struct StreamMat {
-  const uint8_t* w;
-  const void* wscales;
-  const void* zeros;
-  float* out;
-  int tile_end;               // cumulative tile count up to and including this matrix
-  // per-matrix activation tables (bitlut_mpgemv_multi_tab), or null: the launch's
-  const uint8_t* qtab;
-  const float* tscales;
-  const float* rowsums;
-};
 
 // Fused all-gather epilogue (SURVEY §8(e) "B200-native upgrade"): every
 // output element is also stored into the gathered output buffer of each of
@@ -61,7 +48,6 @@ struct GemvArgs {
   bl::LayoutV2 L;
   bl::DepSync dep;           // op-list counters (n_wait == 0 and done == null otherwise)
   int* grid_out;             // host: receives the launch's CTA count (op-list executor), or null
-  int force_stream;          // BITLUT_FLAG_STREAM: batch-1 fast lookups through gemv_stream.cu
   int f16_tables;            // BITLUT_TABLE_F16 (batch-1 fast lean kernel only; 0 = int8 tables)
   int mixed_tables;          // matrices carry their own tables (bitlut_mpgemv_multi_tab): lean kernel only
   const GatherArgs* gather;  // host side: fused all-gather epilogue (batch-1 fast kernel), or null

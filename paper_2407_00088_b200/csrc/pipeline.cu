@@ -1,270 +1,16 @@
-// Persistent pipeline executor: a whole sequence of table builds and
-// lookup GEMVs (e.g. every projection of every decoder layer) in ONE
-// cooperative launch.
-//
-// Why: a batch-1 decode is a chain of small dependent GEMVs.  Launched one
-// kernel per op (even with CUDA graphs + programmatic dependent launch) each
-// op pays the grid-completion -> dependent-release latency (~0.6 us
-// measured) on top of its own critical path (tools/timeline.py).  Here every
-// CTA stays resident and walks the op list in order; an op's work units
-// (one tile per unit for lookups, 128 k-groups per unit for table builds)
-// are claimed dynamically by CTAs (one atomic per unit, so a busy CTA never
-// holds work back), and each op waits only for the ops it
-// names in `dep` through per-op completion counters in global memory
-// (release: __threadfence + atomicAdd; acquire: ld.acquire.gpu polled by one
-// thread, then bar.sync).  A CTA that finishes its share of op j moves on
-// to op j+1 at once and starts the TMA copies of its first tile before
-// waiting, so weight streaming overlaps the tail of the previous op (and
-// independent ops -- q/k/v, gate/up -- simply run concurrently).
-//
-// Deadlock freedom: cooperative launch => all CTAs resident; a CTA only
-// waits on ops earlier than the one it is working on, and it has finished
-// all of its own units of earlier ops, so the wait graph is acyclic.
-//
-// Per-unit arithmetic is exactly the per-call kernels' (gemv_core.cuh
-// tile_body, lut_core.cuh lut_block), so results are bitwise identical to
-// bitlut_build_lut + bitlut_mpgemm.
+// Op-list executors over per-op launches (pipeline.py): the planner that
+// gives each op its launch flags (PDL waits, INDEPENDENT launches, grouped
+// table builds and lookups, fused table ops) and the stream-ordered
+// launchers -- programmatic dependent launch (bitlut_pipeline_launch_ops) or
+// per-launch completion counters (bitlut_pipeline_launch_ops_counted).
+// Per-op arithmetic is the per-call kernels', so results are bitwise
+// identical to bitlut_build_lut + bitlut_mpgemm.
 #include "gemv_core.cuh"
 #include "lut_core.cuh"
 
 #include <cstdlib>
 
-namespace {
-
 using namespace blk;
-
-constexpr int kPipeThreads = 128;
-constexpr int kLutUnitKG = kPipeThreads;   // k-groups per table-build unit
-
-struct PipeOp {
-  int type;              // BITLUT_OP_TABLES / BITLUT_OP_LOOKUP
-  int n_units;
-  int dep[3];
-  // table build
-  const void* a;
-  int a_dtype, k, gs, row_units;
-  void* tables;
-  float* tscales;
-  float* rowsums;
-  // lookup (rows = n in blockIdx.y order: unit = row * n_tiles + tile)
-  GemvArgs g;
-};
-
-struct PipeHeader {      // first bytes of an encoded op table (host copy)
-  int n_ops, R, LG, scale_dtype;
-  size_t smem_bytes;
-};
-
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void wait_deps(const PipeOp& op, const PipeOp* ops, const unsigned* done) {
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int i = 0; i < 3; i++) {
-      const int d = op.dep[i];
-      if (d < 0) continue;
-      const unsigned target = (unsigned)ops[d].n_units;
-      while (ld_acquire(done + d) < target) __nanosleep(32);
-    }
-  }
-  __syncthreads();
-}
-
-template <int R, int LG, typename ST>
-__global__ void __launch_bounds__(kPipeThreads)
-pipeline_kernel(const PipeOp* __restrict__ ops, int n_ops, unsigned* __restrict__ done,
-                unsigned long long* __restrict__ trace, const int* __restrict__ unit_base) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  const int tid = threadIdx.x;
-  const int G = gridDim.x;
-  // the mbarrier sits in the last 16 bytes of the dynamic smem
-  uint64_t* bar;
-  {
-    unsigned dyn;
-    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
-    bar = reinterpret_cast<uint64_t*>(smem + dyn - 16);
-  }
-  if (tid == 0) {
-    mbar_init(bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  uint32_t phase = 0;
-  __shared__ int next_unit;
-  unsigned* claim = done + n_ops;            // per-op work counters (dynamic assignment)
-  for (int j = 0; j < n_ops; j++) {
-    const PipeOp& op = ops[j];
-    const int nu = op.n_units;
-    for (;;) {
-      // grab the next unit of op j: a CTA that is busy never holds work back
-      if (tid == 0) next_unit = (int)atomicAdd(claim + j, 1u);
-      __syncthreads();
-      const int u = next_unit;
-      __syncthreads();
-      if (u >= nu) break;
-      unsigned long long* tr = trace ? trace + ((size_t)unit_base[j] + u) * 4 : nullptr;
-      if (tr && tid == 0) tr[0] = gtimer();
-      if (op.type == BITLUT_OP_LOOKUP) {
-        const GemvArgs& g = op.g;
-        const SmemPlan sp = smem_plan<ST>(g.L, g.zeros != nullptr, true);
-        const int tile = u % g.L.n_tiles, row = u / g.L.n_tiles;
-        tile_issue<ST, true>(g, tile, sp, smem, bar);          // independent of deps
-        wait_deps(op, ops, done);
-        if (tr && tid == 0) tr[1] = gtimer();
-        uint4 tq0[R / 2];
-        prefetch_tables_q8<R>(g, row, tq0);
-        load_row_vectors<BITLUT_TABLE_Q8>(g, row, sp, smem);
-        mbar_wait(bar, phase);
-        phase ^= 1u;
-        __syncthreads();
-        if (tr && tid == 0) tr[2] = gtimer();
-        tile_body<R, LG, ST, true, BITLUT_TABLE_Q8>(g, tile, row, sp, smem, tq0);
-      } else {
-        wait_deps(op, ops, done);
-        if (tr && tid == 0) tr[1] = tr[2] = gtimer();
-        const int row = u / op.row_units, kg0 = (u - row * op.row_units) * kLutUnitKG;
-        float* sa = reinterpret_cast<float*>(smem);
-        float* red = sa + 4 * kPipeThreads;
-        if (op.a_dtype == BITLUT_DT_F16)
-          lutk::lut_block<BITLUT_TABLE_Q8, __half>(reinterpret_cast<const __half*>(op.a), op.k, op.gs,
-                                                   op.tables, op.tscales, op.rowsums, row, kg0, sa, red);
-        else
-          lutk::lut_block<BITLUT_TABLE_Q8, float>(reinterpret_cast<const float*>(op.a), op.k, op.gs,
-                                                  op.tables, op.tscales, op.rowsums, row, kg0, sa, red);
-      }
-      __syncthreads();
-      if (tid == 0) {
-        __threadfence();
-        atomicAdd(done + j, 1u);
-        if (tr) tr[3] = gtimer();
-      }
-    }
-  }
-}
-
-template <int R, int LG, typename ST>
-int launch_pipeline(const PipeHeader& h, const PipeOp* ops_dev, unsigned* done, unsigned long long* trace,
-                    const int* unit_base, cudaStream_t stream) {
-  auto kern = pipeline_kernel<R, LG, ST>;
-  const int smem = (int)h.smem_bytes;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-    return BITLUT_EINTERNAL;
-  int per_sm = 0, dev = 0, sms = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return BITLUT_EINTERNAL;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPipeThreads, smem) != cudaSuccess ||
-      per_sm < 1)
-    return BITLUT_ELAYOUT;
-  if (per_sm > 4) per_sm = 4;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(sms * per_sm);
-  cfg.blockDim = dim3(kPipeThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr; cfg.numAttrs = 1;
-  if (cudaMemsetAsync(done, 0, sizeof(unsigned) * 2 * (size_t)h.n_ops, stream) != cudaSuccess)
-    return BITLUT_EINTERNAL;
-  return cudaLaunchKernelEx(&cfg, kern, ops_dev, h.n_ops, done, trace, unit_base) == cudaSuccess
-             ? BITLUT_OK : BITLUT_EINTERNAL;
-}
-
-}  // namespace
-
-extern "C" size_t bitlut_pipeline_table_bytes(int n_ops) {
-  return sizeof(PipeHeader) + 16 + sizeof(PipeOp) * (size_t)n_ops;
-}
-
-extern "C" int bitlut_pipeline_encode(const bitlut_pipe_op* specs, int n_ops, void* table_host,
-                                      size_t table_bytes) {
-  if (n_ops <= 0 || !specs || !table_host) return BITLUT_EPARAM;
-  if (table_bytes < bitlut_pipeline_table_bytes(n_ops)) return BITLUT_ESHAPE;
-  PipeHeader h = {};
-  h.n_ops = n_ops;
-  h.R = h.LG = 0;
-  h.scale_dtype = -1;
-  size_t smem = 4 * kPipeThreads * 4 + 64;            // table-build scratch
-  PipeOp* ops = reinterpret_cast<PipeOp*>(reinterpret_cast<uint8_t*>(table_host) + sizeof(PipeHeader) + 16);
-  for (int j = 0; j < n_ops; j++) {
-    const bitlut_pipe_op& s = specs[j];
-    PipeOp o = {};
-    o.type = s.type;
-    for (int i = 0; i < 3; i++) {
-      o.dep[i] = s.dep[i];
-      if (s.dep[i] >= j || s.dep[i] < -1) return BITLUT_EPARAM;    // deps must precede
-    }
-    if (s.type == BITLUT_OP_TABLES) {
-      if (s.a_dtype != BITLUT_DT_F16 && s.a_dtype != BITLUT_DT_F32) return BITLUT_EPARAM;
-      const int gpg = s.group_size / 4;
-      if (s.group_size % 16 != 0 || gpg > 128 || (gpg & (gpg - 1)) || s.k % s.group_size != 0)
-        return BITLUT_EPARAM;
-      const int KG = s.k / 4;
-      o.a = s.a; o.a_dtype = s.a_dtype; o.k = s.k; o.gs = s.group_size;
-      o.row_units = (KG + kLutUnitKG - 1) / kLutUnitKG;
-      o.n_units = o.row_units * s.n;
-      o.tables = s.tables; o.tscales = s.tscales; o.rowsums = s.rowsums;
-    } else if (s.type == BITLUT_OP_LOOKUP) {
-      bl::LayoutV2 L;
-      int rc = bl::make_layout(s.m, s.k, s.bits, s.group_size, &L);
-      if (rc) return rc;
-      if (s.scale_dtype != BITLUT_DT_F16 && s.scale_dtype != BITLUT_DT_F32) return BITLUT_EPARAM;
-      if (h.scale_dtype < 0) { h.R = L.R; h.LG = L.Lg; h.scale_dtype = s.scale_dtype; }
-      if (h.R != L.R || h.LG != L.Lg || h.scale_dtype != s.scale_dtype) return BITLUT_EPARAM;  // one instantiation
-      if (L.n_sg * L.U > 512) return BITLUT_ELAYOUT;
-      const size_t need = s.scale_dtype == BITLUT_DT_F16 ? smem_plan<__half>(L, s.zeros != nullptr, true).total
-                                                         : smem_plan<float>(L, s.zeros != nullptr, true).total;
-      if (need > smem) smem = need;
-      GemvArgs& g = o.g;
-      g.w = s.wgpu; g.wscales = s.wscales; g.zeros = s.zeros;
-      g.qtab = reinterpret_cast<const uint8_t*>(s.tables); g.tscales = s.tscales; g.rowsums = s.rowsums;
-      g.out = s.out; g.partials = nullptr; g.trace = nullptr; g.independent = 0; g.L = L;
-      g.fast = (s.flags & BITLUT_FLAG_FAST_EPILOGUE) != 0;
-      g.rows_per_cta = 1; g.n_rows = s.n;
-      o.n_units = L.n_tiles * s.n;
-    } else {
-      return BITLUT_EPARAM;
-    }
-    ops[j] = o;
-  }
-  if (h.scale_dtype < 0) { h.R = 8; h.LG = 1; h.scale_dtype = BITLUT_DT_F16; }
-  h.smem_bytes = ((smem + 15) & ~(size_t)15) + 16;      // + mbarrier slot
-  if (h.smem_bytes > 227 * 1024) return BITLUT_ELAYOUT;
-  *reinterpret_cast<PipeHeader*>(table_host) = h;
-  return BITLUT_OK;
-}
-
-extern "C" int bitlut_pipeline_launch_traced(const void* table_host, const void* table_dev,
-                                             unsigned* counters, unsigned long long* trace,
-                                             const int* unit_base, void* stream);
-
-extern "C" int bitlut_pipeline_launch(const void* table_host, const void* table_dev, unsigned* counters,
-                                      void* stream) {
-  return bitlut_pipeline_launch_traced(table_host, table_dev, counters, nullptr, nullptr, stream);
-}
-
-extern "C" int bitlut_pipeline_launch_traced(const void* table_host, const void* table_dev,
-                                             unsigned* counters, unsigned long long* trace,
-                                             const int* unit_base, void* stream) {
-  if (!table_host || !table_dev || !counters) return BITLUT_EPARAM;
-  const PipeHeader& h = *reinterpret_cast<const PipeHeader*>(table_host);
-  const PipeOp* ops = reinterpret_cast<const PipeOp*>(reinterpret_cast<const uint8_t*>(table_dev) +
-                                                      sizeof(PipeHeader) + 16);
-  cudaStream_t s = (cudaStream_t)stream;
-  const bool f16 = h.scale_dtype == BITLUT_DT_F16;
-#define BL_PIPE(R_, LG_)                                                                  \
-  if (h.R == R_ && h.LG == LG_)                                                           \
-    return f16 ? launch_pipeline<R_, LG_, __half>(h, ops, counters, trace, unit_base, s)  \
-               : launch_pipeline<R_, LG_, float>(h, ops, counters, trace, unit_base, s);
-  BL_PIPE(8, 1) BL_PIPE(8, 2) BL_PIPE(8, 4) BL_PIPE(8, 8) BL_PIPE(8, 16) BL_PIPE(4, 1)
-#undef BL_PIPE
-  return BITLUT_EPARAM;
-}
 
 // ---------------------------------------------------------------------------
 // Per-op executor: the same op list as stream-ordered launches of the

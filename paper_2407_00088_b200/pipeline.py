@@ -6,8 +6,6 @@ replayed.  Two executors run the same list, bitwise identically to calling
 * ``"graph"`` (default): per-op kernels chained with programmatic dependent
   launch (lookups whose inputs are already complete skip the start-of-kernel
   wait), captured into one CUDA graph; a replay is one graph launch.
-* ``"persistent"``: ONE cooperative launch; every CTA walks the op list and
-  per-op completion counters replace kernel boundaries.
 * ``"batch"``: for op lists of INDEPENDENT batch-1 calls only (table builds
   without dependencies, each lookup reading one of them, fast epilogue, int8
   tables: a layer set): every table build in one launch
@@ -50,13 +48,6 @@ class PipeOpSpec(ctypes.Structure):
 
 def _bind():
     L = N.lib()
-    L.bitlut_pipeline_table_bytes.restype = ctypes.c_size_t
-    L.bitlut_pipeline_table_bytes.argtypes = [ctypes.c_int]
-    L.bitlut_pipeline_encode.restype = ctypes.c_int
-    L.bitlut_pipeline_encode.argtypes = [ctypes.POINTER(PipeOpSpec), ctypes.c_int, ctypes.c_void_p,
-                                         ctypes.c_size_t]
-    L.bitlut_pipeline_launch.restype = ctypes.c_int
-    L.bitlut_pipeline_launch.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
     L.bitlut_pipeline_plan_flags.restype = ctypes.c_int
     L.bitlut_pipeline_plan_flags.argtypes = [ctypes.POINTER(PipeOpSpec), ctypes.c_int,
                                              ctypes.POINTER(ctypes.c_int)]
@@ -82,9 +73,9 @@ class TableRef(OpRef):
 
 
 class Pipeline:
-    """Records ops, then runs them in one persistent launch."""
+    """Records ops, then runs them as one CUDA graph replay."""
 
-    EXECUTORS = ("graph", "persistent", "batch")
+    EXECUTORS = ("graph", "batch")
     SYNCS = ("counters", "pdl")
 
     def __init__(self, device=None, executor: str = "graph", sync: str = "pdl"):
@@ -92,7 +83,8 @@ class Pipeline:
         inputs are tracked by programmatic-dependent-launch waits
         (sync="pdl", default) or by completion counters (sync="counters": no
         launch drains the stream, but measured slower on B200 -- DESIGN.md
-        §4.6).  executor "persistent": one cooperative launch."""
+        §4.6).  executor "batch": independent batch-1 calls, one lookup
+        launch per (K, encoding)."""
         if executor not in self.EXECUTORS:
             raise ParameterError(f"executor must be one of {self.EXECUTORS}, got {executor!r}")
         if sync not in self.SYNCS:
@@ -122,7 +114,7 @@ class Pipeline:
         """Table build (kernel.py:226-251) for activations a (n, k) f16/f32.
         fuse=True lets the graph executor fold it into its consumers when they
         are all batch-1 fast-epilogue lookups (one launch per GEMV,
-        bitlut_mpgemv_fused); the persistent executor ignores it."""
+        bitlut_mpgemv_fused)."""
         N.require_cuda(a, "activations")
         if a.dim() == 1:
             a = a.reshape(1, -1)
@@ -201,14 +193,6 @@ class Pipeline:
         self._arr = (PipeOpSpec * n)(*self.specs)
         if self.executor == "batch":
             self._compile_batch()
-        elif self.executor == "persistent":
-            nbytes = L.bitlut_pipeline_table_bytes(n)
-            host = torch.empty(nbytes, dtype=torch.uint8)
-            rc = L.bitlut_pipeline_encode(self._arr, n, ctypes.c_void_p(host.data_ptr()), nbytes)
-            raise_for_status(rc, "bitlut_pipeline_encode")
-            self._host = host
-            self._dev = host.to(self.device)
-            self._counters = torch.zeros(2 * n, dtype=torch.int32, device=self.device)
         else:
             self.plan_flags()                       # validates the list before capture
             if self.sync == "counters":
@@ -294,8 +278,6 @@ class Pipeline:
 
     def n_launches(self) -> int:
         """Kernel launches per run (graph executor: launch units of the plan)."""
-        if self.executor == "persistent":
-            return 1
         if self.executor == "batch":
             if self._arr is None:
                 self.compile()
@@ -308,15 +290,8 @@ class Pipeline:
         if self._arr is None:
             self.compile()
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
-        if self.executor in ("graph", "batch"):
-            with torch.cuda.stream(st):
-                self._graph.replay()
-            return
-        rc = _bind().bitlut_pipeline_launch(ctypes.c_void_p(self._host.data_ptr()),
-                                            ctypes.c_void_p(self._dev.data_ptr()),
-                                            ctypes.c_void_p(self._counters.data_ptr()),
-                                            ctypes.c_void_p(st.cuda_stream))
-        raise_for_status(rc, "bitlut_pipeline_launch")
+        with torch.cuda.stream(st):
+            self._graph.replay()
 
     def run_eager(self, stream: Optional[torch.cuda.Stream] = None) -> None:
         """Graph executor without the graph: launch the op list directly."""

@@ -1,6 +1,5 @@
 """Per-shape batch-1 lookup timings (bench.py per_shape_table) as a compact
-table: python tools/per_shape.py [bits,...]; BITLUT_STREAM=0 selects the
-persistent gemv_b1 kernel instead of the streaming one."""
+table: python tools/per_shape.py [bits,...]."""
 import os
 import sys
 
