@@ -131,9 +131,14 @@ def _host_rows(a):
         arr = arr.reshape(1, -1)
     if arr.ndim != 2:
         raise ShapeError("activations must be 1-D or 2-D")
-    if not np.isfinite(arr).all():
+    arr = np.ascontiguousarray(arr)
+    if arr.dtype == np.float16:      # finite <=> exponent bits not all ones (fast integer test)
+        bad = bool(((arr.view(np.uint16) & 0x7C00) == 0x7C00).any())
+    else:
+        bad = not np.isfinite(arr).all()
+    if bad:
         raise DataError("activations contain non-finite values")
-    return np.ascontiguousarray(arr)
+    return arr
 
 
 def _activation_rows(a, check_finite=None):
