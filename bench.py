@@ -795,6 +795,18 @@ def main():
         summary["compute_only_ms"] = round(executors[best]["compute_only_ms"], 4)
         summary["collective_only_ms"] = round(executors[best]["collective_only_ms"], 4)
 
+    # ---- N > 1: the all-gather fused into the lookup epilogue (peer stores
+    #      over NVLink into torch symmetric memory + release flags), next to
+    #      lookup + NCCL all-gather, on one 4096x4096 W2 GEMV ----
+    if world > 1:
+        try:
+            fg_res = fused_gather_run(device, stream, world, group, rank, time_runs)
+        except Exception as e:                         # report, never fake
+            fg_res = {"error": f"{type(e).__name__}: {e}"[:300]}
+        details["fused_gather"] = fg_res
+        summary["fused_gather"] = {k: fg_res[k] for k in ("fused_us", "nccl_us", "bitwise_equal", "error")
+                                   if k in fg_res}
+
     # ---- the dominant kernel alone: the batch executor's lookup launches
     #      (tables built by one eager run of the step), same flags ----
     pb = pipes[best][0]
@@ -894,6 +906,67 @@ def main():
         emit(line, details, details_path(args.details))
     if world > 1:
         dist.destroy_process_group()
+
+
+def fused_gather_run(device, stream, world, group, rank, time_runs):
+    """One 4096x4096 W2 g64 batch-1 GEMV sharded by output channel over the
+    ranks: (a) FusedGather.symmetric -- the lookup kernel stores every output
+    into every rank's gathered row over NVLink and releases the peers' flags;
+    a bounded stream-ordered wait -- and (b) the lookup + NCCL
+    all_gather_into_tensor.  Time per gathered GEMV (max over ranks) and a
+    bitwise comparison of the two gathered rows."""
+    import torch
+    import torch.distributed as dist
+    import paper_2407_00088_b200 as B
+    from paper_2407_00088_b200 import _native as N
+    from paper_2407_00088_b200 import parallel as PP
+    m, k, bits, gs = 4096, 4096, 2, 64
+    gen = torch.Generator(device=device)
+    gen.manual_seed(4096)                                # identical weights / row on every rank
+    q = torch.randint(0, 1 << bits, (m, k), dtype=torch.uint8, device=device, generator=gen)
+    sc = (torch.randn((m, k // gs), device=device, generator=gen).abs() * 0.02 + 1e-3).half()
+    x = torch.randn((1, k), device=device, generator=gen).half()
+    qw = B.QuantizedWeights(m=m, k=k, bits=bits, group_size=gs, qvalues=q, scales=sc)
+    shard = B.prepare_weights(PP.shard_quantized_weights(qw, rank, world))
+    # every rank must be able to allocate symmetric memory before any enters
+    # the (collective) rendezvous, else the others would wait there forever
+    ok = torch.ones(1, device=device)
+    try:
+        import torch.distributed._symmetric_memory as symm_mem
+        symm_mem.empty((1, 16), dtype=torch.float32, device=device)
+    except Exception:
+        ok.zero_()
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+    if float(ok.item()) < 1:
+        raise RuntimeError("torch symmetric memory unavailable on some rank")
+    fg = PP.FusedGather.symmetric(m, group)
+    with torch.cuda.stream(stream):
+        fg.launch(x[0], shard)
+        row = fg.wait().clone()
+    torch.cuda.synchronize()
+    if int(fg.timed_out.item()):
+        raise RuntimeError("fused gather: a peer never arrived (bounded wait timed out)")
+    gat = torch.empty((world, shard.m), dtype=torch.float32, device=device)
+    fl = N.FLAG_PDL | N.FLAG_FAST_EPILOGUE
+
+    def nccl_step():
+        t = N.build_lut(x, gs, N.TABLE_Q8)
+        y, _ = N.lookup(shard.gpu, shard.scales, None, *t, shard.m, k, bits, gs, N.TABLE_Q8, fl, False)
+        dist.all_gather_into_tensor(gat, y.reshape(-1), group=group)
+
+    def fused_step():
+        fg.launch(x[0], shard)
+        fg.wait()
+    with torch.cuda.stream(stream):
+        nccl_step()
+    torch.cuda.synchronize()
+    equal = bool(torch.equal(row.reshape(-1), gat.reshape(-1)))
+    ms_f = time_runs(fused_step)
+    ms_n = time_runs(nccl_step)
+    if int(fg.timed_out.item()):
+        raise RuntimeError("fused gather: a peer never arrived during timing")
+    return {"shape": "4096x4096 W2 g64, channel shards", "world": world, "fused_us": round(ms_f * 1e3, 2),
+            "nccl_us": round(ms_n * 1e3, 2), "bitwise_equal": equal}
 
 
 def time_graph_max(g, reps, warmup, barrier, stream, world, device):

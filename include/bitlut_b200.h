@@ -312,8 +312,10 @@ int bitlut_mpgemv_gather(const uint8_t* wgpu, int m, int k, int bits, int group_
                          float* const* peer_out, unsigned* const* peer_flags, unsigned* ticket,
                          int col_offset, int flags, void* stream);
 /* Stream-ordered wait (one thread, ld.acquire.sys) until *flag - target >= 0
- * as signed 32-bit (wrap-around safe). */
-int bitlut_gather_wait(const unsigned* flag, unsigned target, void* stream);
+ * as signed 32-bit (wrap-around safe).  Bounded: after 10 s without the
+ * peers' arrivals it gives up and sets *timed_out (device u32, nullable), so
+ * a missing peer cannot hang the stream. */
+int bitlut_gather_wait(const unsigned* flag, unsigned target, unsigned* timed_out, void* stream);
 
 /* bitlut_mpgemm plus a timeline: `trace` (device, (n * tiles) x 8 u64) gets
  * per-CTA %globaltimer stamps [start, loads issued, after griddepcontrol.wait,

@@ -54,7 +54,7 @@ _SIGS = {
     "bitlut_mpgemv_multi": [_vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _i, _vp],
     "bitlut_mpgemv_gather": [_vp, _i, _i, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _i,
                              _vp],
-    "bitlut_gather_wait": [_vp, ctypes.c_uint32, _vp],
+    "bitlut_gather_wait": [_vp, ctypes.c_uint32, _vp, _vp],
     "bitlut_mpgemv_multi_tab": [_vp, _i, _i, _i, _i, _i, _i, _vp],
     "bitlut_mpgemv_batch_encode": [_vp, _i, _i, _i, _i, _i, _vp],
     "bitlut_mpgemv_batch": [_vp, _i, _i, _i, _i, _i, _i, _i, _i, _vp],
@@ -348,10 +348,11 @@ def mpgemv_gather(wgpu: torch.Tensor, wscales: torch.Tensor, zeros: Optional[tor
     return out
 
 
-def gather_wait(flag: torch.Tensor, target: int) -> None:
-    """bitlut_gather_wait on the flag's stream."""
+def gather_wait(flag: torch.Tensor, target: int, timed_out: Optional[torch.Tensor] = None) -> None:
+    """bitlut_gather_wait on the flag's stream (bounded; sets `timed_out`
+    (device int32) when the peers never arrive)."""
     require_cuda(flag, "gather flag")
-    raise_for_status(lib().bitlut_gather_wait(ptr(flag), target & 0xFFFFFFFF, stream_of(flag)),
+    raise_for_status(lib().bitlut_gather_wait(ptr(flag), target & 0xFFFFFFFF, ptr(timed_out), stream_of(flag)),
                      "bitlut_gather_wait")
 
 

@@ -1574,12 +1574,20 @@ extern "C" int bitlut_mpgemv_gather(const uint8_t* wgpu, int m, int k, int bits,
 }
 
 namespace {
-__global__ void gather_wait_kernel(const unsigned* flag, unsigned target) {
+// bounded: gives up after timeout_ns (a peer that never arrives must not
+// hang the stream) and then sets *timed_out, when given
+__global__ void gather_wait_kernel(const unsigned* flag, unsigned target, unsigned long long timeout_ns,
+                                   unsigned* timed_out) {
   if (threadIdx.x == 0) {
+    const unsigned long long t0 = gtimer();
     unsigned v;
     for (;;) {
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
       if ((int)(v - target) >= 0) break;
+      if (gtimer() - t0 > timeout_ns) {
+        if (timed_out) *timed_out = 1u;
+        break;
+      }
       __nanosleep(100);
     }
   }
@@ -1588,9 +1596,9 @@ __global__ void gather_wait_kernel(const unsigned* flag, unsigned target) {
 
 // Stream-ordered wait until this rank's gather flag reaches `target`
 // (wrap-around safe): kernels after it on `stream` see the gathered row.
-extern "C" int bitlut_gather_wait(const unsigned* flag, unsigned target, void* stream) {
+extern "C" int bitlut_gather_wait(const unsigned* flag, unsigned target, unsigned* timed_out, void* stream) {
   if (!flag) return BITLUT_EPARAM;
-  gather_wait_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(flag, target);
+  gather_wait_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(flag, target, 10000000000ull, timed_out);
   return bl_launch_status();
 }
 

@@ -160,6 +160,7 @@ class FusedGather:
         self.row, self.flag = row, flag
         self.out_ptrs, self.flag_ptrs = out_ptrs, flag_ptrs
         self.ticket = torch.zeros(1, dtype=torch.int32, device=row.device)
+        self.timed_out = torch.zeros(1, dtype=torch.int32, device=row.device)   # set by a bounded wait
         self.epoch = 0
         self._keep = keep                      # keeps peer allocations / handles alive
 
@@ -212,7 +213,7 @@ class FusedGather:
         returns this epoch's gathered (1, m_total) row (valid until launch
         epoch + 2 -- see the reuse protocol above)."""
         from . import _native as N
-        N.gather_wait(self.flag, self.epoch * self.world)
+        N.gather_wait(self.flag, self.epoch * self.world, self.timed_out)
         return self.row[self.epoch & 1:(self.epoch & 1) + 1]
 
 
