@@ -320,3 +320,37 @@ def test_nmse_acceptance_through_cuda_path():
             o2 = B.mpgemv(a, pw, **kw)
             n2 = float(((y - o2) ** 2).sum()) / float((y ** 2).sum())
             assert lo <= n2 <= hi and abs(n2 - nmse) <= 0.01 * nmse, (kw, n2, nmse)
+
+
+# ---------------------------------------------------------------- random-instance sweep (criterion C1)
+
+def test_random_instance_sweep_1000():
+    """The reference's 1000-instance property run (pkg/tests/
+    test_acceptance.py:85-118) restated for the CUDA path: random m, k,
+    tile, bits in 1..4, weights quantized by the reference's quantizer (C
+    port, refine=False, gs = 32), 1 or 2 activation rows.  cuda-q8 exact ==
+    the oracle's vector-q8 bitwise (the reference's own vector == scalar
+    pairing is bitwise), the fast epilogue within 1e-5, cuda-f16 within
+    1e-3 of the oracle's fp32-table scalar-real (max-norm)."""
+    rng = np.random.default_rng(20250809)
+    worst = {"fast": 0.0, "f16": 0.0}
+    for i in range(1000):
+        m = 32 * int(rng.integers(1, 17))
+        k = 32 * int(rng.integers(1, 17))
+        k_tile = int(rng.choice([kt for kt in (32, 64, 128) if k % kt == 0]))
+        bits = int(rng.integers(1, 5))
+        w = rng.standard_normal((m, k), dtype=np.float32)
+        q, d = O.c_quantize_weights(w, bits, 32, refine=False)
+        pw = B.prepare_weights(B.QuantizedWeights(m=m, k=k, bits=bits, group_size=32, qvalues=q, scales=d),
+                               B.TileConfig(n_tile=1, m_tile=32, k_tile=k_tile))
+        n_rows = 2 if i % 10 == 0 else 1
+        a = rng.standard_normal((n_rows, k), dtype=np.float32)
+        ref = O.mpgemm_q8(a, q, d, bits, 32)
+        assert np.array_equal(B.mpgemm(a, pw), ref), i
+        scale = max(float(np.abs(ref).max()), 1e-6)
+        if bits != 3:
+            worst["fast"] = max(worst["fast"], float(np.abs(B.mpgemm(a, pw, exact_epilogue=False) - ref).max()) / scale)
+        real = O.mpgemm_real(a, q, d, bits, 32)
+        rs = max(float(np.abs(real).max()), 1e-6)
+        worst["f16"] = max(worst["f16"], float(np.abs(B.mpgemm(a, pw, variant="cuda-f16") - real).max()) / rs)
+    assert worst["fast"] <= 1e-5 and worst["f16"] <= 1e-3, worst
