@@ -285,7 +285,9 @@ int bitlut_mpgemv_batch(const bitlut_batch_mat* dev_mats, int n_mats, int total_
  * build + lookup launch), looks up, copies the (n, m) f32 result to out_host
  * and synchronizes `stream`.  The device scratch (a_dev, tables, tscales,
  * rowsums, out_dev: sizes as for bitlut_build_lut / bitlut_mpgemm) is the
- * caller's; flags as bitlut_mpgemm.  csrc/host_api.cu. */
+ * caller's; flags as bitlut_mpgemm.  Passing a_dev == a_host (out_dev ==
+ * out_host) makes the kernels read (write) the pinned, UVA-mapped host
+ * buffer directly instead of a copy operation.  csrc/host_api.cu. */
 int bitlut_mpgemm_host(const void* a_host, int a_dtype, int n, int k, const uint8_t* wgpu, int m, int bits,
                        int group_size, const void* wscales, const void* zeros, int scale_dtype, int mode,
                        int flags, void* a_dev, void* tables, float* tscales, float* rowsums, float* out_dev,

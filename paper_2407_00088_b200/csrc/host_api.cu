@@ -28,7 +28,11 @@ extern "C" int bitlut_mpgemm_host(const void* a_host, int a_dtype, int n, int k,
   if (a_dtype != BITLUT_DT_F32 && a_dtype != BITLUT_DT_F16) return BITLUT_EPARAM;
   const cudaStream_t st = (cudaStream_t)stream;
   const size_t a_bytes = (size_t)n * k * (a_dtype == BITLUT_DT_F16 ? 2 : 4);
-  if (cudaMemcpyAsync(a_dev, a_host, a_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess) return BITLUT_EINTERNAL;
+  // a_dev == a_host / out_dev == out_host: pinned (mapped) host memory the
+  // kernels read / write directly over the bus -- no copy operations
+  if (a_dev != a_host &&
+      cudaMemcpyAsync(a_dev, a_host, a_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return BITLUT_EINTERNAL;
   int rc = BITLUT_ELAYOUT;
   // batch 1, fast epilogue, fp16 row: table build + lookup in one launch
   if (n == 1 && mode == BITLUT_TABLE_Q8 && (flags & BITLUT_FLAG_FAST_EPILOGUE) && a_dtype == BITLUT_DT_F16 &&
@@ -43,7 +47,8 @@ extern "C" int bitlut_mpgemm_host(const void* a_host, int a_dtype, int n, int k,
                        n, out_dev, nullptr, flags, stream);
   }
   if (rc) return rc;
-  if (cudaMemcpyAsync(out_host, out_dev, (size_t)n * m * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+  if (out_dev != out_host &&
+      cudaMemcpyAsync(out_host, out_dev, (size_t)n * m * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess)
     return BITLUT_EINTERNAL;
   return cudaStreamSynchronize(st) == cudaSuccess ? BITLUT_OK : BITLUT_EINTERNAL;
 }

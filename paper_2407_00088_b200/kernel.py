@@ -178,6 +178,12 @@ def _activation_rows(a, check_finite=None):
 
 _TLS = threading.local()
 _SCRATCH_MAX = 16
+# the lookup writes the result straight into the pinned (UVA-mapped) staging
+# buffer (no D2H copy operation: -5..-8 us per call, tools/per_call_profile.py);
+# reading the activations the same way was slower (the fused build reads them
+# from every CTA).  BITLUT_ZERO_COPY = "in,out" (diagnostic)
+import os as _os
+_ZERO_COPY = tuple(bool(int(x)) for x in _os.environ.get("BITLUT_ZERO_COPY", "0,1").split(","))
 
 
 class _HostScratch:
@@ -222,11 +228,13 @@ def _host_call(rows: np.ndarray, pw: PackedWeights, mode: int, flags: int) -> np
     np.copyto(b.a_np, rows)
     if torch.cuda.current_device() != dev.index:
         torch.cuda.set_device(dev)
+    zc_in, zc_out = _ZERO_COPY
     rc = N.lib().bitlut_mpgemm_host(
         b.a_host.data_ptr(), N.DT_F16 if a_dtype == torch.float16 else N.DT_F32, n, k, pw.gpu.data_ptr(), pw.m,
         pw.bits, pw.group_size, pw.scales.data_ptr(), None if pw.zeros is None else pw.zeros.data_ptr(),
-        N.dtype_code(pw.scales), mode, flags, b.a_dev.data_ptr(), b.tables.data_ptr(), b.ts.data_ptr(),
-        b.rs.data_ptr(), b.out_dev.data_ptr(), b.out_host.data_ptr(),
+        N.dtype_code(pw.scales), mode, flags, b.a_host.data_ptr() if zc_in else b.a_dev.data_ptr(),
+        b.tables.data_ptr(), b.ts.data_ptr(), b.rs.data_ptr(),
+        b.out_host.data_ptr() if zc_out else b.out_dev.data_ptr(), b.out_host.data_ptr(),
         torch.cuda.current_stream(dev).cuda_stream)
     raise_for_status(rc, "bitlut_mpgemm_host")
     return b.out_np.copy()
