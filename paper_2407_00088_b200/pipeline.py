@@ -111,19 +111,22 @@ class Pipeline:
         return idx + [-1] * (3 - len(idx))
 
     def tables(self, a: torch.Tensor, group_size: int, deps: Sequence = (), fuse: bool = False) -> TableRef:
-        """Table build (kernel.py:226-251) for activations a (n, k) f16/f32.
+        """Table build (kernel.py:226-251) for activations a (n, k) f16/f32
+        on the device, or in pinned host memory (read over the bus).
         fuse=True lets the graph executor fold it into its consumers when they
         are all batch-1 fast-epilogue lookups (one launch per GEMV,
         bitlut_mpgemv_fused)."""
-        N.require_cuda(a, "activations")
+        if not (a.is_cuda or a.is_pinned()):          # pinned host rows: read over the bus (UVA)
+            N.require_cuda(a, "activations")
         if a.dim() == 1:
             a = a.reshape(1, -1)
         a = a.contiguous()
         n, k = a.shape
         nq = k // group_size
-        tables = torch.empty((n, k // 4, 8), dtype=torch.int8, device=a.device)
-        ts = torch.empty((n, nq), dtype=torch.float32, device=a.device)
-        rs = torch.empty((n, nq), dtype=torch.float32, device=a.device)
+        dev = a.device if a.is_cuda else self.device
+        tables = torch.empty((n, k // 4, 8), dtype=torch.int8, device=dev)
+        ts = torch.empty((n, nq), dtype=torch.float32, device=dev)
+        rs = torch.empty((n, nq), dtype=torch.float32, device=dev)
         s = PipeOpSpec()
         s.type = OP_TABLES
         s.dep[:] = self._deps(deps)
@@ -141,7 +144,9 @@ class Pipeline:
         """Lookup GEMV with packed weights pw over table op t; returns the
         (n, m) float32 output tensor (filled when the pipeline runs; pass
         ``out`` to choose it, e.g. a view of one output arena).  By default
-        the op depends on its table build only.  ``partials`` (batch
+        the op depends on its table build only; ``out`` may also be a
+        pinned host tensor (the kernel then writes the result over the bus,
+        no copy operation).  ``partials`` (batch
         executor only): an (m, k/gs) int32 tensor that receives the exact
         integer sums S = sum_p 2^p P_p."""
         if pw.gpu is None:
@@ -150,9 +155,12 @@ class Pipeline:
             raise ParameterError("table op does not match the weights' k / group_size")
         if out is None:
             out = torch.empty((t.n, pw.m), dtype=torch.float32, device=pw.gpu.device)
-        elif (out.dtype != torch.float32 or not out.is_contiguous() or out.device != pw.gpu.device
-              or out.numel() != t.n * pw.m):
-            raise ParameterError("out must be a contiguous float32 (n, m) tensor on the weights' device")
+        elif (out.dtype != torch.float32 or not out.is_contiguous() or out.numel() != t.n * pw.m
+              or not (out.device == pw.gpu.device or (out.device.type == "cpu" and out.is_pinned()))):
+            # a PINNED host tensor is allowed: the kernel writes the result
+            # over the bus into the UVA-mapped page (no D2H copy operation)
+            raise ParameterError("out must be a contiguous float32 (n, m) tensor on the weights' device "
+                                 "or in pinned host memory")
         tables, ts, rs = t.tensors
         s = PipeOpSpec()
         s.type = OP_LOOKUP
