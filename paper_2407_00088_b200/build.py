@@ -27,12 +27,12 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def lib_path() -> str:
-    return os.path.join(PKG, "_lib", "libbitlut_b200.so")
+def lib_path(checks: bool = False) -> str:
+    return os.path.join(PKG, "_lib", "libbitlut_b200_checks.so" if checks else "libbitlut_b200.so")
 
 
-def needs_build() -> bool:
-    out = lib_path()
+def needs_build(checks: bool = False) -> bool:
+    out = lib_path(checks)
     if not os.path.exists(out):
         return True
     t = os.path.getmtime(out)
@@ -41,16 +41,19 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build_lib(force: bool = False, verbose: bool = False) -> str:
-    """nvcc each translation unit (in parallel), then link the shared library."""
+def build_lib(force: bool = False, verbose: bool = False, checks: bool = False) -> str:
+    """nvcc each translation unit (in parallel), then link the shared library.
+    checks=True builds the diagnostic libbitlut_b200_checks.so with the
+    device-side bounds checks (BL_CHECK, common.cuh) compiled in; select it
+    with BITLUT_B200_LIB."""
     from concurrent.futures import ThreadPoolExecutor
-    out = lib_path()
-    if not force and not needs_build():
+    out = lib_path(checks)
+    if not force and not needs_build(checks):
         return out
     os.makedirs(os.path.dirname(out), exist_ok=True)
-    objdir = os.path.join(os.path.dirname(out), "obj")
+    objdir = os.path.join(os.path.dirname(out), "obj_checks" if checks else "obj")
     os.makedirs(objdir, exist_ok=True)
-    flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    flags = [f for f in NVCC_FLAGS if f != "-shared"] + (["-DBITLUT_CHECKS=1"] if checks else [])
 
     csrc = os.path.join(PKG, "csrc")
     headers = [os.path.join(csrc, f) for f in os.listdir(csrc) if f.endswith(".cuh")]
@@ -81,7 +84,7 @@ def build_lib(force: bool = False, verbose: bool = False) -> str:
                          + [o for o, _ in results], capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed linking libbitlut_b200.so")
+        raise RuntimeError(f"nvcc failed linking {os.path.basename(out)}")
     os.replace(tmp, out)
     return out
 
@@ -93,5 +96,5 @@ def build_oracle() -> None:
 
 
 if __name__ == "__main__":
-    print(build_lib(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build_lib(force="--force" in sys.argv, verbose="-v" in sys.argv, checks="--checks" in sys.argv))
     build_oracle()

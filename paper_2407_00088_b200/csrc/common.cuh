@@ -8,6 +8,34 @@
 
 #define BL_DEV __device__ __forceinline__
 
+// Device-side bounds checks of the checks build (build.py build_lib(checks=
+// True) -> libbitlut_b200_checks.so, -DBITLUT_CHECKS): a violated index
+// bound prints the condition and traps.  compute-sanitizer is closed on the
+// GPU pool, so the GPU tests are also run against that build.  Compiled out
+// of the product library.
+#ifdef BITLUT_CHECKS
+#include <cstdio>
+#define BL_CHECK(c)                                                                       \
+  do {                                                                                    \
+    if (!(c)) {                                                                           \
+      printf("BL_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, \
+             (int)blockIdx.x, (int)threadIdx.x);                                          \
+      __trap();                                                                           \
+    }                                                                                     \
+  } while (0)
+#else
+#define BL_CHECK(c) \
+  do {              \
+  } while (0)
+#endif
+namespace bl {
+__device__ __forceinline__ uint32_t dyn_smem_bytes() {
+  uint32_t r;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+  return r;
+}
+}  // namespace bl
+
 namespace bl {
 
 // prmt.b32 in its default mode.  Unlike __byte_perm (which masks each

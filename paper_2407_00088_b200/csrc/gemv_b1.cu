@@ -641,6 +641,8 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
     rs = bl::ld_cg_f32(rsum + g);
   }
   const uint32_t woff = (uint32_t)(ub * (32 * R * 16) + l * 16);
+  BL_CHECK(a.bar_off + 8u * (kMaxStages + 1) <= bl::dyn_smem_bytes());
+  BL_CHECK(!live || woff + (R - 1) * (nu_b == 32 ? 512 : nu_b * 16) + 16 <= a.w_bytes);
   __syncthreads();                                      // barriers initialised
   int it = 0;
   for (int tile = t_first; tile < ntl; tile += step, it++) {
@@ -765,6 +767,7 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
       for (int w = 0; w < NW; w++) s += yr[w * TCH];
       int local;
       const int j = find_mat(a, tile, local);
+      BL_CHECK(j < a.n_mats && local >= 0 && local * TCH + tid < (a.mats[j].tile_end - (j ? a.mats[j - 1].tile_end : 0)) * TCH);
       a.mats[j].out[(int64_t)local * TCH + tid] = 0.5f * s;
     }
   }

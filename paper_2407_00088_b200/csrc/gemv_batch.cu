@@ -163,6 +163,8 @@ __global__ void __launch_bounds__(384) gemv_batch_kernel(const __grid_constant__
   load_matrix(dm[jc]);
   const uint32_t woff = (uint32_t)(ub * (32 * R * 16) + l * 16);
   const int stride = nu_b == 32 ? 512 : nu_b * 16;
+  BL_CHECK(a.bar_off + 8u * kStagesMax <= bl::dyn_smem_bytes());
+  BL_CHECK(!live || woff + (R - 1) * stride + 16 <= a.w_bytes);
   __syncthreads();                                      // barriers initialised
   int it = 0;
   for (int tile = t0; tile < t1; tile++, it++) {
@@ -189,6 +191,8 @@ __global__ void __launch_bounds__(384) gemv_batch_kernel(const __grid_constant__
     const int base = reduce_lanes<NACC, 1, LG>(acc, lane);
     const int ch0 = BITS == 1 ? 2 * base : base;
     const int local = tile - jc_begin;
+    BL_CHECK(jc < n_mats && local >= 0 && (local + 1) * TCH <= dm[jc].m);
+    BL_CHECK(!live || (ch0 + NCH - 1) * NQ + g < TCH * NQ);
     float y[NCH];
     if (live) {
       int Sv[NCH];
@@ -233,6 +237,7 @@ __global__ void __launch_bounds__(384) gemv_batch_kernel(const __grid_constant__
     }
     const int fb = reduce_lanes<NCH, LG, 32>(y, lane);
     float* yb = ysm + (it & 1) * NW * TCH + warp * TCH;
+    BL_CHECK(ch0 + fb + NF <= TCH);
 #pragma unroll
     for (int j = 0; j < NF; j++) yb[ch0 + fb + j] = y[j];
     __syncthreads();                                    // stage consumed, ysm complete

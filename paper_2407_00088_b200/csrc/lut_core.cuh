@@ -83,6 +83,7 @@ __device__ __forceinline__ void lut_block(const AT* __restrict__ a, int k, int g
       const int u = kg / R, r = kg - u * R, ub = u >> 5, l = u & 31;
       const int nu_b = min(32, U - 32 * ub);
       const int64_t off = (int64_t)ub * (32 * R * 8) + (int64_t)((r >> 1) * nu_b + l) * 16 + (r & 1) * 8;
+      BL_CHECK(off >= 0 && off + 8 <= (int64_t)KG * 8);
       *reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(tables) + (int64_t)row * KG * 8 + off) =
           make_uint2(e0, e1);
       if ((kg & (gpg - 1)) == 0) tscales[(int64_t)row * NQ + kg / gpg] = scale;
@@ -103,6 +104,7 @@ __device__ __forceinline__ void lut_block(const AT* __restrict__ a, int k, int g
       const int u = kg / R, r = kg - u * R, ub = u >> 5, l = u & 31;
       const int nu_b = min(32, U - 32 * ub);
       const int64_t off = (int64_t)ub * (32 * R * 16) + (int64_t)(r * nu_b + l) * 16;
+      BL_CHECK(off >= 0 && off + 16 <= (int64_t)KG * 16);
       *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(tables) + (int64_t)row * KG * 16 + off) =
           make_uint4(lo[0], lo[1], hi[0], hi[1]);
     }
