@@ -7,25 +7,29 @@ weights in [0,4), group 64, fp16 scales, implicit zero 2, int8-quantized
 tables (bit-exact vs the reference's vector-q8), fp16 activations ~N(0,1).
 A STEP = one pass over L layers (default 32 = the whole 7B model, 1.62 GB of
 packed weights > 126 MB L2, so no L2 flush is needed): per layer 4 table
-builds (qkv / o / gate-up / down inputs) + 7 lookup GEMVs, run through the
-package's op-list executors (pipeline.Pipeline: "batch" = every table build
-in one launch + one lookup launch per K -- the headline; "graph" = per-op
-kernels chained with programmatic dependent launch in one CUDA graph, also
-the dependent decode chain).
+builds (qkv / o / gate-up / down inputs) + 7 lookup GEMVs as independent
+calls, through the package's batch executor (pipeline.Pipeline
+executor="batch": every table build in one launch + one lookup launch per
+K -- 3 launches per step).
 
-value  = packed-weight bytes (bits*M*K/8, the reference's weight_bytes,
-         cli.py:153) per step / device time, GB/s, all ranks aggregated.
-e2e    = the same step from pinned HOST buffers: H2D of the activation rows,
-         the op list, D2H of every GEMV output, inside the timed region.
-         (e2e_per_call_api: the per-call drop-in mpgemv(numpy) path.)
-roofline = the dominant kernel (gemv_q8_kernel) timed alone in a graph of
-         the step's 7*L lookups: algorithmic bytes / average launch time vs
-         the measured HBM peak.
-Also reported: per-shape us/launch for every 7B shape (the metric's "us"),
-and the CPU baseline (C port of the reference's vector-q8 kernel).
+value    = packed-weight bytes (bits*M*K/8, the reference's weight_bytes,
+           cli.py:153) per step / device time, GB/s, all ranks aggregated.
+e2e      = the same step through the Pipeline API with pinned HOST buffers on
+           both sides (the table launch reads the activation rows, the lookup
+           kernels write the results over the bus), inside the timed region.
+roofline = the dominant kernel (gemv_batch_kernel) timed alone: the step's
+           lookup launches (tables prebuilt), algorithmic bytes / time vs the
+           measured HBM peak.
+cpu_baseline = the C port of the reference's vector-q8 path on the host
+           cores; --impl reference runs the real reference package
+           (baseline/_ref) on the same host.
+stdout: ONE compact JSON line (< 2 KB); the detail sections (--full: per
+shape, configs[0], Llama-2-70B shards, prefill mpGEMM, every executor) go to
+bench_details.json.
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
-Multi-GPU (torchrun): output-channel sharding + NCCL all-gather of slices.
+    python bench.py [--gpus N --steps K --warmup W] [--full] [--impl reference]
+Multi-GPU (torchrun): output-channel sharding, one NCCL all-gather per step,
+and the fused all-gather epilogue next to it.
 """
 from __future__ import annotations
 
@@ -169,28 +173,6 @@ def make_acts(n_layers, device, seed=7, arena=None):
     return acts, arena
 
 
-def step_fn(layers, acts, world, group, fast=False):
-    """One pass of the hot path (device-resident inputs)."""
-    import torch
-    from paper_2407_00088_b200 import _native as N
-    res = []
-    for L, A in zip(layers, acts):
-        for gname, k, names in LUT_GROUPS:
-            tables, ts, rs = N.build_lut(A[gname], L[names[0]].group_size, N.TABLE_Q8, N.FLAG_PDL)
-            for j, nm in enumerate(names):
-                pw = L[nm]
-                # the first GEMV after a table build depends on it; the others
-                # (k, v after q; up after gate) read the same finished table
-                fl = N.FLAG_PDL | (N.FLAG_INDEPENDENT if j > 0 else 0) | (N.FLAG_FAST_EPILOGUE if fast else 0)
-                y, _ = N.lookup(pw.gpu, pw.scales, None, tables, ts, rs, pw.m, pw.k, pw.bits,
-                                pw.group_size, N.TABLE_Q8, fl, False)
-                if world > 1:
-                    from paper_2407_00088_b200.parallel import gather_rows
-                    y = gather_rows(y, [pw.m] * world, group)
-                res.append(y)
-    return res
-
-
 def build_pipeline(layers, acts, fast=False, executor="graph", chain=True, sync="pdl", lookahead=None,
                    groups=None):
     """The step as a pipeline.Pipeline op list.  chain=True: the decode
@@ -246,25 +228,6 @@ def build_pipeline(layers, acts, fast=False, executor="graph", chain=True, sync=
                     off += m
     pl.compile()
     return pl, outs, out_arena
-
-
-def lookups_only(layers, tabs, fast=False, chain=False):
-    """The step's 7*L lookups with tables prebuilt and the step's launch
-    flags: layer set (chain=False) -- every lookup but the first INDEPENDENT;
-    decode chain -- the first GEMV after each table build dependent."""
-    from paper_2407_00088_b200 import _native as N
-    first = True
-    for L, T in zip(layers, tabs):
-        for gname, k, names in LUT_GROUPS:
-            tables, ts, rs = T[gname]
-            for j, nm in enumerate(names):
-                pw = L[nm]
-                ind = (j > 0) if chain else not first
-                first = False
-                fl = (N.FLAG_PDL | (N.FLAG_INDEPENDENT if ind else 0)
-                      | (N.FLAG_FAST_EPILOGUE if fast else 0))
-                N.lookup(pw.gpu, pw.scales, None, tables, ts, rs, pw.m, pw.k, pw.bits,
-                         pw.group_size, N.TABLE_Q8, fl, False)
 
 
 def capture(fn, stream):
@@ -818,7 +781,7 @@ def main():
     del g_look
     local_bytes = sum(pw.packed_bytes for L in layers for pw in L.values())
     achieved = local_bytes / (ms_look * 1e-3) / 1e9
-    kernel_name = "gemv_b1_batch_kernel"
+    kernel_name = "gemv_batch_kernel"
     details["roofline_how"] = (
         f"the step's {n_look} batched lookup launches (one per K; {args.layers} layers' q,k,v,o,gate,up and "
         f"down; tables prebuilt) per graph replay; algorithmic bytes = sum bits*M*K/8 = {local_bytes} per "
@@ -1176,7 +1139,7 @@ def cpu_baseline_run(layers, acts, bits, gs, args):
         return {"value": None, "unit": "GB/s", "cores": 0, "kind": "port", "sample": f"unavailable: {e}"}
 
 
-def load_traffic(kernel="gemv_b1_batch_kernel"):
+def load_traffic(kernel="gemv_batch_kernel"):
     """ncu DRAM bytes (read + write) per launch of the headline's dominant
     kernel from one committed `ncu --set full` capture of the batch
     executor's lookup launches (mean per launch; roofline.achieved is per
