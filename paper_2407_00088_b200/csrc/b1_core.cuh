@@ -4,7 +4,24 @@
 #pragma once
 #include "gemv_core.cuh"
 
+#ifndef BITLUT_AB
+#define BITLUT_AB 0
+#endif
+
 namespace blk {
+
+// The high half of a selector word.  The PRMT lookups, the selector
+// preparation (LOP3, PRMT, SHF) and the epilogue's SEL/FSEL/I2FP all issue to
+// the ALU pipe and the dot products (IDP) to the FMA-heavy pipe, each at one
+// warp instruction per two clocks per scheduler (tools/microbench/pipes2.cu,
+// profiles/r02cc_pipes.txt).  W2 has 9 ALU and 4 IDP instructions per weight
+// word, so its two shifts go to the IDP pipe (7 + 6): +8 % on the W2 layer
+// set.  W1 is already IDP-heavy (7 ALU, 8 IDP) and keeps SHF.
+template <bool IDP>
+__device__ __forceinline__ uint32_t sel_hi(uint32_t x) {
+  if constexpr (IDP) return bl::shr16_idp(x);
+  return x >> 16;
+}
 
 // Lookup of one k-group for 32 streams with plane-merging multipliers (the
 // A/Y form of gemv_core.cuh lookup_kg: A - Y = sQ exactly, Y enters with the
@@ -23,13 +40,14 @@ __device__ __forceinline__ void lookup_kg_merged(const uint4 w, uint32_t a0, uin
       // per 8 lookups
       const uint32_t s01 = bl::prmt(x, xx, 0x5140u), s23 = bl::prmt(x, xx, 0x7362u);
       acc[4 * q + 0] = bl::dp4a(bl::prmt(a0, a1, s01), 0xFEFF0201u, acc[4 * q + 0]);
-      acc[4 * q + 1] = bl::dp4a(bl::prmt(a0, a1, s01 >> 16), 0xFEFF0201u, acc[4 * q + 1]);
+      acc[4 * q + 1] = bl::dp4a(bl::prmt(a0, a1, sel_hi<true>(s01)), 0xFEFF0201u, acc[4 * q + 1]);
       acc[4 * q + 2] = bl::dp4a(bl::prmt(a0, a1, s23), 0xFEFF0201u, acc[4 * q + 2]);
-      acc[4 * q + 3] = bl::dp4a(bl::prmt(a0, a1, s23 >> 16), 0xFEFF0201u, acc[4 * q + 3]);
+      acc[4 * q + 3] = bl::dp4a(bl::prmt(a0, a1, sel_hi<true>(s23)), 0xFEFF0201u, acc[4 * q + 3]);
       continue;
     }
     const uint32_t A0 = bl::prmt(a0, a1, x), Y0 = bl::prmt(a0, a1, xx);
-    const uint32_t A1 = bl::prmt(a0, a1, x >> 16), Y1 = bl::prmt(a0, a1, xx >> 16);
+    // W4: 7 ALU + 4 IDP per word -> one of the two shifts on the IDP pipe
+    const uint32_t A1 = bl::prmt(a0, a1, sel_hi<BITS == 4>(x)), Y1 = bl::prmt(a0, a1, xx >> 16);
     if constexpr (BITS == 4) {
       // bytes 0..3 of A0/Y0 = planes 0..3 of channel 2q, of A1/Y1: channel
       // 2q+1; dp4a with (1,2,4,8) adds a channel's planes in one instruction
@@ -67,6 +85,21 @@ __host__ __device__ constexpr int reduced_count() {
 template <int NV, int O0, int O1, typename T>
 __device__ __forceinline__ int reduce_lanes(T (&v)[NV], int lane) {
   int base = 0;
+#if BITLUT_AB & 2
+  // TIMING EXPERIMENT ONLY (wrong channel mapping): no selects in the halving
+#pragma unroll
+  for (int o = O0, n = NV; o < O1; o <<= 1) {
+    if (n > 1) {
+      n >>= 1;
+#pragma unroll
+      for (int i = 0; i < NV / 2; i++)
+        if (i < n) v[i] = v[i] + __shfl_xor_sync(0xffffffffu, v[i + n], o);
+      if (lane & o) base += n;
+    } else {
+      v[0] = v[0] + __shfl_xor_sync(0xffffffffu, v[0], o);
+    }
+  }
+#else
 #pragma unroll
   for (int o = O0, n = NV; o < O1; o <<= 1) {
     if (n > 1) {
@@ -85,6 +118,7 @@ __device__ __forceinline__ int reduce_lanes(T (&v)[NV], int lane) {
       v[0] = v[0] + __shfl_xor_sync(0xffffffffu, v[0], o);
     }
   }
+#endif
   return base;
 }
 

@@ -73,6 +73,16 @@ BL_DEV int dp2a_hi_u(uint32_t mult, uint32_t b, int c) {
   return d;
 }
 
+// x >> 16 on the FMA-heavy pipe (IDP.2A: x.b2 * 1 + x.b3 * 256) instead of a
+// SHF on the ALU pipe, which the lookups' PRMTs saturate (IDP.2A/4A and IMAD
+// share one half-rate pipe, PRMT/SHF/LOP3/I2FP another: tools/microbench/pipes2.cu)
+BL_DEV uint32_t shr16_idp(uint32_t x) {
+  uint32_t d;
+  asm("dp2a.hi.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(0x01000001u), "r"(x), "r"(0u));
+  return d;
+}
+
+
 // d = c + sum_i a.byte_i * b.byte_i   (signed x signed)
 BL_DEV int dp4a(uint32_t a, uint32_t b, int c) {
   int d;

@@ -46,6 +46,7 @@ namespace {
 using namespace blk;
 
 constexpr int kStagesMax = 2;
+constexpr int kYBufs = 2;             // cross-warp sum buffers (power of two)
 
 struct BatchArgs {
   bl::LayoutV2 L;             // the launch's k, bits, group size (m unused)
@@ -236,7 +237,7 @@ __global__ void __launch_bounds__(384) gemv_batch_kernel(const __grid_constant__
       for (int j = 0; j < NCH; j++) y[j] = 0.f;
     }
     const int fb = reduce_lanes<NCH, LG, 32>(y, lane);
-    float* yb = ysm + (it & 1) * NW * TCH + warp * TCH;
+    float* yb = ysm + (it & (kYBufs - 1)) * NW * TCH + warp * TCH;
     BL_CHECK(ch0 + fb + NF <= TCH);
 #pragma unroll
     for (int j = 0; j < NF; j++) yb[ch0 + fb + j] = y[j];
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(384) gemv_batch_kernel(const __grid_constant__
       }
     }
     if (tid < TCH) {                                    // fixed warp order: deterministic
-      const float* yr = ysm + (it & 1) * NW * TCH + tid;
+      const float* yr = ysm + (it & (kYBufs - 1)) * NW * TCH + tid;
       float s = 0.f;
       for (int w = 0; w < NW; w++) s += yr[w * TCH];
       outp[(int64_t)local * TCH + tid] = fin * s;
@@ -303,7 +304,7 @@ int launch(const bl::LayoutV2& L, const bitlut_batch_mat* dm, int n_mats, int to
   a.stage_bytes = (a.stage_bytes + 127) & ~127u;
   auto total_for = [&](int stages) {
     const uint32_t y_off = stages * a.stage_bytes;
-    const uint32_t bar_off = y_off + al16((size_t)2 * NW * TCH * 4);
+    const uint32_t bar_off = y_off + al16((size_t)kYBufs * NW * TCH * 4);
     return bar_off + 8u * kStagesMax;
   };
   static int st_env = -1;
@@ -328,7 +329,7 @@ int launch(const bl::LayoutV2& L, const bitlut_batch_mat* dm, int n_mats, int to
   if (best_per < 1) return BITLUT_ELAYOUT;
   a.stages = best_s;
   a.y_off = best_s * a.stage_bytes;
-  a.bar_off = a.y_off + al16((size_t)2 * NW * TCH * 4);
+  a.bar_off = a.y_off + al16((size_t)kYBufs * NW * TCH * 4);
   int grid = device_sms(dev) * best_per;
   if (grid > total_tiles) grid = total_tiles;
   cudaLaunchConfig_t cfg = {};

@@ -1,0 +1,34 @@
+"""Builds an A/B variant of the product library: gemv_batch.cu and gemv_b1.cu
+recompiled with -DBITLUT_AB=<n> (experiment switches in csrc/b1_core.cuh and
+csrc/gemv_batch.cu), linked with the product objects into
+_ab/libbitlut_ab_<n>.so.  Select it with BITLUT_B200_LIB.
+
+    python tools/build_ab.py 1 3      # builds variants 1 and 3
+"""
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2407_00088_b200 import build as B  # noqa: E402
+
+B.build_lib()
+objdir = os.path.join(B.PKG, "_lib", "obj")
+outdir = os.path.join(ROOT, "_ab")
+os.makedirs(outdir, exist_ok=True)
+flags = [f for f in B.NVCC_FLAGS if f not in ("-shared", "-Xptxas", "-v")]
+VARIANT_TUS = ["gemv_batch.cu"]
+for n in sys.argv[1:]:
+    objs = []
+    for src in B.SOURCES:
+        if src in VARIANT_TUS:
+            o = os.path.join(outdir, f"{src[:-3]}_ab{n}.o")
+            subprocess.run([B.nvcc(), *flags, f"-DBITLUT_AB={n}", "-c", "-o", o, os.path.join(B.PKG, "csrc", src)],
+                           check=True)
+            objs.append(o)
+        else:
+            objs.append(os.path.join(objdir, src.replace(".cu", ".o")))
+    out = os.path.join(outdir, f"libbitlut_ab_{n}.so")
+    subprocess.run([B.nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, *objs], check=True)
+    print(out)
