@@ -194,7 +194,8 @@ def build_pipeline(layers, acts, fast=False, executor="graph", chain=True, sync=
     if chain:
         for L, A in zip(layers, acts):
             for gname, k, names in lut_groups:
-                t = pl.tables(A[gname], L[names[0]].group_size, deps=prev)
+                t = pl.tables(A[gname], L[names[0]].group_size, deps=prev,
+                              fuse=fast and os.environ.get("BENCH_CHAIN_FUSE", "0") == "1")
                 ys = []
                 for nm in names:
                     m = L[nm].m

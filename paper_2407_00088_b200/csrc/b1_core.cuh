@@ -82,6 +82,20 @@ __host__ __device__ constexpr int reduced_count() {
   return n;
 }
 
+// The base index reduce_lanes<NV, O0, O1> returns for this lane.
+template <int NV, int O0, int O1>
+__device__ __forceinline__ int reduced_base(int lane) {
+  int base = 0;
+#pragma unroll
+  for (int o = O0, n = NV; o < O1; o <<= 1) {
+    if (n > 1) {
+      n >>= 1;
+      if (lane & o) base += n;
+    }
+  }
+  return base;
+}
+
 template <int NV, int O0, int O1, typename T>
 __device__ __forceinline__ int reduce_lanes(T (&v)[NV], int lane) {
   int base = 0;

@@ -620,8 +620,10 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
   else if (!p.independent) bl::pdl_wait();
   bl::pdl_launch_dependents();
   // the thread's unit, group and tables: fixed for the launch
-  const int u = tid;
-  const bool live = u < U;
+  // a thread past the last unit shadows the last unit with all-zero int8
+  // tables (exact zeros everywhere): the int8 tile loop has no "live" branch
+  const bool live = tid < U;
+  const int u = live ? tid : U - 1;
   const int ub = u >> 5, l = u & 31;
   const int nu_b = min(32, U - 32 * ub);
   const int g = u / LG;
@@ -639,6 +641,9 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
       ts = bl::ld_cg_f32(tsc + g);
     }
     rs = bl::ld_cg_f32(rsum + g);
+  } else if constexpr (!F16) {
+#pragma unroll
+    for (int jp = 0; jp < R / 2; jp++) tq[jp] = make_uint4(0, 0, 0, 0);
   }
   const uint32_t woff = (uint32_t)(ub * (32 * R * 16) + l * 16);
   BL_CHECK(a.bar_off + 8u * (kMaxStages + 1) <= bl::dyn_smem_bytes());
@@ -696,7 +701,7 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
     int acc[NACC];
 #pragma unroll
     for (int i = 0; i < NACC; i++) acc[i] = 0;
-    if (live) {
+    {
       const uint8_t* wsrc = sb + woff;
       if (nu_b == 32) {
 #pragma unroll
@@ -719,7 +724,7 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
     }
     const int base = reduce_lanes<NACC, 1, LG>(acc, lane);
     ch0 = BITS == 1 ? 2 * base : base;
-    if (live) {
+    {
       int Sv[NCH];
       if constexpr (BITS == 1) {
 #pragma unroll
@@ -747,9 +752,6 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
 #pragma unroll
         for (int j = 0; j < NCH; j++) y[j] = bl::to_f32(sp[j * NQ]) * fmaf(ts, (float)Sv[j], -rs);
       }
-    } else {
-#pragma unroll
-      for (int j = 0; j < NCH; j++) y[j] = 0.f;
     }
     }
     const int fb = reduce_lanes<NCH, LG, 32>(y, lane);

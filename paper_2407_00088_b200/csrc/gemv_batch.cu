@@ -140,8 +140,11 @@ __global__ void __launch_bounds__(384) gemv_batch_kernel(const __grid_constant__
   }
   if (!a.independent) bl::pdl_wait();
   bl::pdl_launch_dependents();
-  const int u = tid;                                    // thread u looks up unit u
-  const bool live = u < U;
+  // thread u looks up unit u; a thread past the last unit (U is not a
+  // multiple of 32) shadows the last unit with all-zero tables, so it adds
+  // exact zeros everywhere and the tile loop needs no "live" branches
+  const bool live = tid < U;
+  const int u = live ? tid : U - 1;
   const int ub = u >> 5, l = u & 31;
   const int nu_b = min(32, U - 32 * ub);
   const int g = u / LG;
@@ -153,19 +156,17 @@ __global__ void __launch_bounds__(384) gemv_batch_kernel(const __grid_constant__
     outp = mt.out;
     if constexpr (PART) part = mt.partials;
     if constexpr (MODE == BITLUT_W_TERNARY) fin = 0.5f * bl::to_f32(*reinterpret_cast<const ST*>(mt.wscales));
-    if (live) {
-      const uint8_t* tb = reinterpret_cast<const uint8_t*>(mt.tables) + (int64_t)ub * (32 * R * 8) + l * 16;
+    const uint8_t* tb = reinterpret_cast<const uint8_t*>(mt.tables) + (int64_t)ub * (32 * R * 8) + l * 16;
 #pragma unroll
-      for (int jp = 0; jp < R / 2; jp++) tq[jp] = bl::ld_cg_128(tb + jp * nu_b * 16);
-      ts = bl::ld_cg_f32(mt.tscales + g);
-      rs = bl::ld_cg_f32(mt.rowsums + g);
-    }
+    for (int jp = 0; jp < R / 2; jp++) tq[jp] = live ? bl::ld_cg_128(tb + jp * nu_b * 16) : make_uint4(0, 0, 0, 0);
+    ts = live ? bl::ld_cg_f32(mt.tscales + g) : 0.f;
+    rs = live ? bl::ld_cg_f32(mt.rowsums + g) : 0.f;
   };
   load_matrix(dm[jc]);
   const uint32_t woff = (uint32_t)(ub * (32 * R * 16) + l * 16);
   const int stride = nu_b == 32 ? 512 : nu_b * 16;
   BL_CHECK(a.bar_off + 8u * kStagesMax <= bl::dyn_smem_bytes());
-  BL_CHECK(!live || woff + (R - 1) * stride + 16 <= a.w_bytes);
+  BL_CHECK(woff + (R - 1) * stride + 16 <= a.w_bytes);
   __syncthreads();                                      // barriers initialised
   int it = 0;
   for (int tile = t0; tile < t1; tile++, it++) {
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__(384) gemv_batch_kernel(const __grid_constant__
     int acc[NACC];
 #pragma unroll
     for (int i = 0; i < NACC; i++) acc[i] = 0;
-    if (live) {
+    {
       const uint8_t* wsrc = sb + woff;
 #pragma unroll
       for (int j = 0; j < R; j += 2) {
@@ -193,9 +194,9 @@ __global__ void __launch_bounds__(384) gemv_batch_kernel(const __grid_constant__
     const int ch0 = BITS == 1 ? 2 * base : base;
     const int local = tile - jc_begin;
     BL_CHECK(jc < n_mats && local >= 0 && (local + 1) * TCH <= dm[jc].m);
-    BL_CHECK(!live || (ch0 + NCH - 1) * NQ + g < TCH * NQ);
+    BL_CHECK((ch0 + NCH - 1) * NQ + g < TCH * NQ);
     float y[NCH];
-    if (live) {
+    {
       int Sv[NCH];
       if constexpr (BITS == 1) {
 #pragma unroll
@@ -209,7 +210,7 @@ __global__ void __launch_bounds__(384) gemv_batch_kernel(const __grid_constant__
 #pragma unroll
         for (int i = 0; i < NV; i++) Sv[i] = acc[i];
       }
-      if constexpr (PART) {                             // exact integer sums (parity tests)
+      if (PART && live) {                               // exact integer sums (parity tests)
         int32_t* pp = part + ((int64_t)local * TCH + ch0) * NQ + g;
 #pragma unroll
         for (int j = 0; j < NCH; j++) pp[(int64_t)j * NQ] = Sv[j];
@@ -232,9 +233,6 @@ __global__ void __launch_bounds__(384) gemv_batch_kernel(const __grid_constant__
 #pragma unroll
         for (int j = 0; j < NCH; j++) y[j] = fmaf(ts, (float)Sv[j], rs);
       }
-    } else {
-#pragma unroll
-      for (int j = 0; j < NCH; j++) y[j] = 0.f;
     }
     const int fb = reduce_lanes<NCH, LG, 32>(y, lane);
     float* yb = ysm + (it & (kYBufs - 1)) * NW * TCH + warp * TCH;

@@ -209,7 +209,8 @@ __device__ __forceinline__ void lookup_kg_f16(const uint4 w, const uint4 t, floa
     const uint32_t e = x & 0x77777777u;
 #pragma unroll
     for (int h = 0; h < 2; h++) {
-      const uint32_t eh = h ? e >> 16 : e, xh = h ? x >> 16 : x;
+      // high halves on the FMA-heavy pipe (the five PRMTs below saturate the ALU pipe)
+      const uint32_t eh = h ? bl::shr16_idp(e) : e, xh = h ? bl::shr16_idp(x) : x;
       const uint32_t lo = bl::prmt(t.x, t.y, eh);
       uint32_t hi = bl::prmt(t.z, t.w, eh);
       const uint32_t one = bl::prmt(0x01010101u, 0x01010101u, xh);   // 1 where s = 0
