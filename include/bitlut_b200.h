@@ -257,15 +257,25 @@ int bitlut_mpgemv_multi_tab(const bitlut_mat_tab* mats, int n_mats, int k, int b
  *                     per-group scale stream) (configs[2])
  * partials (optional, all or none, BITLUT_FLAG_COMBINED_PARTIALS): the exact
  * int32 S = sum_p 2^p P_p per (channel, group), (m, k/gs) row-major -- the
- * integer object SURVEY §8(c) pins against the reference's staging values. */
+ * integer object SURVEY §8(c) pins against the reference's staging values.
+ *
+ * Operand format: the LAYER-SET layout (csrc/layout.cuh), made from the
+ * layout-v2 weights and the (m, k/gs) group scales / zero points by
+ * bitlut_layer_set_weights / bitlut_layer_set_scales below: the chunks of
+ * v2 with the streams of each chunk permuted per lane (so the kernel's lane
+ * reductions exchange without selects) and the scales regrouped per unit
+ * (one vector load per lane).  `wgpu`, `wscales` (BITLUT_W_OFFSET / ZEROS /
+ * SIGN) and `zeros` of bitlut_batch_mat are in that format; the per-tensor
+ * BITLUT_W_TERNARY scale is one plain value.  The outputs are bitwise those
+ * of the per-call fast lookups on the v2 operand. */
 #define BITLUT_W_OFFSET 0
 #define BITLUT_W_ZEROS 1
 #define BITLUT_W_SIGN 2
 #define BITLUT_W_TERNARY 3
 typedef struct {
-  const uint8_t* wgpu;
-  const void* wscales;      /* (m, k/gs), or 1 value (BITLUT_W_TERNARY) */
-  const void* zeros;        /* (m, k/gs) for BITLUT_W_ZEROS, else NULL */
+  const uint8_t* wgpu;      /* layer-set weights */
+  const void* wscales;      /* layer-set scales, or 1 value (BITLUT_W_TERNARY) */
+  const void* zeros;        /* layer-set zero points for BITLUT_W_ZEROS, else NULL */
   float* out;               /* (1, m) f32 */
   const void* tables;       /* (1, k/4*8) int8 kernel format */
   const float* tscales;     /* (1, k/gs) */
@@ -278,6 +288,22 @@ int bitlut_mpgemv_batch_encode(bitlut_batch_mat* mats, int n_mats, int k, int bi
                                int weight_mode, int* total_tiles);
 int bitlut_mpgemv_batch(const bitlut_batch_mat* dev_mats, int n_mats, int total_tiles, int k, int bits,
                         int group_size, int scale_dtype, int weight_mode, int flags, void* stream);
+
+/* Layer-set layout conversion (offline; part of the north star's repack
+ * step, replaces nothing in the reference -- weight_prep.py:193-246 is the
+ * analogous pack_and_permute).  bitlut_layer_set_weights: layout v2 ->
+ * layer-set weights, same size (m*bits*k/8 bytes), out != wgpu; it is an
+ * involution (applying it to layer-set weights gives v2 back).
+ * bitlut_layer_set_scales: (m, k/gs) f16/f32 scales or zero points ->
+ * bitlut_layer_set_scales_bytes(...) bytes (the same m*k/gs elements,
+ * reordered; more only when a group spans more lanes than a lane has
+ * accumulators: 4-bit gs >= 256, 2-bit gs = 512).  1/2/4-bit weights only
+ * (BITLUT_ELAYOUT otherwise). */
+int64_t bitlut_layer_set_scales_bytes(int m, int k, int bits, int group_size, int scale_dtype);
+int bitlut_layer_set_weights(const uint8_t* wgpu, int bits, int m, int k, int group_size, uint8_t* out,
+                             void* stream);
+int bitlut_layer_set_scales(const void* scales, int scale_dtype, int bits, int m, int k, int group_size,
+                            void* out, void* stream);
 
 /* The drop-in call with HOST buffers (replaces kernel.py:280-371 mpgemm /
  * :374-382 mpgemv as a numpy caller sees them): copies a_host (n, k) f16/f32

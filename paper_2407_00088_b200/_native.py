@@ -58,6 +58,8 @@ _SIGS = {
     "bitlut_mpgemv_multi_tab": [_vp, _i, _i, _i, _i, _i, _i, _vp],
     "bitlut_mpgemv_batch_encode": [_vp, _i, _i, _i, _i, _i, _vp],
     "bitlut_mpgemv_batch": [_vp, _i, _i, _i, _i, _i, _i, _i, _i, _vp],
+    "bitlut_layer_set_weights": [_vp, _i, _i, _i, _i, _vp, _vp],
+    "bitlut_layer_set_scales": [_vp, _i, _i, _i, _i, _i, _vp, _vp],
     "bitlut_build_lut_batch_encode": [_vp, _i, _vp, _vp],
     "bitlut_build_lut_batch": [_vp, _vp, _i, _i, _i, _i, _i, _vp],
 }
@@ -102,6 +104,32 @@ def _to_device_bytes(arr, device) -> torch.Tensor:
     return host.to(device)
 
 
+def layer_set_weights(wgpu: torch.Tensor, bits: int, m: int, k: int, group_size: int) -> torch.Tensor:
+    """Layout-v2 weights -> the layer-set layout bitlut_mpgemv_batch reads
+    (csrc/layout.cuh; an involution)."""
+    require_cuda(wgpu, "wgpu")
+    out = torch.empty_like(wgpu)
+    rc = lib().bitlut_layer_set_weights(ptr(wgpu), bits, m, k, group_size, ptr(out),
+                                        ctypes.c_void_p(torch.cuda.current_stream(wgpu.device).cuda_stream))
+    raise_for_status(rc, "bitlut_layer_set_weights")
+    return out
+
+
+def layer_set_scales(t: torch.Tensor, bits: int, m: int, k: int, group_size: int) -> torch.Tensor:
+    """(m, k/gs) f16/f32 group scales or zero points -> layer-set order (flat)."""
+    require_cuda(t, "scales")
+    t = t.contiguous()
+    dt = dtype_code(t)
+    nbytes = lib().bitlut_layer_set_scales_bytes(m, k, bits, group_size, dt)
+    if nbytes < 0:
+        raise_for_status(-4, "bitlut_layer_set_scales_bytes")
+    out = torch.empty((nbytes // t.element_size(),), dtype=t.dtype, device=t.device)
+    rc = lib().bitlut_layer_set_scales(ptr(t), dt, bits, m, k, group_size, ptr(out),
+                                       ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream))
+    raise_for_status(rc, "bitlut_layer_set_scales")
+    return out
+
+
 class LookupBatch:
     """Encoded bitlut_mpgemv_batch launch: independent batch-1 fast GEMVs of
     one (k, bits, group_size, scale dtype), each with its own int8 tables.
@@ -119,19 +147,29 @@ class LookupBatch:
 
     @classmethod
     def from_tensors(cls, mats, k: int, bits: int, group_size: int, weight_mode: int = W_OFFSET) -> "LookupBatch":
-        """mats = [(wgpu, wscales, m, out (1, m) f32, tables, tscales, rowsums[, zeros[, partials]]), ...]"""
+        """mats = [(wgpu, wscales, m, out (1, m) f32, tables, tscales, rowsums[, zeros[, partials]]), ...]
+        with layout-v2 weights and (m, k/gs) scales / zero points: converted
+        here to the layer-set layout the launch reads (one copy per call --
+        Pipeline caches the converted operand per PackedWeights instead)."""
         arr = (BitlutBatchMat * len(mats))()
+        conv = []
         for i, mt in enumerate(mats):
             w, sc, m, out, t, ts, rs = mt[:7]
             z = mt[7] if len(mt) > 7 else None
             pp = mt[8] if len(mt) > 8 else None
+            w = layer_set_weights(w, bits, m, k, group_size)
+            if weight_mode != W_TERNARY:
+                sc = layer_set_scales(sc, bits, m, k, group_size)
+            if z is not None:
+                z = layer_set_scales(z, bits, m, k, group_size)
+            conv += [w, sc, z]
             arr[i].wgpu, arr[i].wscales, arr[i].out = w.data_ptr(), sc.data_ptr(), out.data_ptr()
             arr[i].tables, arr[i].tscales, arr[i].rowsums = t.data_ptr(), ts.data_ptr(), rs.data_ptr()
             arr[i].zeros = z.data_ptr() if z is not None else None
             arr[i].partials = pp.data_ptr() if pp is not None else None
             arr[i].m = m
         b = cls(arr, k, bits, group_size, dtype_code(mats[0][1]), mats[0][0].device, weight_mode)
-        b.keep = [x for mt in mats for x in mt if isinstance(x, torch.Tensor)]
+        b.keep = [x for mt in mats for x in mt if isinstance(x, torch.Tensor)] + conv
         return b
 
     def launch(self, flags: int, stream) -> None:
@@ -198,12 +236,14 @@ def lib() -> ctypes.CDLL:
             fn.restype = ctypes.c_int
         L.bitlut_version.restype = ctypes.c_char_p
         L.bitlut_version.argtypes = []
+        L.bitlut_layer_set_scales_bytes.restype = ctypes.c_int64
+        L.bitlut_layer_set_scales_bytes.argtypes = [_i, _i, _i, _i, _i]
         _LIB = L
     return _LIB
 
 
 def exported_symbols() -> list[str]:
-    return list(_SIGS) + ["bitlut_version",
+    return list(_SIGS) + ["bitlut_version", "bitlut_layer_set_scales_bytes",
                           "bitlut_pipeline_plan_flags", "bitlut_pipeline_launch_ops",
                           "bitlut_build_lut_multi", "bitlut_mpgemv_multi",
                           "bitlut_pipeline_launch_ops_counted"]

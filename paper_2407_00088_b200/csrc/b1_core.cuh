@@ -4,10 +4,6 @@
 #pragma once
 #include "gemv_core.cuh"
 
-#ifndef BITLUT_AB
-#define BITLUT_AB 0
-#endif
-
 namespace blk {
 
 // The high half of a selector word.  The PRMT lookups, the selector
@@ -82,38 +78,9 @@ __host__ __device__ constexpr int reduced_count() {
   return n;
 }
 
-// The base index reduce_lanes<NV, O0, O1> returns for this lane.
-template <int NV, int O0, int O1>
-__device__ __forceinline__ int reduced_base(int lane) {
-  int base = 0;
-#pragma unroll
-  for (int o = O0, n = NV; o < O1; o <<= 1) {
-    if (n > 1) {
-      n >>= 1;
-      if (lane & o) base += n;
-    }
-  }
-  return base;
-}
-
 template <int NV, int O0, int O1, typename T>
 __device__ __forceinline__ int reduce_lanes(T (&v)[NV], int lane) {
   int base = 0;
-#if BITLUT_AB & 2
-  // TIMING EXPERIMENT ONLY (wrong channel mapping): no selects in the halving
-#pragma unroll
-  for (int o = O0, n = NV; o < O1; o <<= 1) {
-    if (n > 1) {
-      n >>= 1;
-#pragma unroll
-      for (int i = 0; i < NV / 2; i++)
-        if (i < n) v[i] = v[i] + __shfl_xor_sync(0xffffffffu, v[i + n], o);
-      if (lane & o) base += n;
-    } else {
-      v[0] = v[0] + __shfl_xor_sync(0xffffffffu, v[0], o);
-    }
-  }
-#else
 #pragma unroll
   for (int o = O0, n = NV; o < O1; o <<= 1) {
     if (n > 1) {
@@ -132,8 +99,68 @@ __device__ __forceinline__ int reduce_lanes(T (&v)[NV], int lane) {
       v[0] = v[0] + __shfl_xor_sync(0xffffffffu, v[0], o);
     }
   }
-#endif
   return base;
+}
+
+// ---- layer-set layout (layout.cuh: lane-permuted chunks) ----
+// In a chunk of lane l, position pos holds stream pos ^ (BITS * perm_mask<TCH>(l)):
+// value index i of lane l means logical index i ^ mask(l), and the mask of
+// the partner at halving step o differs exactly in the bit that step splits
+// on, so BOTH lanes keep the low half and send the high half -- the halving
+// needs no selects (reduce_lanes spends 2 SEL/FSEL per exchanged value), and
+// after all steps lane l holds logical index perm_mask(l).
+template <int NIDX>
+__host__ __device__ constexpr int perm_mask(int lane) {
+  int m = 0;
+  for (int o = 1, n = NIDX >> 1; n >= 1; o <<= 1, n >>= 1)
+    if (lane & o) m |= n;
+  return m;
+}
+
+template <int NV, int O0, int O1, typename T>
+__device__ __forceinline__ void reduce_lanes_perm(T (&v)[NV]) {
+#pragma unroll
+  for (int o = O0, n = NV; o < O1; o <<= 1) {
+    if (n > 1) {
+      n >>= 1;
+#pragma unroll
+      for (int i = 0; i < NV / 2; i++)
+        if (i < n) v[i] = v[i] + __shfl_xor_sync(0xffffffffu, v[i + n], o);
+    } else {
+      v[0] = v[0] + __shfl_xor_sync(0xffffffffu, v[0], o);
+    }
+  }
+}
+
+// NB consecutive bytes from shared memory (NB = 4, 8 or a multiple of 16)
+template <int NB>
+__device__ __forceinline__ void lds_vec(const void* p, uint32_t (&d)[(NB + 3) / 4]) {
+  if constexpr (NB % 16 == 0) {
+#pragma unroll
+    for (int i = 0; i < NB / 16; i++) {
+      const uint4 v = reinterpret_cast<const uint4*>(p)[i];
+      d[4 * i] = v.x; d[4 * i + 1] = v.y; d[4 * i + 2] = v.z; d[4 * i + 3] = v.w;
+    }
+  } else if constexpr (NB == 8) {
+    const uint2 v = *reinterpret_cast<const uint2*>(p);
+    d[0] = v.x; d[1] = v.y;
+  } else if constexpr (NB == 4) {
+    d[0] = *reinterpret_cast<const uint32_t*>(p);
+  } else {
+    static_assert(NB == 2, "vector width");
+    d[0] = *reinterpret_cast<const uint16_t*>(p);
+  }
+}
+
+// element j of a packed fp16 / fp32 vector held in 32-bit registers
+template <typename ST, int NW>
+__device__ __forceinline__ float vec_elem(const uint32_t (&d)[NW], int j) {
+  if constexpr (sizeof(ST) == 4) {
+    return __uint_as_float(d[j]);
+  } else {
+    const __half2 h = *reinterpret_cast<const __half2*>(&d[j >> 1]);
+    return (j & 1) ? __high2float(h) : __low2float(h);
+  }
 }
 
 }  // namespace blk

@@ -72,10 +72,10 @@ __device__ __forceinline__ void issue_tile(const BatchArgs& a, const bitlut_batc
     bulk_g2s(sb + off, src + off, nb, bar, pol);
   }
   if constexpr (MODE != BITLUT_W_TERNARY) {
-    const int64_t e0 = (int64_t)local * L.tile_ch * L.NQ;
-    bulk_g2s(sb + a.s_off, reinterpret_cast<const ST*>(mt.wscales) + e0, s_bytes, bar, pol);
+    const int64_t b0 = (int64_t)local * s_bytes;        // layer-set layout: s_bytes per tile
+    bulk_g2s(sb + a.s_off, reinterpret_cast<const uint8_t*>(mt.wscales) + b0, s_bytes, bar, pol);
     if constexpr (MODE == BITLUT_W_ZEROS)
-      bulk_g2s(sb + a.z_off, reinterpret_cast<const ST*>(mt.zeros) + e0, s_bytes, bar, pol);
+      bulk_g2s(sb + a.z_off, reinterpret_cast<const uint8_t*>(mt.zeros) + b0, s_bytes, bar, pol);
   }
 }
 
@@ -165,6 +165,12 @@ __global__ void __launch_bounds__(384) gemv_batch_kernel(const __grid_constant__
   load_matrix(dm[jc]);
   const uint32_t woff = (uint32_t)(ub * (32 * R * 16) + l * 16);
   const int stride = nu_b == 32 ? 512 : nu_b * 16;
+  // layer-set layout: value j of this lane is channel j ^ cmask; the unit's
+  // NCH scales (zero points) are contiguous at unit * NCH
+  const int cmask = perm_mask<TCH>(lane);
+  const uint32_t soff = a.s_off + (uint32_t)u * (NCH * (uint32_t)sizeof(ST));
+  const uint32_t zoff = a.z_off + (uint32_t)u * (NCH * (uint32_t)sizeof(ST));
+  BL_CHECK(MODE == BITLUT_W_TERNARY || (u + 1) * NCH * (int)sizeof(ST) <= (int)a.s_bytes);
   BL_CHECK(a.bar_off + 8u * kStagesMax <= bl::dyn_smem_bytes());
   BL_CHECK(woff + (R - 1) * stride + 16 <= a.w_bytes);
   __syncthreads();                                      // barriers initialised
@@ -190,11 +196,9 @@ __global__ void __launch_bounds__(384) gemv_batch_kernel(const __grid_constant__
         lookup_kg_merged<BITS, NACC>(wc, tq[j >> 1].z, tq[j >> 1].w, acc);
       }
     }
-    const int base = reduce_lanes<NACC, 1, LG>(acc, lane);
-    const int ch0 = BITS == 1 ? 2 * base : base;
+    reduce_lanes_perm<NACC, 1, LG>(acc);                // exact integer sums of the quantization group
     const int local = tile - jc_begin;
     BL_CHECK(jc < n_mats && local >= 0 && (local + 1) * TCH <= dm[jc].m);
-    BL_CHECK((ch0 + NCH - 1) * NQ + g < TCH * NQ);
     float y[NCH];
     {
       int Sv[NCH];
@@ -211,34 +215,38 @@ __global__ void __launch_bounds__(384) gemv_batch_kernel(const __grid_constant__
         for (int i = 0; i < NV; i++) Sv[i] = acc[i];
       }
       if (PART && live) {                               // exact integer sums (parity tests)
-        int32_t* pp = part + ((int64_t)local * TCH + ch0) * NQ + g;
 #pragma unroll
-        for (int j = 0; j < NCH; j++) pp[(int64_t)j * NQ] = Sv[j];
+        for (int j = 0; j < NCH; j++)                   // value j of this lane = channel j ^ cmask
+          part[((int64_t)local * TCH + (j ^ cmask)) * NQ + g] = Sv[j];
       }
-      const ST* sp = reinterpret_cast<const ST*>(sb + a.s_off) + ch0 * NQ + g;
+      // the lane's NCH scales (+ zero points) are one vector in the layer-set
+      // layout; __fmul_rn: the products must not contract into the first add
+      // of the reduction (outputs stay bitwise those of the per-call lookups)
+      constexpr int SB = NCH * (int)sizeof(ST);
+      uint32_t sv[(SB + 3) / 4];
+      if constexpr (MODE != BITLUT_W_TERNARY) lds_vec<SB>(sb + soff, sv);
       if constexpr (MODE == BITLUT_W_OFFSET) {
 #pragma unroll
-        for (int j = 0; j < NCH; j++) y[j] = bl::to_f32(sp[j * NQ]) * fmaf(ts, (float)Sv[j], -rs);
+        for (int j = 0; j < NCH; j++) y[j] = __fmul_rn(vec_elem<ST>(sv, j), fmaf(ts, (float)Sv[j], -rs));
       } else if constexpr (MODE == BITLUT_W_ZEROS) {
-        const ST* zp = reinterpret_cast<const ST*>(sb + a.z_off) + ch0 * NQ + g;
+        uint32_t zv[(SB + 3) / 4];
+        lds_vec<SB>(sb + zoff, zv);
         const float h2 = (float)(2 << (BITS - 1));
 #pragma unroll
         for (int j = 0; j < NCH; j++)
-          y[j] = bl::to_f32(sp[j * NQ]) *
-                 fmaf(fmaf(-2.f, bl::to_f32(zp[j * NQ]), h2), rs, fmaf(ts, (float)Sv[j], -rs));
+          y[j] = __fmul_rn(vec_elem<ST>(sv, j),
+                           fmaf(fmaf(-2.f, vec_elem<ST>(zv, j), h2), rs, fmaf(ts, (float)Sv[j], -rs)));
       } else if constexpr (MODE == BITLUT_W_SIGN) {
 #pragma unroll
-        for (int j = 0; j < NCH; j++) y[j] = bl::to_f32(sp[j * NQ]) * (ts * (float)Sv[j]);
+        for (int j = 0; j < NCH; j++) y[j] = __fmul_rn(vec_elem<ST>(sv, j), __fmul_rn(ts, (float)Sv[j]));
       } else {
 #pragma unroll
         for (int j = 0; j < NCH; j++) y[j] = fmaf(ts, (float)Sv[j], rs);
       }
     }
-    const int fb = reduce_lanes<NCH, LG, 32>(y, lane);
-    float* yb = ysm + (it & (kYBufs - 1)) * NW * TCH + warp * TCH;
-    BL_CHECK(ch0 + fb + NF <= TCH);
-#pragma unroll
-    for (int j = 0; j < NF; j++) yb[ch0 + fb + j] = y[j];
+    reduce_lanes_perm<NCH, LG, 32>(y);                  // over the groups of the warp: y[0] = channel cmask
+    static_assert(NF == 1, "one channel sum per lane");
+    ysm[(it & (kYBufs - 1)) * NW * TCH + warp * TCH + cmask] = y[0];
     __syncthreads();                                    // stage consumed, ysm complete
     if (tid == 0) {                                     // refill the consumed stage
       const int t = tile + S;
@@ -295,7 +303,11 @@ int launch(const bl::LayoutV2& L, const bitlut_batch_mat* dm, int n_mats, int to
   a.L = L;
   a.independent = independent ? 1 : 0;
   a.w_bytes = (uint32_t)((size_t)L.KG * 16);
-  a.s_bytes = MODE == BITLUT_W_TERNARY ? 0u : (uint32_t)((size_t)L.tile_ch * L.NQ * sizeof(ST));
+  constexpr int NV = reduced_count<BITS == 4 ? 8 : 16, 1, LG>();
+  constexpr int NCH = BITS == 1 ? 2 * NV : NV;
+  a.s_bytes = MODE == BITLUT_W_TERNARY ? 0u : (uint32_t)((size_t)L.U * NCH * sizeof(ST));
+  if (a.s_bytes != (uint32_t)bl::layer_set_scale_bytes(L, (int)sizeof(ST)) && MODE != BITLUT_W_TERNARY)
+    return BITLUT_EINTERNAL;
   a.s_off = al16(a.w_bytes);
   a.z_off = a.s_off + al16(a.s_bytes);
   a.stage_bytes = a.z_off + (MODE == BITLUT_W_ZEROS ? al16(a.s_bytes) : 0u);

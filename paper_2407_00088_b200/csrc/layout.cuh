@@ -74,4 +74,28 @@ inline int make_layout(int m, int k, int bits, int gs, LayoutV2* L) {
   return 0;
 }
 
+// ---- layer-set layout (consumed by bitlut_mpgemv_batch, csrc/gemv_batch.cu) ----
+// The same chunks at the same offsets as layout v2, but inside the chunk of
+// lane l (l = unit & 31) position pos holds stream pos ^ pmask(l), with
+// pmask(l) = bits * bitrev_{log2 tile_ch}(l): the lane reductions of the
+// batch kernel then need no selects (b1_core.cuh reduce_lanes_perm).  The
+// group scales (zero points) of a tile are stored per unit: unit u holds the
+// NCH = max(1, tile_ch / Lg) values of its quantization group g = u / Lg in
+// the order of the lane's reduced sums, value j = channel j ^ cmask(u & 31)
+// -- one vector load per lane instead of NCH strided 2-byte loads.
+__host__ __device__ inline int layer_set_cmask(int lane, int tile_ch) {
+  int m = 0;
+  for (int o = 1, n = tile_ch >> 1; n >= 1; o <<= 1, n >>= 1)
+    if (lane & o) m |= n;
+  return m;
+}
+__host__ __device__ inline int layer_set_nch(const LayoutV2& L) {
+  const int nacc = L.bits == 4 ? 8 : 16;                 // accumulators per lane (W1: stream pairs)
+  int nv = nacc / L.Lg; if (nv < 1) nv = 1;
+  return L.bits == 1 ? 2 * nv : nv;
+}
+__host__ __device__ inline int64_t layer_set_scale_bytes(const LayoutV2& L, int elem_bytes) {
+  return (int64_t)L.U * layer_set_nch(L) * elem_bytes;   // per tile
+}
+
 }  // namespace bl

@@ -180,6 +180,44 @@ __global__ void unrepack_kernel(const uint8_t* __restrict__ in, bl::LayoutV2 L, 
   }
 }
 
+// ---- layer-set layout (layout.cuh) ----  one thread per 16-byte chunk:
+// nibble pos of the output = nibble pos ^ pmask(lane) of the v2 chunk (an
+// involution, so the same kernel converts back)
+__global__ void layer_set_weights_kernel(const uint8_t* __restrict__ in, bl::LayoutV2 L, uint8_t* __restrict__ out) {
+  const int64_t chunks = (int64_t)L.n_tiles * L.KG;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < chunks;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int kg = (int)(t % L.KG);
+    const int tile = (int)(t / L.KG);
+    const int64_t off = L.chunk_offset(tile, 0, kg);
+    const int lane = (kg / L.R) & 31;
+    const int pmask = L.bits * bl::layer_set_cmask(lane, L.tile_ch);
+    const uint4 v = *reinterpret_cast<const uint4*>(in + off);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t o[4] = {0, 0, 0, 0};
+    for (int pos = 0; pos < 32; pos++) {
+      const int src = pos ^ pmask;
+      o[pos >> 3] |= ((w[src >> 3] >> (4 * (src & 7))) & 15u) << (4 * (pos & 7));
+    }
+    *reinterpret_cast<uint4*>(out + off) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+// group scales / zero points (m, NQ) -> per tile, per unit, the lane's NCH values
+template <typename ST>
+__global__ void layer_set_scales_kernel(const ST* __restrict__ in, bl::LayoutV2 L, int nch, ST* __restrict__ out) {
+  const int64_t per_tile = (int64_t)L.U * nch;
+  const int64_t total = per_tile * L.n_tiles;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int tile = (int)(t / per_tile);
+    const int r = (int)(t - (int64_t)tile * per_tile);
+    const int u = r / nch, j = r - u * nch;
+    const int c = j ^ bl::layer_set_cmask(u & 31, L.tile_ch);
+    out[t] = in[((int64_t)tile * L.tile_ch + c) * L.NQ + u / L.Lg];
+  }
+}
+
 int check_v1(int bits, int m, int k, int g, int m_tile, int k_tile, int lanes) {
   if (bits < 1 || bits > 4 || g < 1 || g > 8 || lanes < 1 || m_tile < 1 || k_tile < 1)
     return BITLUT_EPARAM;
@@ -254,5 +292,45 @@ extern "C" int bitlut_unrepack_gpu(const uint8_t* wgpu, int bits, int m, int k, 
   if (rc) return rc;
   int64_t n = (int64_t)L.n_tiles * L.n_sg * L.KG;
   unrepack_kernel<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(wgpu, L, indices);
+  return bl_launch_status();
+}
+
+// Layer-set layout (the operand format of bitlut_mpgemv_batch): see layout.cuh.
+extern "C" int64_t bitlut_layer_set_scales_bytes(int m, int k, int bits, int group_size, int scale_dtype) {
+  bl::LayoutV2 L;
+  if (bl::make_layout(m, k, bits, group_size, &L) != 0 || L.n_sg != 1) return -1;
+  if (scale_dtype != BITLUT_DT_F32 && scale_dtype != BITLUT_DT_F16) return -1;
+  return bl::layer_set_scale_bytes(L, scale_dtype == BITLUT_DT_F16 ? 2 : 4) * L.n_tiles;
+}
+
+extern "C" int bitlut_layer_set_weights(const uint8_t* wgpu, int bits, int m, int k, int group_size,
+                                        uint8_t* out, void* stream) {
+  bl::LayoutV2 L;
+  int rc = bl::make_layout(m, k, bits, group_size, &L);
+  if (rc) return rc;
+  if (L.n_sg != 1) return BITLUT_ELAYOUT;
+  if (!wgpu || !out || wgpu == out) return BITLUT_EPARAM;
+  int64_t n = (int64_t)L.n_tiles * L.KG;
+  layer_set_weights_kernel<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(wgpu, L, out);
+  return bl_launch_status();
+}
+
+extern "C" int bitlut_layer_set_scales(const void* scales, int scale_dtype, int bits, int m, int k,
+                                       int group_size, void* out, void* stream) {
+  bl::LayoutV2 L;
+  int rc = bl::make_layout(m, k, bits, group_size, &L);
+  if (rc) return rc;
+  if (L.n_sg != 1) return BITLUT_ELAYOUT;
+  if (!scales || !out || scales == out) return BITLUT_EPARAM;
+  const int nch = bl::layer_set_nch(L);
+  int64_t n = (int64_t)L.n_tiles * L.U * nch;
+  if (scale_dtype == BITLUT_DT_F16)
+    layer_set_scales_kernel<__half><<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<const __half*>(scales), L, nch, reinterpret_cast<__half*>(out));
+  else if (scale_dtype == BITLUT_DT_F32)
+    layer_set_scales_kernel<float><<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<const float*>(scales), L, nch, reinterpret_cast<float*>(out));
+  else
+    return BITLUT_EPARAM;
   return bl_launch_status();
 }

@@ -235,11 +235,14 @@ class Pipeline:
             pw, partials = self._wextra[i]
             mode = N.W_MODES[pw.encoding]
             m = N.BitlutBatchMat()
-            m.wgpu, m.out, m.m = s.wgpu, s.out, s.m
-            # sign / ternary: the native scale (s of w = s (2q - 1); the
-            # per-tensor scale), no zero points; zeros: the zero-point array
-            m.wscales = pw.native_scales.data_ptr() if mode in (N.W_SIGN, N.W_TERNARY) else s.wscales
-            m.zeros = s.zeros if mode == N.W_ZEROS else None
+            # the layer-set layout of the operand (converted once per PackedWeights);
+            # sign: the native scale s of w = s (2q - 1); ternary: the one
+            # per-tensor scale, no scale stream; zeros: + the zero points
+            lw, lsc, lz = pw.layer_set_operand()
+            self.keep += [lw, lsc, lz]
+            m.wgpu, m.out, m.m = lw.data_ptr(), s.out, s.m
+            m.wscales = pw.native_scales.data_ptr() if mode == N.W_TERNARY else lsc.data_ptr()
+            m.zeros = lz.data_ptr() if mode == N.W_ZEROS else None
             m.partials = partials.data_ptr() if partials is not None else None
             m.tables, m.tscales, m.rowsums = s.tables, s.tscales, s.rowsums
             sd = N.dtype_code(pw.native_scales) if mode in (N.W_SIGN, N.W_TERNARY) else s.scale_dtype

@@ -83,6 +83,25 @@ class PackedWeights:
         if self.encoding == "offset" and self.zeros is not None:
             object.__setattr__(self, "encoding", "zeros")
 
+    def layer_set_operand(self):
+        """(weights, scales, zeros) in the layer-set layout the batch executor
+        reads (include/bitlut_b200.h bitlut_layer_set_*; csrc/layout.cuh),
+        converted from the v2 operand on first use and cached.  scales: the
+        encoding's scale stream (sign planes: native_scales; ternary: None,
+        the one per-tensor value is passed as is)."""
+        cached = self.__dict__.get("_layer_set")
+        if cached is None:
+            if self.gpu is None:
+                raise LayoutError("packed weights carry no GPU layout")
+            args = (self.bits, self.m, self.k, self.group_size)
+            w = N.layer_set_weights(self.gpu, *args)
+            src = self.native_scales if self.encoding == "sign" else self.scales
+            sc = None if self.encoding == "ternary" else N.layer_set_scales(src, *args)
+            z = N.layer_set_scales(self.zeros, *args) if self.encoding == "zeros" else None
+            cached = (w, sc, z)
+            object.__setattr__(self, "_layer_set", cached)
+        return cached
+
     @property
     def plane_bytes(self) -> int:
         return self.planes.shape[1]
