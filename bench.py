@@ -1145,7 +1145,7 @@ def load_traffic(kernel="gemv_batch_kernel"):
     kernel from one committed `ncu --set full` capture of the batch
     executor's lookup launches (mean per launch; roofline.achieved is per
     replay of the same launches)."""
-    for name in ("r02_batch_w2_full.json", "r01h_batch_full.json"):
+    for name in ("r02d_batch_w2_full.json", "r02_batch_w2_full.json", "r01h_batch_full.json"):
         p = os.path.join(ROOT, "profiles", name)
         if os.path.exists(p):
             with open(p) as f:

@@ -65,6 +65,58 @@ __device__ __forceinline__ void lookup_kg_merged(const uint4 w, uint32_t a0, uin
   }
 }
 
+// The same k-group of weights against the tables of TWO activation rows
+// (mpGEMM row blocks): the selector preparation -- the LOP3, the shifts and
+// W2's two selector PRMTs -- is done once per weight word and only the
+// lookups and dot products repeat per row (W2: 5.5 ALU + 5 IDP instructions
+// per word and row instead of 7 + 6).  Same sums as lookup_kg_merged.
+template <int BITS, int NACC>
+__device__ __forceinline__ void lookup_kg_merged2(const uint4 w, uint32_t a0, uint32_t a1, uint32_t b0, uint32_t b1,
+                                                  int (&accA)[NACC], int (&accB)[NACC]) {
+  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const uint32_t x = ws[q];
+    const uint32_t xx = x ^ 0x88888888u;
+    if constexpr (BITS == 2) {
+      const uint32_t s01 = bl::prmt(x, xx, 0x5140u), s23 = bl::prmt(x, xx, 0x7362u);
+      const uint32_t h01 = sel_hi<true>(s01), h23 = sel_hi<true>(s23);
+      accA[4 * q + 0] = bl::dp4a(bl::prmt(a0, a1, s01), 0xFEFF0201u, accA[4 * q + 0]);
+      accA[4 * q + 1] = bl::dp4a(bl::prmt(a0, a1, h01), 0xFEFF0201u, accA[4 * q + 1]);
+      accA[4 * q + 2] = bl::dp4a(bl::prmt(a0, a1, s23), 0xFEFF0201u, accA[4 * q + 2]);
+      accA[4 * q + 3] = bl::dp4a(bl::prmt(a0, a1, h23), 0xFEFF0201u, accA[4 * q + 3]);
+      accB[4 * q + 0] = bl::dp4a(bl::prmt(b0, b1, s01), 0xFEFF0201u, accB[4 * q + 0]);
+      accB[4 * q + 1] = bl::dp4a(bl::prmt(b0, b1, h01), 0xFEFF0201u, accB[4 * q + 1]);
+      accB[4 * q + 2] = bl::dp4a(bl::prmt(b0, b1, s23), 0xFEFF0201u, accB[4 * q + 2]);
+      accB[4 * q + 3] = bl::dp4a(bl::prmt(b0, b1, h23), 0xFEFF0201u, accB[4 * q + 3]);
+      continue;
+    }
+    const uint32_t xh = sel_hi<BITS == 4>(x), xxh = xx >> 16;
+#pragma unroll
+    for (int r = 0; r < 2; r++) {
+      const uint32_t t0 = r ? b0 : a0, t1 = r ? b1 : a1;
+      int (&acc)[NACC] = r ? accB : accA;
+      const uint32_t A0 = bl::prmt(t0, t1, x), Y0 = bl::prmt(t0, t1, xx);
+      const uint32_t A1 = bl::prmt(t0, t1, xh), Y1 = bl::prmt(t0, t1, xxh);
+      if constexpr (BITS == 4) {
+        acc[2 * q] = bl::dp4a(A0, 0x08040201u, acc[2 * q]);
+        acc[2 * q] = bl::dp4a(Y0, 0xF8FCFEFFu, acc[2 * q]);
+        acc[2 * q + 1] = bl::dp4a(A1, 0x08040201u, acc[2 * q + 1]);
+        acc[2 * q + 1] = bl::dp4a(Y1, 0xF8FCFEFFu, acc[2 * q + 1]);
+      } else {
+        acc[4 * q + 0] = bl::dp2a_lo_u(kMult, A0, acc[4 * q + 0]);
+        acc[4 * q + 0] = bl::dp2a_lo(kMultNeg, Y0, acc[4 * q + 0]);
+        acc[4 * q + 1] = bl::dp2a_hi_u(kMult, A0, acc[4 * q + 1]);
+        acc[4 * q + 1] = bl::dp2a_hi(kMultNeg, Y0, acc[4 * q + 1]);
+        acc[4 * q + 2] = bl::dp2a_lo_u(kMult, A1, acc[4 * q + 2]);
+        acc[4 * q + 2] = bl::dp2a_lo(kMultNeg, Y1, acc[4 * q + 2]);
+        acc[4 * q + 3] = bl::dp2a_hi_u(kMult, A1, acc[4 * q + 3]);
+        acc[4 * q + 3] = bl::dp2a_hi(kMultNeg, Y1, acc[4 * q + 3]);
+      }
+    }
+  }
+}
+
 // Reduce NV values across the lanes that differ in lane bits [O0, O1):
 // halving exchanges while more than one value is left (each lane keeps a
 // disjoint half, no redundant adds), plain butterfly adds afterwards.
@@ -76,6 +128,20 @@ __host__ __device__ constexpr int reduced_count() {
   for (int o = O0; o < O1; o <<= 1)
     if (n > 1) n >>= 1;
   return n;
+}
+
+// The index reduce_lanes<NV, O0, O1> returns for this lane (it depends on the lane only).
+template <int NV, int O0, int O1>
+__device__ __forceinline__ int lane_base(int lane) {
+  int base = 0;
+#pragma unroll
+  for (int o = O0, n = NV; o < O1; o <<= 1) {
+    if (n > 1) {
+      n >>= 1;
+      if (lane & o) base += n;
+    }
+  }
+  return base;
 }
 
 template <int NV, int O0, int O1, typename T>

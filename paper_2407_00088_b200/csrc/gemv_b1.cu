@@ -95,7 +95,7 @@ B1Plan b1_plan(const bl::LayoutV2& L, bool zeros, bool tab_smem, int T, int stag
   s.ts_off = s.tab_off + (tab_smem ? al16((size_t)L.KG * 8) : 0);
   s.rs_off = s.ts_off + al16((size_t)L.NQ * 4);
   s.y_off = s.rs_off + al16((size_t)L.NQ * 4);
-  s.sa_off = s.y_off + al16((size_t)2 * (T / 32) * L.tile_ch * 4);
+  s.sa_off = s.y_off + al16((size_t)4 * (T / 32) * L.tile_ch * 4);   // rows kernel: 2 pairs x 2 rows
   s.red_off = s.sa_off + (fused ? al16((size_t)4 * T * 4) : 0);
   s.psm_off = s.red_off + (fused ? al16((size_t)(T / 32) * 4) : 0);
   // exact epilogue (reference order): staging values NQ x 33 int32, products
@@ -780,9 +780,10 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
 
 // Lean mpGEMM rows kernel (kFastRows common case: one unit round, register
 // tables, no zeros / partials): the tile is staged once and stays in shared
-// memory while the CTA walks its rows; per row the thread's tables, table
-// scale and row sum are prefetched one row ahead (registers, from L2), and
-// one barrier per row publishes the cross-warp partial sums (double-buffered).
+// memory while the CTA walks its rows TWO AT A TIME -- the weights are read
+// from shared memory once per row pair and the selector preparation is
+// shared (lookup_kg_merged2); one barrier per pair publishes the cross-warp
+// partial sums (double-buffered).
 // Bitwise equal to gemv_b1_kernel<kFastRows>.
 template <int R, int LG, int BITS, typename ST>
 __global__ void __launch_bounds__(384) gemv_b1_rows_lean_kernel(const __grid_constant__ B1Args a) {
@@ -798,7 +799,7 @@ __global__ void __launch_bounds__(384) gemv_b1_rows_lean_kernel(const __grid_con
   const int NW = blockDim.x >> 5;
   const int NQ = L.NQ, KG = L.KG, U = L.U;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + a.bar_off);
-  float* ysm = reinterpret_cast<float*>(smem + a.y_off);
+  float* ysm = reinterpret_cast<float*>(smem + a.y_off);     // [2 pairs][2 rows][NW][TCH]
   const int tile = blockIdx.x;
   const int row0 = blockIdx.y * a.rows_per_cta;
   const int row1 = min(row0 + a.rows_per_cta, a.n_rows);
@@ -816,8 +817,8 @@ __global__ void __launch_bounds__(384) gemv_b1_rows_lean_kernel(const __grid_con
   const int nu_b = min(32, U - 32 * ub);
   const int g = u / LG;
   const uint8_t* tb0 = p.qtab + (int64_t)ub * (32 * R * 8) + l * 16;
-  uint4 tq[R / 2], tn[R / 2];
-  float ts = 0.f, rs = 0.f, tsn = 0.f, rsn = 0.f;
+  uint4 tqA[R / 2], tqB[R / 2];
+  float tsA = 0.f, rsA = 0.f, tsB = 0.f, rsB = 0.f;
   auto fetch = [&](int row, uint4 (&t)[R / 2], float& s1, float& s2) {
     if (live && row < row1) {
       const uint8_t* tb = tb0 + (int64_t)row * KG * 8;
@@ -827,7 +828,6 @@ __global__ void __launch_bounds__(384) gemv_b1_rows_lean_kernel(const __grid_con
       s2 = bl::ld_cg_f32(p.rowsums + (int64_t)row * NQ + g);
     }
   };
-  fetch(row0, tq, ts, rs);
   __syncthreads();                                      // barrier initialised
   mbar_wait(bar, 0);
   const uint8_t* wsrc = smem + (uint32_t)(ub * (32 * R * 16) + l * 16);
@@ -835,20 +835,16 @@ __global__ void __launch_bounds__(384) gemv_b1_rows_lean_kernel(const __grid_con
   const int mj = find_mat(a, tile, local);
   float* outp = a.mats[mj].out + (int64_t)local * TCH;
   const int stride = nu_b * 16;
-  for (int row = row0, it = 0; row < row1; row++, it++) {
-    fetch(row + 1, tn, tsn, rsn);                       // next row's tables stream in meanwhile
-    int acc[NACC];
+  // the lane's NCH weight scales are the same for every row: converted once
+  float wsf[NCH];
+  {
+    const int b0 = lane_base<NACC, 1, LG>(lane);
+    const ST* sp = reinterpret_cast<const ST*>(smem + a.s_off) + (BITS == 1 ? 2 * b0 : b0) * NQ + g;
 #pragma unroll
-    for (int i = 0; i < NACC; i++) acc[i] = 0;
-    if (live) {
-#pragma unroll
-      for (int j = 0; j < R; j += 2) {
-        const uint4 wa = *reinterpret_cast<const uint4*>(wsrc + j * stride);
-        const uint4 wc = *reinterpret_cast<const uint4*>(wsrc + (j + 1) * stride);
-        lookup_kg_merged<BITS, NACC>(wa, tq[j >> 1].x, tq[j >> 1].y, acc);
-        lookup_kg_merged<BITS, NACC>(wc, tq[j >> 1].z, tq[j >> 1].w, acc);
-      }
-    }
+    for (int j = 0; j < NCH; j++) wsf[j] = live ? bl::to_f32(sp[j * NQ]) : 0.f;
+  }
+  // one row's sums: group reduction, scaling, reduction over the warp's groups -> ysm
+  auto finish_row = [&](int (&acc)[NACC], float ts, float rs, float* ybuf) {
     const int base = reduce_lanes<NACC, 1, LG>(acc, lane);
     const int ch0 = BITS == 1 ? 2 * base : base;
     float y[NCH];
@@ -866,28 +862,56 @@ __global__ void __launch_bounds__(384) gemv_b1_rows_lean_kernel(const __grid_con
 #pragma unroll
         for (int i = 0; i < NV; i++) Sv[i] = acc[i];
       }
-      const ST* sp = reinterpret_cast<const ST*>(smem + a.s_off) + ch0 * NQ + g;
 #pragma unroll
-      for (int j = 0; j < NCH; j++) y[j] = bl::to_f32(sp[j * NQ]) * fmaf(ts, (float)Sv[j], -rs);
+      for (int j = 0; j < NCH; j++) y[j] = wsf[j] * fmaf(ts, (float)Sv[j], -rs);
     } else {
 #pragma unroll
       for (int j = 0; j < NCH; j++) y[j] = 0.f;
     }
     const int fb = reduce_lanes<NCH, LG, 32>(y, lane);
-    float* yb = ysm + (it & 1) * NW * TCH + warp * TCH;
+    float* yb = ybuf + warp * TCH;
 #pragma unroll
     for (int j = 0; j < NF; j++) yb[ch0 + fb + j] = y[j];
-    __syncthreads();                                    // this row's partials complete
-    if (tid < TCH) {
-      const float* yr = ysm + (it & 1) * NW * TCH + tid;
-      float sum = 0.f;
-      for (int w = 0; w < NW; w++) sum += yr[w * TCH];
-      outp[(int64_t)row * L.m + tid] = 0.5f * sum;
-    }
+  };
+  for (int row = row0, it = 0; row < row1; row += 2, it++) {
+    const bool two = row + 1 < row1;                    // uniform over the CTA
+    fetch(row, tqA, tsA, rsA);                          // (other CTAs of the SM hide the L2 latency)
+    fetch(row + 1, tqB, tsB, rsB);
+    int accA[NACC], accB[NACC];
 #pragma unroll
-    for (int jp = 0; jp < R / 2; jp++) tq[jp] = tn[jp];
-    ts = tsn;
-    rs = rsn;
+    for (int i = 0; i < NACC; i++) accA[i] = accB[i] = 0;
+    if (live) {
+      if (two) {
+#pragma unroll
+        for (int j = 0; j < R; j += 2) {
+          const uint4 wa = *reinterpret_cast<const uint4*>(wsrc + j * stride);
+          const uint4 wc = *reinterpret_cast<const uint4*>(wsrc + (j + 1) * stride);
+          lookup_kg_merged2<BITS, NACC>(wa, tqA[j >> 1].x, tqA[j >> 1].y, tqB[j >> 1].x, tqB[j >> 1].y, accA, accB);
+          lookup_kg_merged2<BITS, NACC>(wc, tqA[j >> 1].z, tqA[j >> 1].w, tqB[j >> 1].z, tqB[j >> 1].w, accA, accB);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < R; j += 2) {
+          const uint4 wa = *reinterpret_cast<const uint4*>(wsrc + j * stride);
+          const uint4 wc = *reinterpret_cast<const uint4*>(wsrc + (j + 1) * stride);
+          lookup_kg_merged<BITS, NACC>(wa, tqA[j >> 1].x, tqA[j >> 1].y, accA);
+          lookup_kg_merged<BITS, NACC>(wc, tqA[j >> 1].z, tqA[j >> 1].w, accA);
+        }
+      }
+    }
+    float* ybase = ysm + (it & 1) * 2 * NW * TCH;
+    finish_row(accA, tsA, rsA, ybase);
+    if (two) finish_row(accB, tsB, rsB, ybase + NW * TCH);
+    __syncthreads();                                    // this pair's partials complete
+    if (tid < TCH) {
+      const int nr = two ? 2 : 1;
+      for (int r = 0; r < nr; r++) {
+        const float* yr = ybase + r * NW * TCH + tid;
+        float sum = 0.f;
+        for (int w = 0; w < NW; w++) sum += yr[w * TCH];
+        outp[(int64_t)(row + r) * L.m + tid] = 0.5f * sum;
+      }
+    }
   }
   bl::dep_signal(p.dep);
   if (p.independent) bl::pdl_wait();

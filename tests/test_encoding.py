@@ -158,3 +158,59 @@ def test_layout_v2_bijection(m, k, bits, gs):
     assert off.min() == 0 and off.max() == total - 16
     assert np.all(off % 16 == 0)
     assert np.unique(off).size == off.size
+
+
+# ---- layer-set layout (csrc/layout.cuh, b1_core.cuh reduce_lanes_perm) ----
+
+def perm_mask(lane: int, nidx: int) -> int:
+    """b1_core.cuh perm_mask<NIDX> / layout.cuh layer_set_cmask."""
+    m, o, n = 0, 1, nidx >> 1
+    while n >= 1:
+        if lane & o:
+            m |= n
+        o, n = o << 1, n >> 1
+    return m
+
+
+def shr16_idp(x: int) -> int:
+    """common.cuh shr16_idp: dp2a.hi.u32.u32 with 16-bit multipliers (1, 256)."""
+    return ((x >> 16) & 0xFF) * 1 + ((x >> 24) & 0xFF) * 256
+
+
+def test_shr16_idp_is_a_shift():
+    rng = np.random.default_rng(0)
+    for x in rng.integers(0, 1 << 32, 2000, dtype=np.uint64):
+        assert shr16_idp(int(x)) == int(x) >> 16
+
+
+@pytest.mark.parametrize("nacc,lg", [(16, 1), (16, 2), (16, 4), (16, 8), (16, 16), (8, 1), (8, 4), (8, 16), (32, 4)])
+def test_select_free_halving_reduces_every_index(nacc, lg):
+    """A warp of 32 lanes, lane l holding logical index i ^ perm_mask(l) at
+    value index i (what the lane-permuted chunks give the lookup core): the
+    select-free halving (keep the low half, send the high half, first over
+    the lg lanes of a quantization group, then over the groups) leaves lane l
+    with the complete sum of logical index perm_mask(l), and every partial
+    sum only ever adds values of ONE logical index."""
+    rng = np.random.default_rng(nacc * 100 + lg)
+    vals = rng.integers(-1000, 1000, (32, nacc))            # [lane][logical index]
+    # v[lane][i] = (logical index, group set, sum)
+    v = [[(i ^ perm_mask(l, nacc), vals[l][i ^ perm_mask(l, nacc)]) for i in range(nacc)] for l in range(32)]
+    n, o = nacc, 1
+    while o < 32:
+        if n > 1:
+            n >>= 1
+            nv = [[None] * nacc for _ in range(32)]
+            for l in range(32):
+                for i in range(n):
+                    a, b = v[l][i], v[l ^ o][i + n]
+                    assert a[0] == b[0], "partner sends a different logical index"
+                    nv[l][i] = (a[0], a[1] + b[1])
+            v = nv
+        else:
+            v = [[(v[l][0][0], v[l][0][1] + v[l ^ o][0][1])] + [None] * (nacc - 1) for l in range(32)]
+        o <<= 1
+    # lanes that differ only in bits above log2(nacc) all hold the same index: the total is over 32 lanes
+    for l in range(32):
+        idx, s = v[l][0]
+        assert idx == perm_mask(l, nacc) % nacc
+        assert s == vals[:, idx].sum()

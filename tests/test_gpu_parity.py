@@ -832,3 +832,55 @@ def test_batch_executor_bitwise(bits, gs, scale_dtype):
     exact.lookup(pws[0], exact.tables(xs[0], gs))
     with pytest.raises(B.ParameterError):
         exact.compile()
+
+
+# ---- layer-set layout conversion (bitlut_layer_set_weights / _scales) ----
+
+def _perm_mask(lane, nidx):
+    m, o, n = 0, 1, nidx >> 1
+    while n >= 1:
+        if lane & o:
+            m |= n
+        o, n = o << 1, n >> 1
+    return m
+
+
+@pytest.mark.parametrize("m,k,bits,gs", [(64, 1024, 2, 64), (32, 2048, 1, 128), (64, 512, 4, 128),
+                                         (32, 1376, 2, 32), (32, 1024, 4, 512), (64, 2752, 2, 64)])
+def test_layer_set_conversion(m, k, bits, gs):
+    """The batch executor's operand format against a numpy restatement of
+    csrc/layout.cuh: nibble pos of lane l's chunk = nibble pos ^ (bits *
+    cmask(l)) of the v2 chunk (an involution), and the unit-major scales."""
+    from paper_2407_00088_b200 import _native as N
+    g = torch.Generator(device="cuda").manual_seed(m + k + bits)
+    nbytes = m * bits * k // 8
+    w = torch.randint(0, 256, (nbytes,), dtype=torch.uint8, device="cuda", generator=g)
+    w3 = N.layer_set_weights(w, bits, m, k, gs)
+    assert torch.equal(N.layer_set_weights(w3, bits, m, k, gs), w)
+    tch, R = 32 // bits, (8 if (gs // 4) % 8 == 0 else 4)
+    KG, U = k // 4, k // 4 // R
+    wn, w3n = w.cpu().numpy(), w3.cpu().numpy()
+    nib = lambda a: np.stack([a & 15, a >> 4], axis=-1).reshape(a.shape[0], -1)   # noqa: E731
+    rng = np.random.default_rng(0)
+    for _ in range(64):                      # sampled chunks
+        tile, kg = int(rng.integers(m // tch)), int(rng.integers(KG))
+        u, r = kg // R, kg % R
+        ub, l = u >> 5, u & 31
+        nu_b = min(32, U - 32 * ub)
+        off = tile * KG * 16 + ub * (32 * R * 16) + (r * nu_b + l) * 16
+        a, b = nib(wn[off:off + 16][None])[0], nib(w3n[off:off + 16][None])[0]
+        pm = bits * _perm_mask(l, tch)
+        assert np.array_equal(b, a[np.arange(32) ^ pm])
+    # scales: unit u of a tile holds scale[(tile*tch + (j ^ cmask(u & 31))), u // Lg], j < NCH
+    Lg = (gs // 4) // R
+    nacc = 8 if bits == 4 else 16
+    nch = max(1, nacc // Lg) * (2 if bits == 1 else 1)
+    for dt in (torch.float16, torch.float32):
+        sc = torch.randn((m, k // gs), device="cuda", generator=g).to(dt)
+        s3 = N.layer_set_scales(sc, bits, m, k, gs).cpu().numpy().reshape(m // tch, U, nch)
+        scn = sc.cpu().numpy()
+        uu = np.arange(U)
+        for j in range(nch):
+            c = j ^ np.array([_perm_mask(int(x) & 31, tch) for x in uu])
+            for tile in range(m // tch):
+                assert np.array_equal(s3[tile, :, j], scn[tile * tch + c, uu // Lg])
