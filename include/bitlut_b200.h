@@ -46,6 +46,17 @@ extern "C" {
 /* lookup-table modes */
 #define BITLUT_TABLE_Q8  0  /* int8 half tables + per-group table scales (vector-q8 semantics) */
 #define BITLUT_TABLE_F16 1  /* fp16 half tables (BASELINE "fp16 tables") */
+/* 16-bit block fixed point: per quantization group scale = max|entry| / 16129,
+ * entry = scale * (127 H + L) with two balanced base-127 digits H in
+ * [-127, 127], L in [-63, 63] -- each an int8 half table, so the mirror flag
+ * negates digit by digit and the int8 lookup core applies twice.  At least
+ * fp16-table accuracy (<= 3.1e-5 of the group maximum per entry; fp16:
+ * 4.9e-4 of the entry).  The fast batch-1 path of variant "cuda-f16":
+ * bitlut_build_lut (single row) + bitlut_mpgemm with
+ * BITLUT_FLAG_FAST_EPILOGUE, n = 1, 1/2/4-bit weights; anything else
+ * returns BITLUT_ELAYOUT (use BITLUT_TABLE_F16).  16 bytes per k-group
+ * like BITLUT_TABLE_F16; table scales are written. */
+#define BITLUT_TABLE_X16 2
 
 /* launch flags (bitlut_build_lut, bitlut_mpgemm) */
 #define BITLUT_FLAG_PDL 1   /* launch with programmatic dependent launch */

@@ -22,7 +22,7 @@ LIB_PATH = os.environ.get("BITLUT_B200_LIB") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "_lib", "libbitlut_b200.so")   # env: A/B builds
 
 DT_F32, DT_F16 = 0, 1
-TABLE_Q8, TABLE_F16 = 0, 1
+TABLE_Q8, TABLE_F16, TABLE_X16 = 0, 1, 2     # X16: 16-bit block fixed point (bitlut_b200.h)
 FLAG_PDL = 1
 FLAG_INDEPENDENT = 2
 FLAG_FAST_EPILOGUE = 4

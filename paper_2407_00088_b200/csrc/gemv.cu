@@ -243,8 +243,8 @@ int bl_mpgemm_launch(const uint8_t* wgpu, int m, int k, int bits, int group_size
   if (n < 0) return BITLUT_ESHAPE;
   if (n == 0) return BITLUT_OK;
   if (scale_dtype != BITLUT_DT_F32 && scale_dtype != BITLUT_DT_F16) return BITLUT_EPARAM;
-  if (mode != BITLUT_TABLE_Q8 && mode != BITLUT_TABLE_F16) return BITLUT_EPARAM;
-  if (mode == BITLUT_TABLE_F16 && partials) return BITLUT_EPARAM;   // int32 partials: Q8 only
+  if (mode != BITLUT_TABLE_Q8 && mode != BITLUT_TABLE_F16 && mode != BITLUT_TABLE_X16) return BITLUT_EPARAM;
+  if (mode != BITLUT_TABLE_Q8 && partials) return BITLUT_EPARAM;    // int32 partials: Q8 only
   if (n > 65535) return BITLUT_ESHAPE;
   const bool pdl = (flags & BITLUT_FLAG_PDL) != 0;
   GemvArgs a = {};
@@ -266,11 +266,12 @@ int bl_mpgemm_launch(const uint8_t* wgpu, int m, int k, int bits, int group_size
   }
   const bool combined = (flags & BITLUT_FLAG_COMBINED_PARTIALS) != 0;
   if (combined && (!a.fast || mode != BITLUT_TABLE_Q8 || L.n_sg != 1 || trace)) return BITLUT_EPARAM;
-  if (mode == BITLUT_TABLE_F16 && a.fast && n == 1 && !partials && !trace && L.n_sg == 1 && b1_enabled()) {
-    a.f16_tables = 1;                                  // lean batch-1 kernel, fp16-table mode
-    rc = bl_gemv_b1_launch(a, scale_dtype, (cudaStream_t)stream, pdl);
-    a.f16_tables = 0;
-    if (rc != BITLUT_ELAYOUT) return rc;
+  if (mode == BITLUT_TABLE_X16) {
+    // 16-bit block-fixed-point tables: the lean batch-1 kernel only (the
+    // caller uses BITLUT_TABLE_F16 for everything else)
+    if (!(a.fast && n == 1 && !trace && L.n_sg == 1)) return BITLUT_ELAYOUT;
+    a.f16_tables = BITLUT_TABLE_X16;
+    return bl_gemv_b1_launch(a, scale_dtype, (cudaStream_t)stream, pdl);
   }
   if (mode == BITLUT_TABLE_Q8 && (a.fast ? (!partials || combined) : !partials) && !trace &&
       L.n_sg == 1 && (b1_enabled() || combined)) {

@@ -95,7 +95,9 @@ B1Plan b1_plan(const bl::LayoutV2& L, bool zeros, bool tab_smem, int T, int stag
   s.ts_off = s.tab_off + (tab_smem ? al16((size_t)L.KG * 8) : 0);
   s.rs_off = s.ts_off + al16((size_t)L.NQ * 4);
   s.y_off = s.rs_off + al16((size_t)L.NQ * 4);
-  s.sa_off = s.y_off + al16((size_t)4 * (T / 32) * L.tile_ch * 4);   // rows kernel: 2 pairs x 2 rows
+  // cross-warp sums, double-buffered; the rows kernel stores two rows per buffer
+  // (batch-1 plans stay as small as before: K = 4096 fits six CTAs per SM)
+  s.sa_off = s.y_off + al16((size_t)(kind_rows(kind) ? 4 : 2) * (T / 32) * L.tile_ch * 4);
   s.red_off = s.sa_off + (fused ? al16((size_t)4 * T * 4) : 0);
   s.psm_off = s.red_off + (fused ? al16((size_t)(T / 32) * 4) : 0);
   // exact epilogue (reference order): staging values NQ x 33 int32, products
@@ -566,11 +568,13 @@ __global__ void __launch_bounds__(384) gemv_b1_kernel(const __grid_constant__ B1
 // the per-tile cost of the general kernel's mode branches, round / row loops
 // and per-tile reloads: the thread's group, table scale, row sum and smem
 // addresses are fixed for the launch.
-// F16: fp16 tables (cuda-f16): 16 B per k-group in registers, per-stream
-// fp32 accumulators (add.f32.f16), planes merged in fp32 (S = sum_p 2^p P_p,
-// powers of two: exact scaling) before the group reduction; no table scale
-// (y = ws * (S - rs) [+ zero term], out = 0.5 * sum, scalar-real semantics
-// _kernels.py:101-137 regrouped, tolerance-tested).
+// F16: the fast path of variant cuda-f16, on 16-bit block-fixed-point tables
+// (BITLUT_TABLE_X16: two balanced base-127 int8 digit tables per k-group, 16 B
+// in registers): the int8 core runs once per digit with shared selectors,
+// S = 127 S_H + S_L exactly, then the int8 epilogue with the 16-bit table
+// scale (scalar-real semantics _kernels.py:101-137 within the fp16-table
+// tolerance, tested).  Round 1's fp16 byte-plane lookups (5 PRMT + sign fix
+// per 4 lookups, fp32 adds) ran at 0.49 of the HBM peak.
 template <int R, int LG, int BITS, typename ST, bool ZEROS, bool F16 = false>
 __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant__ B1Args a) {
   const GemvArgs& p = a.g;
@@ -634,6 +638,7 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
       const uint8_t* tb = qtab + (int64_t)ub * (32 * R * 16) + l * 16;
 #pragma unroll
       for (int j = 0; j < R; j++) tq[j] = bl::ld_cg_128(tb + j * nu_b * 16);
+      ts = bl::ld_cg_f32(tsc + g);
     } else {
       const uint8_t* tb = qtab + (int64_t)ub * (32 * R * 8) + l * 16;
 #pragma unroll
@@ -657,41 +662,49 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
     float y[NCH];
     int ch0;
     if constexpr (F16) {
-      float fa[32];
+      // 16-bit block-fixed-point tables (BITLUT_TABLE_X16): the H and L digit
+      // tables of a k-group are one uint4; the int8 core runs once per digit
+      // with shared selectors, S = 127 S_H + S_L exactly
+      int accH[NACC], accL[NACC];
 #pragma unroll
-      for (int i = 0; i < 32; i++) fa[i] = 0.f;
+      for (int i = 0; i < NACC; i++) accH[i] = accL[i] = 0;
       if (live) {
         const uint8_t* wsrc = sb + woff;
         const int stride = nu_b == 32 ? 512 : nu_b * 16;
 #pragma unroll
         for (int j = 0; j < R; j++)
-          lookup_kg_f16(*reinterpret_cast<const uint4*>(wsrc + j * stride), tq[j], fa);
+          lookup_kg_merged2<BITS, NACC>(*reinterpret_cast<const uint4*>(wsrc + j * stride), tq[j].x, tq[j].y,
+                                        tq[j].z, tq[j].w, accH, accL);
       }
-      // streams are channel-major (c * BITS + p): merge the planes, exact 2^p
-      constexpr int NCHAN = 32 / BITS;
-      float sc[NCHAN];
-#pragma unroll
-      for (int c = 0; c < NCHAN; c++) {
-        float v = fa[c * BITS];
-#pragma unroll
-        for (int q = 1; q < BITS; q++) v = fmaf((float)(1 << q), fa[c * BITS + q], v);
-        sc[c] = v;
-      }
-      const int basef = reduce_lanes<NCHAN, 1, LG>(sc, lane);
-      ch0 = basef;
-      constexpr int NVF = reduced_count<NCHAN, 1, LG>();
-      static_assert(NVF == NCH, "fp16 mode: channel counts agree");
+      const int base = reduce_lanes<NACC, 1, LG>(accH, lane);
+      reduce_lanes<NACC, 1, LG>(accL, lane);
+      ch0 = BITS == 1 ? 2 * base : base;
       if (live) {
+        int Sv[NCH];
+        if constexpr (BITS == 1) {
+#pragma unroll
+          for (int i = 0; i < NV; i++) {
+            const int vh = accH[i], vl = accL[i];
+            const int he = (vh << 17) >> 17, le = (vl << 17) >> 17;
+            Sv[2 * i] = 127 * he + le;
+            Sv[2 * i + 1] = 127 * ((vh - he) >> 15) + ((vl - le) >> 15);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < NV; i++) Sv[i] = 127 * accH[i] + accL[i];
+        }
         const ST* sp = reinterpret_cast<const ST*>(sb + a.s_off) + ch0 * NQ + g;
         if constexpr (ZEROS) {
           const ST* zp = reinterpret_cast<const ST*>(sb + a.z_off) + ch0 * NQ + g;
           const float h2 = (float)(2 << (BITS - 1));
 #pragma unroll
-          for (int j = 0; j < NCH; j++)
-            y[j] = bl::to_f32(sp[j * NQ]) * fmaf(fmaf(-2.f, bl::to_f32(zp[j * NQ]), h2), rs, sc[j] - rs);
+          for (int j = 0; j < NCH; j++) {
+            const float t = fmaf(fmaf(-2.f, bl::to_f32(zp[j * NQ]), h2), rs, fmaf(ts, (float)Sv[j], -rs));
+            y[j] = bl::to_f32(sp[j * NQ]) * t;
+          }
         } else {
 #pragma unroll
-          for (int j = 0; j < NCH; j++) y[j] = bl::to_f32(sp[j * NQ]) * (sc[j] - rs);
+          for (int j = 0; j < NCH; j++) y[j] = bl::to_f32(sp[j * NQ]) * fmaf(ts, (float)Sv[j], -rs);
         }
       } else {
 #pragma unroll
@@ -1285,7 +1298,7 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
   const bool has_z = mats[0].zeros != nullptr;
   const bool lean = KIND == kFast && lean_common;
   const bool lean_rows = KIND == kFastRows && lean_common && n_mats == 1 && !has_z && !g.f16_tables;
-  if (g.f16_tables && !lean) return BITLUT_ELAYOUT;     // fp16 tables: the lean kernel or gemv_kernel
+  if (g.f16_tables && !lean) return BITLUT_ELAYOUT;     // X16 tables: the lean kernel only
   const bool f16 = g.f16_tables != 0;
   auto kern = lean ? (f16 ? (has_z ? gemv_b1_lean_kernel<R, LG, BITS, ST, true, true>
                                    : gemv_b1_lean_kernel<R, LG, BITS, ST, false, true>)

@@ -249,6 +249,12 @@ int bl_build_lut_launch(const void* a, int a_dtype, int n, int k, int group_size
                                  tables, tscales, rowsums, ind, dep)
             : cudaLaunchKernelEx(&cfg, build_lut_kernel<BITLUT_TABLE_Q8, float>, (const float*)a, k, group_size,
                                  tables, tscales, rowsums, ind, dep);
+  } else if (mode == BITLUT_TABLE_X16) {
+    e = a_dtype == BITLUT_DT_F16
+            ? cudaLaunchKernelEx(&cfg, build_lut_kernel<BITLUT_TABLE_X16, __half>, (const __half*)a, k, group_size,
+                                 tables, tscales, rowsums, ind, dep)
+            : cudaLaunchKernelEx(&cfg, build_lut_kernel<BITLUT_TABLE_X16, float>, (const float*)a, k, group_size,
+                                 tables, tscales, rowsums, ind, dep);
   } else {
     e = a_dtype == BITLUT_DT_F16
             ? cudaLaunchKernelEx(&cfg, build_lut_kernel<BITLUT_TABLE_F16, __half>, (const __half*)a, k, group_size,
@@ -262,7 +268,7 @@ int bl_build_lut_launch(const void* a, int a_dtype, int n, int k, int group_size
 extern "C" int bitlut_build_lut(const void* a, int a_dtype, int n, int k, int group_size, int mode,
                                 void* tables, float* tscales, float* rowsums, int flags, void* stream) {
   if (a_dtype != BITLUT_DT_F32 && a_dtype != BITLUT_DT_F16) return BITLUT_EPARAM;
-  if (mode != BITLUT_TABLE_Q8 && mode != BITLUT_TABLE_F16) return BITLUT_EPARAM;
+  if (mode != BITLUT_TABLE_Q8 && mode != BITLUT_TABLE_F16 && mode != BITLUT_TABLE_X16) return BITLUT_EPARAM;
   if (n < 0 || k < 0 || group_size < 4) return BITLUT_EPARAM;
   if (k % group_size != 0 || group_size % 4 != 0) return BITLUT_ELAYOUT;
   int gpg = group_size / 4;

@@ -50,7 +50,7 @@ __device__ __forceinline__ void lut_block(const AT* __restrict__ a, int k, int g
     e[idx] = __fsub_rn(x, v[3]);
   }
 
-  if (MODE == BITLUT_TABLE_Q8) {
+  if (MODE == BITLUT_TABLE_Q8 || MODE == BITLUT_TABLE_X16) {
     float mx = 0.f;
 #pragma unroll
     for (int idx = 0; idx < 8; idx++) mx = bl::fmax_nan(mx, fabsf(e[idx]));
@@ -64,6 +64,37 @@ __device__ __forceinline__ void lut_block(const AT* __restrict__ a, int k, int g
       mx = 0.f;
       for (int w = 0; w < wpg; w++) mx = bl::fmax_nan(mx, red[w0 + w]);
     }
+    if (MODE == BITLUT_TABLE_X16) {
+      // two balanced base-127 digits per entry (bitlut_b200.h BITLUT_TABLE_X16)
+      float scale = __fdiv_rn(mx, 16129.0f);
+      if (scale == 0.0f) scale = 1.0f;
+      uint32_t ph[2] = {0u, 0u}, pl[2] = {0u, 0u};
+#pragma unroll
+      for (int idx = 0; idx < 8; idx++) {
+        float s = __fdiv_rn(e[idx], scale);
+        float r = truncf(__fadd_rn(s, copysignf(0.5f, s)));
+        r = fminf(fmaxf(r, -16129.f), 16129.f);
+        const int q = (int)r;
+        const int h = (q + (q >= 0 ? 63 : -63)) / 127;      // nearest, ties cannot occur (127 odd)
+        const int lo = q - 127 * h;                          // [-63, 63]
+        ph[idx >> 2] |= ((uint32_t)h & 0xffu) << (8 * (idx & 3));
+        pl[idx >> 2] |= ((uint32_t)lo & 0xffu) << (8 * (idx & 3));
+      }
+      if (live) {
+        // both digit tables in the kernel's encoded form a = Q - (Q < 0), at
+        // the 16-byte-per-k-group offsets of the fp16 tables
+        uint4 o;
+        o.x = ph[0] - ((ph[0] >> 7) & 0x01010101u); o.y = ph[1] - ((ph[1] >> 7) & 0x01010101u);
+        o.z = pl[0] - ((pl[0] >> 7) & 0x01010101u); o.w = pl[1] - ((pl[1] >> 7) & 0x01010101u);
+        const int R = bl::unit_kg_for(gs), U = KG / R;
+        const int u = kg / R, r = kg - u * R, ub = u >> 5, l = u & 31;
+        const int nu_b = min(32, U - 32 * ub);
+        const int64_t off = (int64_t)ub * (32 * R * 16) + (int64_t)(r * nu_b + l) * 16;
+        BL_CHECK(off >= 0 && off + 16 <= (int64_t)KG * 16);
+        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(tables) + (int64_t)row * KG * 16 + off) = o;
+        if ((kg & (gpg - 1)) == 0) tscales[(int64_t)row * NQ + kg / gpg] = scale;
+      }
+    } else {
     float scale = __fdiv_rn(mx, 127.0f);
     if (scale == 0.0f) scale = 1.0f;
     uint32_t packed[2] = {0u, 0u};
@@ -87,6 +118,7 @@ __device__ __forceinline__ void lut_block(const AT* __restrict__ a, int k, int g
       *reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(tables) + (int64_t)row * KG * 8 + off) =
           make_uint2(e0, e1);
       if ((kg & (gpg - 1)) == 0) tscales[(int64_t)row * NQ + kg / gpg] = scale;
+    }
     }
   } else {
     // fp16 half table, kernel format: 8 low bytes then 8 high bytes of the

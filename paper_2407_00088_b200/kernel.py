@@ -272,7 +272,14 @@ def mpgemm(a, pw: PackedWeights, cfg: TileConfig | None = None,
     if host is not None:                       # numpy in, numpy out: one C call, one sync
         if host.shape[1] != pw.k:
             raise ShapeError(f"activation length {host.shape[1]} != weight k {pw.k}")
-        out = _host_call(host, pw, mode, flags)
+        # cuda-f16 fast at batch 1: 16-bit block-fixed-point tables (BITLUT_TABLE_X16)
+        x16 = mode == N.TABLE_F16 and not exact_epilogue and host.shape[0] == 1 and pw.bits != 3
+        try:
+            out = _host_call(host, pw, N.TABLE_X16 if x16 else mode, flags)
+        except LayoutError:
+            if not x16:
+                raise
+            out = _host_call(host, pw, mode, flags)
         if stats is not None:
             stats.lookups += pw.bits * host.shape[0] * pw.m * (pw.k // pw.g)
             stats.lut_builds += -(-host.shape[0] // cfg.n_tile) * (pw.k // cfg.k_tile)
@@ -290,6 +297,13 @@ def mpgemm(a, pw: PackedWeights, cfg: TileConfig | None = None,
             out = N.mpgemv_fused(rows, pw.gpu, pw.scales, pw.zeros, pw.m, pw.k, pw.bits,
                                  pw.group_size, flags)
             partials = None
+        except LayoutError:
+            out = None
+    if out is None and mode == N.TABLE_F16 and not exact_epilogue and n == 1 and pw.bits != 3:
+        try:      # cuda-f16 fast at batch 1: 16-bit block-fixed-point tables (BITLUT_TABLE_X16)
+            tables, ts, rs = N.build_lut(rows, pw.group_size, N.TABLE_X16, N.FLAG_PDL if pdl else 0)
+            out, partials = N.lookup(pw.gpu, pw.scales, pw.zeros, tables, ts, rs, pw.m, pw.k, pw.bits,
+                                     pw.group_size, N.TABLE_X16, flags, False)
         except LayoutError:
             out = None
     if out is None:

@@ -716,10 +716,12 @@ def test_long_k_cluster_kernel(bits, gs, m, zeros):
 
 
 def test_f16_fast_batch1_lean(config_golden):
-    """fp16 tables, batch 1, fast epilogue (the lean kernel's fp16 mode):
-    BASELINE config 1 within 1e-3 of the reference (scalar-real + zero
-    correction), equal to the reference-order fp16 path within 1e-5, and
-    deterministic; plus W2 / W1 shapes against the exact fp16 path."""
+    """Variant cuda-f16, batch 1, fast epilogue (16-bit block-fixed-point
+    tables, BITLUT_TABLE_X16, in the lean kernel): BASELINE config 1 within
+    1e-3 of the reference (scalar-real + zero correction) and no further from
+    it than the reference-order fp16-table path, which it matches within the
+    fp16 tables' own rounding (1e-3); deterministic; plus W2 / W1 / W4 shapes
+    against the fp16-table path."""
     inst = W.config1()
     g = config_golden[inst["name"]]
     _, pw = make_pw(inst)
@@ -728,7 +730,8 @@ def test_f16_fast_batch1_lean(config_golden):
     rs = O.row_sums(inst["a"].astype(np.float32), inst["group_size"])
     ref = (g["y_scalar-real"][0] + O.zero_correction(inst["scales"], inst["zeros"], 4, rs[0])).astype(np.float32)
     assert rel_maxnorm(yf, ref) <= 1e-3, rel_maxnorm(yf, ref)
-    assert rel_maxnorm(yf, ye) <= 1e-5, rel_maxnorm(yf, ye)
+    assert rel_maxnorm(yf, ref) <= rel_maxnorm(ye, ref) + 1e-5, (rel_maxnorm(yf, ref), rel_maxnorm(ye, ref))
+    assert rel_maxnorm(yf, ye) <= 1e-3, rel_maxnorm(yf, ye)
     assert np.array_equal(yf, B.mpgemm(inst["a"], pw, variant="cuda-f16", exact_epilogue=False)[0])
     gen = torch.Generator(device="cuda").manual_seed(16)
     for bits, gs, m, k in ((2, 64, 512, 4096), (1, 128, 1024, 4096), (4, 64, 256, 11008), (2, 32, 352, 2048)):
@@ -738,7 +741,13 @@ def test_f16_fast_batch1_lean(config_golden):
         x = torch.randn((1, k), device="cuda", generator=gen).half()
         a = B.mpgemm(x, pw2, variant="cuda-f16", exact_epilogue=False)
         b = B.mpgemm(x, pw2, variant="cuda-f16")
-        assert rel_maxnorm(a.cpu().numpy(), b.cpu().numpy()) <= 1e-5, (bits, gs, m, k)
+        assert rel_maxnorm(a.cpu().numpy(), b.cpu().numpy()) <= 1e-3, (bits, gs, m, k)
+        # against float64 arithmetic on the dequantized weights: closer than the fp16 tables
+        wd = (q.double() - float(1 << (bits - 1))) * sc.double().repeat_interleave(gs, dim=1)
+        ref64 = (wd @ x[0].double()).cpu().numpy()
+        ea = np.abs(a.cpu().numpy()[0] - ref64).max() / np.abs(ref64).max()
+        eb = np.abs(b.cpu().numpy()[0] - ref64).max() / np.abs(ref64).max()
+        assert ea <= 1e-3 and ea <= eb + 1e-5, (bits, gs, m, k, ea, eb)
 
 
 @pytest.mark.parametrize("bits,gs", [(2, 64), (4, 128), (1, 128)])
