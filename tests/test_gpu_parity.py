@@ -893,3 +893,49 @@ def test_layer_set_conversion(m, k, bits, gs):
             c = j ^ np.array([_perm_mask(int(x) & 31, tch) for x in uu])
             for tile in range(m // tch):
                 assert np.array_equal(s3[tile, :, j], scn[tile * tch + c, uu // Lg])
+
+
+@pytest.mark.parametrize("bits,gs", [(4, 256), (4, 512), (2, 512), (2, 256), (1, 512), (1, 64), (2, 32), (4, 32),
+                                     (2, 16), (4, 16), (1, 32)])
+@pytest.mark.parametrize("zeros", [False, True])
+def test_batch_executor_group_sizes(bits, gs, zeros):
+    """The batch executor over every lanes-per-group class of the layer-set
+    layout -- a group narrower than a lane's unit (R = 4), one to sixteen
+    lanes per group, and groups spanning more lanes than a lane has
+    accumulators (the per-unit scale vectors then repeat: 4-bit gs >= 256,
+    2-bit gs = 512) -- with fp16 and fp32 scales, with and without zero
+    points, K with a partial unit block: outputs == the per-call fast
+    lookups on the v2 operand, bitwise, and the exported integer sums equal
+    the exact kernel's staging values combined."""
+    from paper_2407_00088_b200.pipeline import Pipeline
+    g = torch.Generator(device="cuda").manual_seed(bits * 1000 + gs + int(zeros))
+    k = 1536 if gs <= 512 and 1536 % gs == 0 else 2048
+    shapes = [(96, k), (32, k), (256, 2 * k)]
+    items = []
+    for i, (m, kk) in enumerate(shapes):
+        q = torch.randint(0, 1 << bits, (m, kk), dtype=torch.uint8, device="cuda", generator=g)
+        sdt = torch.float16 if i != 1 else torch.float32
+        sc = (torch.randn((m, kk // gs), device="cuda", generator=g).abs() * 0.02 + 1e-3).to(sdt)
+        z = (torch.rand((m, kk // gs), device="cuda", generator=g) * ((1 << bits) - 1)).to(sdt) if zeros else None
+        pw = B.prepare_weights(B.QuantizedWeights(m=m, k=kk, bits=bits, group_size=gs, qvalues=q, scales=sc, zeros=z))
+        items.append((pw, torch.randn((1, kk), device="cuda", generator=g).half()))
+    # scale dtypes differ -> separate launches; run each dtype group as its own pipeline
+    for grp in ([items[0], items[2]], [items[1]]):
+        pl = Pipeline(executor="batch")
+        outs, parts = [], []
+        for pw, x in grp:
+            t = pl.tables(x, gs)
+            p = torch.full((pw.m, pw.k // gs), -(1 << 30), dtype=torch.int32, device="cuda")
+            outs.append(pl.lookup(pw, t, fast_epilogue=True, partials=p))
+            parts.append(p)
+        for o in outs:
+            o.fill_(float("nan"))
+        pl.compile()
+        pl.run()
+        torch.cuda.synchronize()
+        for (pw, x), o, p in zip(grp, outs, parts):
+            ref = B.mpgemm(x, pw, exact_epilogue=False)
+            assert torch.equal(o.reshape(ref.shape), ref), (pw.m, pw.k)
+            _, P = B.mpgemm(x, pw, return_partials=True)
+            want = sum((1 << b) * P[0, b].to(torch.int64) for b in range(bits))
+            assert torch.equal(p.to(torch.int64), want), (pw.m, pw.k)
