@@ -776,14 +776,15 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
       const int t = tile + S * step;
       if (t < ntl) issue_stage<ST>(a, t, sb, bar + stage, policy_evict_first());
     }
-    if (tid < TCH) {
-      const float* yr = ysm + (it & 1) * NW * TCH + tid;
+    if (tid >= 32 && tid < 32 + TCH) {                  // warp 1 adds the sums (thread 0 refills: gemv_batch.cu)
+      const int c = tid - 32;
+      const float* yr = ysm + (it & 1) * NW * TCH + c;
       float s = 0.f;
       for (int w = 0; w < NW; w++) s += yr[w * TCH];
       int local;
       const int j = find_mat(a, tile, local);
-      BL_CHECK(j < a.n_mats && local >= 0 && local * TCH + tid < (a.mats[j].tile_end - (j ? a.mats[j - 1].tile_end : 0)) * TCH);
-      a.mats[j].out[(int64_t)local * TCH + tid] = 0.5f * s;
+      BL_CHECK(j < a.n_mats && local >= 0 && local * TCH + c < (a.mats[j].tile_end - (j ? a.mats[j - 1].tile_end : 0)) * TCH);
+      a.mats[j].out[(int64_t)local * TCH + c] = 0.5f * s;
     }
   }
   bl::dep_signal(p.dep);

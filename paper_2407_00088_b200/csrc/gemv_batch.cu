@@ -47,6 +47,19 @@ using namespace blk;
 
 constexpr int kStagesMax = 2;
 constexpr int kYBufs = 2;             // cross-warp sum buffers (power of two)
+// Per-tile duties after the CTA barrier: thread kRefillThread refills the
+// consumed stage, warp kSumWarp adds the cross-warp sums.  On different warps
+// neither delays the other's arrival at the next barrier (same-box A/B over
+// thread 0/32/64 x warp 0/1/2: refill on warp 0, sums on warp 1 is +1.1..1.5 %
+// on the W2 / W1 / ternary layer sets; macros for further A/Bs).
+#ifndef BITLUT_REFILL_THREAD
+#define BITLUT_REFILL_THREAD 0
+#endif
+constexpr int kRefillThread = BITLUT_REFILL_THREAD;   // (a thread's own issue cursor: advance() catches up)
+#ifndef BITLUT_SUM_WARP
+#define BITLUT_SUM_WARP 1
+#endif
+constexpr int kSumWarp = BITLUT_SUM_WARP;
 
 struct BatchArgs {
   bl::LayoutV2 L;             // the launch's k, bits, group size (m unused)
@@ -248,7 +261,7 @@ __global__ void __launch_bounds__(384) gemv_batch_kernel(const __grid_constant__
     static_assert(NF == 1, "one channel sum per lane");
     ysm[(it & (kYBufs - 1)) * NW * TCH + warp * TCH + cmask] = y[0];
     __syncthreads();                                    // stage consumed, ysm complete
-    if (tid == 0) {                                     // refill the consumed stage
+    if (tid == kRefillThread) {                         // refill the consumed stage
       const int t = tile + S;
       if (t < t1) {
         advance(dm, n_mats, t, ji, ji_begin, ji_end);
@@ -256,11 +269,12 @@ __global__ void __launch_bounds__(384) gemv_batch_kernel(const __grid_constant__
         issue_tile<ST, MODE>(a, dm[ji], t - ji_begin, sb, bar + stage, policy_evict_first());
       }
     }
-    if (tid < TCH) {                                    // fixed warp order: deterministic
-      const float* yr = ysm + (it & (kYBufs - 1)) * NW * TCH + tid;
+    if (tid >= kSumWarp * 32 && tid < kSumWarp * 32 + TCH) {   // fixed warp order: deterministic
+      const int c = tid - kSumWarp * 32;
+      const float* yr = ysm + (it & (kYBufs - 1)) * NW * TCH + c;
       float s = 0.f;
       for (int w = 0; w < NW; w++) s += yr[w * TCH];
-      outp[(int64_t)local * TCH + tid] = fin * s;
+      outp[(int64_t)local * TCH + c] = fin * s;
     }
   }
   if (a.independent) bl::pdl_wait();

@@ -20,12 +20,17 @@ os.makedirs(outdir, exist_ok=True)
 flags = [f for f in B.NVCC_FLAGS if f not in ("-shared", "-Xptxas", "-v")]
 VARIANT_TUS = ["gemv_batch.cu"]
 for n in sys.argv[1:]:
+    # n = "<name>" or "<name>:-DX=1,-DY=2" (extra defines for the variant TUs)
+    extra = []
+    if ":" in n:
+        n, defs = n.split(":", 1)
+        extra = defs.split(",")
     objs = []
     for src in B.SOURCES:
         if src in VARIANT_TUS:
             o = os.path.join(outdir, f"{src[:-3]}_ab{n}.o")
-            subprocess.run([B.nvcc(), *flags, f"-DBITLUT_AB={n}", "-c", "-o", o, os.path.join(B.PKG, "csrc", src)],
-                           check=True)
+            subprocess.run([B.nvcc(), *flags, *(extra or [f"-DBITLUT_AB={n}"]), "-c", "-o", o,
+                            os.path.join(B.PKG, "csrc", src)], check=True)
             objs.append(o)
         else:
             objs.append(os.path.join(objdir, src.replace(".cu", ".o")))
