@@ -73,22 +73,33 @@ __host__ __device__ inline uint32_t al16(size_t x) { return (uint32_t)((x + 15) 
 
 
 
+// The issuing thread keeps the current matrix's operand pointers in registers
+// (reloaded at a matrix change only): the per-tile refill, which sits between
+// the CTA barrier and the thread's own lookups, reads no descriptor memory.
+struct IssuePtrs {
+  const uint8_t* w;
+  const uint8_t* s;
+  const uint8_t* z;
+};
+__device__ __forceinline__ IssuePtrs issue_ptrs(const bitlut_batch_mat& mt) {
+  return {mt.wgpu, reinterpret_cast<const uint8_t*>(mt.wscales), reinterpret_cast<const uint8_t*>(mt.zeros)};
+}
+
 template <typename ST, int MODE>
-__device__ __forceinline__ void issue_tile(const BatchArgs& a, const bitlut_batch_mat& mt, int local, uint8_t* sb,
+__device__ __forceinline__ void issue_tile(const BatchArgs& a, const IssuePtrs& mt, int local, uint8_t* sb,
                                            uint64_t* bar, uint64_t pol) {
   const bl::LayoutV2& L = a.L;
   const uint32_t s_bytes = MODE == BITLUT_W_TERNARY ? 0u : a.s_bytes;
   mbar_expect_tx(bar, a.w_bytes + s_bytes * (MODE == BITLUT_W_ZEROS ? 2u : 1u));
-  const uint8_t* src = mt.wgpu + (int64_t)local * L.KG * 16;
+  const uint8_t* src = mt.w + (int64_t)local * L.KG * 16;
   for (uint32_t off = 0; off < a.w_bytes; off += 32768u) {
     const uint32_t nb = a.w_bytes - off < 32768u ? a.w_bytes - off : 32768u;
     bulk_g2s(sb + off, src + off, nb, bar, pol);
   }
   if constexpr (MODE != BITLUT_W_TERNARY) {
     const int64_t b0 = (int64_t)local * s_bytes;        // layer-set layout: s_bytes per tile
-    bulk_g2s(sb + a.s_off, reinterpret_cast<const uint8_t*>(mt.wscales) + b0, s_bytes, bar, pol);
-    if constexpr (MODE == BITLUT_W_ZEROS)
-      bulk_g2s(sb + a.z_off, reinterpret_cast<const uint8_t*>(mt.zeros) + b0, s_bytes, bar, pol);
+    bulk_g2s(sb + a.s_off, mt.s + b0, s_bytes, bar, pol);
+    if constexpr (MODE == BITLUT_W_ZEROS) bulk_g2s(sb + a.z_off, mt.z + b0, s_bytes, bar, pol);
   }
 }
 
@@ -138,19 +149,26 @@ __global__ void __launch_bounds__(384) gemv_batch_kernel(const __grid_constant__
   int jc = j0, jc_begin = j0 ? dm[j0 - 1].tile_end : 0, jc_end = dm[j0].tile_end;
   // issue cursor (thread 0): the matrix of the next tile to stage
   int ji = jc, ji_begin = jc_begin, ji_end = jc_end;
+  IssuePtrs ip = {nullptr, nullptr, nullptr};
+  if (tid == kRefillThread) ip = issue_ptrs(dm[ji]);
   if (tid == 0) {
     for (int s = 0; s < kStagesMax; s++) {
       mbar_init(bar + s, 1);                            // the stage's TMA bytes landed
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     const uint64_t pol = policy_evict_first();
+    static_assert(kRefillThread == 0, "the initial stages are issued by the refill thread");
     for (int s = 0; s < S; s++) {
       const int t = t0 + s;
       if (t >= t1) break;
-      advance(dm, n_mats, t, ji, ji_begin, ji_end);
-      issue_tile<ST, MODE>(a, dm[ji], t - ji_begin, smem + s * a.stage_bytes, bar + s, pol);
+      if (t >= ji_end) {
+        advance(dm, n_mats, t, ji, ji_begin, ji_end);
+        ip = issue_ptrs(dm[ji]);
+      }
+      issue_tile<ST, MODE>(a, ip, t - ji_begin, smem + s * a.stage_bytes, bar + s, pol);
     }
   }
+  const uint64_t pol = policy_evict_first();
   if (!a.independent) bl::pdl_wait();
   bl::pdl_launch_dependents();
   // thread u looks up unit u; a thread past the last unit (U is not a
@@ -264,9 +282,11 @@ __global__ void __launch_bounds__(384) gemv_batch_kernel(const __grid_constant__
     if (tid == kRefillThread) {                         // refill the consumed stage
       const int t = tile + S;
       if (t < t1) {
-        advance(dm, n_mats, t, ji, ji_begin, ji_end);
-        // the warps' generic writes (smem lane reduction) before the async-proxy refill
-        issue_tile<ST, MODE>(a, dm[ji], t - ji_begin, sb, bar + stage, policy_evict_first());
+        if (t >= ji_end) {
+          advance(dm, n_mats, t, ji, ji_begin, ji_end);
+          ip = issue_ptrs(dm[ji]);
+        }
+        issue_tile<ST, MODE>(a, ip, t - ji_begin, sb, bar + stage, pol);
       }
     }
     if (tid >= kSumWarp * 32 && tid < kSumWarp * 32 + TCH) {   // fixed warp order: deterministic
