@@ -917,13 +917,13 @@ __global__ void __launch_bounds__(384) gemv_b1_rows_lean_kernel(const __grid_con
     finish_row(accA, tsA, rsA, ybase);
     if (two) finish_row(accB, tsB, rsB, ybase + NW * TCH);
     __syncthreads();                                    // this pair's partials complete
-    if (tid < TCH) {
-      const int nr = two ? 2 : 1;
-      for (int r = 0; r < nr; r++) {
-        const float* yr = ybase + r * NW * TCH + tid;
+    if (tid >= 32 && tid < 32 + 2 * TCH) {              // warps 1.. add the sums: one thread per (row, channel)
+      const int r = (tid - 32) / TCH, c = (tid - 32) - r * TCH;
+      if (r == 0 || two) {
+        const float* yr = ybase + r * NW * TCH + c;
         float sum = 0.f;
         for (int w = 0; w < NW; w++) sum += yr[w * TCH];
-        outp[(int64_t)(row + r) * L.m + tid] = 0.5f * sum;
+        outp[(int64_t)(row + r) * L.m + c] = 0.5f * sum;
       }
     }
   }
