@@ -231,6 +231,21 @@ def build_pipeline(layers, acts, fast=False, executor="graph", chain=True, sync=
     return pl, outs, out_arena
 
 
+def fast_operand(pw, tabs, n_rows=1):
+    """(weights, scales, zeros, extra flag) for fast-epilogue int8-table
+    lookups: the layer-set operand (BITLUT_FLAG_LAYER_SET: select-free lean
+    kernels) where those kernels take the call, else the v2 operand."""
+    from paper_2407_00088_b200 import _native as N
+    from paper_2407_00088_b200.errors import LayoutError
+    try:
+        lw, lsc, lz = pw.layer_set_operand()
+        N.lookup(lw, lsc, lz, *tabs, pw.m, pw.k, pw.bits, pw.group_size, N.TABLE_Q8,
+                 N.FLAG_PDL | N.FLAG_FAST_EPILOGUE | N.FLAG_LAYER_SET, False)
+        return lw, lsc, lz, N.FLAG_LAYER_SET
+    except LayoutError:
+        return pw.gpu, pw.scales, pw.zeros, 0
+
+
 def capture(fn, stream):
     import torch
     g = torch.cuda.CUDAGraph()
@@ -305,10 +320,17 @@ def per_shape_table(device, stream, reps, warmup, barrier, peak, world, bits_lis
             for epi in ("fast", "exact"):
                 e = {}
                 base = N.FLAG_PDL | (N.FLAG_FAST_EPILOGUE if epi == "fast" else 0)
+                wsel, scl = ws, pw.scales
+                if epi == "fast":                      # the layer-set operand where the lean kernel takes it
+                    lw, scl, _, lsf = fast_operand(pw, tabs)
+                    if lsf:
+                        wsel = [lw] + [lw.clone() for _ in range(copies - 1)]
+                        base |= lsf
+                    e["operand"] = "layer-set" if lsf else "v2"
                 for mode, fl in (("overlapped", base | N.FLAG_INDEPENDENT), ("chained", base)):
-                    def body(fl=fl):
-                        for w in ws:
-                            N.lookup(w, pw.scales, None, *tabs, pw.m, k, bits, gs, N.TABLE_Q8, fl, False)
+                    def body(fl=fl, wsel=wsel, scl=scl):
+                        for w in wsel:
+                            N.lookup(w, scl, None, *tabs, pw.m, k, bits, gs, N.TABLE_Q8, fl, False)
                     g = capture(body, stream)
                     with torch.cuda.stream(stream):
                         ms = time_graph(g, reps, warmup, barrier)
@@ -325,12 +347,13 @@ def per_shape_table(device, stream, reps, warmup, barrier, peak, world, bits_lis
                         flush_sum.copy_(flush.sum(dtype=torch.int64))
                         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                         e0.record(stream)
-                        N.lookup(ws[0], pw.scales, None, *tabs, pw.m, k, bits, gs, N.TABLE_Q8, base, False)
+                        N.lookup(wsel[0], scl, None, *tabs, pw.m, k, bits, gs, N.TABLE_Q8, base, False)
                         e1.record(stream)
                         torch.cuda.synchronize()
                         ts_.append(e0.elapsed_time(e1) * 1e3)
                 e["single_launch_l2_flushed_us"] = round(float(np.median(ts_)), 3)
                 entry[epi] = e
+                del wsel
             res[name] = entry
             del ws, pw
         out[f"W{bits}"] = res
@@ -540,10 +563,14 @@ def gemm_table(device, stream, reps, warmup, barrier, world):
                 a = torch.randn((n, k), device=device, generator=gen).half()
                 for epi in ("exact", "fast"):
                     fl = N.FLAG_PDL | (N.FLAG_FAST_EPILOGUE if epi == "fast" else 0)
+                    wsel, scl = pw.gpu, pw.scales
+                    if epi == "fast":                  # the layer-set operand where the rows kernel takes it
+                        wsel, scl, _, lsf = fast_operand(pw, N.build_lut(a, 128, N.TABLE_Q8))
+                        fl |= lsf
 
-                    def body():
+                    def body(fl=fl, wsel=wsel, scl=scl):
                         t = N.build_lut(a, 128, N.TABLE_Q8, N.FLAG_PDL)
-                        N.lookup(pw.gpu, pw.scales, None, *t, m_loc, k, bits, 128, N.TABLE_Q8, fl, False)
+                        N.lookup(wsel, scl, None, *t, m_loc, k, bits, 128, N.TABLE_Q8, fl, False)
                     g = capture(body, stream)
                     with torch.cuda.stream(stream):
                         ms = time_graph(g, reps, warmup, barrier)

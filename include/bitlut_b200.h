@@ -75,6 +75,14 @@ extern "C" {
  * integer combination S[m][gq] = sum_p 2^p P_p (shape (1, m, k/gs)) that the
  * fast kernel scales -- SURVEY §8(c)'s bit-exactness object. */
 #define BITLUT_FLAG_COMBINED_PARTIALS 32
+/* bitlut_mpgemm: wgpu / wscales / zeros are in the LAYER-SET layout
+ * (bitlut_layer_set_weights / _scales) instead of layout v2.  Fast epilogue,
+ * int8 tables; served by the lean batch-1 and mpGEMM rows kernels with
+ * select-free lane reductions (outputs bitwise those of the v2 operand);
+ * BITLUT_ELAYOUT where those kernels do not apply (exact epilogue, long K,
+ * zero points at N >= 8, groups wider than a lane's accumulators) -- pass
+ * the v2 operand then. */
+#define BITLUT_FLAG_LAYER_SET 64
 
 /*
  * GPU weight layout ("layout v2", this library's own; the reference's v1

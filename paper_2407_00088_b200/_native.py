@@ -29,6 +29,7 @@ FLAG_FAST_EPILOGUE = 4
 FLAG_FUSED_TABLES = 8       # table op may fold into its consumers (graph executor)
 PLAN_JOINED = 16            # plan: launched together with the previous op
 FLAG_COMBINED_PARTIALS = 32
+FLAG_LAYER_SET = 64         # lookup operand in the layer-set layout (lean kernels)
 
 _vp, _i = ctypes.c_void_p, ctypes.c_int
 

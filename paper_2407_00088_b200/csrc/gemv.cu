@@ -266,6 +266,13 @@ int bl_mpgemm_launch(const uint8_t* wgpu, int m, int k, int bits, int group_size
   }
   const bool combined = (flags & BITLUT_FLAG_COMBINED_PARTIALS) != 0;
   if (combined && (!a.fast || mode != BITLUT_TABLE_Q8 || L.n_sg != 1 || trace)) return BITLUT_EPARAM;
+  if (flags & BITLUT_FLAG_LAYER_SET) {
+    // operand in the layer-set layout: fast epilogue, int8 tables, the lean
+    // batch-1 / rows kernels only (else the caller passes the v2 operand)
+    if (!(mode == BITLUT_TABLE_Q8 && a.fast && !partials && !trace && L.n_sg == 1)) return BITLUT_ELAYOUT;
+    a.layer_set = 1;
+    return bl_gemv_b1_launch(a, scale_dtype, (cudaStream_t)stream, pdl);
+  }
   if (mode == BITLUT_TABLE_X16) {
     // 16-bit block-fixed-point tables: the lean batch-1 kernel only (the
     // caller uses BITLUT_TABLE_F16 for everything else)

@@ -575,7 +575,9 @@ __global__ void __launch_bounds__(384) gemv_b1_kernel(const __grid_constant__ B1
 // scale (scalar-real semantics _kernels.py:101-137 within the fp16-table
 // tolerance, tested).  Round 1's fp16 byte-plane lookups (5 PRMT + sign fix
 // per 4 lookups, fp32 adds) ran at 0.49 of the HBM peak.
-template <int R, int LG, int BITS, typename ST, bool ZEROS, bool F16 = false>
+// PERM: the operand is in the layer-set layout (layout.cuh; BITLUT_FLAG_LAYER_SET):
+// select-free lane reductions and one scale vector per lane, like gemv_batch_kernel.
+template <int R, int LG, int BITS, typename ST, bool ZEROS, bool F16 = false, bool PERM = false>
 __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant__ B1Args a) {
   const GemvArgs& p = a.g;
   const bl::LayoutV2& L = p.L;
@@ -735,8 +737,13 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
         }
       }
     }
-    const int base = reduce_lanes<NACC, 1, LG>(acc, lane);
-    ch0 = BITS == 1 ? 2 * base : base;
+    if constexpr (PERM) {
+      reduce_lanes_perm<NACC, 1, LG>(acc);
+      ch0 = 0;
+    } else {
+      const int base = reduce_lanes<NACC, 1, LG>(acc, lane);
+      ch0 = BITS == 1 ? 2 * base : base;
+    }
     {
       int Sv[NCH];
       if constexpr (BITS == 1) {
@@ -751,6 +758,25 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
 #pragma unroll
         for (int i = 0; i < NV; i++) Sv[i] = acc[i];
       }
+      if constexpr (PERM) {
+        // the unit's NCH scales (zero points) are one vector; __fmul_rn keeps the
+        // products out of the reduction's first add (bitwise == the v2 path)
+        constexpr int SB = NCH * (int)sizeof(ST);
+        uint32_t sv[(SB + 3) / 4];
+        lds_vec<SB>(sb + a.s_off + (uint32_t)u * SB, sv);
+        if constexpr (ZEROS) {
+          uint32_t zv[(SB + 3) / 4];
+          lds_vec<SB>(sb + a.z_off + (uint32_t)u * SB, zv);
+          const float h2 = (float)(2 << (BITS - 1));
+#pragma unroll
+          for (int j = 0; j < NCH; j++)
+            y[j] = __fmul_rn(vec_elem<ST>(sv, j),
+                             fmaf(fmaf(-2.f, vec_elem<ST>(zv, j), h2), rs, fmaf(ts, (float)Sv[j], -rs)));
+        } else {
+#pragma unroll
+          for (int j = 0; j < NCH; j++) y[j] = __fmul_rn(vec_elem<ST>(sv, j), fmaf(ts, (float)Sv[j], -rs));
+        }
+      } else {
       const ST* sp = reinterpret_cast<const ST*>(sb + a.s_off) + ch0 * NQ + g;
       if constexpr (ZEROS) {
         // asymmetric zero points: + 2 (2^(b-1) - z) rs per (channel, group)
@@ -765,12 +791,18 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
 #pragma unroll
         for (int j = 0; j < NCH; j++) y[j] = bl::to_f32(sp[j * NQ]) * fmaf(ts, (float)Sv[j], -rs);
       }
+      }
     }
     }
-    const int fb = reduce_lanes<NCH, LG, 32>(y, lane);
     float* yb = ysm + (it & 1) * NW * TCH + warp * TCH;
+    if constexpr (PERM && !F16) {
+      reduce_lanes_perm<NCH, LG, 32>(y);
+      yb[perm_mask<TCH>(lane)] = y[0];
+    } else {
+      const int fb = reduce_lanes<NCH, LG, 32>(y, lane);
 #pragma unroll
-    for (int j = 0; j < NF; j++) yb[ch0 + fb + j] = y[j];
+      for (int j = 0; j < NF; j++) yb[ch0 + fb + j] = y[j];
+    }
     __syncthreads();                                    // stage consumed, ysm complete
     if (tid == 0) {
       const int t = tile + S * step;
@@ -799,7 +831,7 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
 // shared (lookup_kg_merged2); one barrier per pair publishes the cross-warp
 // partial sums (double-buffered).
 // Bitwise equal to gemv_b1_kernel<kFastRows>.
-template <int R, int LG, int BITS, typename ST>
+template <int R, int LG, int BITS, typename ST, bool PERM = false>
 __global__ void __launch_bounds__(384) gemv_b1_rows_lean_kernel(const __grid_constant__ B1Args a) {
   const GemvArgs& p = a.g;
   const bl::LayoutV2& L = p.L;
@@ -851,7 +883,13 @@ __global__ void __launch_bounds__(384) gemv_b1_rows_lean_kernel(const __grid_con
   const int stride = nu_b * 16;
   // the lane's NCH weight scales are the same for every row: converted once
   float wsf[NCH];
-  {
+  if constexpr (PERM) {                                 // layer-set operand: the unit's scale vector
+    constexpr int SB = NCH * (int)sizeof(ST);
+    uint32_t sv[(SB + 3) / 4];
+    lds_vec<SB>(smem + a.s_off + (uint32_t)(live ? u : U - 1) * SB, sv);
+#pragma unroll
+    for (int j = 0; j < NCH; j++) wsf[j] = live ? vec_elem<ST>(sv, j) : 0.f;
+  } else {
     const int b0 = lane_base<NACC, 1, LG>(lane);
     const ST* sp = reinterpret_cast<const ST*>(smem + a.s_off) + (BITS == 1 ? 2 * b0 : b0) * NQ + g;
 #pragma unroll
@@ -859,8 +897,13 @@ __global__ void __launch_bounds__(384) gemv_b1_rows_lean_kernel(const __grid_con
   }
   // one row's sums: group reduction, scaling, reduction over the warp's groups -> ysm
   auto finish_row = [&](int (&acc)[NACC], float ts, float rs, float* ybuf) {
-    const int base = reduce_lanes<NACC, 1, LG>(acc, lane);
-    const int ch0 = BITS == 1 ? 2 * base : base;
+    int ch0 = 0;
+    if constexpr (PERM) {
+      reduce_lanes_perm<NACC, 1, LG>(acc);
+    } else {
+      const int base = reduce_lanes<NACC, 1, LG>(acc, lane);
+      ch0 = BITS == 1 ? 2 * base : base;
+    }
     float y[NCH];
     if (live) {
       int Sv[NCH];
@@ -877,15 +920,20 @@ __global__ void __launch_bounds__(384) gemv_b1_rows_lean_kernel(const __grid_con
         for (int i = 0; i < NV; i++) Sv[i] = acc[i];
       }
 #pragma unroll
-      for (int j = 0; j < NCH; j++) y[j] = wsf[j] * fmaf(ts, (float)Sv[j], -rs);
+      for (int j = 0; j < NCH; j++) y[j] = __fmul_rn(wsf[j], fmaf(ts, (float)Sv[j], -rs));
     } else {
 #pragma unroll
       for (int j = 0; j < NCH; j++) y[j] = 0.f;
     }
-    const int fb = reduce_lanes<NCH, LG, 32>(y, lane);
     float* yb = ybuf + warp * TCH;
+    if constexpr (PERM) {
+      reduce_lanes_perm<NCH, LG, 32>(y);
+      yb[perm_mask<TCH>(lane)] = y[0];
+    } else {
+      const int fb = reduce_lanes<NCH, LG, 32>(y, lane);
 #pragma unroll
-    for (int j = 0; j < NF; j++) yb[ch0 + fb + j] = y[j];
+      for (int j = 0; j < NF; j++) yb[ch0 + fb + j] = y[j];
+    }
   };
   for (int row = row0, it = 0; row < row1; row += 2, it++) {
     const bool two = row + 1 < row1;                    // uniform over the CTA
@@ -1253,7 +1301,7 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
     // its shards): 4096x28672 W2 8.3 vs 11.0 us, 2048x28672 4.7 vs 5.9 us;
     // at K = 11008 the unsplit lean kernel is faster (2.6 vs 3.8 us)
     if (cl_env != 0 && (size_t)L.KG * 16 > 65536 && L.U > 256 && !g.partials && !g.gather && !g.trace &&
-        g.n_rows <= 1 && !g.f16_tables) {
+        g.n_rows <= 1 && !g.f16_tables && !g.layer_set) {
       bool handled = false;
       const int rc = launch_b1_cluster<R, LG, BITS, ST>(g, mats, n_mats, stream, pdl, &handled);
       if (handled || rc != BITLUT_OK) return rc;
@@ -1301,13 +1349,23 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
   const bool lean_rows = KIND == kFastRows && lean_common && n_mats == 1 && !has_z && !g.f16_tables;
   if (g.f16_tables && !lean) return BITLUT_ELAYOUT;     // X16 tables: the lean kernel only
   const bool f16 = g.f16_tables != 0;
+  // layer-set operand: the lean kernels only, and only where the per-unit scale
+  // vectors are a permutation of the (channel, group) block (same stage plan)
+  const bool perm = g.layer_set != 0;
+  if (perm && (f16 || !(lean || lean_rows) ||
+               bl::layer_set_scale_bytes(L, (int)sizeof(ST)) != (int64_t)L.tile_ch * L.NQ * (int64_t)sizeof(ST)))
+    return BITLUT_ELAYOUT;
   auto kern = lean ? (f16 ? (has_z ? gemv_b1_lean_kernel<R, LG, BITS, ST, true, true>
                                    : gemv_b1_lean_kernel<R, LG, BITS, ST, false, true>)
-                          : (has_z ? gemv_b1_lean_kernel<R, LG, BITS, ST, true>
-                                   : gemv_b1_lean_kernel<R, LG, BITS, ST, false>))
-                   : (lean_rows ? gemv_b1_rows_lean_kernel<R, LG, BITS, ST> : gemv_b1_kernel<R, LG, BITS, ST, KIND>);
-  static bool configured_k[64][7] = {};                // per device and kernel variant
-  const int ki = lean ? (has_z ? 2 : 1) + (f16 ? 3 : 0) : (lean_rows ? 6 : 0);
+                          : (perm ? (has_z ? gemv_b1_lean_kernel<R, LG, BITS, ST, true, false, true>
+                                           : gemv_b1_lean_kernel<R, LG, BITS, ST, false, false, true>)
+                                  : (has_z ? gemv_b1_lean_kernel<R, LG, BITS, ST, true>
+                                           : gemv_b1_lean_kernel<R, LG, BITS, ST, false>)))
+                   : (lean_rows ? (perm ? gemv_b1_rows_lean_kernel<R, LG, BITS, ST, true>
+                                        : gemv_b1_rows_lean_kernel<R, LG, BITS, ST, false>)
+                                : gemv_b1_kernel<R, LG, BITS, ST, KIND>);
+  static bool configured_k[64][12] = {};               // per device and kernel variant
+  const int ki = (lean ? (has_z ? 2 : 1) + (f16 ? 3 : 0) : (lean_rows ? 6 : 0)) + (perm ? 7 : 0) - (perm && lean_rows ? 2 : 0);
   bool& configured = configured_k[bl_device()][ki];
   if (!configured) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||

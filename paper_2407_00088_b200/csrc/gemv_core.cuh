@@ -50,6 +50,7 @@ struct GemvArgs {
   int* grid_out;             // host: receives the launch's CTA count (op-list executor), or null
   int f16_tables;            // BITLUT_TABLE_F16 (batch-1 fast lean kernel only; 0 = int8 tables)
   int mixed_tables;          // matrices carry their own tables (bitlut_mpgemv_multi_tab): lean kernel only
+  int layer_set;             // BITLUT_FLAG_LAYER_SET: operand in the layer-set layout (lean / rows-lean kernels only)
   const GatherArgs* gather;  // host side: fused all-gather epilogue (batch-1 fast kernel), or null
 };
 

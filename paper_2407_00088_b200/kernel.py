@@ -308,6 +308,15 @@ def mpgemm(a, pw: PackedWeights, cfg: TileConfig | None = None,
             out = None
     if out is None:
         tables, ts, rs = N.build_lut(rows, pw.group_size, mode, N.FLAG_PDL if pdl else 0)
+        ls = pw.__dict__.get("_layer_set")        # set by pw.layer_set_operand() (opt-in, second copy)
+        if (ls is not None and mode == N.TABLE_Q8 and not exact_epilogue and not return_partials
+                and pw.encoding in ("offset", "zeros")):   # (sign / ternary: their layer-set scales are the native ones)
+            try:      # the layer-set operand in the lean kernels (select-free reductions): same bits
+                out, partials = N.lookup(ls[0], ls[1], ls[2], tables, ts, rs,
+                                         pw.m, pw.k, pw.bits, pw.group_size, mode, flags | N.FLAG_LAYER_SET, False)
+            except LayoutError:
+                out = None
+    if out is None:
         out, partials = N.lookup(pw.gpu, pw.scales, pw.zeros, tables, ts, rs, pw.m, pw.k, pw.bits,
                                  pw.group_size, mode, flags, return_partials)
     if stats is not None:

@@ -939,3 +939,38 @@ def test_batch_executor_group_sizes(bits, gs, zeros):
             _, P = B.mpgemm(x, pw, return_partials=True)
             want = sum((1 << b) * P[0, b].to(torch.int64) for b in range(bits))
             assert torch.equal(p.to(torch.int64), want), (pw.m, pw.k)
+
+
+@pytest.mark.parametrize("bits,gs,k", [(2, 64, 4096), (1, 128, 4096), (4, 128, 2048), (2, 64, 11008), (4, 32, 1536),
+                                       (2, 16, 1024)])
+def test_lookup_layer_set_operand(bits, gs, k):
+    """bitlut_mpgemm with BITLUT_FLAG_LAYER_SET (the layer-set operand in the
+    lean batch-1 and mpGEMM rows kernels: select-free reductions, scale
+    vectors): outputs bitwise those of the v2 operand at batch 1 (with and
+    without zero points) and over row blocks with an odd tail; BITLUT_ELAYOUT
+    where those kernels do not apply."""
+    from paper_2407_00088_b200 import _native as N
+    g = torch.Generator(device="cuda").manual_seed(bits * 31 + gs + k)
+    m = 416
+    q = torch.randint(0, 1 << bits, (m, k), dtype=torch.uint8, device="cuda", generator=g)
+    sc = (torch.randn((m, k // gs), device="cuda", generator=g).abs() * 0.02 + 1e-3).half()
+    z = (torch.rand((m, k // gs), device="cuda", generator=g) * ((1 << bits) - 1)).half()
+    F = N.FLAG_PDL | N.FLAG_FAST_EPILOGUE
+    for zeros in (None, z):
+        pw = B.prepare_weights(B.QuantizedWeights(m=m, k=k, bits=bits, group_size=gs, qvalues=q, scales=sc,
+                                                  zeros=zeros))
+        lw, lsc, lz = pw.layer_set_operand()
+        for n in ((1, 9, 16) if zeros is None else (1,)):
+            x = torch.randn((n, k), device="cuda", generator=g).half()
+            tabs = N.build_lut(x, gs, N.TABLE_Q8)
+            ref, _ = N.lookup(pw.gpu, pw.scales, pw.zeros, *tabs, m, k, bits, gs, N.TABLE_Q8, F, False)
+            out, _ = N.lookup(lw, lsc, lz, *tabs, m, k, bits, gs, N.TABLE_Q8, F | N.FLAG_LAYER_SET, False)
+            assert torch.equal(out, ref), (zeros is not None, n)
+    with pytest.raises(B.LayoutError):       # exact epilogue: v2 operand only
+        N.lookup(lw, lsc, lz, *tabs, m, k, bits, gs, N.TABLE_Q8, N.FLAG_PDL | N.FLAG_LAYER_SET, False)
+    # mpgemm picks the cached layer-set operand for fast multi-row calls: same bits as without it
+    pw0 = B.prepare_weights(B.QuantizedWeights(m=m, k=k, bits=bits, group_size=gs, qvalues=q, scales=sc))
+    x = torch.randn((12, k), device="cuda", generator=g).half()
+    ref = B.mpgemm(x, pw0, exact_epilogue=False)
+    pw0.layer_set_operand()
+    assert torch.equal(B.mpgemm(x, pw0, exact_epilogue=False), ref)

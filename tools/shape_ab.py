@@ -19,6 +19,7 @@ ap.add_argument("--gs", type=int, default=64)
 ap.add_argument("--n", type=int, default=1)
 ap.add_argument("--fast", type=int, default=0)
 ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--ls", type=int, default=0, help="1: layer-set operand (BITLUT_FLAG_LAYER_SET)")
 ap.add_argument("--shapes", default="4096x4096,11008x4096,4096x11008")
 args = ap.parse_args()
 dev = torch.device("cuda", 0)
@@ -31,16 +32,20 @@ for (m, k) in (tuple(int(v) for v in sh.split("x")) for sh in args.shapes.split(
     s = (torch.randn((m, k // args.gs), device=dev, generator=g).abs() * 0.02 + 1e-3).half()
     pw0 = B.prepare_weights(B.QuantizedWeights(m=m, k=k, bits=args.bits, group_size=args.gs,
                                                qvalues=q, scales=s))
-    ws = [pw0.gpu.clone() for _ in range(copies)]
+    w0, sc0 = pw0.gpu, pw0.scales
+    if args.ls:
+        w0, sc0, _ = pw0.layer_set_operand()
+    ws = [w0.clone() for _ in range(copies)]
     x = torch.randn((args.n, k), device=dev, generator=g).half()
     tabs = N.build_lut(x, args.gs, N.TABLE_Q8)
     res = {}
     for mode, fl in (("dep", N.FLAG_PDL), ("indep", N.FLAG_PDL | N.FLAG_INDEPENDENT)):
         fl |= N.FLAG_FAST_EPILOGUE if args.fast else 0
+        fl |= N.FLAG_LAYER_SET if args.ls else 0
 
         def body():
             for w in ws:
-                N.lookup(w, pw0.scales, None, *tabs, m, k, args.bits, args.gs, N.TABLE_Q8, fl, False)
+                N.lookup(w, sc0, None, *tabs, m, k, args.bits, args.gs, N.TABLE_Q8, fl, False)
         st = torch.cuda.Stream()
         with torch.cuda.stream(st):
             body()
