@@ -1625,6 +1625,8 @@ int bl_mpgemv_multi_launch(const bitlut_mat* mats, int n_mats, int k, int bits, 
   g.grid_out = grid_out;
   g.independent = pdl && (flags & BITLUT_FLAG_INDEPENDENT) != 0;
   g.fast = (flags & BITLUT_FLAG_FAST_EPILOGUE) != 0;
+  g.layer_set = (flags & BITLUT_FLAG_LAYER_SET) != 0;   // operands in the layer-set layout (fast, lean kernel)
+  if (g.layer_set && !g.fast) return BITLUT_ELAYOUT;
   g.zeros = mats[0].zeros;                              // presence flag for the epilogue
   g.rows_per_cta = 1; g.n_rows = 1;
   const cudaStream_t st = (cudaStream_t)stream;
@@ -1757,6 +1759,7 @@ int bl_mpgemv_multi_tab_launch(const bitlut_mat_tab* mats, int n_mats, int k, in
   g.L = L;
   g.independent = pdl && (flags & BITLUT_FLAG_INDEPENDENT) != 0;
   g.fast = 1;
+  g.layer_set = (flags & BITLUT_FLAG_LAYER_SET) != 0;   // operands in the layer-set layout
   g.zeros = mats[0].zeros;
   g.rows_per_cta = 1; g.n_rows = 1;
   g.mixed_tables = 1;

@@ -45,6 +45,7 @@ bool bl_gemv_b1_fused_fits(const bl::LayoutV2& L, bool zeros, int scale_dtype); 
 static bool fusable_lookup(const bitlut_pipe_op& s, const bitlut_pipe_op& t) {
   if (s.type != BITLUT_OP_LOOKUP || t.type != BITLUT_OP_TABLES) return false;
   if (!(s.flags & BITLUT_FLAG_FAST_EPILOGUE) || s.n != 1 || t.n != 1 || t.a_dtype != BITLUT_DT_F16) return false;
+  if (s.flags & BITLUT_FLAG_LAYER_SET) return false;    // the fused kernel reads layout v2
   if (s.k != t.k || s.group_size != t.group_size) return false;
   bl::LayoutV2 L;
   if (bl::make_layout(s.m, s.k, s.bits, s.group_size, &L) || L.n_sg != 1) return false;
@@ -74,6 +75,7 @@ static bool groupable_lookups(const bitlut_pipe_op& a, const bitlut_pipe_op& b, 
     if (specs[a.dep[0]].n != 1 || specs[b.dep[0]].n != 1) return false;
   }
   if ((a.flags & BITLUT_FLAG_FAST_EPILOGUE) != (b.flags & BITLUT_FLAG_FAST_EPILOGUE)) return false;
+  if ((a.flags & BITLUT_FLAG_LAYER_SET) != (b.flags & BITLUT_FLAG_LAYER_SET)) return false;
   if (a.n != 1 || b.n != 1 || a.k != b.k || a.bits != b.bits || a.group_size != b.group_size) return false;
   if (a.scale_dtype != b.scale_dtype || (a.zeros != nullptr) != (b.zeros != nullptr)) return false;
   if (specs[a.dep[0]].type != BITLUT_OP_TABLES) return false;
@@ -161,7 +163,7 @@ extern "C" int bitlut_pipeline_plan_flags(const bitlut_pipe_op* specs, int n_ops
     for (int u = i; u < j; u++) {
       int fl = BITLUT_FLAG_PDL | flags_out[u];
       if (ok) fl |= BITLUT_FLAG_INDEPENDENT;
-      if (lookup) fl |= specs[u].flags & BITLUT_FLAG_FAST_EPILOGUE;
+      if (lookup) fl |= specs[u].flags & (BITLUT_FLAG_FAST_EPILOGUE | BITLUT_FLAG_LAYER_SET);
       flags_out[u] = fl;
     }
     if (lookup && !ok) done_below = i;   // waits for its predecessor (hence all earlier), then releases
@@ -182,7 +184,8 @@ extern "C" int bitlut_pipeline_launch_ops(const bitlut_pipe_op* specs, int n_ops
     if (fl == BITLUT_PLAN_SKIP) { i++; continue; }
     int j = i + 1;
     while (j < n_ops && flags[j] != BITLUT_PLAN_SKIP && (flags[j] & BITLUT_PLAN_JOINED)) j++;
-    const int lf = fl & (BITLUT_FLAG_PDL | BITLUT_FLAG_INDEPENDENT | BITLUT_FLAG_FAST_EPILOGUE);
+    const int lf = fl & (BITLUT_FLAG_PDL | BITLUT_FLAG_INDEPENDENT | BITLUT_FLAG_FAST_EPILOGUE |
+                         (s.type == BITLUT_OP_LOOKUP ? BITLUT_FLAG_LAYER_SET : 0));
     if (s.type == BITLUT_OP_TABLES) {
       if (j - i == 1) {
         rc = bitlut_build_lut(s.a, s.a_dtype, s.n, s.k, s.group_size, BITLUT_TABLE_Q8, s.tables,
@@ -325,7 +328,8 @@ extern "C" int bitlut_pipeline_launch_ops_counted(const bitlut_pipe_op* specs, i
       }
     }
     if (overflow) { rc = BITLUT_EPARAM; break; }   // > 8 producer launches: use sync="pdl"
-    const int lf = BITLUT_FLAG_PDL | (fl & BITLUT_FLAG_FAST_EPILOGUE);
+    const int lf = BITLUT_FLAG_PDL | (fl & BITLUT_FLAG_FAST_EPILOGUE) |
+                   (s.type == BITLUT_OP_LOOKUP ? (fl & BITLUT_FLAG_LAYER_SET) : 0);
     dep.counted = 1;
     dep.done = counters + i;
     dep.total = nullptr;

@@ -172,11 +172,39 @@ class Pipeline:
         s.scale_dtype, s.m, s.bits = N.dtype_code(pw.scales), pw.m, pw.bits
         s.out = out.data_ptr()
         s.flags = N.FLAG_FAST_EPILOGUE if fast_epilogue else 0
+        ls = pw.__dict__.get("_layer_set")
+        if (self.executor == "graph" and fast_epilogue and t.n == 1 and ls is not None
+                and pw.encoding in ("offset", "zeros") and self._layer_set_ok(pw, ls, t, out)):
+            # the cached layer-set operand (pw.layer_set_operand()) in the lean kernel: same bits
+            s.wgpu, s.wscales = ls[0].data_ptr(), ls[1].data_ptr()
+            s.zeros = ls[2].data_ptr() if ls[2] is not None else None
+            s.flags |= N.FLAG_LAYER_SET
+            self.keep += list(ls)
         self.specs.append(s)
         self.keep += [pw.gpu, pw.scales, pw.zeros, out, pw.native_scales, partials]
         self._wextra[len(self.specs) - 1] = (pw, partials)
         self.outputs.append(out)
         return out
+
+    @staticmethod
+    def _layer_set_ok(pw, ls, t: "TableRef", out: torch.Tensor) -> bool:
+        """Probe launch: does bitlut_mpgemm take this call with the layer-set
+        operand (BITLUT_ELAYOUT where the lean kernel does not apply)?  The
+        op's own buffers are used; they are rewritten when the pipeline runs."""
+        from .errors import LayoutError
+        tables, ts, rs = t.tensors
+        if not out.is_cuda:
+            return False
+        try:
+            rc = N.lib().bitlut_mpgemm(ls[0].data_ptr(), pw.m, pw.k, pw.bits, pw.group_size, ls[1].data_ptr(),
+                                       ls[2].data_ptr() if ls[2] is not None else None, N.dtype_code(ls[1]),
+                                       tables.data_ptr(), ts.data_ptr(), rs.data_ptr(), N.TABLE_Q8, 1,
+                                       out.data_ptr(), None, N.FLAG_FAST_EPILOGUE | N.FLAG_LAYER_SET,
+                                       ctypes.c_void_p(torch.cuda.current_stream(out.device).cuda_stream))
+            raise_for_status(rc, "bitlut_mpgemm")
+            return True
+        except LayoutError:
+            return False
 
     def op_of(self, out: torch.Tensor) -> int:
         """Op index of a lookup output (to name it as a dependency)."""

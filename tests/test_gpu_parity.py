@@ -974,3 +974,50 @@ def test_lookup_layer_set_operand(bits, gs, k):
     ref = B.mpgemm(x, pw0, exact_epilogue=False)
     pw0.layer_set_operand()
     assert torch.equal(B.mpgemm(x, pw0, exact_epilogue=False), ref)
+
+
+def test_graph_executor_layer_set_operand():
+    """The graph executor with PackedWeights that carry the layer-set operand
+    (pw.layer_set_operand()): grouped launches over one table (q,k,v), over
+    different tables, a dependent chain and a zero-point matrix all run the
+    lean kernel's layer-set path (plan flag 64) and give the bits of the v2
+    operand; an exact-epilogue lookup in the same list keeps v2."""
+    from paper_2407_00088_b200 import _native as N
+    from paper_2407_00088_b200.pipeline import Pipeline
+    g = torch.Generator(device="cuda").manual_seed(99)
+    k, gs, bits = 2048, 64, 2
+
+    def mk(m, zeros=False):
+        q = torch.randint(0, 1 << bits, (m, k), dtype=torch.uint8, device="cuda", generator=g)
+        sc = (torch.randn((m, k // gs), device="cuda", generator=g).abs() * 0.02 + 1e-3).half()
+        z = (torch.rand((m, k // gs), device="cuda", generator=g) * 3).half() if zeros else None
+        return B.QuantizedWeights(m=m, k=k, bits=bits, group_size=gs, qvalues=q, scales=sc, zeros=z)
+
+    qws = [mk(512), mk(256), mk(256), mk(1024), mk(128, zeros=True)]
+    xs = [torch.randn((1, k), device="cuda", generator=g).half() for _ in range(3)]
+
+    def run(use_ls):
+        pws = [B.prepare_weights(qw) for qw in qws]
+        if use_ls:
+            for p in pws:
+                p.layer_set_operand()
+        pl = Pipeline()
+        t0 = pl.tables(xs[0], gs)
+        ys = [pl.lookup(p, t0, fast_epilogue=True) for p in pws[:3]]          # one table: grouped
+        t1 = pl.tables(xs[1], gs, deps=[pl.op_of(y) for y in ys])              # chain
+        ys.append(pl.lookup(pws[3], t1, fast_epilogue=True))
+        t2 = pl.tables(xs[2], gs)
+        ys.append(pl.lookup(pws[4], t2, fast_epilogue=True))                   # zero points
+        ys.append(pl.lookup(pws[0], t2))                                       # exact: v2 operand
+        pl.compile()
+        flags = [f for f in pl.plan_flags() if f != -1]
+        pl.run()
+        torch.cuda.synchronize()
+        return ys, flags, pws
+
+    ref, f0, _ = run(False)
+    out, f1, keep = run(True)
+    assert not any(f & N.FLAG_LAYER_SET for f in f0)
+    assert sum(1 for f in f1 if f & N.FLAG_LAYER_SET) == 5
+    for a, b in zip(ref, out):
+        assert torch.equal(a, b)

@@ -18,6 +18,10 @@ torch.cuda.set_device(dev)
 st = torch.cuda.Stream(dev)
 L = bench.build_layers(32, 2, 64, 0, 1, dev)
 acts, _ = bench.make_acts(32, dev)
+if os.environ.get("CHAIN_LAYER_SET", "1") == "1":       # the lean kernels' layer-set operand (second weight copy)
+    for layer in L:
+        for pw in layer.values():
+            pw.layer_set_operand()
 res = {"label": sys.argv[1] if len(sys.argv) > 1 else os.environ.get("BITLUT_L2_PREFETCH", "1")}
 nb = bench.packed_bytes_full(32, 2)
 for name, fast, chain, ex in (("decode_chain_fast", True, True, "graph"),
