@@ -459,14 +459,21 @@ def llama70b_table(device, stream, reps, warmup, barrier, peak):
                     x = torch.randn((nrow, k), device=device, generator=gen).half()
                     tabs = N.build_lut(x, gs, N.TABLE_Q8)
                     fl = N.FLAG_PDL | N.FLAG_FAST_EPILOGUE | (N.FLAG_INDEPENDENT if nrow == 1 else 0)
+                    wsel, ssel = ws, scs
+                    lw, lsc, _, lsf = fast_operand(pw, tabs)     # layer-set operand where the lean kernels apply
+                    if lsf:
+                        wsel = [lw] + [lw.clone() for _ in range(copies - 1)]
+                        ssel = [lsc] + [lsc.clone() for _ in range(copies - 1)]
+                        fl |= lsf
 
-                    def body(fl=fl, tabs=tabs):
-                        for w, sc_ in zip(ws, scs):
+                    def body(fl=fl, tabs=tabs, wsel=wsel, ssel=ssel):
+                        for w, sc_ in zip(wsel, ssel):
                             N.lookup(w, sc_, None, *tabs, m_loc, k, bits, gs, N.TABLE_Q8, fl, False)
                     g = capture(body, stream)
                     with torch.cuda.stream(stream):
                         ms = time_graph(g, reps, warmup, barrier)
                     del g
+                    del wsel, ssel
                     us = ms * 1e3 / len(ws)
                     e[f"n{nrow}_us"] = round(us, 3)
                     e[f"n{nrow}_GBps"] = round(nbytes / (us * 1e-6) / 1e9, 1)
@@ -515,20 +522,31 @@ def _llama70b_layer_graph(device, stream, reps, warmup, barrier, bits, gs, P, ge
     xs = {kk: torch.randn((1, kk), device=device, generator=gen).half() for kk in (8192, 28672)}
     tabs = {kk: N.build_lut(x, gs, N.TABLE_Q8) for kk, x in xs.items()}
     fl = N.FLAG_PDL | N.FLAG_FAST_EPILOGUE | N.FLAG_INDEPENDENT
+    # layer-set operands for the K = 8192 launches where the lean kernel takes them
+    # (the long-K down projection runs the split-K cluster kernel on layout v2)
+    ops = []
+    for L in sets:
+        o = {}
+        for nm, pw in L.items():
+            w_, s_, _, f_ = fast_operand(pw, tabs[pw.k]) if nm != "down" else (pw.gpu, pw.scales, None, 0)
+            o[nm] = (w_, s_, None, pw.m, f_)
+        ops.append(o)
+    ls8 = all(o[n][4] for o in ops for n in ("q", "k", "v", "o", "gate", "up"))
+    f8 = fl | (N.FLAG_LAYER_SET if ls8 else 0)
 
     def body():
-        for L in sets:
-            N.mpgemv_multi([(L[n].gpu, L[n].scales, None, L[n].m) for n in ("q", "k", "v")], *tabs[8192],
-                           8192, bits, gs, fl)
-            N.lookup(L["o"].gpu, L["o"].scales, None, *tabs[8192], L["o"].m, 8192, bits, gs, N.TABLE_Q8, fl, False)
-            N.mpgemv_multi([(L[n].gpu, L[n].scales, None, L[n].m) for n in ("gate", "up")], *tabs[8192],
-                           8192, bits, gs, fl)
+        for L, o in zip(sets, ops):
+            sel = (lambda n: o[n][:4]) if ls8 else (lambda n: (L[n].gpu, L[n].scales, None, L[n].m))
+            N.mpgemv_multi([sel(n) for n in ("q", "k", "v")], *tabs[8192], 8192, bits, gs, f8)
+            wo = sel("o")
+            N.lookup(wo[0], wo[1], None, *tabs[8192], L["o"].m, 8192, bits, gs, N.TABLE_Q8, f8, False)
+            N.mpgemv_multi([sel(n) for n in ("gate", "up")], *tabs[8192], 8192, bits, gs, f8)
             N.lookup(L["down"].gpu, L["down"].scales, None, *tabs[28672], L["down"].m, 28672, bits, gs,
                      N.TABLE_Q8, fl, False)
     g = capture(body, stream)
     with torch.cuda.stream(stream):
         ms = time_graph(g, reps, warmup, barrier)
-    del g, sets
+    del g, sets, ops
     torch.cuda.empty_cache()
     return {"us": round(ms * 1e3 / n_sets, 3), "launches": 4}
 

@@ -81,7 +81,9 @@ extern "C" {
  * select-free lane reductions (outputs bitwise those of the v2 operand);
  * BITLUT_ELAYOUT where those kernels do not apply (exact epilogue, long K,
  * zero points at N >= 8, groups wider than a lane's accumulators) -- pass
- * the v2 operand then. */
+ * the v2 operand then.  Also accepted by bitlut_mpgemv_multi and
+ * bitlut_mpgemv_multi_tab (every matrix of the launch in the layer-set
+ * layout) and, per lookup op, by the op-list executor. */
 #define BITLUT_FLAG_LAYER_SET 64
 
 /*
