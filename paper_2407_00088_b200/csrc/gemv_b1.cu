@@ -1050,8 +1050,10 @@ __global__ void __launch_bounds__(256) gemv_b1_cluster_kernel(const __grid_const
   if (p.dep.counted) bl::dep_wait(p.dep);
   else if (!p.independent) bl::pdl_wait();
   bl::pdl_launch_dependents();
-  const int u = ua + tid;
-  const bool live = u < ue;
+  // a thread past the rank's last unit shadows it with all-zero tables (exact
+  // zeros everywhere): the tile loop has no "live" branches
+  const bool live = ua + tid < ue;
+  const int u = live ? ua + tid : max(ue - 1, ua);
   const int ub = u >> 5, l = u & 31;
   const int nu_b = min(32, U - 32 * ub);
   const int g = u / LG;
@@ -1063,6 +1065,9 @@ __global__ void __launch_bounds__(256) gemv_b1_cluster_kernel(const __grid_const
     for (int jp = 0; jp < R / 2; jp++) tq[jp] = bl::ld_cg_128(tb + jp * nu_b * 16);
     ts = bl::ld_cg_f32(p.tscales + g);
     rs = bl::ld_cg_f32(p.rowsums + g);
+  } else {
+#pragma unroll
+    for (int jp = 0; jp < R / 2; jp++) tq[jp] = make_uint4(0, 0, 0, 0);
   }
   const uint32_t woff = (uint32_t)((ub - b0) * (32 * R * 16) + l * 16);
   __syncthreads();                                      // barriers initialised
@@ -1076,7 +1081,7 @@ __global__ void __launch_bounds__(256) gemv_b1_cluster_kernel(const __grid_const
     int acc[NACC];
 #pragma unroll
     for (int i = 0; i < NACC; i++) acc[i] = 0;
-    if (live) {
+    {
       const uint8_t* wsrc = sb + woff;
       const int stride = nu_b * 16;
 #pragma unroll
@@ -1090,7 +1095,7 @@ __global__ void __launch_bounds__(256) gemv_b1_cluster_kernel(const __grid_const
     const int base = reduce_lanes<NACC, 1, LG>(acc, lane);
     const int ch0 = BITS == 1 ? 2 * base : base;
     float y[NCH];
-    if (live) {
+    {
       int Sv[NCH];
       if constexpr (BITS == 1) {
 #pragma unroll
@@ -1117,9 +1122,6 @@ __global__ void __launch_bounds__(256) gemv_b1_cluster_kernel(const __grid_const
 #pragma unroll
         for (int j = 0; j < NCH; j++) y[j] = bl::to_f32(sp[j * NQ]) * fmaf(ts, (float)Sv[j], -rs);
       }
-    } else {
-#pragma unroll
-      for (int j = 0; j < NCH; j++) y[j] = 0.f;
     }
     const int fb = reduce_lanes<NCH, LG, 32>(y, lane);
     float* yb = ysm + (it & 1) * NW * TCH + warp * TCH;
@@ -1141,11 +1143,12 @@ __global__ void __launch_bounds__(256) gemv_b1_cluster_kernel(const __grid_const
         a.mats[j].out[(int64_t)local * TCH + tid] = 0.5f * sum;
       }
     }
-    if (tid < TCH) {
-      const float* yr = ysm + (it & 1) * NW * TCH + tid;
+    if (tid >= 32 && tid < 32 + TCH) {                  // warp 1 adds the sums (thread 0 refills)
+      const int cc = tid - 32;
+      const float* yr = ysm + (it & 1) * NW * TCH + cc;
       float sum = 0.f;
       for (int w = 0; w < NW; w++) sum += yr[w * TCH];
-      st_cluster_f32(part + (it & 1) * CS * TCH + rank * TCH + tid, 0, sum);
+      st_cluster_f32(part + (it & 1) * CS * TCH + rank * TCH + cc, 0, sum);
     }
     cluster_arrive_release();
     prev_tile = tile;
