@@ -393,10 +393,19 @@ def config1_table(device, stream, reps, warmup, barrier, peak):
         tabs = N.build_lut(x, gs, mode)
         base = N.FLAG_PDL | (N.FLAG_FAST_EPILOGUE if fast else 0)
         e = {}
+        wsel, scl, zl = ws, pw.scales, pw.zeros
+        if fast:                                   # the layer-set operand (the lean kernel takes both table formats)
+            lw, lsc, lz = pw.layer_set_operand()
+            try:
+                N.lookup(lw, lsc, lz, *tabs, m, k, bits, gs, mode, base | N.FLAG_LAYER_SET, False)
+                wsel, scl, zl = [lw] + [lw.clone() for _ in range(copies - 1)], lsc, lz
+                base |= N.FLAG_LAYER_SET
+            except B.LayoutError:
+                pass
         for label, fl in (("overlapped", base | N.FLAG_INDEPENDENT), ("chained", base)):
-            def body(fl=fl, tabs=tabs, mode=mode):
-                for w in ws:
-                    N.lookup(w, pw.scales, pw.zeros, *tabs, m, k, bits, gs, mode, fl, False)
+            def body(fl=fl, tabs=tabs, mode=mode, wsel=wsel, scl=scl, zl=zl):
+                for w in wsel:
+                    N.lookup(w, scl, zl, *tabs, m, k, bits, gs, mode, fl, False)
             g = capture(body, stream)
             with torch.cuda.stream(stream):
                 ms = time_graph(g, reps, warmup, barrier)
@@ -406,10 +415,10 @@ def config1_table(device, stream, reps, warmup, barrier, peak):
             e[label + "_GBps"] = round(nbytes / (us * 1e-6) / 1e9, 1)
             e[label + "_frac_of_peak"] = round(nbytes / (us * 1e-6) / 1e9 / peak, 4)
 
-        def call(mode=mode, base=base):     # the whole call: table build + lookup, chained
-            for w in ws:
+        def call(mode=mode, base=base, wsel=wsel, scl=scl, zl=zl):     # the whole call: table build + lookup, chained
+            for w in wsel:
                 t = N.build_lut(x, gs, mode, N.FLAG_PDL)
-                N.lookup(w, pw.scales, pw.zeros, *t, m, k, bits, gs, mode, base, False)
+                N.lookup(w, scl, zl, *t, m, k, bits, gs, mode, base, False)
         g = capture(call, stream)
         with torch.cuda.stream(stream):
             ms = time_graph(g, reps, warmup, barrier)

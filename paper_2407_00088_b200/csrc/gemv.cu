@@ -269,8 +269,11 @@ int bl_mpgemm_launch(const uint8_t* wgpu, int m, int k, int bits, int group_size
   if (flags & BITLUT_FLAG_LAYER_SET) {
     // operand in the layer-set layout: fast epilogue, int8 tables, the lean
     // batch-1 / rows kernels only (else the caller passes the v2 operand)
-    if (!(mode == BITLUT_TABLE_Q8 && a.fast && !partials && !trace && L.n_sg == 1)) return BITLUT_ELAYOUT;
+    if (!((mode == BITLUT_TABLE_Q8 || (mode == BITLUT_TABLE_X16 && n == 1)) && a.fast && !partials && !trace &&
+          L.n_sg == 1))
+      return BITLUT_ELAYOUT;
     a.layer_set = 1;
+    a.f16_tables = mode == BITLUT_TABLE_X16 ? BITLUT_TABLE_X16 : 0;
     return bl_gemv_b1_launch(a, scale_dtype, (cudaStream_t)stream, pdl);
   }
   if (mode == BITLUT_TABLE_X16) {

@@ -648,9 +648,9 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
       ts = bl::ld_cg_f32(tsc + g);
     }
     rs = bl::ld_cg_f32(rsum + g);
-  } else if constexpr (!F16) {
+  } else {
 #pragma unroll
-    for (int jp = 0; jp < R / 2; jp++) tq[jp] = make_uint4(0, 0, 0, 0);
+    for (int jp = 0; jp < (F16 ? R : R / 2); jp++) tq[jp] = make_uint4(0, 0, 0, 0);
   }
   const uint32_t woff = (uint32_t)(ub * (32 * R * 16) + l * 16);
   BL_CHECK(a.bar_off + 8u * (kMaxStages + 1) <= bl::dyn_smem_bytes());
@@ -662,72 +662,35 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
     uint8_t* sb = smem + stage * a.stage_bytes;
     mbar_wait(bar + stage, (S == 1 ? it : it >> 1) & 1);
     float y[NCH];
-    int ch0;
-    if constexpr (F16) {
-      // 16-bit block-fixed-point tables (BITLUT_TABLE_X16): the H and L digit
-      // tables of a k-group are one uint4; the int8 core runs once per digit
-      // with shared selectors, S = 127 S_H + S_L exactly
-      int accH[NACC], accL[NACC];
-#pragma unroll
-      for (int i = 0; i < NACC; i++) accH[i] = accL[i] = 0;
-      if (live) {
-        const uint8_t* wsrc = sb + woff;
-        const int stride = nu_b == 32 ? 512 : nu_b * 16;
-#pragma unroll
-        for (int j = 0; j < R; j++)
-          lookup_kg_merged2<BITS, NACC>(*reinterpret_cast<const uint4*>(wsrc + j * stride), tq[j].x, tq[j].y,
-                                        tq[j].z, tq[j].w, accH, accL);
-      }
-      const int base = reduce_lanes<NACC, 1, LG>(accH, lane);
-      reduce_lanes<NACC, 1, LG>(accL, lane);
-      ch0 = BITS == 1 ? 2 * base : base;
-      if (live) {
-        int Sv[NCH];
-        if constexpr (BITS == 1) {
-#pragma unroll
-          for (int i = 0; i < NV; i++) {
-            const int vh = accH[i], vl = accL[i];
-            const int he = (vh << 17) >> 17, le = (vl << 17) >> 17;
-            Sv[2 * i] = 127 * he + le;
-            Sv[2 * i + 1] = 127 * ((vh - he) >> 15) + ((vl - le) >> 15);
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < NV; i++) Sv[i] = 127 * accH[i] + accL[i];
-        }
-        const ST* sp = reinterpret_cast<const ST*>(sb + a.s_off) + ch0 * NQ + g;
-        if constexpr (ZEROS) {
-          const ST* zp = reinterpret_cast<const ST*>(sb + a.z_off) + ch0 * NQ + g;
-          const float h2 = (float)(2 << (BITS - 1));
-#pragma unroll
-          for (int j = 0; j < NCH; j++) {
-            const float t = fmaf(fmaf(-2.f, bl::to_f32(zp[j * NQ]), h2), rs, fmaf(ts, (float)Sv[j], -rs));
-            y[j] = bl::to_f32(sp[j * NQ]) * t;
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < NCH; j++) y[j] = bl::to_f32(sp[j * NQ]) * fmaf(ts, (float)Sv[j], -rs);
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < NCH; j++) y[j] = 0.f;
-      }
-    } else {
+    int ch0 = 0;
+    // integer sums: int8 tables, or (F16) the two digit tables of the 16-bit
+    // block-fixed-point tables (BITLUT_TABLE_X16: the H and L digit tables of a
+    // k-group are one uint4; the int8 core runs once per digit with shared
+    // selectors), combined per lane as S = 127 S_H + S_L -- exact -- before
+    // the lane reduction (W1: after it, the packed pair fields would overflow)
     int acc[NACC];
+    int accL[F16 && BITS == 1 ? NACC : 1];
 #pragma unroll
     for (int i = 0; i < NACC; i++) acc[i] = 0;
     {
       const uint8_t* wsrc = sb + woff;
-      if (nu_b == 32) {
+      const int stride = nu_b == 32 ? 512 : nu_b * 16;
+      if constexpr (F16) {
+        int lo[NACC];
 #pragma unroll
-        for (int j = 0; j < R; j += 2) {
-          const uint4 wa = *reinterpret_cast<const uint4*>(wsrc + j * 512);
-          const uint4 wc = *reinterpret_cast<const uint4*>(wsrc + (j + 1) * 512);
-          lookup_kg_merged<BITS, NACC>(wa, tq[j >> 1].x, tq[j >> 1].y, acc);
-          lookup_kg_merged<BITS, NACC>(wc, tq[j >> 1].z, tq[j >> 1].w, acc);
+        for (int i = 0; i < NACC; i++) lo[i] = 0;
+#pragma unroll
+        for (int j = 0; j < R; j++)
+          lookup_kg_merged2<BITS, NACC>(*reinterpret_cast<const uint4*>(wsrc + j * stride), tq[j].x, tq[j].y,
+                                        tq[j].z, tq[j].w, acc, lo);
+        if constexpr (BITS == 1) {
+#pragma unroll
+          for (int i = 0; i < NACC; i++) accL[i] = lo[i];
+        } else {
+#pragma unroll
+          for (int i = 0; i < NACC; i++) acc[i] = 127 * acc[i] + lo[i];
         }
       } else {
-        const int stride = nu_b * 16;
 #pragma unroll
         for (int j = 0; j < R; j += 2) {
           const uint4 wa = *reinterpret_cast<const uint4*>(wsrc + j * stride);
@@ -739,9 +702,10 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
     }
     if constexpr (PERM) {
       reduce_lanes_perm<NACC, 1, LG>(acc);
-      ch0 = 0;
+      if constexpr (F16 && BITS == 1) reduce_lanes_perm<NACC, 1, LG>(accL);
     } else {
       const int base = reduce_lanes<NACC, 1, LG>(acc, lane);
+      if constexpr (F16 && BITS == 1) reduce_lanes<NACC, 1, LG>(accL, lane);
       ch0 = BITS == 1 ? 2 * base : base;
     }
     {
@@ -753,6 +717,12 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
           const int pe = (v << 17) >> 17;
           Sv[2 * i] = pe;
           Sv[2 * i + 1] = (v - pe) >> 15;
+          if constexpr (F16) {
+            const int vl = accL[i];
+            const int le = (vl << 17) >> 17;
+            Sv[2 * i] = 127 * Sv[2 * i] + le;
+            Sv[2 * i + 1] = 127 * Sv[2 * i + 1] + ((vl - le) >> 15);
+          }
         }
       } else {
 #pragma unroll
@@ -777,25 +747,24 @@ __global__ void __launch_bounds__(384) gemv_b1_lean_kernel(const __grid_constant
           for (int j = 0; j < NCH; j++) y[j] = __fmul_rn(vec_elem<ST>(sv, j), fmaf(ts, (float)Sv[j], -rs));
         }
       } else {
-      const ST* sp = reinterpret_cast<const ST*>(sb + a.s_off) + ch0 * NQ + g;
-      if constexpr (ZEROS) {
-        // asymmetric zero points: + 2 (2^(b-1) - z) rs per (channel, group)
-        const ST* zp = reinterpret_cast<const ST*>(sb + a.z_off) + ch0 * NQ + g;
-        const float h2 = (float)(2 << (BITS - 1));
+        const ST* sp = reinterpret_cast<const ST*>(sb + a.s_off) + ch0 * NQ + g;
+        if constexpr (ZEROS) {
+          // asymmetric zero points: + 2 (2^(b-1) - z) rs per (channel, group)
+          const ST* zp = reinterpret_cast<const ST*>(sb + a.z_off) + ch0 * NQ + g;
+          const float h2 = (float)(2 << (BITS - 1));
 #pragma unroll
-        for (int j = 0; j < NCH; j++) {
-          const float t = fmaf(fmaf(-2.f, bl::to_f32(zp[j * NQ]), h2), rs, fmaf(ts, (float)Sv[j], -rs));
-          y[j] = bl::to_f32(sp[j * NQ]) * t;
+          for (int j = 0; j < NCH; j++) {
+            const float t = fmaf(fmaf(-2.f, bl::to_f32(zp[j * NQ]), h2), rs, fmaf(ts, (float)Sv[j], -rs));
+            y[j] = bl::to_f32(sp[j * NQ]) * t;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < NCH; j++) y[j] = bl::to_f32(sp[j * NQ]) * fmaf(ts, (float)Sv[j], -rs);
         }
-      } else {
-#pragma unroll
-        for (int j = 0; j < NCH; j++) y[j] = bl::to_f32(sp[j * NQ]) * fmaf(ts, (float)Sv[j], -rs);
       }
-      }
-    }
     }
     float* yb = ysm + (it & 1) * NW * TCH + warp * TCH;
-    if constexpr (PERM && !F16) {
+    if constexpr (PERM) {
       reduce_lanes_perm<NCH, LG, 32>(y);
       yb[perm_mask<TCH>(lane)] = y[0];
     } else {
@@ -1355,11 +1324,13 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
   // layer-set operand: the lean kernels only, and only where the per-unit scale
   // vectors are a permutation of the (channel, group) block (same stage plan)
   const bool perm = g.layer_set != 0;
-  if (perm && (f16 || !(lean || lean_rows) ||
+  if (perm && (!(lean || lean_rows) ||
                bl::layer_set_scale_bytes(L, (int)sizeof(ST)) != (int64_t)L.tile_ch * L.NQ * (int64_t)sizeof(ST)))
     return BITLUT_ELAYOUT;
-  auto kern = lean ? (f16 ? (has_z ? gemv_b1_lean_kernel<R, LG, BITS, ST, true, true>
-                                   : gemv_b1_lean_kernel<R, LG, BITS, ST, false, true>)
+  auto kern = lean ? (f16 ? (perm ? (has_z ? gemv_b1_lean_kernel<R, LG, BITS, ST, true, true, true>
+                                           : gemv_b1_lean_kernel<R, LG, BITS, ST, false, true, true>)
+                                  : (has_z ? gemv_b1_lean_kernel<R, LG, BITS, ST, true, true>
+                                           : gemv_b1_lean_kernel<R, LG, BITS, ST, false, true>))
                           : (perm ? (has_z ? gemv_b1_lean_kernel<R, LG, BITS, ST, true, false, true>
                                            : gemv_b1_lean_kernel<R, LG, BITS, ST, false, false, true>)
                                   : (has_z ? gemv_b1_lean_kernel<R, LG, BITS, ST, true>
@@ -1367,8 +1338,9 @@ int launch_b1(const GemvArgs& g, const B1Mat* mats, int n_mats, const __half* ac
                    : (lean_rows ? (perm ? gemv_b1_rows_lean_kernel<R, LG, BITS, ST, true>
                                         : gemv_b1_rows_lean_kernel<R, LG, BITS, ST, false>)
                                 : gemv_b1_kernel<R, LG, BITS, ST, KIND>);
-  static bool configured_k[64][12] = {};               // per device and kernel variant
-  const int ki = (lean ? (has_z ? 2 : 1) + (f16 ? 3 : 0) : (lean_rows ? 6 : 0)) + (perm ? 7 : 0) - (perm && lean_rows ? 2 : 0);
+  static bool configured_k[64][16] = {};               // per device and kernel variant
+  // 0 general; 1,2 lean (zeros); 4,5 lean X16; 6 rows; + 8 with the layer-set operand
+  const int ki = (lean ? (has_z ? 2 : 1) + (f16 ? 3 : 0) : (lean_rows ? 6 : 0)) + (perm ? 8 : 0);
   bool& configured = configured_k[bl_device()][ki];
   if (!configured) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||

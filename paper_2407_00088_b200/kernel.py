@@ -302,8 +302,16 @@ def mpgemm(a, pw: PackedWeights, cfg: TileConfig | None = None,
     if out is None and mode == N.TABLE_F16 and not exact_epilogue and n == 1 and pw.bits != 3:
         try:      # cuda-f16 fast at batch 1: 16-bit block-fixed-point tables (BITLUT_TABLE_X16)
             tables, ts, rs = N.build_lut(rows, pw.group_size, N.TABLE_X16, N.FLAG_PDL if pdl else 0)
-            out, partials = N.lookup(pw.gpu, pw.scales, pw.zeros, tables, ts, rs, pw.m, pw.k, pw.bits,
-                                     pw.group_size, N.TABLE_X16, flags, False)
+            ls = pw.__dict__.get("_layer_set") if pw.encoding in ("offset", "zeros") else None
+            if ls is not None:
+                try:
+                    out, partials = N.lookup(ls[0], ls[1], ls[2], tables, ts, rs, pw.m, pw.k, pw.bits,
+                                             pw.group_size, N.TABLE_X16, flags | N.FLAG_LAYER_SET, False)
+                except LayoutError:
+                    out = None
+            if out is None:
+                out, partials = N.lookup(pw.gpu, pw.scales, pw.zeros, tables, ts, rs, pw.m, pw.k, pw.bits,
+                                         pw.group_size, N.TABLE_X16, flags, False)
         except LayoutError:
             out = None
     if out is None:

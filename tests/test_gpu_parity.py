@@ -966,6 +966,11 @@ def test_lookup_layer_set_operand(bits, gs, k):
             ref, _ = N.lookup(pw.gpu, pw.scales, pw.zeros, *tabs, m, k, bits, gs, N.TABLE_Q8, F, False)
             out, _ = N.lookup(lw, lsc, lz, *tabs, m, k, bits, gs, N.TABLE_Q8, F | N.FLAG_LAYER_SET, False)
             assert torch.equal(out, ref), (zeros is not None, n)
+            if n == 1:                        # the 16-bit block-fixed-point tables of cuda-f16 fast
+                t16 = N.build_lut(x, gs, N.TABLE_X16)
+                r16, _ = N.lookup(pw.gpu, pw.scales, pw.zeros, *t16, m, k, bits, gs, N.TABLE_X16, F, False)
+                o16, _ = N.lookup(lw, lsc, lz, *t16, m, k, bits, gs, N.TABLE_X16, F | N.FLAG_LAYER_SET, False)
+                assert torch.equal(o16, r16), (zeros is not None, "x16")
     with pytest.raises(B.LayoutError):       # exact epilogue: v2 operand only
         N.lookup(lw, lsc, lz, *tabs, m, k, bits, gs, N.TABLE_Q8, N.FLAG_PDL | N.FLAG_LAYER_SET, False)
     # mpgemm picks the cached layer-set operand for fast multi-row calls: same bits as without it
