@@ -1280,7 +1280,8 @@ def run_reference(args, bits, gs, rank, world, cfg):
         layer()
         t_layer.append(time.perf_counter() - t0)
     per_layer = min(t_layer[1:])
-    reps = max(1, int(np.ceil(args.ref_min_seconds / max(args.steps, 1) / per_layer)))
+    # 25 % margin: the timed steps run faster than the warm-up estimate (caches, numba threads warm)
+    reps = max(1, int(np.ceil(1.25 * args.ref_min_seconds / max(args.steps, 1) / per_layer)))
     samples = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
