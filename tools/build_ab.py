@@ -1,9 +1,10 @@
-"""Builds an A/B variant of the product library: gemv_batch.cu and gemv_b1.cu
-recompiled with -DBITLUT_AB=<n> (experiment switches in csrc/b1_core.cuh and
-csrc/gemv_batch.cu), linked with the product objects into
-_ab/libbitlut_ab_<n>.so.  Select it with BITLUT_B200_LIB.
+"""Builds A/B variants of the product library for same-box comparisons:
+gemv_batch.cu recompiled with extra defines (e.g. the per-tile duty
+assignment, BITLUT_REFILL_THREAD / BITLUT_SUM_WARP) and linked with the
+product objects into _ab/libbitlut_ab_<name>.so.  Select a variant with
+BITLUT_B200_LIB (tools/batch_ab.py, tools/batch_groups.py).
 
-    python tools/build_ab.py 1 3      # builds variants 1 and 3
+    python tools/build_ab.py "r0s1:-DBITLUT_REFILL_THREAD=0,-DBITLUT_SUM_WARP=1" "r32s0:-DBITLUT_REFILL_THREAD=32,-DBITLUT_SUM_WARP=0"
 """
 import os
 import subprocess

@@ -1,3 +1,5 @@
+"""BASELINE configs[0] (4096x4096 W4 g128, asymmetric zeros) per launch: bench.config1_table
+alone (cuda-f16 exact / fast on X16 tables, cuda-q8 exact / fast)."""
 import sys, json, torch
 sys.path.insert(0, '.')
 import bench
