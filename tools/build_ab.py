@@ -1,10 +1,10 @@
 """Builds A/B variants of the product library for same-box comparisons:
 gemv_batch.cu recompiled with extra defines (e.g. the per-tile duty
-assignment, BITLUT_REFILL_THREAD / BITLUT_SUM_WARP) and linked with the
+assignment, BITLUT_SUM_WARP) and linked with the
 product objects into _ab/libbitlut_ab_<name>.so.  Select a variant with
 BITLUT_B200_LIB (tools/batch_ab.py, tools/batch_groups.py).
 
-    python tools/build_ab.py "r0s1:-DBITLUT_REFILL_THREAD=0,-DBITLUT_SUM_WARP=1" "r32s0:-DBITLUT_REFILL_THREAD=32,-DBITLUT_SUM_WARP=0"
+    python tools/build_ab.py "s0:-DBITLUT_SUM_WARP=0" "s2:-DBITLUT_SUM_WARP=2"
 """
 import os
 import subprocess
