@@ -354,3 +354,35 @@ def test_random_instance_sweep_1000():
         rs = max(float(np.abs(real).max()), 1e-6)
         worst["f16"] = max(worst["f16"], float(np.abs(B.mpgemm(a, pw, variant="cuda-f16") - real).max()) / rs)
     assert worst["fast"] <= 1e-5 and worst["f16"] <= 1e-3, worst
+
+
+@pytest.mark.parametrize("kind,bits,gs", [("sign", 1, 32), ("sign", 1, 64), ("sign", 1, 256), ("sign", 1, 512),
+                                          ("ternary", 2, 32), ("ternary", 2, 64), ("ternary", 2, 512)])
+def test_batch_kernel_native_encodings_group_sizes(kind, bits, gs):
+    """Sign planes and per-tensor ternary weights through the batch executor
+    over the lanes-per-group classes of the layer-set layout (sign: the native
+    scale stream regrouped per unit, also where the vectors repeat; ternary: no
+    scale stream), K with a partial unit block: within 1e-5 of the oracle for
+    the equivalent (scale, zero) weights, exact integer sums."""
+    g = torch.Generator(device="cuda").manual_seed(bits * 100 + gs)
+    items, refs, wants = [], [], []
+    for m, k in ((96, 1536), (256, 3072)):
+        x = torch.randn((1, k), device="cuda", generator=g).half()
+        sc = (torch.randn((m, k // gs), device="cuda", generator=g).abs() * 0.02 + 1e-3).half()
+        if kind == "sign":
+            q = torch.randint(0, 2, (m, k), dtype=torch.uint8, device="cuda", generator=g)
+            qw = B.QuantizedWeights.sign_planes(q, sc, gs)
+        else:
+            v = torch.randint(-1, 2, (m, k), dtype=torch.int8, device="cuda", generator=g)
+            qw = B.QuantizedWeights.ternary(v, sc[0, 0], gs)
+        pw = B.prepare_weights(qw)
+        items.append((pw, x))
+        zz = qw.zeros.float().cpu().numpy()
+        refs.append(O.mpgemm_q8(x.cpu().numpy(), qw.qvalues.cpu().numpy(), qw.scales.float().cpu().numpy(),
+                                qw.bits, gs, zeros=zz)[0])
+        _, P = B.mpgemm(x, pw, return_partials=True)
+        wants.append(sum((1 << b) * P[0, b].to(torch.int64) for b in range(bits)))
+    outs, parts = _batch_run(items, partials=True)
+    for y, S, ref, want in zip(outs, parts, refs, wants):
+        assert rel_maxnorm(y[0].cpu().numpy(), ref) <= 1e-5
+        assert torch.equal(S.to(torch.int64), want)
